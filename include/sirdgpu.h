@@ -1,0 +1,185 @@
+/*
+ * sirdgpu.h — C-ABI of the B200 particle-window cost engine.
+ *
+ * This is the drop-in boundary for the reference's hot path (sirdfit, arXiv
+ * 2204.12346, /root/reference/proj).  Every entry point below replaces one
+ * reference interface; the citation after each declaration names it.
+ *
+ *   boundary 1 (cost only):   sirdfit::make_window_objective -> BatchObjective
+ *                             (include/sirdfit/calibration.hpp:84-85,
+ *                              src/calibration.cpp:120-155, pso.hpp:36-37)
+ *   boundary 2 (optimizer):   sirdfit::optimize / fit_window / fit_all_windows /
+ *                             stability_study / forecast_extension
+ *                             (pso.hpp:92-93, calibration.hpp:89-100, 143, 188-189)
+ *
+ * Conventions
+ *   - Plain C: POD structs, pointers and sizes; no torch or C++ types.
+ *   - Every function returns an sg_status (0 = OK).  The text of the last
+ *     error of a context is available from sg_last_error().  Status codes map
+ *     one-to-one onto the reference's exception types (errors.hpp:8-50).
+ *   - Host buffers are caller-owned and are fully consumed / filled before the
+ *     call returns.  Device memory is owned by the context.
+ *   - One context per device.  Calls on one context are externally serialized
+ *     (the reference's BatchObjective is called from one thread,
+ *     pso.cpp:81); different contexts may be driven from different threads.
+ *   - Numerical blow-up is data, not an error: a particle whose trajectory
+ *     leaves the finite range costs +inf (model.hpp:34-36,
+ *     objectives.cpp:101-103), exactly as in the reference.
+ *   - Results are bit-identical to the reference C++ built without FMA
+ *     contraction (the reference object code has none).
+ */
+#ifndef SIRDGPU_H
+#define SIRDGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SG_ABI_VERSION 1
+
+/* Status codes.  The C++ layer (sirdfit_b200.hpp) rethrows them as the
+ * reference's exception classes (errors.hpp:8-50). */
+typedef enum sg_status {
+    SG_OK = 0,
+    SG_ERR_INVALID_ARGUMENT = 1,        /* sirdfit::Error (e.g. calibration.cpp:141-143)   */
+    SG_ERR_SCHEME = 2,                  /* sirdfit::SchemeError (calibration.cpp:39-44)    */
+    SG_ERR_INSUFFICIENT_POPULATION = 3, /* InsufficientPopulationError (calibration.cpp:113)*/
+    SG_ERR_ALL_INFEASIBLE = 4,          /* AllInfeasibleError (pso.cpp:137-139)            */
+    SG_ERR_NON_FINITE = 5,              /* NonFiniteError (calibration.cpp:302, 318-320)   */
+    SG_ERR_CUDA = 6,                    /* device failure (no reference counterpart)      */
+    SG_ERR_NO_DEVICE = 7,               /* no sm_100 device / extension cannot run        */
+    SG_ERR_OUT_OF_MEMORY = 8            /* device allocation failed                       */
+} sg_status;
+
+/* sirdfit::Family / sirdfit::Metric (objectives.hpp:12-13) */
+enum { SG_FAMILY_D_ONLY = 0, SG_FAMILY_IRD_JOINT = 1 };
+enum { SG_METRIC_MXSE = 0, SG_METRIC_MSE = 1, SG_METRIC_MAE = 2, SG_METRIC_MAPE = 3 };
+
+/* sirdfit::SirdState (model.hpp:25-32) */
+typedef struct sg_state {
+    double S, I, R, D;
+} sg_state;
+
+typedef struct sg_ctx sg_ctx;
+typedef struct sg_window sg_window;
+
+int sg_abi_version(void);
+
+/* --- context ------------------------------------------------------------ */
+int sg_ctx_create(int device, sg_ctx** out);
+void sg_ctx_destroy(sg_ctx* ctx);
+const char* sg_last_error(const sg_ctx* ctx);
+/* Number of CUDA kernels this context has launched (telemetry for bench). */
+uint64_t sg_ctx_launch_count(const sg_ctx* ctx);
+/* Underlying cudaStream_t used by every call of this context. */
+void* sg_ctx_stream(const sg_ctx* ctx);
+
+/* --- boundary 1: the window objective ------------------------------------
+ * sg_window_create replaces the construction half of make_window_objective
+ * (calibration.cpp:120-139): it owns copies of the observed slices, the
+ * initial state, the population and the substep count, and precomputes the
+ * window-constant parts of objective_value (objectives.cpp:61-69: the
+ * per-compartment min-max scale; objectives.cpp:41-55: MAPE reciprocals).
+ * The three series hold n_days >= 1 values each (the window length, tau+1).
+ * Fails with SG_ERR_INVALID_ARGUMENT when integrate_euler would throw
+ * (model.cpp:78-80: n_days < 1, substeps < 1, population <= 0). */
+int sg_window_create(sg_ctx* ctx, const double* infectious, const double* recovered_cum,
+                     const double* deaths_cum, int n_days, sg_state init, double population, int substeps,
+                     int family, int metric, sg_window** out);
+void sg_window_destroy(sg_window* window);
+
+/* The BatchObjective body (calibration.cpp:140-154): costs[k] =
+ * objective_value(spec, slice, integrate_euler(params_from_position(pos[k])))
+ * for k < n.  positions is row-major n x dim host memory; dim must be 6. */
+int sg_eval_costs(sg_window* window, const double* positions, size_t n, size_t dim, double* costs);
+
+/* Same on device memory (row-major n x 6 doubles -> n doubles) on the given
+ * cudaStream_t (NULL = the context stream).  Asynchronous. */
+int sg_eval_costs_device(sg_window* window, const double* d_positions, size_t n, double* d_costs,
+                         void* cuda_stream);
+
+/* --- integrator -------------------------------------------------------------
+ * integrate_batch (model.cpp:116-125) / integrate_euler (model.cpp:76-107):
+ * one trajectory per parameter set, row-major params n x 6 in SirdParams
+ * order [beta1, beta2, t1, t2, gamma, mu].  states receives n x n_days x 4
+ * doubles (S,I,R,D per day, NaN after a blow-up exactly as model.cpp:84-104),
+ * finite receives n flags (Trajectory::finite). */
+int sg_integrate_batch(sg_ctx* ctx, const double* params, size_t n, sg_state init, double population,
+                       int n_days, int substeps, double* states, uint8_t* finite);
+
+/* --- boundary 2: the particle swarm --------------------------------------
+ * One descriptor per independent swarm (Swarm::Swarm + optimize,
+ * pso.cpp:47-143).  Swarms may use different windows, sizes and seeds;
+ * all swarms of one call run concurrently on the device. */
+typedef struct sg_swarm_desc {
+    const sg_window* window;  /* objective: the window's BatchObjective       */
+    double lower[6];          /* SearchBounds (pso.hpp:26-32)                 */
+    double upper[6];
+    uint64_t n_particles;     /* PsoConfig (pso.hpp:14-23)                    */
+    uint64_t max_iters;
+    double inertia;
+    double cognitive;
+    double social;
+    uint64_t seed;            /* particle i draws from mt19937_64(mix_seed(seed,i)) */
+    int repair_time_order;    /* 1: RepairHook = repair_time_order (calibration.cpp:89-93) */
+} sg_swarm_desc;
+
+typedef struct sg_swarm_result {
+    double best_position[6];  /* PsoResult::best_position (pso.hpp:50-54)     */
+    double best_cost;         /* PsoResult::best_cost                         */
+    double* cost_history;     /* caller-owned, max_iters slots, or NULL       */
+    int status;               /* SG_OK or SG_ERR_ALL_INFEASIBLE / SG_ERR_INVALID_ARGUMENT */
+} sg_swarm_result;
+
+/* Runs every swarm for its max_iters iterations.  Per-swarm failures are
+ * reported in results[k].status (the call itself returns SG_OK); a config
+ * that PsoConfig::validate / SearchBounds::validate would reject
+ * (pso.cpp:16-34) makes that swarm fail with SG_ERR_INVALID_ARGUMENT. */
+int sg_fit_swarms(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg_swarm_result* results);
+
+/* Reusable plan: the same work as sg_fit_swarms split into setup (validate,
+ * allocate, upload descriptors), an asynchronous device run on the context
+ * stream (engine seeding + max_iters fused step launches, no host round
+ * trips), and result collection.  Lets callers time or graph the device part
+ * alone; a plan may be run repeatedly (each run restarts from the seeds). */
+typedef struct sg_plan sg_plan;
+int sg_plan_create(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg_plan** out);
+int sg_plan_run(sg_plan* plan);
+int sg_plan_results(sg_plan* plan, sg_swarm_result* results);
+uint64_t sg_plan_evals(const sg_plan* plan);  /* sum of n_particles * max_iters */
+void sg_plan_destroy(sg_plan* plan);
+
+/* --- forecast ---------------------------------------------------------------
+ * forecast_extension (calibration.cpp:298-322), batched: for each k, holds
+ * beta = beta2 and integrates horizon+1 days from junction[k] (the fitted
+ * window's last state).  states receives n x (horizon+1) x 4; finite n flags
+ * (a blow-up is NonFiniteError in the reference: the caller decides). */
+int sg_forecast_batch(sg_ctx* ctx, const double* params, const sg_state* junction, size_t n,
+                      double population, int horizon, int substeps, double* states, uint8_t* finite);
+
+/* Forecast-scenario ensemble on one window: n parameter sets drawn exactly
+ * like the Swarm's initial sample (pso.cpp:55-73 + repair_time_order:
+ * set k = 6 uniform01 draws of mt19937_64(mix_seed(seed, k))), each
+ * integrated over the window and then `horizon` days with beta held at beta2
+ * (calibration.cpp:305-317).  Writes the window cost of each set (costs, n,
+ * optional), the parameter sets (params_out, n x 6, optional) and the deaths
+ * series of the forecast (deaths_out, n x (horizon+1), day 0 = junction;
+ * NaN rows for sets whose window or forecast blew up). */
+int sg_forecast_ensemble(sg_window* window, const double lower[6], const double upper[6], uint64_t seed,
+                         size_t n, int horizon, double* costs, double* params_out, double* deaths_out);
+
+/* --- diagnostics -----------------------------------------------------------
+ * Measured FP64 issue rate of this device: a kernel of independent
+ * DADD/DMUL chains (no FMA), timed with CUDA events.  *ops_per_s receives
+ * double-precision lane operations per second (the roofline denominator of
+ * the non-FMA integrate-and-score kernel). */
+int sg_probe_fp64_rate(sg_ctx* ctx, double* ops_per_s);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* SIRDGPU_H */

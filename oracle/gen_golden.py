@@ -1,0 +1,271 @@
+"""Generate the golden fixtures under tests/golden/ from the REFERENCE build.
+
+TEST INFRASTRUCTURE.  Run in the build container (needs /root/reference to
+build oracle/_ref/libsirdref.so):
+
+    python oracle/gen_golden.py
+
+Every output value below is produced by the unmodified reference library
+(oracle/_ref, kind "reference"); the inputs are generated here from fixed
+seeds.  The fixtures are committed so the C restatement (oracle/) and the
+CUDA path can be checked on machines without /root/reference.
+
+Fixtures
+  poland_like.csv   synthetic Poland-like series, 450 days,
+                    cleaned by the reference's build_epi_series + smooth7.
+  kat.json          mix_seed / mt19937_64 / uniform01 known-answer values.
+  costs.npz         per-particle costs, 8 objective specs x several windows x
+                    particle sets (stage-1/2 uniform, near-optimal, unrepaired
+                    t1>t2, blow-ups, flat and zero windows, MAPE zeros).
+  fits.json         optimize() results (best position, cost, full history).
+  forecast.npz      forecast_extension trajectories.
+"""
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+from oracle import oracle_py as op  # noqa: E402
+
+GOLDEN = ROOT / "tests" / "golden"
+
+# N = 38e6, 450 days, init S=N-200, I=200, gamma 0.1,
+# mu 0.0027, six chained segments (len, beta1, beta2, t1, t2).
+POLAND_N = 38_000_000.0
+POLAND_SEGMENTS = [(30, 0.30, 0.115, 5, 20), (150, 0.115, 0.118, 0, 0), (60, 0.118, 0.145, 5, 35),
+                   (60, 0.145, 0.085, 5, 30), (90, 0.085, 0.135, 40, 70), (60, 0.135, 0.07, 5, 30)]
+POLAND_DAYS = 450
+
+
+def poland_truth(ref) -> np.ndarray:
+    """Chained integrate_euler segments -> (450, 4) true states."""
+    state = np.array([POLAND_N - 200.0, 200.0, 0.0, 0.0])
+    rows = [state]
+    for length, b1, b2, t1, t2 in POLAND_SEGMENTS:
+        st, fin = ref.integrate([b1, b2, t1, t2, 0.1, 0.0027], state, POLAND_N, length + 1)
+        assert fin
+        rows.extend(st[1:])
+        state = st[-1]
+    return np.array(rows[:POLAND_DAYS])
+
+
+def poland_series(ref) -> dict:
+    """Noise on daily increments x(1+U(-0.2,0.2)) (mt19937_64 seeded 2204,
+    uniform01 draws in (day, column) order) and a weekday factor 1.1 / weekend
+    0.7; re-cumulate; clean with the reference's build_epi_series + smooth7."""
+    truth = poland_truth(ref)
+    cum = np.stack([truth[:, 1] + truth[:, 2] + truth[:, 3], truth[:, 2], truth[:, 3]], axis=1)
+    inc = np.diff(cum, axis=0, prepend=0.0)
+    u = ref.uniform01(2204, inc.size).reshape(inc.shape)
+    factor = 1.0 + (-0.2 + 0.4 * u)
+    week = np.where((np.arange(POLAND_DAYS) % 7 >= 5), 0.7, 1.1)[:, None]
+    noisy = np.cumsum(np.maximum(inc * factor * week, 0.0), axis=0)
+    out = {k: np.zeros(POLAND_DAYS) for k in ("I", "R", "D", "new")}
+    dp = op._dp
+    rc = ref.lib.ref_clean_series(np.ascontiguousarray(noisy[:, 0]).ctypes.data_as(dp),
+                                  np.ascontiguousarray(noisy[:, 1]).ctypes.data_as(dp),
+                                  np.ascontiguousarray(noisy[:, 2]).ctypes.data_as(dp), POLAND_DAYS, 1,
+                                  out["I"].ctypes.data_as(dp), out["R"].ctypes.data_as(dp),
+                                  out["D"].ctypes.data_as(dp), out["new"].ctypes.data_as(dp))
+    assert rc == 0, ref.lib.ref_last_error()
+    out["truth"] = truth
+    return out
+
+
+def write_series_csv(path: Path, s: dict) -> None:
+    lines = ["day,infectious,recovered_cum,deaths_cum,new_cases"]
+    for t in range(POLAND_DAYS):
+        lines.append(f"{t},{float(s['I'][t])!r},{float(s['R'][t])!r},{float(s['D'][t])!r},{float(s['new'][t])!r}")
+    path.write_text("\n".join(lines) + "\n")
+
+
+def stage_box(stage: int, tau: int):
+    if stage == 1:
+        return [0, 0, 0, 0, 0, 0], [10, 10, tau, tau, 10, 10]
+    return [0, 0, 0, 0, 0, 0], [2, 2, tau - 7, tau - 7, 1, 0.1]
+
+
+def uniform_particles(seed: int, n: int, lo, hi, repair=False) -> np.ndarray:
+    """acceptance/main.cpp:443-451 style: one engine, row-major draws."""
+    ref = op.load("reference")
+    u = ref.uniform01(seed, n * 6).reshape(n, 6)
+    lo, hi = np.array(lo, float), np.array(hi, float)
+    x = lo + u * (hi - lo)
+    if repair:
+        sw = x[:, 2] > x[:, 3]
+        x[sw, 2], x[sw, 3] = x[sw, 3].copy(), x[sw, 2].copy()
+    return x
+
+
+def special_particles(tau: int) -> np.ndarray:
+    rows = [
+        [0.6, 0.6, 1.0, 2.0, 0.09, 0.01],
+        [1.5, 1.5, 8.0, 2.0, 0.01, 0.09],        # unordered switch times
+        [0.3, 0.9, 5.0, 5.0, 0.1, 0.01],         # t1 == t2: no ramp
+        [0.3, 0.9, 0.0, float(tau), 0.1, 0.01],  # ramp over the whole window
+        [0.0, 2.0, 3.0, 9.0, 0.0, 0.0],          # zero rates
+        [2.0, 0.0, 0.0, 1e-9, 1.0, 0.1],         # razor-thin ramp at t=0
+        [10.0, 10.0, 0.0, 0.0, 0.0, 0.0],        # fast growth
+        [10.0, 10.0, 0.0, 0.0, 10.0, 10.0],      # stage-1 corner
+        [5e3, 5e3, 0.0, 0.0, 0.0, 0.0],          # blow-up
+        [1e300, 1e300, 0.0, 0.0, 1.0, 1.0],      # immediate overflow
+        [0.5, 0.5, 3.0, 7.0, 1e5, 1e5],          # stiff rates -> blow-up
+        [-0.5, 0.4, 2.0, 6.0, 0.1, 0.01],        # negative beta through the ramp (sign crossing)
+        [0.4, 0.8, float("nan"), 6.0, 0.1, 0.01],  # NaN switch time
+        [0.4, 0.8, 2.0, float("nan"), 0.1, 0.01],
+        [0.4, 0.8, 2.0, float("inf"), 0.1, 0.01],  # ramp never ends
+        [1e-310, 0.7, 1.0, 9.0, 0.1, 0.01],      # subnormal beta1
+        [0.7, 1e-310, 1.0, 9.0, 0.1, 0.01],      # subnormal beta2
+        [-0.0, 0.7, 1.0, 9.0, 0.1, 0.01],        # negative zero
+        [1e-200, 3e-200, 1.0, 9.0, 0.1, 0.01],   # tiny betas
+        [0.2, 0.4, 2.0, 2.0 + 2 ** -40, 0.1, 0.01],  # ramp shorter than one substep
+    ]
+    return np.array(rows, dtype=np.float64)
+
+
+def windows_for_costs(ref, poland: dict):
+    """(name, I, R, D, init, N) cases."""
+    out = []
+    # poland-like windows: tau=20 window 0 (config 1) and tau=35 windows 0, 60, 138
+    for tau, widx in ((20, 0), (35, 0), (35, 60), (35, 138)):
+        s = widx * 3
+        L = tau + 1
+        I, R, D = poland["I"][s:s + L], poland["R"][s:s + L], poland["D"][s:s + L]
+        init = [POLAND_N - I[0] - R[0] - D[0], I[0], R[0], D[0]]
+        out.append((f"poland_tau{tau}_w{widx}", tau, I, R, D, init, POLAND_N))
+    # reference test fixture (test_calibration.cpp:139-152)
+    N = 1e6
+    st, _ = ref.integrate([0.6, 0.6, 0.0, 0.0, 0.09, 0.01], [N - 100, 100, 0, 0], N, 25)
+    out.append(("boundary_fixture", 20, st[:21, 1], st[:21, 2], st[:21, 3], st[0], N))
+    # flat window (range 0 -> 1/max(1,|lo|)), zero window (MAPE +inf), MAPE zeros
+    L = 15
+    out.append(("flat", 14, np.full(L, 50.0), np.full(L, 20.0), np.full(L, 0.5), [1000 - 70.5, 50, 20, 0.5], 1000.0))
+    out.append(("zeros", 14, np.zeros(L), np.zeros(L), np.zeros(L), [1000.0, 0, 0, 0], 1000.0))
+    Dz = np.concatenate([np.zeros(5), np.linspace(1, 30, L - 5)])
+    st, _ = ref.integrate([0.5, 0.3, 3, 9, 0.1, 0.02], [5e5 - 40, 40, 0, 0], 5e5, L)
+    out.append(("mape_zeros", 14, st[:, 1], np.concatenate([np.zeros(3), st[3:, 2]]), Dz, st[0], 5e5))
+    return out
+
+
+def gen_costs(ref, poland: dict) -> dict:
+    data = {}
+    for name, tau, I, R, D, init, N in windows_for_costs(ref, poland):
+        lo1, hi1 = stage_box(1, tau)
+        lo2, hi2 = stage_box(2, max(tau, 7))
+        sets = {
+            "stage2": uniform_particles(10, 96, lo2, hi2),
+            "stage1": uniform_particles(11, 64, lo1, hi1),
+            "special": special_particles(tau),
+        }
+        if name.startswith("poland"):
+            # near-optimal: best fit of a short swarm, jittered x(1 +- 1e-6)
+            rc, best, _, _ = ref.fit_swarm("ird-mxse", I, R, D, init, N, lo2, hi2, 256, 30, seed=3)
+            u = ref.uniform01(12, 32 * 6).reshape(32, 6)
+            sets["near_opt"] = best[None, :] * (1.0 + (u - 0.5) * 2e-6)
+        data[f"{name}/obs"] = np.stack([I, R, D])
+        data[f"{name}/init"] = np.array(init, dtype=np.float64)
+        data[f"{name}/N"] = np.array([N])
+        for sname, pos in sets.items():
+            data[f"{name}/{sname}/positions"] = pos
+            for spec in op.SPECS:
+                data[f"{name}/{sname}/{spec}"] = ref.eval_costs(spec, I, R, D, init, N, pos)
+    return data
+
+
+def gen_fits(ref, poland: dict) -> list:
+    cases = []
+    N = 1e6
+    st, _ = ref.integrate([0.6, 0.6, 0.0, 0.0, 0.09, 0.01], [N - 100, 100, 0, 0], N, 25)
+    cases.append(dict(name="appendixA", spec="ird-mxse", I=st[:21, 1], R=st[:21, 2], D=st[:21, 3], init=st[0],
+                      N=N, tau=20, stage=2, n=64, iters=10, w=0.5, c1=0.5, c2=0.5, seed=1))
+    s = poland
+    for spec, n, iters, seed, widx, tau in (("ird-mxse", 256, 60, 1, 0, 20), ("d-mse", 200, 40, 5, 10, 35),
+                                           ("ird-mape", 130, 25, 9, 100, 35), ("d-mae", 97, 30, 2, 138, 35)):
+        a = widx * 3
+        I, R, D = s["I"][a:a + tau + 1], s["R"][a:a + tau + 1], s["D"][a:a + tau + 1]
+        cases.append(dict(name=f"poland_{spec}_w{widx}", spec=spec, I=I, R=R, D=D,
+                          init=[POLAND_N - I[0] - R[0] - D[0], I[0], R[0], D[0]], N=POLAND_N, tau=tau, stage=2,
+                          n=n, iters=iters, w=0.5, c1=0.5, c2=0.5, seed=seed))
+    # constriction coefficients (acceptance #6) and stage-1 bounds
+    a = 30
+    I, R, D = s["I"][a:a + 36], s["R"][a:a + 36], s["D"][a:a + 36]
+    cases.append(dict(name="poland_stage1_constriction", spec="ird-mse", I=I, R=R, D=D,
+                      init=[POLAND_N - I[0] - R[0] - D[0], I[0], R[0], D[0]], N=POLAND_N, tau=35, stage=1,
+                      n=150, iters=40, w=0.7298, c1=1.4962, c2=1.4962, seed=601))
+    # all-zero data (test_calibration.cpp:210-224) and an all-infeasible swarm
+    z = np.zeros(15)
+    cases.append(dict(name="zeros", spec="d-mse", I=z, R=z, D=z, init=[1000.0, 0, 0, 0], N=1000.0, tau=14,
+                      stage=2, n=50, iters=5, w=0.5, c1=0.5, c2=0.5, seed=3))
+    cases.append(dict(name="all_infeasible", spec="ird-mape", I=z, R=z, D=z, init=[1000.0, 0, 0, 0], N=1000.0,
+                      tau=14, stage=2, n=33, iters=4, w=0.5, c1=0.5, c2=0.5, seed=4))
+    out = []
+    for c in cases:
+        lo, hi = stage_box(c["stage"], c["tau"])
+        rc, best, cost, hist = ref.fit_swarm(c["spec"], c["I"], c["R"], c["D"], c["init"], c["N"], lo, hi, c["n"],
+                                             c["iters"], c["w"], c["c1"], c["c2"], c["seed"])
+        rec = {k: (np.asarray(v).tolist() if isinstance(v, (np.ndarray, list)) else v) for k, v in c.items()}
+        rec.update(lower=lo, upper=hi, status=rc, best=[float(x).hex() for x in best], best_cost=float(cost).hex(),
+                   history=[float(x).hex() for x in hist])
+        rec["I"] = [float(x).hex() for x in c["I"]]
+        rec["R"] = [float(x).hex() for x in c["R"]]
+        rec["D"] = [float(x).hex() for x in c["D"]]
+        rec["init"] = [float(x).hex() for x in c["init"]]
+        out.append(rec)
+    return out
+
+
+def gen_forecast(ref, poland: dict) -> dict:
+    data = {}
+    pos = np.concatenate([uniform_particles(21, 24, *stage_box(2, 35), repair=True), special_particles(35)[:12]])
+    a = 414
+    I, R, D = poland["I"][a:a + 36], poland["R"][a:a + 36], poland["D"][a:a + 36]
+    init = [POLAND_N - I[0] - R[0] - D[0], I[0], R[0], D[0]]
+    traj, fin_w, fc, fin_f = [], [], [], []
+    for p in pos:
+        st, fin = ref.integrate(p, init, POLAND_N, 36)
+        traj.append(st)
+        fin_w.append(fin)
+        if fin:
+            f, ff = ref.forecast(p, st[-1], POLAND_N, 21)
+        else:
+            f, ff = np.full((22, 4), np.nan), False
+        fc.append(f)
+        fin_f.append(ff)
+    data.update(positions=pos, init=np.array(init), N=np.array([POLAND_N]), window=np.array(traj),
+                window_finite=np.array(fin_w), forecast=np.array(fc), forecast_finite=np.array(fin_f))
+    return data
+
+
+def gen_kat(ref) -> dict:
+    return {
+        "mix_seed": [[b, i, ref.mix_seed(b, i)] for b, i in ((0, 0), (1, 0), (1, 1), (2204, 7),
+                                                            (2**64 - 1, 12345), (42, 2**63))],
+        "mt_default_10000th": int(ref.mt_raw(5489, 1, skip=9999)[0]),
+        "mt_mix00_first_700": [int(x) for x in ref.mt_raw(ref.mix_seed(0, 0), 700)],
+        "uniform01_mix10_first_3": [float(x).hex() for x in ref.uniform01(ref.mix_seed(1, 0), 3)],
+    }
+
+
+def main() -> None:
+    op.build("ref")
+    ref = op.load("reference")
+    GOLDEN.mkdir(parents=True, exist_ok=True)
+    poland = poland_series(ref)
+    write_series_csv(GOLDEN / "poland_like.csv", poland)
+    truth = poland["truth"]
+    print(f"poland-like: true D[449]={truth[-1, 3]:.1f} confirmed={truth[-1, 1:].sum():.1f} "
+          f"I peak={truth[:, 1].max():.1f} at day {int(truth[:, 1].argmax())}; cleaned D[449]={poland['D'][-1]:.1f}")
+    (GOLDEN / "kat.json").write_text(json.dumps(gen_kat(ref), indent=1))
+    np.savez_compressed(GOLDEN / "costs.npz", **gen_costs(ref, poland))
+    (GOLDEN / "fits.json").write_text(json.dumps(gen_fits(ref, poland), indent=1))
+    np.savez_compressed(GOLDEN / "forecast.npz", **gen_forecast(ref, poland))
+    print("wrote", sorted(p.name for p in GOLDEN.iterdir()))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,795 @@
+// engine.cu — implementation of the C-ABI declared in include/sirdgpu.h.
+//
+// Host side of the B200 particle-window cost engine: contexts, window
+// descriptors, launch planning for batched swarms, and the status/error
+// plumbing that the C++ and Python layers turn back into the reference's
+// exception types.  There is no CPU fallback anywhere: every numeric result
+// is produced by the kernels in kernels.cuh.
+#include "sirdgpu.h"
+
+#include "kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+using namespace sirdgpu;
+
+struct sg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    int sm_count = 0;
+    // reusable scratch for sg_eval_costs (host-buffer path)
+    double* d_pos = nullptr;
+    double* d_cost = nullptr;
+    size_t scratch_n = 0;
+};
+
+struct sg_window {
+    sg_ctx* ctx = nullptr;
+    DevWindow host{};          // device pointers inside
+    DevWindow* d_desc = nullptr;
+    ObsDay* d_obs = nullptr;
+    ObsDay* d_robs = nullptr;
+    unsigned char* d_flag = nullptr;
+    size_t smem = 0;
+};
+
+namespace {
+
+int fail(sg_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+int cuda_fail(sg_ctx* ctx, cudaError_t e, const char* what) {
+    const int code = e == cudaErrorMemoryAllocation ? SG_ERR_OUT_OF_MEMORY : SG_ERR_CUDA;
+    return fail(ctx, code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define SG_CUDA(ctx, call)                                  \
+    do {                                                    \
+        const cudaError_t e_ = (call);                      \
+        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
+    } while (0)
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count) {
+    return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T));
+}
+
+// Divisor admissibility for the 3-op exact division (sird_device.cuh
+// div_exact; proof in DESIGN.md §4): |b| in [2^-60, 2^60] and the odd part of
+// b's 53-bit significand below 2^53/3.
+bool divisor_admits_fast_path(double b) {
+    if (!std::isfinite(b) || b == 0.0) return false;
+    const double a = std::fabs(b);
+    if (a < 0x1.0p-60 || a > 0x1.0p60) return false;
+    uint64_t bits;
+    std::memcpy(&bits, &a, sizeof bits);
+    uint64_t m = (bits & ((1ULL << 52) - 1)) | (1ULL << 52);
+    while ((m & 1ULL) == 0) m >>= 1;
+    return m < (1ULL << 53) / 3;
+}
+
+// objectives.cpp:61-69 — scale of one compartment's residuals.
+double compartment_scale(const double* obs, int n) {
+    const double* lo = std::min_element(obs, obs + n);
+    const double* hi = std::max_element(obs, obs + n);
+    // std::minmax_element returns the first smallest and the last largest;
+    // only the values are used, and equal values are interchangeable.
+    const double range = *hi - *lo;
+    return range > 0.0 ? 1.0 / range : 1.0 / std::max(1.0, std::fabs(*lo));
+}
+
+bool valid_spec(int family, int metric) {
+    return (family == SG_FAMILY_D_ONLY || family == SG_FAMILY_IRD_JOINT) && metric >= SG_METRIC_MXSE &&
+           metric <= SG_METRIC_MAPE;
+}
+
+// ---- template dispatch over (family, metric, substeps == 24) ------------------
+template <template <int, int, int> class K, class... Args>
+void dispatch(int family, int metric, int substeps, Args&&... args) {
+    const bool s24 = substeps == 24;
+#define SG_CASE(F, M)                                              \
+    if (family == F && metric == M) {                              \
+        if (s24) K<F, M, 24>::run(std::forward<Args>(args)...);    \
+        else K<F, M, 0>::run(std::forward<Args>(args)...);         \
+        return;                                                    \
+    }
+    SG_CASE(0, 0) SG_CASE(0, 1) SG_CASE(0, 2) SG_CASE(0, 3)
+    SG_CASE(1, 0) SG_CASE(1, 1) SG_CASE(1, 2) SG_CASE(1, 3)
+#undef SG_CASE
+}
+
+template <class KernelPtr>
+cudaError_t prepare_smem(KernelPtr k, size_t smem) {
+    if (smem > 48 * 1024)
+        return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    return cudaSuccess;
+}
+
+template <int F, int M, int S>
+struct EvalLaunch {
+    static void run(const DevWindow* w, const double* pos, size_t n, double* costs, size_t smem, cudaStream_t st,
+                    cudaError_t* err) {
+        auto k = eval_costs_kernel<F, M, S>;
+        *err = prepare_smem(k, smem);
+        if (*err != cudaSuccess) return;
+        const unsigned grid = static_cast<unsigned>((n + kEvalThreads - 1) / kEvalThreads);
+        k<<<grid, kEvalThreads, smem, st>>>(w, pos, n, costs);
+        *err = cudaGetLastError();
+    }
+};
+
+template <int F, int M, int S>
+struct StepLaunch {
+    static void run(unsigned grid, const DevSwarm* sw, const uint32_t* cta_swarm, const DevWindow* wins,
+                    const PsoPlanes& P, DevSwarmState* state, uint64_t it, size_t smem, cudaStream_t st,
+                    cudaError_t* err) {
+        auto k = pso_step_kernel<F, M, S>;
+        if (it == 0) {
+            *err = prepare_smem(k, smem);
+            if (*err != cudaSuccess) return;
+        }
+        k<<<grid, kStepThreads, smem, st>>>(sw, cta_swarm, wins, P, state, it);
+        *err = cudaGetLastError();
+    }
+};
+
+template <int F, int M, int S>
+struct EnsembleLaunch {
+    static void run(const DevWindow* w, const DevWindow& fwin, const double* lo, const double* hi, uint64_t seed,
+                    size_t n, int horizon, double* costs, double* params, double* deaths, size_t smem,
+                    cudaStream_t st, cudaError_t* err) {
+        auto k = ensemble_kernel<F, M, S>;
+        *err = prepare_smem(k, smem);
+        if (*err != cudaSuccess) return;
+        const unsigned grid = static_cast<unsigned>((n + kEvalThreads - 1) / kEvalThreads);
+        k<<<grid, kEvalThreads, smem, st>>>(w, fwin, lo, hi, seed, n, horizon, costs, params, deaths);
+        *err = cudaGetLastError();
+    }
+};
+
+// Trajectory launcher shared by sg_integrate_batch and sg_forecast_batch.
+int launch_integrate(sg_ctx* ctx, const DevWindow& w, const double* d_params, const double* d_init, int init_stride,
+                     int hold, size_t n, double* d_states, unsigned char* d_fin) {
+    const unsigned grid = static_cast<unsigned>((n + kEvalThreads - 1) / kEvalThreads);
+    const size_t smem = static_cast<size_t>(w.substeps) * sizeof(double);
+    if (w.substeps == 24) {
+        integrate_kernel<24><<<grid, kEvalThreads, smem, ctx->stream>>>(w, d_params, d_init, init_stride, hold, n,
+                                                                        d_states, d_fin);
+    } else {
+        SG_CUDA(ctx, prepare_smem(integrate_kernel<0>, smem));
+        integrate_kernel<0><<<grid, kEvalThreads, smem, ctx->stream>>>(w, d_params, d_init, init_stride, hold, n,
+                                                                       d_states, d_fin);
+    }
+    ctx->launches += 1;
+    SG_CUDA(ctx, cudaGetLastError());
+    return SG_OK;
+}
+
+// RAII bundle of device allocations for one call.
+struct DevBufs {
+    std::vector<void*> ptrs;
+    template <class T>
+    cudaError_t alloc(T** p, size_t count) {
+        const cudaError_t e = dalloc(p, count);
+        if (e == cudaSuccess) ptrs.push_back(*p);
+        return e;
+    }
+    ~DevBufs() {
+        for (void* p : ptrs) cudaFree(p);
+    }
+};
+
+DevWindow integration_window(int n_days, int substeps, double N) {
+    DevWindow w{};
+    w.n_days = n_days;
+    w.substeps = substeps;
+    w.N = N;
+    w.h = 1.0 / static_cast<double>(substeps);  // model.cpp:90
+    w.fast_N = divisor_admits_fast_path(N) ? 1 : 0;
+    w.rN = 1.0 / N;
+    w.init_finite = 1;
+    return w;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sg_abi_version(void) { return SG_ABI_VERSION; }
+
+int sg_ctx_create(int device, sg_ctx** out) {
+    if (!out) return SG_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count <= device || device < 0) return SG_ERR_NO_DEVICE;
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return SG_ERR_NO_DEVICE;
+    if (prop.major != 10) return SG_ERR_NO_DEVICE;  // built for sm_100a only
+    sg_ctx* ctx = new (std::nothrow) sg_ctx;
+    if (!ctx) return SG_ERR_OUT_OF_MEMORY;
+    ctx->device = device;
+    ctx->sm_count = prop.multiProcessorCount;
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        delete ctx;
+        return SG_ERR_CUDA;
+    }
+    *out = ctx;
+    return SG_OK;
+}
+
+void sg_ctx_destroy(sg_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaFree(ctx->d_pos);
+    cudaFree(ctx->d_cost);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* sg_last_error(const sg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+uint64_t sg_ctx_launch_count(const sg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+void* sg_ctx_stream(const sg_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int sg_window_create(sg_ctx* ctx, const double* infectious, const double* recovered_cum, const double* deaths_cum,
+                     int n_days, sg_state init, double population, int substeps, int family, int metric,
+                     sg_window** out) {
+    if (!ctx || !out) return SG_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (!infectious || !recovered_cum || !deaths_cum)
+        return fail(ctx, SG_ERR_INVALID_ARGUMENT, "window series must not be null");
+    if (!valid_spec(family, metric)) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "unknown objective spec");
+    // integrate_euler's guards (model.cpp:78-80)
+    if (n_days < 1 || substeps < 1 || !(population > 0.0))
+        return fail(ctx, SG_ERR_INVALID_ARGUMENT,
+                    "integrate_euler needs n_days >= 1, substeps >= 1 and a positive population");
+    SG_CUDA(ctx, cudaSetDevice(ctx->device));
+    sg_window* w = new (std::nothrow) sg_window;
+    if (!w) return fail(ctx, SG_ERR_OUT_OF_MEMORY, "host allocation failed");
+    w->ctx = ctx;
+    DevWindow& d = w->host;
+    d = integration_window(n_days, substeps, population);
+    d.family = family;
+    d.metric = metric;
+    d.init[0] = init.S;
+    d.init[1] = init.I;
+    d.init[2] = init.R;
+    d.init[3] = init.D;
+    d.init_finite = std::isfinite(init.S + init.I + init.R + init.D) ? 1 : 0;  // model.cpp:83
+    const double* series[3] = {infectious, recovered_cum, deaths_cum};
+    std::vector<ObsDay> obs(n_days), robs(n_days);
+    std::vector<unsigned char> flag(3 * static_cast<size_t>(n_days));
+    for (int c = 0; c < 3; ++c) {
+        d.scale[c] = 1.0;
+        d.kept[c] = 0.0;
+        if (family == SG_FAMILY_IRD_JOINT && metric != SG_METRIC_MAPE) d.scale[c] = compartment_scale(series[c], n_days);
+        size_t kept = 0;
+        for (int k = 0; k < n_days; ++k) {
+            const double o = series[c][k];
+            obs[k].v[c] = o;
+            robs[k].v[c] = 1.0 / o;
+            unsigned char f = kObsSlow;
+            if (o == 0.0) f = kObsSkip;
+            else if (divisor_admits_fast_path(o)) f = kObsFast;
+            flag[3 * static_cast<size_t>(k) + c] = f;
+            if (o != 0.0) ++kept;
+        }
+        d.kept[c] = static_cast<double>(kept);
+    }
+    cudaError_t e = dalloc(&w->d_obs, n_days);
+    if (e == cudaSuccess) e = dalloc(&w->d_robs, n_days);
+    if (e == cudaSuccess) e = dalloc(&w->d_flag, 3 * static_cast<size_t>(n_days));
+    if (e == cudaSuccess) e = dalloc(&w->d_desc, 1);
+    if (e == cudaSuccess) {
+        d.obs = w->d_obs;
+        d.robs = w->d_robs;
+        d.obs_flag = w->d_flag;
+        e = cudaMemcpy(w->d_obs, obs.data(), sizeof(ObsDay) * n_days, cudaMemcpyHostToDevice);
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(w->d_robs, robs.data(), sizeof(ObsDay) * n_days, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(w->d_flag, flag.data(), flag.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(w->d_desc, &d, sizeof d, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        sg_window_destroy(w);
+        return cuda_fail(ctx, e, "sg_window_create");
+    }
+    w->smem = smem_window_bytes(n_days, substeps, metric);
+    if (w->smem > 200 * 1024) {
+        sg_window_destroy(w);
+        return fail(ctx, SG_ERR_INVALID_ARGUMENT, "window too long for shared-memory staging");
+    }
+    *out = w;
+    return SG_OK;
+}
+
+void sg_window_destroy(sg_window* w) {
+    if (!w) return;
+    cudaFree(w->d_obs);
+    cudaFree(w->d_robs);
+    cudaFree(w->d_flag);
+    cudaFree(w->d_desc);
+    delete w;
+}
+
+int sg_eval_costs_device(sg_window* w, const double* d_positions, size_t n, double* d_costs, void* cuda_stream) {
+    if (!w) return SG_ERR_INVALID_ARGUMENT;
+    sg_ctx* ctx = w->ctx;
+    if (n == 0) return SG_OK;
+    if (!d_positions || !d_costs) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null device buffer");
+    cudaStream_t st = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->stream;
+    cudaError_t err = cudaSuccess;
+    dispatch<EvalLaunch>(w->host.family, w->host.metric, w->host.substeps, w->d_desc, d_positions, n, d_costs,
+                         w->smem, st, &err);
+    ctx->launches += 1;
+    if (err != cudaSuccess) return cuda_fail(ctx, err, "eval_costs_kernel");
+    return SG_OK;
+}
+
+int sg_eval_costs(sg_window* w, const double* positions, size_t n, size_t dim, double* costs) {
+    if (!w) return SG_ERR_INVALID_ARGUMENT;
+    sg_ctx* ctx = w->ctx;
+    // calibration.cpp:141-143
+    if (dim != 6) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "window objective expects 6-dim positions");
+    if (n == 0) return SG_OK;
+    if (!positions || !costs) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null host buffer");
+    SG_CUDA(ctx, cudaSetDevice(ctx->device));
+    if (ctx->scratch_n < n) {
+        cudaFree(ctx->d_pos);
+        cudaFree(ctx->d_cost);
+        ctx->d_pos = nullptr;
+        ctx->d_cost = nullptr;
+        ctx->scratch_n = 0;
+        SG_CUDA(ctx, dalloc(&ctx->d_pos, 6 * n));
+        SG_CUDA(ctx, dalloc(&ctx->d_cost, n));
+        ctx->scratch_n = n;
+    }
+    SG_CUDA(ctx, cudaMemcpyAsync(ctx->d_pos, positions, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
+    const int rc = sg_eval_costs_device(w, ctx->d_pos, n, ctx->d_cost, ctx->stream);
+    if (rc) return rc;
+    SG_CUDA(ctx, cudaMemcpyAsync(costs, ctx->d_cost, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SG_OK;
+}
+
+int sg_integrate_batch(sg_ctx* ctx, const double* params, size_t n, sg_state init, double population, int n_days,
+                       int substeps, double* states, uint8_t* finite) {
+    if (!ctx) return SG_ERR_INVALID_ARGUMENT;
+    if (n_days < 1 || substeps < 1 || !(population > 0.0))
+        return fail(ctx, SG_ERR_INVALID_ARGUMENT,
+                    "integrate_euler needs n_days >= 1, substeps >= 1 and a positive population");
+    if (n == 0) return SG_OK;
+    if (!params || !states || !finite) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null host buffer");
+    SG_CUDA(ctx, cudaSetDevice(ctx->device));
+    DevBufs b;
+    double *d_p, *d_init, *d_states;
+    unsigned char* d_fin;
+    SG_CUDA(ctx, b.alloc(&d_p, 6 * n));
+    SG_CUDA(ctx, b.alloc(&d_init, 4));
+    SG_CUDA(ctx, b.alloc(&d_states, n * static_cast<size_t>(n_days) * 4));
+    SG_CUDA(ctx, b.alloc(&d_fin, n));
+    const double s0[4] = {init.S, init.I, init.R, init.D};
+    SG_CUDA(ctx, cudaMemcpyAsync(d_p, params, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, cudaMemcpyAsync(d_init, s0, sizeof s0, cudaMemcpyHostToDevice, ctx->stream));
+    const DevWindow w = integration_window(n_days, substeps, population);
+    const int rc = launch_integrate(ctx, w, d_p, d_init, 0, 0, n, d_states, d_fin);
+    if (rc) return rc;
+    SG_CUDA(ctx, cudaMemcpyAsync(states, d_states, sizeof(double) * n * n_days * 4, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    SG_CUDA(ctx, cudaMemcpyAsync(finite, d_fin, n, cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SG_OK;
+}
+
+int sg_forecast_batch(sg_ctx* ctx, const double* params, const sg_state* junction, size_t n, double population,
+                      int horizon, int substeps, double* states, uint8_t* finite) {
+    if (!ctx) return SG_ERR_INVALID_ARGUMENT;
+    if (horizon < 0 || substeps < 1 || !(population > 0.0))
+        return fail(ctx, SG_ERR_INVALID_ARGUMENT, "forecast needs horizon >= 0, substeps >= 1, population > 0");
+    if (n == 0) return SG_OK;
+    if (!params || !junction || !states || !finite) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null host buffer");
+    SG_CUDA(ctx, cudaSetDevice(ctx->device));
+    const int n_days = horizon + 1;
+    DevBufs b;
+    double *d_p, *d_init, *d_states;
+    unsigned char* d_fin;
+    SG_CUDA(ctx, b.alloc(&d_p, 6 * n));
+    SG_CUDA(ctx, b.alloc(&d_init, 4 * n));
+    SG_CUDA(ctx, b.alloc(&d_states, n * static_cast<size_t>(n_days) * 4));
+    SG_CUDA(ctx, b.alloc(&d_fin, n));
+    static_assert(sizeof(sg_state) == 4 * sizeof(double), "sg_state layout");
+    SG_CUDA(ctx, cudaMemcpyAsync(d_p, params, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, cudaMemcpyAsync(d_init, junction, sizeof(double) * 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+    const DevWindow w = integration_window(n_days, substeps, population);
+    const int rc = launch_integrate(ctx, w, d_p, d_init, 4, 1, n, d_states, d_fin);
+    if (rc) return rc;
+    SG_CUDA(ctx, cudaMemcpyAsync(states, d_states, sizeof(double) * n * n_days * 4, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    SG_CUDA(ctx, cudaMemcpyAsync(finite, d_fin, n, cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SG_OK;
+}
+
+}  // extern "C"
+
+// ---- swarms ---------------------------------------------------------------------
+
+namespace {
+
+bool swarm_config_valid(const sg_swarm_desc& d, std::string* why) {
+    // PsoConfig::validate / SearchBounds::validate (pso.cpp:16-34)
+    if (d.n_particles == 0 || d.max_iters == 0) {
+        *why = "pso: n_particles and max_iters must be positive";
+        return false;
+    }
+    if (!std::isfinite(d.inertia) || !std::isfinite(d.cognitive) || !std::isfinite(d.social)) {
+        *why = "pso: coefficients must be finite";
+        return false;
+    }
+    for (int k = 0; k < 6; ++k) {
+        if (!std::isfinite(d.lower[k]) || !std::isfinite(d.upper[k]) || d.lower[k] > d.upper[k]) {
+            *why = "pso: bound " + std::to_string(k) + " is invalid";
+            return false;
+        }
+    }
+    if (!d.window) {
+        *why = "swarm has no window";
+        return false;
+    }
+    return true;
+}
+
+// One launch group: swarms sharing (family, metric, substeps == 24).  The
+// runtime-substep kernel (SUB == 0) reads the substep count from each
+// swarm's staged window, so mixed counts may share a launch.
+struct SwarmGroup {
+    int family = 0, metric = 0, substeps = 24;
+    std::vector<size_t> idx;          // positions in the caller's descriptor array
+    std::vector<uint64_t> max_iters;  // per swarm
+    size_t n_total = 0, n_ctas = 0, smem = 0;
+    uint64_t iters = 0;               // max over swarms
+    DevSwarm* d_sw = nullptr;
+    uint32_t* d_cta = nullptr;
+    DevWindow* d_win = nullptr;
+    DevSwarmState* d_state = nullptr;
+    PsoPlanes P{};
+    DevBufs bufs;
+};
+
+}  // namespace
+
+struct sg_plan {
+    sg_ctx* ctx = nullptr;
+    std::vector<SwarmGroup*> groups;
+    std::vector<int> status;          // per descriptor: SG_OK or validation failure
+    size_t n_desc = 0;
+    uint64_t evals = 0;
+    bool ran = false;
+    ~sg_plan() {
+        for (SwarmGroup* g : groups) delete g;
+    }
+};
+
+namespace {
+
+int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
+    std::vector<const sg_window*> wins;
+    std::vector<DevSwarm> sw(g.idx.size());
+    std::vector<uint32_t> cta_swarm;
+    uint64_t offset = 0;
+    for (size_t j = 0; j < g.idx.size(); ++j) {
+        const sg_swarm_desc& d = descs[g.idx[j]];
+        auto it = std::find(wins.begin(), wins.end(), d.window);
+        const int wi = static_cast<int>(it - wins.begin());
+        if (it == wins.end()) wins.push_back(d.window);
+        g.smem = std::max(g.smem, d.window->smem);
+        DevSwarm& s = sw[j];
+        s.window = wi;
+        s.repair = d.repair_time_order ? 1 : 0;
+        s.n = d.n_particles;
+        s.offset = offset;
+        s.max_iters = d.max_iters;
+        s.cta_begin = static_cast<uint32_t>(cta_swarm.size());
+        s.n_ctas = static_cast<uint32_t>((d.n_particles + kStepThreads - 1) / kStepThreads);
+        for (int k = 0; k < 6; ++k) {
+            s.lo[k] = d.lower[k];
+            s.hi[k] = d.upper[k];
+        }
+        s.w = d.inertia;
+        s.c1 = d.cognitive;
+        s.c2 = d.social;
+        s.seed = d.seed;
+        for (uint32_t c = 0; c < s.n_ctas; ++c) cta_swarm.push_back(static_cast<uint32_t>(j));
+        offset += d.n_particles;
+        g.iters = std::max(g.iters, d.max_iters);
+        g.max_iters.push_back(d.max_iters);
+    }
+    g.n_total = offset;
+    g.n_ctas = cta_swarm.size();
+    if (g.n_ctas > 0x7FFFFFFFu) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "too many particles in one plan");
+    std::vector<DevWindow> wtab(wins.size());
+    for (size_t k = 0; k < wins.size(); ++k) wtab[k] = wins[k]->host;
+
+    DevBufs& b = g.bufs;
+    PsoPlanes& P = g.P;
+    SG_CUDA(ctx, b.alloc(&g.d_sw, sw.size()));
+    SG_CUDA(ctx, b.alloc(&g.d_cta, g.n_ctas));
+    SG_CUDA(ctx, b.alloc(&g.d_win, wtab.size()));
+    SG_CUDA(ctx, b.alloc(&g.d_state, sw.size()));
+    SG_CUDA(ctx, b.alloc(&P.x, 6 * g.n_total));
+    SG_CUDA(ctx, b.alloc(&P.v, 6 * g.n_total));
+    SG_CUDA(ctx, b.alloc(&P.pb, 6 * g.n_total));
+    SG_CUDA(ctx, b.alloc(&P.pbc, g.n_total));
+    SG_CUDA(ctx, b.alloc(&P.cost, g.n_total));
+    SG_CUDA(ctx, b.alloc(&P.mt, static_cast<size_t>(kMtN) * g.n_total));
+    SG_CUDA(ctx, b.alloc(&P.part_cost, g.n_ctas));
+    SG_CUDA(ctx, b.alloc(&P.part_idx, g.n_ctas));
+    SG_CUDA(ctx, b.alloc(&P.history, sw.size() * g.iters));
+    P.stride = g.n_total;
+    P.hist_stride = g.iters;
+    cudaStream_t st = ctx->stream;
+    SG_CUDA(ctx, cudaMemcpyAsync(g.d_sw, sw.data(), sizeof(DevSwarm) * sw.size(), cudaMemcpyHostToDevice, st));
+    SG_CUDA(ctx, cudaMemcpyAsync(g.d_cta, cta_swarm.data(), sizeof(uint32_t) * g.n_ctas, cudaMemcpyHostToDevice, st));
+    SG_CUDA(ctx, cudaMemcpyAsync(g.d_win, wtab.data(), sizeof(DevWindow) * wtab.size(), cudaMemcpyHostToDevice, st));
+    SG_CUDA(ctx, cudaStreamSynchronize(st));  // host vectors go out of scope
+    return SG_OK;
+}
+
+int run_group(sg_ctx* ctx, SwarmGroup& g) {
+    cudaStream_t st = ctx->stream;
+    pso_init_kernel<<<static_cast<unsigned>(g.n_ctas), kStepThreads, 0, st>>>(g.d_sw, g.d_cta, g.P, g.d_state);
+    ctx->launches += 1;
+    SG_CUDA(ctx, cudaGetLastError());
+    for (uint64_t it = 0; it < g.iters; ++it) {
+        cudaError_t err = cudaSuccess;
+        dispatch<StepLaunch>(g.family, g.metric, g.substeps, static_cast<unsigned>(g.n_ctas), g.d_sw, g.d_cta,
+                             g.d_win, g.P, g.d_state, it, g.smem, st, &err);
+        ctx->launches += 1;
+        if (err != cudaSuccess) return cuda_fail(ctx, err, "pso_step_kernel");
+    }
+    return SG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sg_plan_create(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg_plan** out) {
+    if (!ctx || !out) return SG_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (n_swarms > 0 && !swarms) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null swarm array");
+    SG_CUDA(ctx, cudaSetDevice(ctx->device));
+    sg_plan* plan = new (std::nothrow) sg_plan;
+    if (!plan) return fail(ctx, SG_ERR_OUT_OF_MEMORY, "host allocation failed");
+    plan->ctx = ctx;
+    plan->n_desc = n_swarms;
+    plan->status.assign(n_swarms, SG_OK);
+    std::string why;
+    for (size_t k = 0; k < n_swarms; ++k) {
+        if (!swarm_config_valid(swarms[k], &why)) {
+            plan->status[k] = SG_ERR_INVALID_ARGUMENT;
+            ctx->err = why;
+            continue;
+        }
+        if (swarms[k].window->ctx != ctx) {
+            plan->status[k] = SG_ERR_INVALID_ARGUMENT;
+            ctx->err = "swarm window belongs to another context";
+            continue;
+        }
+        const DevWindow& w = swarms[k].window->host;
+        const int sub = w.substeps == 24 ? 24 : 0;
+        SwarmGroup* g = nullptr;
+        for (SwarmGroup* x : plan->groups)
+            if (x->family == w.family && x->metric == w.metric && x->substeps == sub) g = x;
+        if (!g) {
+            g = new (std::nothrow) SwarmGroup;
+            if (!g) {
+                delete plan;
+                return fail(ctx, SG_ERR_OUT_OF_MEMORY, "host allocation failed");
+            }
+            g->family = w.family;
+            g->metric = w.metric;
+            g->substeps = sub;
+            plan->groups.push_back(g);
+        }
+        g->idx.push_back(k);
+        plan->evals += swarms[k].n_particles * swarms[k].max_iters;
+    }
+    for (SwarmGroup* g : plan->groups) {
+        const int rc = build_group(ctx, swarms, *g);
+        if (rc) {
+            delete plan;
+            return rc;
+        }
+    }
+    *out = plan;
+    return SG_OK;
+}
+
+int sg_plan_run(sg_plan* plan) {
+    if (!plan) return SG_ERR_INVALID_ARGUMENT;
+    sg_ctx* ctx = plan->ctx;
+    SG_CUDA(ctx, cudaSetDevice(ctx->device));
+    for (SwarmGroup* g : plan->groups) {
+        const int rc = run_group(ctx, *g);
+        if (rc) return rc;
+    }
+    plan->ran = true;
+    return SG_OK;
+}
+
+int sg_plan_results(sg_plan* plan, sg_swarm_result* results) {
+    if (!plan || (!results && plan->n_desc)) return SG_ERR_INVALID_ARGUMENT;
+    sg_ctx* ctx = plan->ctx;
+    if (!plan->ran) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "plan has not been run");
+    SG_CUDA(ctx, cudaSetDevice(ctx->device));
+    for (size_t k = 0; k < plan->n_desc; ++k) {
+        results[k].status = plan->status[k];
+        if (plan->status[k] != SG_OK) {
+            results[k].best_cost = HUGE_VAL;
+            for (double& v : results[k].best_position) v = 0.0;
+        }
+    }
+    for (SwarmGroup* g : plan->groups) {
+        std::vector<DevSwarmState> state(g->idx.size());
+        std::vector<double> hist(g->idx.size() * g->iters);
+        SG_CUDA(ctx, cudaMemcpyAsync(state.data(), g->d_state, sizeof(DevSwarmState) * state.size(),
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+        SG_CUDA(ctx, cudaMemcpyAsync(hist.data(), g->P.history, sizeof(double) * hist.size(), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+        SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        for (size_t j = 0; j < g->idx.size(); ++j) {
+            sg_swarm_result& r = results[g->idx[j]];
+            std::memcpy(r.best_position, state[j].best, sizeof r.best_position);
+            r.best_cost = state[j].best_cost;
+            if (r.cost_history)
+                std::memcpy(r.cost_history, hist.data() + j * g->iters, sizeof(double) * g->max_iters[j]);
+            // optimize() throws AllInfeasibleError when nothing finite was
+            // found (pso.cpp:137-139).
+            r.status = state[j].best_cost < HUGE_VAL ? SG_OK : SG_ERR_ALL_INFEASIBLE;
+        }
+    }
+    return SG_OK;
+}
+
+uint64_t sg_plan_evals(const sg_plan* plan) { return plan ? plan->evals : 0; }
+
+void sg_plan_destroy(sg_plan* plan) {
+    if (!plan) return;
+    cudaSetDevice(plan->ctx->device);
+    delete plan;
+}
+
+// Device bytes per particle of a plan (x, v, pb: 18; pbc, cost: 2; 312
+// engine words) — used to split oversized calls into sequential plans.
+static constexpr size_t kBytesPerParticle = (18 + 2 + kMtN) * sizeof(double);
+
+int sg_fit_swarms(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg_swarm_result* results) {
+    if (!ctx) return SG_ERR_INVALID_ARGUMENT;
+    if (n_swarms == 0) return SG_OK;
+    if (!swarms || !results) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null swarm arrays");
+    SG_CUDA(ctx, cudaSetDevice(ctx->device));
+    size_t free_b = 0, total_b = 0;
+    SG_CUDA(ctx, cudaMemGetInfo(&free_b, &total_b));
+    const size_t budget = std::max<size_t>(free_b / 10 * 7, size_t(1) << 28);
+    size_t begin = 0;
+    while (begin < n_swarms) {
+        size_t end = begin, bytes = 0;
+        while (end < n_swarms) {
+            const size_t need = swarms[end].n_particles * kBytesPerParticle;
+            if (end > begin && bytes + need > budget) break;
+            bytes += need;
+            ++end;
+        }
+        sg_plan* plan = nullptr;
+        int rc = sg_plan_create(ctx, swarms + begin, end - begin, &plan);
+        if (!rc) rc = sg_plan_run(plan);
+        if (!rc) rc = sg_plan_results(plan, results + begin);
+        sg_plan_destroy(plan);
+        if (rc) return rc;
+        begin = end;
+    }
+    return SG_OK;
+}
+
+int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper[6], uint64_t seed, size_t n,
+                         int horizon, double* costs, double* params_out, double* deaths_out) {
+    if (!w) return SG_ERR_INVALID_ARGUMENT;
+    sg_ctx* ctx = w->ctx;
+    if (!lower || !upper || !deaths_out) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null buffer");
+    if (horizon < 0) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "horizon must be >= 0");
+    for (int k = 0; k < 6; ++k)
+        if (!std::isfinite(lower[k]) || !std::isfinite(upper[k]) || lower[k] > upper[k])
+            return fail(ctx, SG_ERR_INVALID_ARGUMENT, "pso: bound " + std::to_string(k) + " is invalid");
+    if (n == 0) return SG_OK;
+    SG_CUDA(ctx, cudaSetDevice(ctx->device));
+    DevBufs b;
+    double *d_lo, *d_hi, *d_cost = nullptr, *d_par = nullptr, *d_D;
+    SG_CUDA(ctx, b.alloc(&d_lo, 6));
+    SG_CUDA(ctx, b.alloc(&d_hi, 6));
+    if (costs) SG_CUDA(ctx, b.alloc(&d_cost, n));
+    if (params_out) SG_CUDA(ctx, b.alloc(&d_par, 6 * n));
+    SG_CUDA(ctx, b.alloc(&d_D, n * static_cast<size_t>(horizon + 1)));
+    SG_CUDA(ctx, cudaMemcpyAsync(d_lo, lower, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, cudaMemcpyAsync(d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    DevWindow fwin = integration_window(horizon + 1, w->host.substeps, w->host.N);
+    cudaError_t err = cudaSuccess;
+    dispatch<EnsembleLaunch>(w->host.family, w->host.metric, w->host.substeps, w->d_desc, fwin, d_lo, d_hi, seed, n,
+                             horizon, d_cost, d_par, d_D, w->smem, ctx->stream, &err);
+    ctx->launches += 1;
+    if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
+    if (costs) SG_CUDA(ctx, cudaMemcpyAsync(costs, d_cost, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (params_out)
+        SG_CUDA(ctx, cudaMemcpyAsync(params_out, d_par, 6 * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, cudaMemcpyAsync(deaths_out, d_D, n * (horizon + 1) * sizeof(double), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SG_OK;
+}
+
+}  // extern "C"
+
+// ---- diagnostics -------------------------------------------------------------------
+
+namespace {
+
+// 8 independent DADD/DMUL chains per thread, alternating, no FMA: the FP64
+// pipe's issue rate for the operation mix of euler_substep.
+__global__ void __launch_bounds__(256) fp64_probe_kernel(double* out, int iters, double a, double b) {
+    double x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = a + threadIdx.x * 1e-9 + j;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = __dmul_rn(x[j], b);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = __dadd_rn(x[j], a);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s = __dadd_rn(s, x[j]);
+    if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
+}  // namespace
+
+extern "C" int sg_probe_fp64_rate(sg_ctx* ctx, double* ops_per_s) {
+    if (!ctx || !ops_per_s) return SG_ERR_INVALID_ARGUMENT;
+    SG_CUDA(ctx, cudaSetDevice(ctx->device));
+    DevBufs b;
+    double* d_out;
+    SG_CUDA(ctx, b.alloc(&d_out, 1));
+    const int iters = 4096;
+    const unsigned grid = static_cast<unsigned>(ctx->sm_count * 8);  // 2048 threads / SM
+    cudaEvent_t e0, e1;
+    SG_CUDA(ctx, cudaEventCreate(&e0));
+    SG_CUDA(ctx, cudaEventCreate(&e1));
+    float best_ms = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        SG_CUDA(ctx, cudaEventRecord(e0, ctx->stream));
+        fp64_probe_kernel<<<grid, 256, 0, ctx->stream>>>(d_out, iters, 1.0000001, 0.9999999);
+        SG_CUDA(ctx, cudaEventRecord(e1, ctx->stream));
+        SG_CUDA(ctx, cudaEventSynchronize(e1));
+        float ms = 0.0f;
+        SG_CUDA(ctx, cudaEventElapsedTime(&ms, e0, e1));
+        if (rep > 0) best_ms = std::min(best_ms, ms);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double ops = static_cast<double>(grid) * 256.0 * iters * 16.0;
+    *ops_per_s = ops / (best_ms * 1e-3);
+    return SG_OK;
+}

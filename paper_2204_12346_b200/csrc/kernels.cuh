@@ -1,0 +1,453 @@
+// kernels.cuh — sm_100a kernels of the particle-window cost engine.
+//
+//   eval_costs_kernel     boundary 1: BatchObjective body (calibration.cpp:140-154)
+//   integrate_kernel      integrate_batch / forecast_extension trajectories
+//   pso_init_kernel       Swarm::Swarm (pso.cpp:47-75) for many swarms
+//   pso_step_kernel       Swarm::step (pso.cpp:77-101) fused: move -> evaluate ->
+//                         personal best -> block argmin -> last-block global best
+//   ensemble_kernel       forecast-scenario ensemble (sample, score, forecast)
+//
+// Layout in HBM: particle state is structure-of-arrays (six planes of n
+// doubles for positions, velocities and personal bests; 312 planes for the
+// MT19937-64 engines), so each warp's loads and stores are 256 B coalesced
+// segments.  Observed windows (3 doubles per day) are staged in shared
+// memory once per CTA and read as broadcasts.
+#pragma once
+
+#include "sird_device.cuh"
+
+namespace sirdgpu {
+
+constexpr int kEvalThreads = 128;
+constexpr int kStepThreads = 128;
+
+// Shared-memory staging of one window: the descriptor in static shared memory,
+// obs + subh (+ robs + flags for MAPE) in the dynamic segment.
+struct SmemWindow {
+    const DevWindow* w;  // shared memory
+    const ObsDay* obs;
+    const ObsDay* robs;
+    const unsigned char* flag;
+    const double* subh;
+};
+
+__host__ __device__ inline size_t smem_window_bytes(int n_days, int substeps, int metric) {
+    size_t b = static_cast<size_t>(n_days) * sizeof(ObsDay) + static_cast<size_t>(substeps) * sizeof(double);
+    if (metric == kMetMAPE) b += static_cast<size_t>(n_days) * (sizeof(ObsDay) + 3);
+    return (b + 15) & ~size_t(15);
+}
+
+// Cooperative copy of a window into shared memory (all threads call; ends
+// with a barrier).  subh[sub] = RN(sub*h), the t offsets of model.cpp:94.
+__device__ __forceinline__ SmemWindow stage_window(const DevWindow* __restrict__ gw, DevWindow* sdesc,
+                                                   unsigned char* smem) {
+    if (threadIdx.x == 0) *sdesc = *gw;
+    const int n = gw->n_days;
+    const int ns = gw->substeps;
+    const int metric = gw->metric;
+    ObsDay* obs = reinterpret_cast<ObsDay*>(smem);
+    double* subh = reinterpret_cast<double*>(obs + n);
+    ObsDay* robs = reinterpret_cast<ObsDay*>(subh + ns);
+    unsigned char* flag = reinterpret_cast<unsigned char*>(robs + (metric == kMetMAPE ? n : 0));
+    const double* src = reinterpret_cast<const double*>(gw->obs);
+    double* dst = reinterpret_cast<double*>(obs);
+    for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) dst[i] = src[i];
+    const double h = gw->h;
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) subh[i] = dmul(static_cast<double>(i), h);
+    if (metric == kMetMAPE) {
+        const double* rsrc = reinterpret_cast<const double*>(gw->robs);
+        double* rdst = reinterpret_cast<double*>(robs);
+        for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) rdst[i] = rsrc[i];
+        for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) flag[i] = gw->obs_flag[i];
+    }
+    __syncthreads();
+    return SmemWindow{sdesc, obs, robs, flag, subh};
+}
+
+// ---- boundary 1 -------------------------------------------------------------
+// positions: row-major n x 6 (the BatchObjective layout, pso.hpp:33-37).
+template <int FAM, int MET, int SUB>
+__global__ void __launch_bounds__(kEvalThreads) eval_costs_kernel(const DevWindow* __restrict__ win,
+                                                                  const double* __restrict__ positions, size_t n,
+                                                                  double* __restrict__ costs) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ DevWindow sdesc;
+    const SmemWindow sw = stage_window(win, &sdesc, smem);
+    const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double x[6];
+#pragma unroll
+    for (int d = 0; d < 6; ++d) x[d] = positions[6 * k + d];
+    costs[k] = eval_particle<FAM, MET, SUB>(x, *sw.w, sw.subh, sw.obs, sw.robs, sw.flag);
+}
+
+// ---- trajectories -------------------------------------------------------------
+struct StoreSink {
+    double* out;  // n_days x 4 for this item
+    __device__ __forceinline__ void day(int d, double S, double I, double R, double D) {
+        const bool fin = all_finite(S, I, R, D);
+        const double nan = __longlong_as_double(0x7FF8000000000000LL);
+        out[4 * d + 0] = fin ? S : nan;
+        out[4 * d + 1] = fin ? I : nan;
+        out[4 * d + 2] = fin ? R : nan;
+        out[4 * d + 3] = fin ? D : nan;
+    }
+};
+
+// integrate_euler (model.cpp:76-107) per item.  params row-major n x 6;
+// init: one state (init_stride 0) or one per item (init_stride 4);
+// hold_beta2: forecast_extension's held parameters {b2, b2, 0, 0, g, mu}
+// (calibration.cpp:305-312).  states: n x n_days x 4, NaN after a blow-up.
+template <int SUB>
+__global__ void __launch_bounds__(kEvalThreads) integrate_kernel(DevWindow w, const double* __restrict__ params,
+                                                                 const double* __restrict__ init, int init_stride,
+                                                                 int hold_beta2, size_t n,
+                                                                 double* __restrict__ states,
+                                                                 unsigned char* __restrict__ finite) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* subh = reinterpret_cast<double*>(smem);
+    for (int i = threadIdx.x; i < w.substeps; i += blockDim.x) subh[i] = dmul(static_cast<double>(i), w.h);
+    __syncthreads();
+    const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double* p = params + 6 * k;
+    const double* s0 = init + init_stride * k;
+    double S = s0[0], I = s0[1], R = s0[2], D = s0[3];
+    StoreSink sink{states + k * static_cast<size_t>(w.n_days) * 4};
+    sink.out[0] = S;  // day 0 is the initial state, bit for bit (model.cpp:85)
+    sink.out[1] = I;
+    sink.out[2] = R;
+    sink.out[3] = D;
+    const bool init_ok = isfinite(dadd(dadd(dadd(S, I), R), D));  // SirdState::total (model.hpp:31)
+    if (!init_ok) {
+        const double nan = __longlong_as_double(0x7FF8000000000000LL);
+        for (int d = 1; d < w.n_days; ++d)
+            for (int c = 0; c < 4; ++c) sink.out[4 * d + c] = nan;
+        finite[k] = 0;
+        return;
+    }
+    const Particle part = hold_beta2 ? make_particle(p[1], p[1], 0.0, 0.0, p[4], p[5], w)
+                                     : make_particle(p[0], p[1], p[2], p[3], p[4], p[5], w);
+    integrate_days<SUB>(part, w, subh, S, I, R, D, sink);
+    finite[k] = all_finite(S, I, R, D) ? 1 : 0;
+}
+
+// ---- particle swarm ---------------------------------------------------------------
+
+// One swarm as the kernels see it (pso.hpp:14-32 config + bounds).
+struct DevSwarm {
+    int window;          // index into the window table
+    int repair;          // repair_time_order hook (calibration.cpp:89-93)
+    uint64_t n;          // particles
+    uint64_t offset;     // first particle in the flattened SoA planes
+    uint64_t max_iters;
+    uint32_t cta_begin;  // first CTA of this swarm in pso_step_kernel's grid
+    uint32_t n_ctas;
+    double lo[6], hi[6];
+    double w, c1, c2;
+    uint64_t seed;
+};
+
+// Swarm-global state updated by the last CTA of every iteration.
+struct DevSwarmState {
+    double best_cost;    // Swarm::best_cost_ (pso.cpp:49, +inf initially)
+    double best[6];      // Swarm::best_position_ (0 initially, pso.cpp:63)
+    unsigned int arrived;
+    unsigned int pad;
+};
+
+struct PsoPlanes {
+    double* x;           // 6 planes of `stride` doubles
+    double* v;
+    double* pb;
+    double* pbc;         // personal-best cost
+    double* cost;        // last evaluated cost
+    uint64_t* mt;        // 312 planes
+    size_t stride;       // total particles (plane length)
+    double* part_cost;   // per CTA
+    unsigned long long* part_idx;
+    double* history;     // per swarm, max_iters_max entries
+    uint64_t hist_stride;
+};
+
+__device__ __forceinline__ void repair_order(double* x) {  // calibration.cpp:89-93
+    if (x[2] > x[3]) {
+        const double t = x[2];
+        x[2] = x[3];
+        x[3] = t;
+    }
+}
+
+// std::clamp(v, lo, hi) == std::min(std::max(v, lo), hi) (stl_algo.h:3667-3670)
+__device__ __forceinline__ double std_clamp(double v, double lo, double hi) {
+    const double m = v < lo ? lo : v;
+    return hi < m ? hi : m;
+}
+
+// Swarm::Swarm (pso.cpp:47-75): engine i = mt19937_64(mix_seed(seed, i));
+// x[d] = lo[d] + u*(hi[d]-lo[d]) for d = 0..5 in order; repair; v = 0;
+// pbest = x; pbest cost = +inf.
+__global__ void __launch_bounds__(kStepThreads) pso_init_kernel(const DevSwarm* __restrict__ swarms,
+                                                                const uint32_t* __restrict__ cta_swarm,
+                                                                PsoPlanes P, DevSwarmState* __restrict__ state) {
+    const int s = static_cast<int>(cta_swarm[blockIdx.x]);
+    const DevSwarm& sw = swarms[s];
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x - sw.cta_begin) * blockDim.x + threadIdx.x;
+    if (i == 0) {
+        state[s].best_cost = __longlong_as_double(0x7FF0000000000000LL);
+        for (int d = 0; d < 6; ++d) state[s].best[d] = 0.0;
+        state[s].arrived = 0;
+    }
+    if (i >= sw.n) return;
+    const size_t p = sw.offset + i;
+    const size_t stride = P.stride;
+    // seed: mt[0] = seed; mt[j] = f*(mt[j-1] ^ (mt[j-1] >> 62)) + j
+    uint64_t m = mix_seed(sw.seed, i);
+    P.mt[p] = m;
+    for (int j = 1; j < kMtN; ++j) {
+        m = kMtF * (m ^ (m >> 62)) + static_cast<uint64_t>(j);
+        P.mt[static_cast<size_t>(j) * stride + p] = m;
+    }
+    double u[6];
+    mt_draw<6>(P.mt, stride, p, 0, u);
+    double x[6];
+#pragma unroll
+    for (int d = 0; d < 6; ++d) x[d] = dadd(sw.lo[d], dmul(u[d], dsub(sw.hi[d], sw.lo[d])));
+    if (sw.repair) repair_order(x);
+#pragma unroll
+    for (int d = 0; d < 6; ++d) {
+        P.x[d * stride + p] = x[d];
+        P.v[d * stride + p] = 0.0;
+        P.pb[d * stride + p] = x[d];
+    }
+    P.pbc[p] = __longlong_as_double(0x7FF0000000000000LL);
+}
+
+// (cost, index) ordering of the global-best scan (pso.cpp:90-96): the lowest
+// cost wins, ties go to the lowest index; NaN never wins (pbest costs are never
+// NaN: pbest only takes a cost that compared less, pso.cpp:84).
+__device__ __forceinline__ bool better(double ca, unsigned long long ia, double cb, unsigned long long ib) {
+    return ca < cb || (ca == cb && ia < ib);
+}
+
+// One Swarm::step (pso.cpp:77-101) for every swarm, iteration `it`.
+// it > 0 first applies the move of iteration it-1 (move_particles,
+// pso.cpp:103-127), which in the reference closes step it-1; it reads the
+// global best published by the previous launch.  Then evaluate, personal
+// best, CTA argmin, and the last CTA of each swarm folds the CTA minima into
+// the global best and writes cost_history[it].
+template <int FAM, int MET, int SUB>
+__global__ void __launch_bounds__(kStepThreads) pso_step_kernel(const DevSwarm* __restrict__ swarms,
+                                                                const uint32_t* __restrict__ cta_swarm,
+                                                                const DevWindow* __restrict__ windows,
+                                                                PsoPlanes P, DevSwarmState* __restrict__ state,
+                                                                uint64_t it) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double red_c[kStepThreads / 32];
+    __shared__ unsigned long long red_i[kStepThreads / 32];
+    __shared__ bool is_last;
+
+    __shared__ DevWindow sdesc;
+
+    const int s = static_cast<int>(cta_swarm[blockIdx.x]);
+    const DevSwarm& sw = swarms[s];
+    if (it >= sw.max_iters) return;  // CTA-uniform
+    const SmemWindow win = stage_window(windows + sw.window, &sdesc, smem);
+
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x - sw.cta_begin) * blockDim.x + threadIdx.x;
+    const bool active = i < sw.n;
+    const size_t p = sw.offset + (active ? i : 0);
+    const size_t stride = P.stride;
+    double my_c = __longlong_as_double(0x7FF0000000000000LL);
+    unsigned long long my_i = ~0ULL;
+
+    if (active) {
+        double x[6];
+#pragma unroll
+        for (int d = 0; d < 6; ++d) x[d] = P.x[d * stride + p];
+        if (it > 0) {
+            const double gbc = state[s].best_cost;
+            const bool have_best = gbc < __longlong_as_double(0x7FF0000000000000LL);  // pso.cpp:106
+            double u[12];
+            mt_draw<12>(P.mt, stride, p, 6 + 12 * (it - 1), u);
+#pragma unroll
+            for (int d = 0; d < 6; ++d) {
+                const double r1 = u[2 * d];
+                const double r2 = u[2 * d + 1];
+                const double vd = P.v[d * stride + p];
+                const double pbd = P.pb[d * stride + p];
+                // vel = w*v + (c1*r1)*(pbest - x)   (pso.cpp:116)
+                double vel = dadd(dmul(sw.w, vd), dmul(dmul(sw.c1, r1), dsub(pbd, x[d])));
+                if (have_best) vel = dadd(vel, dmul(dmul(sw.c2, r2), dsub(state[s].best[d], x[d])));  // 117-119
+                P.v[d * stride + p] = vel;
+                x[d] = std_clamp(dadd(x[d], vel), sw.lo[d], sw.hi[d]);  // pso.cpp:121
+            }
+            if (sw.repair) repair_order(x);  // pso.cpp:123-125
+#pragma unroll
+            for (int d = 0; d < 6; ++d) P.x[d * stride + p] = x[d];
+        }
+        const double c = eval_particle<FAM, MET, SUB>(x, *win.w, win.subh, win.obs, win.robs, win.flag);
+        P.cost[p] = c;
+        double pbc = P.pbc[p];
+        if (c < pbc) {  // pso.cpp:83-89
+            pbc = c;
+            P.pbc[p] = c;
+#pragma unroll
+            for (int d = 0; d < 6; ++d) P.pb[d * stride + p] = x[d];
+        }
+        my_c = pbc;
+        my_i = i;
+    }
+
+    // CTA argmin of personal-best costs, lowest index on ties.
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double oc = __shfl_down_sync(0xFFFFFFFFu, my_c, off);
+        const unsigned long long oi = __shfl_down_sync(0xFFFFFFFFu, my_i, off);
+        if (better(oc, oi, my_c, my_i)) {
+            my_c = oc;
+            my_i = oi;
+        }
+    }
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        red_c[warp] = my_c;
+        red_i[warp] = my_i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double bc = red_c[0];
+        unsigned long long bi = red_i[0];
+        for (int k = 1; k < kStepThreads / 32; ++k)
+            if (better(red_c[k], red_i[k], bc, bi)) {
+                bc = red_c[k];
+                bi = red_i[k];
+            }
+        P.part_cost[blockIdx.x] = bc;
+        P.part_idx[blockIdx.x] = bi;
+        __threadfence();
+        const unsigned int ticket = atomicAdd(&state[s].arrived, 1u);
+        is_last = (ticket == sw.n_ctas - 1);
+    }
+    __syncthreads();
+    if (!is_last) return;
+
+    // Last CTA of the swarm: global-best scan (pso.cpp:90-96) over the CTA
+    // minima; (cost, index) order makes the parallel fold equal the
+    // sequential lowest-index scan.
+    __threadfence();
+    double bc = __longlong_as_double(0x7FF0000000000000LL);
+    unsigned long long bi = ~0ULL;
+    for (uint32_t k = threadIdx.x; k < sw.n_ctas; k += blockDim.x) {
+        const double c = __ldcg(&P.part_cost[sw.cta_begin + k]);
+        const unsigned long long ix = __ldcg(&P.part_idx[sw.cta_begin + k]);
+        if (better(c, ix, bc, bi)) {
+            bc = c;
+            bi = ix;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double oc = __shfl_down_sync(0xFFFFFFFFu, bc, off);
+        const unsigned long long oi = __shfl_down_sync(0xFFFFFFFFu, bi, off);
+        if (better(oc, oi, bc, bi)) {
+            bc = oc;
+            bi = oi;
+        }
+    }
+    __syncthreads();  // red_c/red_i reuse
+    if (lane == 0) {
+        red_c[warp] = bc;
+        red_i[warp] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        bc = red_c[0];
+        bi = red_i[0];
+        for (int k = 1; k < kStepThreads / 32; ++k)
+            if (better(red_c[k], red_i[k], bc, bi)) {
+                bc = red_c[k];
+                bi = red_i[k];
+            }
+        DevSwarmState& st = state[s];
+        if (bc < st.best_cost) {  // strict: an equal later cost never replaces (pso.cpp:91)
+            st.best_cost = bc;
+            const size_t q = sw.offset + bi;
+            for (int d = 0; d < 6; ++d) st.best[d] = __ldcg(&P.pb[d * stride + q]);
+        }
+        P.history[static_cast<size_t>(s) * P.hist_stride + it] = st.best_cost;
+        st.arrived = 0;
+    }
+}
+
+// ---- forecast-scenario ensemble ----------------------------------------------------
+// Sample k: 6 uniform01 draws of mt19937_64(mix_seed(seed, k)) mapped into the
+// box like Swarm::Swarm (pso.cpp:65-72) + repair; score it on the window
+// (cost), then continue `horizon` days holding beta = beta2
+// (forecast_extension, calibration.cpp:305-317) and write D per forecast day.
+struct ForecastDSink {
+    double* out;
+    __device__ __forceinline__ void day(int d, double S, double I, double R, double D) {
+        (void)S;
+        (void)I;
+        (void)R;
+        out[d] = D;
+    }
+};
+
+template <int FAM, int MET, int SUB>
+__global__ void __launch_bounds__(kEvalThreads) ensemble_kernel(const DevWindow* __restrict__ win, DevWindow fwin,
+                                                                const double* __restrict__ lo,
+                                                                const double* __restrict__ hi, uint64_t seed,
+                                                                size_t n, int horizon, double* __restrict__ costs,
+                                                                double* __restrict__ params_out,
+                                                                double* __restrict__ deaths_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ DevWindow sdesc;
+    const SmemWindow sw = stage_window(win, &sdesc, smem);
+    const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double u[6];
+    mt_first_uniforms<6>(mix_seed(seed, k), u);
+    double x[6];
+#pragma unroll
+    for (int d = 0; d < 6; ++d) x[d] = dadd(lo[d], dmul(u[d], dsub(hi[d], lo[d])));
+    repair_order(x);
+    if (params_out) {
+#pragma unroll
+        for (int d = 0; d < 6; ++d) params_out[6 * k + d] = x[d];
+    }
+    const DevWindow& w = *sw.w;
+    const double nan = __longlong_as_double(0x7FF8000000000000LL);
+    double* drow = deaths_out + k * static_cast<size_t>(horizon + 1);
+    if (!w.init_finite) {
+        if (costs) costs[k] = __longlong_as_double(0x7FF0000000000000LL);
+        for (int d = 0; d <= horizon; ++d) drow[d] = nan;
+        return;
+    }
+    const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w);
+    double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
+    ScoreSink<FAM, MET> score(w, sw.obs, sw.robs, sw.flag);
+    score.day(0, S, I, R, D);
+    integrate_days<SUB>(p, w, sw.subh, S, I, R, D, score);
+    const bool fin_w = all_finite(S, I, R, D);
+    // forecast_extension re-checks the junction through integrate_euler's
+    // isfinite(init.total()) (model.cpp:83).
+    const bool fin_j = fin_w && isfinite(dadd(dadd(dadd(S, I), R), D));
+    if (costs) costs[k] = score.finish(fin_w);
+    if (!fin_j) {  // forecast_extension throws NonFiniteError (calibration.cpp:301-303, 318-320)
+        for (int d = 0; d <= horizon; ++d) drow[d] = nan;
+        return;
+    }
+    // Forecast: fwin carries n_days = horizon + 1 and the same N, h, substeps.
+    const Particle held = make_particle(x[1], x[1], 0.0, 0.0, x[4], x[5], fwin);
+    drow[0] = D;
+    ForecastDSink fs{drow};
+    integrate_days<SUB>(held, fwin, sw.subh, S, I, R, D, fs);
+    if (!all_finite(S, I, R, D)) {  // calibration.cpp:318-320
+        for (int d = 0; d <= horizon; ++d) drow[d] = nan;
+    }
+}
+
+}  // namespace sirdgpu

@@ -1,0 +1,352 @@
+// sird_device.cuh — device-side arithmetic of the particle-window cost engine.
+//
+// Bit-exactness contract: every function here reproduces the reference's
+// IEEE-754 double arithmetic operation by operation (the reference object
+// code contains no FMA, SURVEY.md §0 key finding 2).  The file is compiled
+// with -fmad=false and additionally spells every rounded operation with an
+// explicit __dmul_rn/__dadd_rn/__dsub_rn intrinsic, so no contraction can
+// ever be introduced.  The only fma() uses are the exact-division sequence
+// in div_exact(), whose result is proven equal to the correctly rounded
+// quotient.
+#pragma once
+
+#include <cstdint>
+
+namespace sirdgpu {
+
+constexpr int kFamD = 0;
+constexpr int kFamIRD = 1;
+constexpr int kMetMXSE = 0;
+constexpr int kMetMSE = 1;
+constexpr int kMetMAE = 2;
+constexpr int kMetMAPE = 3;
+
+// Per-day observation flags (MAPE): skip (obs == 0), fast reciprocal division,
+// or plain IEEE division.
+constexpr unsigned char kObsSkip = 0;
+constexpr unsigned char kObsFast = 1;
+constexpr unsigned char kObsSlow = 2;
+
+// One observed day, staged in shared memory (I, R, D).
+struct ObsDay {
+    double v[3];
+};
+
+// Window descriptor as the kernels see it (device memory, one per window).
+// Built on the host by sg_window_create from the reference's
+// make_window_objective inputs (calibration.cpp:120-139).
+struct DevWindow {
+    int n_days;
+    int substeps;
+    int family;
+    int metric;
+    double N;             // population
+    double rN;            // RN(1/N), valid when fast_N
+    double h;             // 1.0 / substeps (model.cpp:90)
+    int fast_N;           // divisor N admits the 3-op exact division
+    int init_finite;      // isfinite(init.total()) (model.cpp:83)
+    double init[4];       // S, I, R, D
+    double scale[3];      // compartment_cost scale (objectives.cpp:61-69); 1 for D-only
+    double kept[3];       // MAPE: number of days with obs != 0 (objectives.cpp:41-55)
+    const ObsDay* obs;    // n_days
+    const ObsDay* robs;   // RN(1/obs) per day (MAPE)
+    const unsigned char* obs_flag;  // 3 per day (MAPE)
+};
+
+// ---- exact arithmetic ---------------------------------------------------------
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// std::max(a, b) == (a < b) ? b : a (stl_algobase.h), NaN-preserving order.
+__device__ __forceinline__ double std_max(double a, double b) { return a < b ? b : a; }
+
+// Biased exponent of a double, from its high word (integer pipe only).
+__device__ __forceinline__ int dexp(double a) {
+    return (__double2hiint(a) >> 20) & 0x7FF;
+}
+
+// a / b, correctly rounded, given rb = RN(1/b) and a divisor b that passed the
+// host-side admissibility test (divisor_admits_fast_path in engine.cu:
+// |b| in [2^-60, 2^60] and the odd part of b's significand below 2^53/3).
+// The Markstein step q0 = RN(a*rb); r = a - q0*b (exact by fma);
+// q = RN(q0 + r*rb) then equals RN(a/b) for every dividend with
+// |a| in [2^-700, 2^701) (proof in DESIGN.md §4: a quotient of such b lies at
+// least ulp/(2*oddpart(b)) from any rounding boundary, farther than the
+// sequence's error of 1.5 ulp * 2^-53).  Every other dividend (0, subnormal,
+// huge, inf, NaN) goes through the IEEE division.
+__device__ __forceinline__ double div_exact(double a, double b, double rb) {
+    const int e = dexp(a);
+    if (e >= 1023 - 700 && e <= 1023 + 700) {
+        const double q0 = __dmul_rn(a, rb);
+        const double r = __fma_rn(-q0, b, a);
+        return __fma_rn(r, rb, q0);
+    }
+    return __ddiv_rn(a, b);
+}
+
+// ---- beta(t) regimes --------------------------------------------------------
+//
+// beta_at (model.cpp:55-64) compares t = (day-1) + sub*h (model.cpp:94)
+// against t1 and t2.  t is non-decreasing in the substep index
+// k = (day-1)*S + sub, so {k : t_k < x} is a prefix; the kernel resolves both
+// comparisons once per particle into prefix lengths k1, k2 and then selects
+// the regime with integer compares only.
+
+__device__ __forceinline__ double t_of(int k, int S, double h) {
+    const int day_m1 = k / S;
+    const int sub = k - day_m1 * S;
+    return dadd(static_cast<double>(day_m1), dmul(static_cast<double>(sub), h));
+}
+
+// Number of k in [0, K) with t_k < x (x may be NaN -> 0).
+__device__ __forceinline__ int count_t_below(double x, int K, int S, double h) {
+    int lo = 0, hi = K;  // answer in [lo, hi]
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (t_of(mid, S, h) < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Per-particle constants of the integration.
+struct Particle {
+    double b1, b2, t1, g, mu;
+    double bp1, bp2;  // beta1/N, beta2/N (model.cpp:67, constant regimes)
+    double slope;     // (beta2-beta1)/(t2-t1) (model.cpp:62)
+    int k1, k2;       // regime prefix lengths: k<k1 -> beta1; k>=k2 -> beta2; else ramp
+};
+
+__device__ __forceinline__ Particle make_particle(double b1, double b2, double t1, double t2, double g, double mu,
+                                                  const DevWindow& w) {
+    Particle p;
+    p.b1 = b1;
+    p.b2 = b2;
+    p.t1 = t1;
+    p.g = g;
+    p.mu = mu;
+    p.bp1 = ddiv(b1, w.N);
+    p.bp2 = ddiv(b2, w.N);
+    p.slope = ddiv(dsub(b2, b1), dsub(t2, t1));
+    const int K = (w.n_days - 1) * w.substeps;
+    p.k1 = count_t_below(t1, K, w.substeps, w.h);
+    // "t >= t2" is the complement of "t < t2" except for NaN t2, where both
+    // comparisons are false and the ramp branch is taken (model.cpp:59-63).
+    p.k2 = (t2 != t2) ? K : count_t_below(t2, K, w.substeps, w.h);
+    if (p.k2 < p.k1) p.k2 = p.k1;  // t1 > t2: no ramp (k >= k1 implies t >= t2)
+    return p;
+}
+
+// One Euler substep of sird_rhs (model.cpp:66-74) + update (model.cpp:96-99),
+// in the reference's exact operation order:
+//   inf = ((beta/N)*S)*I;  dI = (inf - g*I) - mu*I
+//   S += h*(-inf); I += h*dI; R += h*(g*I); D += h*(mu*I)
+__device__ __forceinline__ void euler_substep(double bp, double g, double mu, double h, double& S, double& I,
+                                              double& R, double& D) {
+    const double inf = dmul(dmul(bp, S), I);
+    const double gI = dmul(g, I);
+    const double mI = dmul(mu, I);
+    const double dI = dsub(dsub(inf, gI), mI);
+    S = dsub(S, dmul(h, inf));  // S + h*(-inf) == S - h*inf exactly (RN is symmetric)
+    I = dadd(I, dmul(h, dI));
+    R = dadd(R, dmul(h, gI));
+    D = dadd(D, dmul(h, mI));
+}
+
+// beta(t_k)/N for a ramp substep (model.cpp:62-63 then model.cpp:67).
+__device__ __forceinline__ double ramp_bp(const Particle& p, double dayf, double subh, const DevWindow& w) {
+    const double t = dadd(dayf, subh);
+    const double beta = dadd(p.b1, dmul(p.slope, dsub(t, p.t1)));
+    return w.fast_N ? div_exact(beta, w.N, w.rN) : ddiv(beta, w.N);
+}
+
+// Integrate days 1..n_days-1 (model.cpp:92-106), calling sink.day(day, S, I, R, D)
+// after every day.  SUB > 0 fixes the substep count at compile time
+// (the reference default kDefaultSubsteps = 24, model.hpp:12); SUB == 0 reads
+// it from the window.  `subh` is the table RN(sub*h), sub < substeps.
+template <int SUB, class Sink>
+__device__ __forceinline__ void integrate_days(const Particle& p, const DevWindow& w, const double* subh,
+                                               double& S, double& I, double& R, double& D, Sink& sink) {
+    const int nsub = SUB > 0 ? SUB : w.substeps;
+    const double h = w.h;
+    int kbase = 0;
+    for (int day = 1; day < w.n_days; ++day) {
+        const double dayf = static_cast<double>(day - 1);
+        const int lo = p.k1 - kbase;  // sub < lo  -> beta1
+        const int hi = p.k2 - kbase;  // sub >= hi -> beta2
+#pragma unroll
+        for (int sub = 0; sub < nsub; ++sub) {
+            double bp = sub < lo ? p.bp1 : p.bp2;
+            if (sub >= lo && sub < hi) bp = ramp_bp(p, dayf, subh[sub], w);
+            euler_substep(bp, p.g, p.mu, h, S, I, R, D);
+        }
+        kbase += nsub;
+        sink.day(day, S, I, R, D);
+    }
+}
+
+__device__ __forceinline__ bool all_finite(double S, double I, double R, double D) {
+    return isfinite(S) && isfinite(I) && isfinite(R) && isfinite(D);
+}
+
+// ---- scoring (objectives.cpp:15-120), fused into the day loop ----------------
+//
+// Accumulates per compartment exactly like metric_on_scaled_residuals / mape
+// do over k = 0..n-1, one day at a time, so trajectories never leave
+// registers.  Non-finiteness is absorbing under x + h*dx, so checking the
+// final state once equals the per-day check of model.cpp:101-104.
+template <int FAM, int MET>
+struct ScoreSink {
+    const DevWindow& w;
+    const ObsDay* obs;    // shared memory
+    const ObsDay* robs;   // shared memory (MAPE)
+    const unsigned char* flag;  // shared memory (MAPE)
+    double acc[3];
+
+    __device__ __forceinline__ ScoreSink(const DevWindow& win, const ObsDay* o, const ObsDay* ro,
+                                         const unsigned char* f)
+        : w(win), obs(o), robs(ro), flag(f) {
+        acc[0] = acc[1] = acc[2] = 0.0;
+    }
+
+    __device__ __forceinline__ void one(int c, int day, double pred) {
+        const double o = obs[day].v[c];
+        if (MET == kMetMAPE) {
+            const unsigned char f = flag[3 * day + c];
+            if (f == kObsSkip) return;  // objectives.cpp:46-48
+            const double num = dsub(o, pred);
+            const double q = f == kObsFast ? div_exact(num, o, robs[day].v[c]) : ddiv(num, o);
+            acc[c] = dadd(acc[c], fabs(q));
+            return;
+        }
+        double e = dsub(o, pred);
+        if (FAM == kFamIRD) e = dmul(e, w.scale[c]);  // D-only scales by 1.0: identity
+        if (MET == kMetMXSE) acc[c] = std_max(acc[c], dmul(e, e));
+        else if (MET == kMetMSE) acc[c] = dadd(acc[c], dmul(e, e));
+        else acc[c] = dadd(acc[c], fabs(e));
+    }
+
+    __device__ __forceinline__ void day(int d, double S, double I, double R, double D) {
+        (void)S;
+        if (FAM == kFamIRD) {
+            one(0, d, I);
+            one(1, d, R);
+        }
+        one(2, d, D);
+    }
+
+    __device__ __forceinline__ double finish_one(int c) const {
+        if (MET == kMetMAPE) {
+            if (w.kept[c] == 0.0) return __longlong_as_double(0x7FF0000000000000LL);
+            return ddiv(dmul(100.0, acc[c]), w.kept[c]);
+        }
+        if (MET == kMetMSE || MET == kMetMAE) return ddiv(acc[c], static_cast<double>(w.n_days));
+        return acc[c];
+    }
+
+    __device__ __forceinline__ double finish(bool finite) const {
+        if (!finite) return __longlong_as_double(0x7FF0000000000000LL);  // objectives.cpp:101-103
+        if (FAM == kFamD) return finish_one(2);
+        double worst = finish_one(0);           // objectives.cpp:116-119
+        worst = std_max(worst, finish_one(1));
+        worst = std_max(worst, finish_one(2));
+        return worst;
+    }
+};
+
+// Full particle-window evaluation: objective_value(spec, slice,
+// integrate_euler(params)) (calibration.cpp:148-152).
+template <int FAM, int MET, int SUB>
+__device__ __forceinline__ double eval_particle(const double* x, const DevWindow& w, const double* subh,
+                                                const ObsDay* obs, const ObsDay* robs, const unsigned char* flag) {
+    if (!w.init_finite) return __longlong_as_double(0x7FF0000000000000LL);
+    const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w);
+    double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
+    ScoreSink<FAM, MET> sink(w, obs, robs, flag);
+    sink.day(0, S, I, R, D);  // day 0 is the initial state, bit for bit (model.cpp:85)
+    integrate_days<SUB>(p, w, subh, S, I, R, D, sink);
+    return sink.finish(all_finite(S, I, R, D));
+}
+
+// ---- std::mt19937_64, structure-of-arrays ---------------------------------
+//
+// Each particle owns one engine (pso.hpp:79) seeded mix_seed(seed, i)
+// (pso.cpp:55-57).  State word j of particle p lives at st[j*stride + p] so a
+// warp touches 32 consecutive words.  Every particle of a swarm has drawn the
+// same number of values at any time, so the generation position `count` is
+// uniform and the standard in-place twist is evaluated lazily, one word per
+// draw: word i of the next generation depends on words i, i+1 (old) and
+// (i+156)%312 (old for i<156, already new for i>=156) — exactly the order of
+// the sequential twist.
+
+constexpr int kMtN = 312;
+constexpr int kMtM = 156;
+constexpr uint64_t kMtA = 0xB5026F5AA96619E9ULL;
+constexpr uint64_t kMtF = 6364136223846793005ULL;
+
+__host__ __device__ __forceinline__ uint64_t mix_seed(uint64_t base, uint64_t index) {  // pso.cpp:36-41
+    uint64_t z = base + 0x9E3779B97F4A7C15ULL * (index + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t mt_temper(uint64_t x) {
+    x ^= (x >> 29) & 0x5555555555555555ULL;
+    x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+    x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+    x ^= x >> 43;
+    return x;
+}
+
+__device__ __forceinline__ uint64_t mt_twist_word(uint64_t cur, uint64_t next, uint64_t far) {
+    const uint64_t y = (cur & 0xFFFFFFFF80000000ULL) | (next & 0x7FFFFFFFULL);
+    return far ^ (y >> 1) ^ ((y & 1ULL) ? kMtA : 0ULL);
+}
+
+// uniform01 (pso.cpp:43-45)
+__device__ __forceinline__ double to_uniform01(uint64_t x) {
+    return dmul(static_cast<double>(x >> 11), 0x1.0p-53);
+}
+
+// Draw `n` consecutive values (n <= 312) starting at the uniform stream
+// position `count` (values drawn so far) from the SoA engine of particle p.
+template <int NDRAW>
+__device__ __forceinline__ void mt_draw(uint64_t* __restrict__ st, size_t stride, size_t p, uint64_t count,
+                                        double* out) {
+#pragma unroll
+    for (int j = 0; j < NDRAW; ++j) {
+        const int i = static_cast<int>((count + j) % kMtN);
+        const uint64_t cur = st[static_cast<size_t>(i) * stride + p];
+        const int i1 = i + 1 == kMtN ? 0 : i + 1;
+        const uint64_t nxt = st[static_cast<size_t>(i1) * stride + p];
+        const int im = i + kMtM >= kMtN ? i + kMtM - kMtN : i + kMtM;
+        const uint64_t far = st[static_cast<size_t>(im) * stride + p];
+        const uint64_t w = mt_twist_word(cur, nxt, far);
+        st[static_cast<size_t>(i) * stride + p] = w;
+        out[j] = to_uniform01(mt_temper(w));
+    }
+}
+
+// First `n` (<= 156) outputs of mt19937_64(seed) without materialising the
+// state: generation-1 word i needs seeded words i, i+1 and i+156 only.
+template <int NDRAW>
+__device__ __forceinline__ void mt_first_uniforms(uint64_t seed, double* out) {
+    static_assert(NDRAW <= 155, "needs words i+1 and i+156 of the seeded state");
+    uint64_t lowv[NDRAW + 1];
+    uint64_t farv[NDRAW];
+    uint64_t x = seed;
+#pragma unroll
+    for (int i = 0; i <= kMtM + NDRAW - 1; ++i) {
+        if (i > 0) x = kMtF * (x ^ (x >> 62)) + static_cast<uint64_t>(i);
+        if (i <= NDRAW) lowv[i] = x;
+        if (i >= kMtM) farv[i - kMtM] = x;
+    }
+#pragma unroll
+    for (int j = 0; j < NDRAW; ++j) out[j] = to_uniform01(mt_temper(mt_twist_word(lowv[j], lowv[j + 1], farv[j])));
+}
+
+}  // namespace sirdgpu

@@ -1,0 +1,221 @@
+"""CUDA path vs the reference, through the C-ABI (include/sirdgpu.h).
+
+Bar: bit-identical doubles (NaN == NaN).  The golden costs/fits/forecasts in
+tests/golden/ were produced by the unmodified reference (oracle/gen_golden.py);
+the on-the-fly comparisons use the C restatement (oracle/), itself pinned to
+the same goldens by tests/test_oracle.py.  Mirrors the reference's own
+pins: test_calibration.cpp:139-164 (batch objective == serial
+objective_value), test_pso.cpp:78-93 (bitwise reproducibility), 133-216
+(first iteration, ties, all-infeasible), test_model.cpp:50-58, 116-148.
+"""
+import json
+
+import numpy as np
+import pytest
+
+from helpers import assert_bitwise
+
+pytestmark = pytest.mark.gpu
+
+SPECS = [f"{f}-{m}" for f in ("d", "ird") for m in ("mxse", "mse", "mae", "mape")]
+
+
+@pytest.fixture(scope="module")
+def golden_costs():
+    from conftest import GOLDEN
+    return dict(np.load(GOLDEN / "costs.npz"))
+
+
+def _cases(g):
+    return sorted({k.split("/")[0] for k in g})
+
+
+def test_costs_match_reference_goldens(ctx, golden_costs):
+    import paper_2204_12346_b200 as eng
+    g = golden_costs
+    checked = 0
+    for case in _cases(g):
+        I, R, D = g[f"{case}/obs"]
+        init, N = g[f"{case}/init"], float(g[f"{case}/N"][0])
+        sets = sorted({k.split("/")[1] for k in g if k.startswith(case + "/") and k.count("/") == 2})
+        for spec in SPECS:
+            win = eng.Window(ctx, I, R, D, init, N, spec)
+            for s in sets:
+                got = win.eval_costs(g[f"{case}/{s}/positions"])
+                assert_bitwise(got, g[f"{case}/{s}/{spec}"], f"{case}/{s}/{spec}")
+                checked += got.size
+    assert checked > 5000
+
+
+@pytest.mark.parametrize("spec", SPECS)
+def test_costs_match_oracle_random_poland_windows(ctx, port, poland, spec):
+    import paper_2204_12346_b200 as eng
+    rng = np.random.default_rng(hash(spec) & 0xFFFF)
+    for w in (0, 17, 77, 138):
+        a = 3 * w
+        I, R, D = poland["I"][a:a + 36], poland["R"][a:a + 36], poland["D"][a:a + 36]
+        N = poland["N"]
+        init = [N - I[0] - R[0] - D[0], I[0], R[0], D[0]]
+        win = eng.Window(ctx, I, R, D, init, N, spec)
+        for hi in ([2, 2, 28, 28, 1, 0.1], [10, 10, 35, 35, 10, 10]):
+            pos = rng.random((700, 6)) * np.array(hi)
+            assert_bitwise(win.eval_costs(pos), port.eval_costs(spec, I, R, D, init, N, pos), f"w{w} {spec}")
+
+
+def test_costs_non_default_substeps_and_populations(ctx, port, poland):
+    import paper_2204_12346_b200 as eng
+    rng = np.random.default_rng(5)
+    I, R, D = poland["I"][30:51], poland["R"][30:51], poland["D"][30:51]
+    for N, substeps in ((38e6, 7), (38e6 + 0.3, 24), (1.0 / 3.0 * 1e8, 24), (38e6, 1), (38e6, 50)):
+        init = [N - I[0] - R[0] - D[0], I[0], R[0], D[0]]
+        pos = rng.random((300, 6)) * np.array([2, 2, 20, 20, 1, 0.1])
+        for spec in ("ird-mxse", "d-mape"):
+            win = eng.Window(ctx, I, R, D, init, N, spec, substeps=substeps)
+            assert_bitwise(win.eval_costs(pos), port.eval_costs(spec, I, R, D, init, N, pos, substeps=substeps),
+                           f"N={N} S={substeps} {spec}")
+
+
+def test_single_day_window_and_empty_batch(ctx, port):
+    import paper_2204_12346_b200 as eng
+    I, R, D = np.array([5.0]), np.array([1.0]), np.array([0.5])
+    init = [100 - 6.5, 5.0, 1.0, 0.5]
+    pos = np.array([[0.5, 0.5, 0, 0, 0.1, 0.01], [9, 9, 0, 0, 9, 9]])
+    for spec in SPECS:
+        win = eng.Window(ctx, I, R, D, init, 100.0, spec)
+        assert_bitwise(win.eval_costs(pos), port.eval_costs(spec, I, R, D, init, 100.0, pos), spec)
+        assert win.eval_costs(np.zeros((0, 6))).size == 0
+
+
+def test_non_finite_initial_state_costs_infinity(ctx):
+    import paper_2204_12346_b200 as eng
+    I = R = D = np.ones(5)
+    win = eng.Window(ctx, I, R, D, [np.inf, 1, 1, 1], 10.0, "ird-mse")
+    assert np.all(np.isposinf(win.eval_costs(np.full((3, 6), 0.1))))
+
+
+def test_rejects_non_six_dim_positions(ctx):
+    import paper_2204_12346_b200 as eng
+    from paper_2204_12346_b200 import _capi
+    win = eng.Window(ctx, np.ones(5), np.ones(5), np.ones(5), [7, 1, 1, 1], 10.0, "ird-mse")
+    costs = np.empty(2)
+    rc = _capi.lib().sg_eval_costs(win.handle, _capi._d(np.zeros(10)), 2, 5, _capi._d(costs))
+    assert rc == 1
+    with pytest.raises(eng.errors.Error):
+        eng.Window(ctx, np.ones(5), np.ones(5), np.ones(5), [7, 1, 1, 1], 0.0, "ird-mse")
+
+
+def test_integrate_batch_matches_reference_trajectories(ctx, port):
+    from conftest import GOLDEN
+    g = np.load(GOLDEN / "forecast.npz")
+    pos, init, N = g["positions"], g["init"], float(g["N"][0])
+    states, fin = ctx.integrate_batch(pos, init, N, 36)
+    assert_bitwise(states, g["window"], "window trajectories")
+    assert np.array_equal(fin, g["window_finite"])
+    # day 0 is the initial state bit for bit (test_model.cpp:50-58)
+    assert_bitwise(states[:, 0, :], np.broadcast_to(init, (len(pos), 4)), "day 0")
+
+
+def test_forecast_batch_matches_reference(ctx):
+    from conftest import GOLDEN
+    g = np.load(GOLDEN / "forecast.npz")
+    ok = g["window_finite"]
+    junction = g["window"][ok, -1, :]
+    states, fin = ctx.forecast_batch(g["positions"][ok], junction, float(g["N"][0]), 21)
+    assert_bitwise(states[fin], g["forecast"][ok][fin], "forecast")
+    assert np.array_equal(fin, g["forecast_finite"][ok])
+
+
+def test_integrate_random_parameters_match_oracle(ctx, port):
+    rng = np.random.default_rng(17)
+    N = 1e6
+    init = [N - 300, 200, 80, 20]
+    pos = rng.random((400, 6)) * np.array([10, 10, 35, 35, 10, 10])
+    states, fin = ctx.integrate_batch(pos, init, N, 36)
+    for k in range(0, 400, 7):
+        want, wf = port.integrate(pos[k], init, N, 36)
+        assert_bitwise(states[k], want, f"trajectory {k}")
+        assert fin[k] == wf
+
+
+def _unhex(v):
+    return np.array([float.fromhex(x) for x in v])
+
+
+@pytest.fixture(scope="module")
+def golden_fits():
+    from conftest import GOLDEN
+    return json.loads((GOLDEN / "fits.json").read_text())
+
+
+def test_swarms_match_reference_goldens(ctx, golden_fits):
+    """All golden swarms in ONE sg_fit_swarms call (mixed specs, sizes, windows)."""
+    import paper_2204_12346_b200 as eng
+    wins, descs = [], []
+    for c in golden_fits:
+        win = eng.Window(ctx, _unhex(c["I"]), _unhex(c["R"]), _unhex(c["D"]), _unhex(c["init"]), c["N"], c["spec"])
+        wins.append(win)
+        descs.append(dict(window=win, lower=c["lower"], upper=c["upper"], n_particles=c["n"], max_iters=c["iters"],
+                          inertia=c["w"], cognitive=c["c1"], social=c["c2"], seed=c["seed"]))
+    out = ctx.fit_swarms(descs)
+    for c, (status, best, cost, hist) in zip(golden_fits, out):
+        assert status == c["status"], c["name"]
+        assert_bitwise(hist, _unhex(c["history"]), c["name"] + " history")
+        if status == 0:
+            assert_bitwise(best, _unhex(c["best"]), c["name"] + " best")
+            assert cost == float.fromhex(c["best_cost"])
+
+
+def test_swarm_matches_oracle_and_is_reproducible(ctx, port, poland):
+    import paper_2204_12346_b200 as eng
+    a = 60
+    I, R, D = poland["I"][a:a + 36], poland["R"][a:a + 36], poland["D"][a:a + 36]
+    N = poland["N"]
+    init = [N - I[0] - R[0] - D[0], I[0], R[0], D[0]]
+    lo, hi = [0] * 6, [2, 2, 28, 28, 1, 0.1]
+    win = eng.Window(ctx, I, R, D, init, N, "ird-mxse")
+    # 700 particles -> 6 CTAs incl. a ragged one; 400 iterations -> engine wraps twice (312 words)
+    desc = dict(window=win, lower=lo, upper=hi, n_particles=700, max_iters=60, seed=99)
+    (s1, b1, c1, h1), (s2, b2, c2, h2) = ctx.fit_swarms([desc, desc])
+    rc, bo, co, ho = port.fit_swarm("ird-mxse", I, R, D, init, N, lo, hi, 700, 60, seed=99)
+    assert s1 == s2 == rc == 0
+    assert_bitwise(h1, ho, "history")
+    assert_bitwise(b1, bo, "best")
+    assert_bitwise(h2, h1, "reproducible")
+    assert np.all(np.diff(h1) <= 0)  # best-so-far never increases (test_pso.cpp:95-107)
+
+
+def test_invalid_swarm_config_is_reported_per_swarm(ctx, poland):
+    import paper_2204_12346_b200 as eng
+    I, R, D = poland["I"][:21], poland["R"][:21], poland["D"][:21]
+    N = poland["N"]
+    win = eng.Window(ctx, I, R, D, [N - I[0] - R[0] - D[0], I[0], R[0], D[0]], N, "d-mse")
+    good = dict(window=win, lower=[0] * 6, upper=[2, 2, 13, 13, 1, 0.1], n_particles=40, max_iters=3, seed=1)
+    bad = dict(good, lower=[0, 0, 0, 5, 0, 0], upper=[2, 2, 13, 4, 1, 0.1])
+    out = ctx.fit_swarms([good, bad, dict(good, inertia=float("nan"))])
+    assert out[0][0] == 0 and out[1][0] == 1 and out[2][0] == 1
+
+
+def test_forecast_ensemble_matches_oracle(ctx, port, poland):
+    import paper_2204_12346_b200 as eng
+    a = 414
+    I, R, D = poland["I"][a:a + 36], poland["R"][a:a + 36], poland["D"][a:a + 36]
+    N = poland["N"]
+    init = [N - I[0] - R[0] - D[0], I[0], R[0], D[0]]
+    win = eng.Window(ctx, I, R, D, init, N, "ird-mxse")
+    lo, hi = np.zeros(6), np.array([2, 2, 28, 28, 1, 0.1])
+    costs, params, deaths = win.forecast_ensemble(lo, hi, seed=2204, n=300, horizon=21)
+    for k in range(0, 300, 11):
+        u = port.uniform01(port.mix_seed(2204, k), 6)
+        x = lo + u * (hi - lo)
+        if x[2] > x[3]:
+            x[2], x[3] = x[3], x[2]
+        assert_bitwise(params[k], x, f"sample {k}")
+        c = port.eval_costs("ird-mxse", I, R, D, init, N, x[None, :])
+        assert_bitwise(costs[k:k + 1], c, f"cost {k}")
+        st, fin = port.integrate(x, init, N, 36)
+        if fin:
+            fc, ff = port.forecast(x, st[-1], N, 21)
+            if ff:
+                assert_bitwise(deaths[k], fc[:, 3], f"forecast {k}")
+                continue
+        assert np.all(np.isnan(deaths[k]))
