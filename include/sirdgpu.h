@@ -110,6 +110,11 @@ int sg_eval_costs_device(sg_window* window, const double* d_positions, size_t n,
 int sg_integrate_batch(sg_ctx* ctx, const double* params, size_t n, sg_state init, double population,
                        int n_days, int substeps, double* states, uint8_t* finite);
 
+/* Same with one initial state per item (inits: n states), as fit_window's
+ * final re-integration of every fitted window needs (calibration.cpp:175-176). */
+int sg_integrate_states(sg_ctx* ctx, const double* params, const sg_state* inits, size_t n, double population,
+                        int n_days, int substeps, double* states, uint8_t* finite);
+
 /* --- boundary 2: the particle swarm --------------------------------------
  * One descriptor per independent swarm (Swarm::Swarm + optimize,
  * pso.cpp:47-143).  Swarms may use different windows, sizes and seeds;
@@ -148,8 +153,13 @@ int sg_fit_swarms(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg_
 typedef struct sg_plan sg_plan;
 int sg_plan_create(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg_plan** out);
 int sg_plan_run(sg_plan* plan);
+/* Same as sg_plan_run, synchronous, and reports device time measured with
+ * CUDA events on the context stream: *seed_ms for the engine-seeding
+ * launches, *steps_ms for all fused step launches (max_iters per group). */
+int sg_plan_run_timed(sg_plan* plan, double* seed_ms, double* steps_ms);
 int sg_plan_results(sg_plan* plan, sg_swarm_result* results);
 uint64_t sg_plan_evals(const sg_plan* plan);  /* sum of n_particles * max_iters */
+uint64_t sg_plan_step_launches(const sg_plan* plan);  /* fused step launches per run */
 void sg_plan_destroy(sg_plan* plan);
 
 /* --- forecast ---------------------------------------------------------------
@@ -170,6 +180,62 @@ int sg_forecast_batch(sg_ctx* ctx, const double* params, const sg_state* junctio
  * NaN rows for sets whose window or forecast blew up). */
 int sg_forecast_ensemble(sg_window* window, const double lower[6], const double upper[6], uint64_t seed,
                          size_t n, int horizon, double* costs, double* params_out, double* deaths_out);
+
+/* --- calibration layer (C++ host side, src: csrc/host_api.cpp) --------------
+ * The reference's window scheduler / restart driver as C entry points, for
+ * bindings (Python, CLI).  They run the C++ API of include/sirdfit_b200.hpp
+ * on the given context.  Series are the cleaned EpiSeries columns
+ * (timeseries.hpp:37-46) of n_series days. */
+typedef struct sg_fit_settings {  /* FitSettings (calibration.hpp:58-65) */
+    int family, metric;           /* ObjectiveSpec                            */
+    double beta_lo, beta_hi, gamma_lo, gamma_hi, mu_lo, mu_hi;  /* ParamBounds */
+    uint64_t t_margin;
+    uint64_t n_particles, max_iters;  /* PsoConfig                            */
+    double inertia, cognitive, social;
+    double population;
+    int substeps;
+} sg_fit_settings;
+
+typedef struct sg_fit_record {    /* FitResult (calibration.hpp:67-76)        */
+    uint64_t index, start, length;
+    double params[6];             /* beta1, beta2, t1, t2, gamma, mu          */
+    double objective;
+    double r2_d;
+    int ok;
+    int status;                   /* sg_status of the failure (0 when ok)     */
+    char failure[192];            /* FitResult::failure (truncated)           */
+} sg_fit_record;
+
+/* fit_window (calibration.cpp:157-188).  Returns the status of the exception
+ * the reference would throw (record->failure holds its message).
+ * trajectory: length x 4 doubles or NULL; history: max_iters doubles or NULL. */
+int sg_fit_window_series(sg_ctx* ctx, const double* infectious, const double* recovered_cum,
+                         const double* deaths_cum, size_t n_series, uint64_t start, uint64_t length,
+                         const sg_fit_settings* settings, uint64_t seed, sg_fit_record* record, double* trajectory,
+                         double* history);
+
+/* fit_all_windows (calibration.cpp:190-216): window w is fitted with seed
+ * mix_seed(base_seed, w); failures are recorded per window.  records holds
+ * max_windows entries, trajectories (optional) max_windows x (tau+1) x 4.
+ * Returns SG_ERR_SCHEME when make_windows throws. */
+int sg_fit_all_windows_series(sg_ctx* ctx, const double* infectious, const double* recovered_cum,
+                              const double* deaths_cum, size_t n_series, uint64_t tau, uint64_t delta,
+                              const sg_fit_settings* settings, uint64_t base_seed, size_t max_windows,
+                              size_t* n_windows, sg_fit_record* records, double* trajectories, double* mean_r2_d,
+                              size_t* failed_count);
+
+/* stability_study (calibration.cpp:378-436): repetitions fits of one window
+ * (seeds mix_seed(base_seed, rep)) + forecast_extension(horizon).
+ * records: repetitions entries.  day_bands: 5 blocks (beta, r0: length days;
+ * infectious, recovered, deaths: length + horizon days), each block 7 rows
+ * (median, p50_lo, p50_hi, p90_lo, p90_hi, p95_lo, p95_hi) of its days,
+ * laid out consecutively; day_counts: the per-day sample counts of the same
+ * 5 blocks; scalar_bands: gamma then mu, 7 values each; scalar_counts: 2. */
+int sg_stability_study_series(sg_ctx* ctx, const double* infectious, const double* recovered_cum,
+                              const double* deaths_cum, size_t n_series, uint64_t start, uint64_t length,
+                              const sg_fit_settings* settings, uint64_t repetitions, uint64_t horizon,
+                              uint64_t base_seed, sg_fit_record* records, double* day_bands, uint64_t* day_counts,
+                              double* scalar_bands, uint64_t* scalar_counts, uint64_t* failed);
 
 /* --- diagnostics -----------------------------------------------------------
  * Measured FP64 issue rate of this device: a kernel of independent

@@ -241,6 +241,136 @@ def gen_forecast(ref, poland: dict) -> dict:
     return data
 
 
+def _hex(a):
+    return [float(x).hex() for x in np.asarray(a, dtype=np.float64).ravel()]
+
+
+def synthetic_series(ref, params, n_days, N=1e6, i0=100.0):
+    """tests/synthetic.hpp:22-49: the model's own trajectory as the series."""
+    st, _ = ref.integrate(params, [N - i0, i0, 0, 0], N, n_days)
+    return st[:, 1].copy(), st[:, 2].copy(), st[:, 3].copy()
+
+
+STAGE_BOUNDS7 = {1: [0, 10, 0, 10, 0, 10, 0], 2: [0, 2, 0, 1, 0, 0.1, 7]}
+
+
+def gen_calibration(ref, poland: dict) -> dict:
+    """fit_window / fit_all_windows / stability_study / forecast_extension
+    of the reference on small cases (calibration.cpp:157-436)."""
+    dp = op._dp
+    out = {"fit_window": [], "fit_all_windows": [], "stability": []}
+
+    def arr(x):
+        return np.ascontiguousarray(x, dtype=np.float64)
+
+    fw_cases = []
+    I, R, D = synthetic_series(ref, [0.6, 0.6, 0, 0, 0.09, 0.01], 25)
+    fw_cases.append(("appendixA", I, R, D, 0, 21, "ird-mxse", 2, 1e6, 64, 10, 1, 21))
+    fw_cases.append(("poland_c1_small", poland["I"], poland["R"], poland["D"], 0, 21, "ird-mxse", 2, POLAND_N, 256,
+                     50, 1, 21))
+    fw_cases.append(("poland_w100_dmape", poland["I"], poland["R"], poland["D"], 300, 36, "d-mape", 2, POLAND_N,
+                     200, 20, 7, 21))
+    fw_cases.append(("poland_stage1", poland["I"], poland["R"], poland["D"], 150, 36, "ird-mae", 1, POLAND_N, 100,
+                     15, 3, 10))
+    z = np.zeros(15)
+    fw_cases.append(("zeros", z, z, z, 0, 15, "d-mse", 2, 1000.0, 50, 5, 3, 5))
+    fw_cases.append(("too_small_population", I, R, D, 0, 21, "ird-mse", 2, 10.0, 30, 5, 4, 5))
+    fw_cases.append(("window_outside", I, R, D, 10, 21, "ird-mse", 2, 1e6, 30, 5, 4, 5))
+    fw_cases.append(("margin_too_big", I, R, D, 0, 5, "ird-mse", 2, 1e6, 30, 5, 4, 5))
+    fw_cases.append(("all_infeasible", z, z, z, 0, 15, "ird-mape", 2, 1000.0, 33, 4, 4, 5))
+    for name, I, R, D, start, length, spec, stage, N, n, iters, seed, horizon in fw_cases:
+        fam, met = op.parse_spec(spec)
+        I, R, D = arr(I), arr(R), arr(D)
+        b7 = arr(STAGE_BOUNDS7[stage])
+        best, obj, r2, fin = np.zeros(6), np.zeros(1), np.zeros(1), ctypes_int()
+        traj = np.zeros((length, 4))
+        rc = ref.lib.ref_fit_window(I.ctypes.data_as(dp), R.ctypes.data_as(dp), D.ctypes.data_as(dp), len(I), start,
+                                    length, fam, met, b7.ctypes.data_as(dp), N, 24, 1, n, iters, 0.5, 0.5, 0.5, seed,
+                                    best.ctypes.data_as(dp), obj.ctypes.data_as(dp), r2.ctypes.data_as(dp),
+                                    traj.ctypes.data_as(dp), fin)
+        rec = dict(name=name, I=_hex(I), R=_hex(R), D=_hex(D), start=start, length=length, spec=spec, stage=stage,
+                   N=N, n=n, iters=iters, seed=seed, horizon=horizon, status=rc)
+        if rc == 0:
+            fc = np.zeros((horizon + 1, 4))
+            frc = ref.lib.ref_fit_window_forecast(I.ctypes.data_as(dp), R.ctypes.data_as(dp), D.ctypes.data_as(dp),
+                                                  len(I), start, length, fam, met, b7.ctypes.data_as(dp), N, 24, n,
+                                                  iters, seed, horizon, fc.ctypes.data_as(dp))
+            rec.update(params=_hex(best), objective=float(obj[0]).hex(), r2=float(r2[0]).hex(),
+                       trajectory=_hex(traj), forecast_status=frc, forecast=_hex(fc) if frc == 0 else None)
+        else:
+            rec["error"] = ref.lib.ref_last_error().decode()
+        out["fit_window"].append(rec)
+
+    fa_cases = []
+    I, R, D = synthetic_series(ref, [0.5, 0.3, 5.0, 12.0, 0.1, 0.02], 31)
+    fa_cases.append(("test_calibration_seeded", I, R, D, 14, 8, "ird-mxse", 2, 1e6, 150, 40, 11))
+    I2, R2, D2 = synthetic_series(ref, [0.5, 0.5, 0, 0, 0.1, 0.02], 31, i0=500.0)
+    I2 = I2.copy()
+    I2[14:] = 2e6  # test_calibration.cpp:255-275: the third window covers the flood
+    fa_cases.append(("population_flood", I2, R2, D2, 10, 7, "ird-mxse", 2, 1e6, 60, 10, 5))
+    fa_cases.append(("poland_first_120d", poland["I"][:120], poland["R"][:120], poland["D"][:120], 35, 3, "ird-mse",
+                     2, POLAND_N, 64, 20, 2204))
+    for name, I, R, D, tau, delta, spec, stage, N, n, iters, seed in fa_cases:
+        fam, met = op.parse_spec(spec)
+        I, R, D = arr(I), arr(R), arr(D)
+        b7 = arr(STAGE_BOUNDS7[stage])
+        mw = 64
+        nw, failed = (ctypes_size(), ctypes_size())
+        ok = np.zeros(mw, dtype=np.int32)
+        best, obj, r2, mean = np.zeros(6 * mw), np.zeros(mw), np.zeros(mw), np.zeros(1)
+        rc = ref.lib.ref_fit_all_windows(I.ctypes.data_as(dp), R.ctypes.data_as(dp), D.ctypes.data_as(dp), len(I),
+                                         tau, delta, fam, met, b7.ctypes.data_as(dp), N, 24, 1, n, iters, 0.5, 0.5,
+                                         0.5, seed, mw, nw, ok.ctypes.data_as(op._ip), best.ctypes.data_as(dp),
+                                         obj.ctypes.data_as(dp), r2.ctypes.data_as(dp), mean.ctypes.data_as(dp), failed)
+        assert rc == 0, name
+        k = nw.value
+        out["fit_all_windows"].append(dict(
+            name=name, I=_hex(I), R=_hex(R), D=_hex(D), tau=tau, delta=delta, spec=spec, stage=stage, N=N, n=n,
+            iters=iters, seed=seed, n_windows=k, ok=ok[:k].tolist(), params=_hex(best[:6 * k]), objective=_hex(obj[:k]),
+            r2=_hex(r2[:k]), mean_r2=float(mean[0]).hex(), failed=failed.value))
+
+    st_cases = []
+    I, R, D = synthetic_series(ref, [0.5, 0.4, 2.0, 6.0, 0.1, 0.02], 31)
+    st_cases.append(("one_repetition", I, R, D, 5, 11, "ird-mxse", 2, 1e6, 120, 30, 1, 4, 99))
+    st_cases.append(("seven_repetitions", I, R, D, 5, 11, "d-mse", 2, 1e6, 80, 25, 7, 6, 901))
+    I3, R3, D3 = synthetic_series(ref, [0.5, 0.5, 0, 0, 0.1, 0.02], 20)
+    st_cases.append(("population_too_small", I3, R3, D3, 0, 11, "ird-mxse", 2, 1.0, 30, 5, 3, 2, 1))
+    st_cases.append(("poland_last_window", poland["I"], poland["R"], poland["D"], 414, 36, "ird-mxse", 2, POLAND_N,
+                     64, 15, 5, 21, 2204))
+    for name, I, R, D, start, length, spec, stage, N, n, iters, reps, horizon, seed in st_cases:
+        fam, met = op.parse_spec(spec)
+        I, R, D = arr(I), arr(R), arr(D)
+        b7 = arr(STAGE_BOUNDS7[stage])
+        sizes = [length, length, length + horizon, length + horizon, length + horizon]
+        ok = np.zeros(reps, dtype=np.int32)
+        params, obj = np.zeros(6 * reps), np.zeros(reps)
+        bands, counts = np.zeros(7 * sum(sizes)), np.zeros(sum(sizes), dtype=np.uint64)
+        sc, scc, failed = np.zeros(14), np.zeros(2, dtype=np.uint64), np.zeros(1, dtype=np.uint64)
+        u64 = lambda a: a.ctypes.data_as(op._u64p)  # noqa: E731
+        rc = ref.lib.ref_stability_study(I.ctypes.data_as(dp), R.ctypes.data_as(dp), D.ctypes.data_as(dp), len(I),
+                                         start, length, fam, met, b7.ctypes.data_as(dp), N, 24, n, iters, 0.5, 0.5,
+                                         0.5, reps, horizon, seed, ok.ctypes.data_as(op._ip),
+                                         params.ctypes.data_as(dp), obj.ctypes.data_as(dp), bands.ctypes.data_as(dp),
+                                         u64(counts), sc.ctypes.data_as(dp), u64(scc), u64(failed))
+        assert rc == 0, name
+        out["stability"].append(dict(
+            name=name, I=_hex(I), R=_hex(R), D=_hex(D), start=start, length=length, spec=spec, stage=stage, N=N, n=n,
+            iters=iters, reps=reps, horizon=horizon, seed=seed, ok=ok.tolist(), params=_hex(params),
+            objective=_hex(obj), day_bands=_hex(bands), day_counts=counts.astype(int).tolist(), scalar_bands=_hex(sc),
+            scalar_counts=scc.astype(int).tolist(), failed=int(failed[0])))
+    return out
+
+
+def ctypes_int():
+    import ctypes
+    return ctypes.byref(ctypes.c_int(0))
+
+
+def ctypes_size():
+    import ctypes
+    return ctypes.c_size_t(0)
+
+
 def gen_kat(ref) -> dict:
     return {
         "mix_seed": [[b, i, ref.mix_seed(b, i)] for b, i in ((0, 0), (1, 0), (1, 1), (2204, 7),
@@ -264,6 +394,7 @@ def main() -> None:
     np.savez_compressed(GOLDEN / "costs.npz", **gen_costs(ref, poland))
     (GOLDEN / "fits.json").write_text(json.dumps(gen_fits(ref, poland), indent=1))
     np.savez_compressed(GOLDEN / "forecast.npz", **gen_forecast(ref, poland))
+    (GOLDEN / "calibration.json").write_text(json.dumps(gen_calibration(ref, poland)))
     print("wrote", sorted(p.name for p in GOLDEN.iterdir()))
 
 

@@ -82,6 +82,15 @@ class Oracle:
                                                 _szp, _ip, _dp, _dp, _dp, _dp, _szp]
             lib.ref_clean_series.argtypes = [_dp, _dp, _dp, ctypes.c_size_t, ctypes.c_int, _dp, _dp, _dp, _dp]
             lib.ref_quantile_bands.argtypes = [_dp, ctypes.c_size_t, ctypes.c_size_t, _dp, _szp]
+            lib.ref_stability_study.argtypes = [_dp, _dp, _dp, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t,
+                                                ctypes.c_int, ctypes.c_int, _dp, ctypes.c_double, ctypes.c_int,
+                                                ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
+                                                ctypes.c_double, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                                _ip, _dp, _dp, _dp, _u64p, _dp, _u64p, _u64p]
+            lib.ref_fit_window_forecast.argtypes = [_dp, _dp, _dp, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t,
+                                                    ctypes.c_int, ctypes.c_int, _dp, ctypes.c_double, ctypes.c_int,
+                                                    ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                                    ctypes.c_uint64, _dp]
 
     # -- streams --------------------------------------------------------------
     def mix_seed(self, base: int, index: int) -> int:

@@ -256,6 +256,88 @@ int ref_fit_all_windows(const double* I, const double* R, const double* D, size_
     }
 }
 
+// stability_study (calibration.cpp:378-436) in the layout of
+// sg_stability_study_series (include/sirdgpu.h): per repetition ok/params/
+// objective; 5 day-band blocks x 7 rows; day counts; gamma/mu scalar bands.
+int ref_stability_study(const double* I, const double* R, const double* D, size_t n_series, size_t start,
+                        size_t length, int family, int metric, const double* bounds7, double population,
+                        int substeps, uint64_t n_particles, uint64_t max_iters, double inertia, double cognitive,
+                        double social, uint64_t repetitions, uint64_t horizon, uint64_t base_seed, int* ok,
+                        double* params, double* objective, double* day_bands, uint64_t* day_counts,
+                        double* scalar_bands, uint64_t* scalar_counts, uint64_t* failed) {
+    try {
+        const EpiSeries epi = series_of(I, R, D, n_series);
+        FitSettings settings;
+        settings.spec = spec_of(family, metric);
+        settings.bounds = ParamBounds{.beta_lo = bounds7[0], .beta_hi = bounds7[1], .gamma_lo = bounds7[2],
+                                      .gamma_hi = bounds7[3], .mu_lo = bounds7[4], .mu_hi = bounds7[5],
+                                      .t_margin = static_cast<std::size_t>(bounds7[6])};
+        settings.population = population;
+        settings.substeps = substeps;
+        settings.pso.n_particles = n_particles;
+        settings.pso.max_iters = max_iters;
+        settings.pso.inertia = inertia;
+        settings.pso.cognitive = cognitive;
+        settings.pso.social = social;
+        const StabilityResult st = stability_study(epi, Window{.index = 0, .start = start, .length = length},
+                                                   settings, repetitions, horizon, base_seed);
+        for (std::size_t r = 0; r < st.fits.size(); ++r) {
+            const FitResult& f = st.fits[r];
+            ok[r] = f.ok ? 1 : 0;
+            const double p[6] = {f.params.beta1, f.params.beta2, f.params.t1, f.params.t2, f.params.gamma, f.params.mu};
+            std::memcpy(params + 6 * r, p, sizeof p);
+            objective[r] = f.objective;
+        }
+        double* out = day_bands;
+        uint64_t* cnt = day_counts;
+        for (const QuantileBands* b : {&st.beta, &st.r0, &st.infectious, &st.recovered, &st.deaths}) {
+            const std::size_t n = b->days();
+            for (const std::vector<double>* v : {&b->median, &b->p50_lo, &b->p50_hi, &b->p90_lo, &b->p90_hi,
+                                                 &b->p95_lo, &b->p95_hi}) {
+                std::copy(v->begin(), v->end(), out);
+                out += n;
+            }
+            for (std::size_t d = 0; d < n; ++d) *cnt++ = b->count[d];
+        }
+        const ScalarBands* sb[2] = {&st.gamma, &st.mu};
+        for (int k = 0; k < 2; ++k) {
+            const double v[7] = {sb[k]->median, sb[k]->p50_lo, sb[k]->p50_hi, sb[k]->p90_lo,
+                                 sb[k]->p90_hi, sb[k]->p95_lo, sb[k]->p95_hi};
+            std::copy(v, v + 7, scalar_bands + 7 * k);
+            scalar_counts[k] = sb[k]->count;
+        }
+        *failed = st.failed;
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// forecast_extension (calibration.cpp:298-322) of a fit_window result.
+int ref_fit_window_forecast(const double* I, const double* R, const double* D, size_t n_series, size_t start,
+                            size_t length, int family, int metric, const double* bounds7, double population,
+                            int substeps, uint64_t n_particles, uint64_t max_iters, uint64_t seed, uint64_t horizon,
+                            double* states) {
+    try {
+        const EpiSeries epi = series_of(I, R, D, n_series);
+        FitSettings settings;
+        settings.spec = spec_of(family, metric);
+        settings.bounds = ParamBounds{.beta_lo = bounds7[0], .beta_hi = bounds7[1], .gamma_lo = bounds7[2],
+                                      .gamma_hi = bounds7[3], .mu_lo = bounds7[4], .mu_hi = bounds7[5],
+                                      .t_margin = static_cast<std::size_t>(bounds7[6])};
+        settings.population = population;
+        settings.substeps = substeps;
+        settings.pso.n_particles = n_particles;
+        settings.pso.max_iters = max_iters;
+        const FitResult fit = fit_window(epi, Window{.index = 0, .start = start, .length = length}, settings, seed);
+        const Forecast fc = forecast_extension(fit, horizon, substeps);
+        write_states(fc.trajectory, states);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
 // Cleaning pipeline for fixture generation: build_epi_series then smooth7
 // (timeseries.cpp:127-179).  Raw rows are daily (no gaps), cumulative.
 // Output columns have n values each.

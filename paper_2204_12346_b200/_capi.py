@@ -51,6 +51,25 @@ class sg_swarm_result(ctypes.Structure):
     ]
 
 
+class sg_fit_settings(ctypes.Structure):
+    _fields_ = [("family", ctypes.c_int), ("metric", ctypes.c_int),
+                ("beta_lo", ctypes.c_double), ("beta_hi", ctypes.c_double),
+                ("gamma_lo", ctypes.c_double), ("gamma_hi", ctypes.c_double),
+                ("mu_lo", ctypes.c_double), ("mu_hi", ctypes.c_double),
+                ("t_margin", ctypes.c_uint64), ("n_particles", ctypes.c_uint64), ("max_iters", ctypes.c_uint64),
+                ("inertia", ctypes.c_double), ("cognitive", ctypes.c_double), ("social", ctypes.c_double),
+                ("population", ctypes.c_double), ("substeps", ctypes.c_int)]
+
+
+class sg_fit_record(ctypes.Structure):
+    _fields_ = [("index", ctypes.c_uint64), ("start", ctypes.c_uint64), ("length", ctypes.c_uint64),
+                ("params", ctypes.c_double * 6), ("objective", ctypes.c_double), ("r2_d", ctypes.c_double),
+                ("ok", ctypes.c_int), ("status", ctypes.c_int), ("failure", ctypes.c_char * 192)]
+
+
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+_szp = ctypes.POINTER(ctypes.c_size_t)
+
 # Every symbol include/sirdgpu.h declares, with its ctypes signature.
 SIGNATURES = {
     "sg_abi_version": (ctypes.c_int, []),
@@ -72,10 +91,25 @@ SIGNATURES = {
     "sg_plan_create": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(sg_swarm_desc), ctypes.c_size_t,
                                       ctypes.POINTER(ctypes.c_void_p)]),
     "sg_plan_run": (ctypes.c_int, [ctypes.c_void_p]),
+    "sg_plan_run_timed": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp]),
+    "sg_plan_step_launches": (ctypes.c_uint64, [ctypes.c_void_p]),
     "sg_plan_results": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(sg_swarm_result)]),
     "sg_plan_evals": (ctypes.c_uint64, [ctypes.c_void_p]),
     "sg_plan_destroy": (None, [ctypes.c_void_p]),
     "sg_probe_fp64_rate": (ctypes.c_int, [ctypes.c_void_p, _dp]),
+    "sg_integrate_states": (ctypes.c_int, [ctypes.c_void_p, _dp, ctypes.POINTER(sg_state), ctypes.c_size_t,
+                                           ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp, _u8p]),
+    "sg_fit_window_series": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, ctypes.c_size_t, ctypes.c_uint64,
+                                            ctypes.c_uint64, ctypes.POINTER(sg_fit_settings), ctypes.c_uint64,
+                                            ctypes.POINTER(sg_fit_record), _dp, _dp]),
+    "sg_fit_all_windows_series": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, ctypes.c_size_t, ctypes.c_uint64,
+                                                 ctypes.c_uint64, ctypes.POINTER(sg_fit_settings), ctypes.c_uint64,
+                                                 ctypes.c_size_t, _szp, ctypes.POINTER(sg_fit_record), _dp, _dp,
+                                                 _szp]),
+    "sg_stability_study_series": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, ctypes.c_size_t, ctypes.c_uint64,
+                                                 ctypes.c_uint64, ctypes.POINTER(sg_fit_settings), ctypes.c_uint64,
+                                                 ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(sg_fit_record),
+                                                 _dp, _u64p, _dp, _u64p, _u64p]),
     "sg_forecast_batch": (ctypes.c_int, [ctypes.c_void_p, _dp, ctypes.POINTER(sg_state), ctypes.c_size_t,
                                          ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp, _u8p]),
     "sg_forecast_ensemble": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, ctypes.c_uint64, ctypes.c_size_t,
@@ -304,6 +338,16 @@ class Plan:
 
     def run(self) -> None:
         self.ctx.check(lib().sg_plan_run(self._h))
+
+    def run_timed(self) -> tuple[float, float]:
+        """Synchronous run; returns (seed_ms, steps_ms) from CUDA events on the context stream."""
+        a, b = ctypes.c_double(), ctypes.c_double()
+        self.ctx.check(lib().sg_plan_run_timed(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    @property
+    def step_launches(self) -> int:
+        return int(lib().sg_plan_step_launches(self._h))
 
     def results(self):
         n = len(self.swarms)

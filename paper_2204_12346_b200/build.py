@@ -19,7 +19,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 SOURCES = [CSRC / "engine.cu", CSRC / "host_api.cpp"]
-HEADERS = [CSRC / "sird_device.cuh", CSRC / "kernels.cuh", ROOT / "include" / "sirdgpu.h",
+HEADERS = [CSRC / "sird_device.cuh", CSRC / "kernels.cuh", CSRC / "engine_internal.h", ROOT / "include" / "sirdgpu.h",
            ROOT / "include" / "sirdfit_b200.hpp"]
 OUT = PKG / "libsirdgpu.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

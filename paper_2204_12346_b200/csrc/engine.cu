@@ -7,6 +7,7 @@
 // is produced by the kernels in kernels.cuh.
 #include "sirdgpu.h"
 
+#include "engine_internal.h"
 #include "kernels.cuh"
 
 #include <cuda_runtime.h>
@@ -90,6 +91,10 @@ double compartment_scale(const double* obs, int n) {
     return range > 0.0 ? 1.0 / range : 1.0 / std::max(1.0, std::fabs(*lo));
 }
 
+// Kernel specialisation of a window: 24 = the reference default substep count
+// with the t_k table in shared memory; 0 = generic runtime substeps.
+int kernel_sub(int n_days, int substeps) { return uses_fast_grid(n_days, substeps) ? 24 : 0; }
+
 bool valid_spec(int family, int metric) {
     return (family == SG_FAMILY_D_ONLY || family == SG_FAMILY_IRD_JOINT) && metric >= SG_METRIC_MXSE &&
            metric <= SG_METRIC_MAPE;
@@ -98,7 +103,7 @@ bool valid_spec(int family, int metric) {
 // ---- template dispatch over (family, metric, substeps == 24) ------------------
 template <template <int, int, int> class K, class... Args>
 void dispatch(int family, int metric, int substeps, Args&&... args) {
-    const bool s24 = substeps == 24;
+    const bool s24 = substeps == 24;  // callers pass 0 when the window is too long for the table
 #define SG_CASE(F, M)                                              \
     if (family == F && metric == M) {                              \
         if (s24) K<F, M, 24>::run(std::forward<Args>(args)...);    \
@@ -163,8 +168,8 @@ struct EnsembleLaunch {
 int launch_integrate(sg_ctx* ctx, const DevWindow& w, const double* d_params, const double* d_init, int init_stride,
                      int hold, size_t n, double* d_states, unsigned char* d_fin) {
     const unsigned grid = static_cast<unsigned>((n + kEvalThreads - 1) / kEvalThreads);
-    const size_t smem = static_cast<size_t>(w.substeps) * sizeof(double);
-    if (w.substeps == 24) {
+    const size_t smem = static_cast<size_t>(w.substeps + tgrid_entries(w.n_days, w.substeps)) * sizeof(double);
+    if (uses_fast_grid(w.n_days, w.substeps)) {
         integrate_kernel<24><<<grid, kEvalThreads, smem, ctx->stream>>>(w, d_params, d_init, init_stride, hold, n,
                                                                         d_states, d_fin);
     } else {
@@ -240,6 +245,14 @@ void sg_ctx_destroy(sg_ctx* ctx) {
 }
 
 const char* sg_last_error(const sg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+}  // extern "C"
+
+void sg_set_last_error(sg_ctx* ctx, const std::string& message) {
+    if (ctx) ctx->err = message;
+}
+
+extern "C" {
 
 uint64_t sg_ctx_launch_count(const sg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
@@ -332,7 +345,7 @@ int sg_eval_costs_device(sg_window* w, const double* d_positions, size_t n, doub
     if (!d_positions || !d_costs) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null device buffer");
     cudaStream_t st = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->stream;
     cudaError_t err = cudaSuccess;
-    dispatch<EvalLaunch>(w->host.family, w->host.metric, w->host.substeps, w->d_desc, d_positions, n, d_costs,
+    dispatch<EvalLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc, d_positions, n, d_costs,
                          w->smem, st, &err);
     ctx->launches += 1;
     if (err != cudaSuccess) return cuda_fail(ctx, err, "eval_costs_kernel");
@@ -386,6 +399,34 @@ int sg_integrate_batch(sg_ctx* ctx, const double* params, size_t n, sg_state ini
     SG_CUDA(ctx, cudaMemcpyAsync(d_init, s0, sizeof s0, cudaMemcpyHostToDevice, ctx->stream));
     const DevWindow w = integration_window(n_days, substeps, population);
     const int rc = launch_integrate(ctx, w, d_p, d_init, 0, 0, n, d_states, d_fin);
+    if (rc) return rc;
+    SG_CUDA(ctx, cudaMemcpyAsync(states, d_states, sizeof(double) * n * n_days * 4, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    SG_CUDA(ctx, cudaMemcpyAsync(finite, d_fin, n, cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SG_OK;
+}
+
+int sg_integrate_states(sg_ctx* ctx, const double* params, const sg_state* inits, size_t n, double population,
+                        int n_days, int substeps, double* states, uint8_t* finite) {
+    if (!ctx) return SG_ERR_INVALID_ARGUMENT;
+    if (n_days < 1 || substeps < 1 || !(population > 0.0))
+        return fail(ctx, SG_ERR_INVALID_ARGUMENT,
+                    "integrate_euler needs n_days >= 1, substeps >= 1 and a positive population");
+    if (n == 0) return SG_OK;
+    if (!params || !inits || !states || !finite) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null host buffer");
+    SG_CUDA(ctx, cudaSetDevice(ctx->device));
+    DevBufs b;
+    double *d_p, *d_init, *d_states;
+    unsigned char* d_fin;
+    SG_CUDA(ctx, b.alloc(&d_p, 6 * n));
+    SG_CUDA(ctx, b.alloc(&d_init, 4 * n));
+    SG_CUDA(ctx, b.alloc(&d_states, n * static_cast<size_t>(n_days) * 4));
+    SG_CUDA(ctx, b.alloc(&d_fin, n));
+    SG_CUDA(ctx, cudaMemcpyAsync(d_p, params, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, cudaMemcpyAsync(d_init, inits, sizeof(double) * 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+    const DevWindow w = integration_window(n_days, substeps, population);
+    const int rc = launch_integrate(ctx, w, d_p, d_init, 4, 0, n, d_states, d_fin);
     if (rc) return rc;
     SG_CUDA(ctx, cudaMemcpyAsync(states, d_states, sizeof(double) * n * n_days * 4, cudaMemcpyDeviceToHost,
                                  ctx->stream));
@@ -548,15 +589,19 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     return SG_OK;
 }
 
-int run_group(sg_ctx* ctx, SwarmGroup& g) {
-    cudaStream_t st = ctx->stream;
-    pso_init_kernel<<<static_cast<unsigned>(g.n_ctas), kStepThreads, 0, st>>>(g.d_sw, g.d_cta, g.P, g.d_state);
+int seed_group(sg_ctx* ctx, SwarmGroup& g) {
+    pso_init_kernel<<<static_cast<unsigned>(g.n_ctas), kStepThreads, 0, ctx->stream>>>(g.d_sw, g.d_cta, g.P,
+                                                                                      g.d_state);
     ctx->launches += 1;
     SG_CUDA(ctx, cudaGetLastError());
+    return SG_OK;
+}
+
+int step_group(sg_ctx* ctx, SwarmGroup& g) {
     for (uint64_t it = 0; it < g.iters; ++it) {
         cudaError_t err = cudaSuccess;
         dispatch<StepLaunch>(g.family, g.metric, g.substeps, static_cast<unsigned>(g.n_ctas), g.d_sw, g.d_cta,
-                             g.d_win, g.P, g.d_state, it, g.smem, st, &err);
+                             g.d_win, g.P, g.d_state, it, g.smem, ctx->stream, &err);
         ctx->launches += 1;
         if (err != cudaSuccess) return cuda_fail(ctx, err, "pso_step_kernel");
     }
@@ -590,7 +635,7 @@ int sg_plan_create(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg
             continue;
         }
         const DevWindow& w = swarms[k].window->host;
-        const int sub = w.substeps == 24 ? 24 : 0;
+        const int sub = kernel_sub(w.n_days, w.substeps);
         SwarmGroup* g = nullptr;
         for (SwarmGroup* x : plan->groups)
             if (x->family == w.family && x->metric == w.metric && x->substeps == sub) g = x;
@@ -624,11 +669,52 @@ int sg_plan_run(sg_plan* plan) {
     sg_ctx* ctx = plan->ctx;
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     for (SwarmGroup* g : plan->groups) {
-        const int rc = run_group(ctx, *g);
+        int rc = seed_group(ctx, *g);
+        if (!rc) rc = step_group(ctx, *g);
         if (rc) return rc;
     }
     plan->ran = true;
     return SG_OK;
+}
+
+int sg_plan_run_timed(sg_plan* plan, double* seed_ms, double* steps_ms) {
+    if (!plan || !seed_ms || !steps_ms) return SG_ERR_INVALID_ARGUMENT;
+    sg_ctx* ctx = plan->ctx;
+    SG_CUDA(ctx, cudaSetDevice(ctx->device));
+    cudaEvent_t ev[3];
+    for (cudaEvent_t& e : ev) SG_CUDA(ctx, cudaEventCreate(&e));
+    *seed_ms = 0.0;
+    *steps_ms = 0.0;
+    int rc = SG_OK;
+    for (SwarmGroup* g : plan->groups) {
+        cudaEventRecord(ev[0], ctx->stream);
+        rc = seed_group(ctx, *g);
+        if (rc) break;
+        cudaEventRecord(ev[1], ctx->stream);
+        rc = step_group(ctx, *g);
+        if (rc) break;
+        cudaEventRecord(ev[2], ctx->stream);
+        const cudaError_t e = cudaEventSynchronize(ev[2]);
+        if (e != cudaSuccess) {
+            rc = cuda_fail(ctx, e, "sg_plan_run_timed");
+            break;
+        }
+        float a = 0.f, b = 0.f;
+        cudaEventElapsedTime(&a, ev[0], ev[1]);
+        cudaEventElapsedTime(&b, ev[1], ev[2]);
+        *seed_ms += a;
+        *steps_ms += b;
+    }
+    for (cudaEvent_t& e : ev) cudaEventDestroy(e);
+    if (!rc) plan->ran = true;
+    return rc;
+}
+
+uint64_t sg_plan_step_launches(const sg_plan* plan) {
+    uint64_t n = 0;
+    if (plan)
+        for (const SwarmGroup* g : plan->groups) n += g->iters;
+    return n;
 }
 
 int sg_plan_results(sg_plan* plan, sg_swarm_result* results) {
@@ -727,7 +813,7 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
     SG_CUDA(ctx, cudaMemcpyAsync(d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     DevWindow fwin = integration_window(horizon + 1, w->host.substeps, w->host.N);
     cudaError_t err = cudaSuccess;
-    dispatch<EnsembleLaunch>(w->host.family, w->host.metric, w->host.substeps, w->d_desc, fwin, d_lo, d_hi, seed, n,
+    dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc, fwin, d_lo, d_hi, seed, n,
                              horizon, d_cost, d_par, d_D, w->smem, ctx->stream, &err);
     ctx->launches += 1;
     if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");

@@ -1,0 +1,10 @@
+// engine_internal.h — engine functions shared by engine.cu and host_api.cpp
+// that are not part of the public C-ABI.
+#pragma once
+
+#include "sirdgpu.h"
+
+#include <string>
+
+// Sets the text sg_last_error(ctx) returns.
+void sg_set_last_error(sg_ctx* ctx, const std::string& message);

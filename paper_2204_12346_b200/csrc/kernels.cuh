@@ -22,23 +22,42 @@ constexpr int kEvalThreads = 128;
 constexpr int kStepThreads = 128;
 
 // Shared-memory staging of one window: the descriptor in static shared memory,
-// obs + subh (+ robs + flags for MAPE) in the dynamic segment.
+// obs, the substep-time tables (+ robs + flags for MAPE) in the dynamic segment.
 struct SmemWindow {
     const DevWindow* w;  // shared memory
     const ObsDay* obs;
     const ObsDay* robs;
     const unsigned char* flag;
-    const double* subh;
+    TimeGrid tg;
 };
 
+__host__ __device__ inline int tgrid_entries(int n_days, int substeps) {
+    return uses_fast_grid(n_days, substeps) ? (n_days - 1) * substeps : 0;
+}
+
 __host__ __device__ inline size_t smem_window_bytes(int n_days, int substeps, int metric) {
-    size_t b = static_cast<size_t>(n_days) * sizeof(ObsDay) + static_cast<size_t>(substeps) * sizeof(double);
+    size_t b = static_cast<size_t>(n_days) * sizeof(ObsDay) +
+               static_cast<size_t>(substeps + tgrid_entries(n_days, substeps)) * sizeof(double);
     if (metric == kMetMAPE) b += static_cast<size_t>(n_days) * (sizeof(ObsDay) + 3);
     return (b + 15) & ~size_t(15);
 }
 
+// Fill subh[sub] = RN(sub*h) and, when it fits, tgrid[k] = RN(RN(day-1) +
+// subh[sub]) for k = (day-1)*S + sub — the t of model.cpp:94, bit for bit.
+__device__ __forceinline__ TimeGrid stage_times(double* base, int n_days, int ns, double h) {
+    double* subh = base;
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) subh[i] = dmul(static_cast<double>(i), h);
+    const int K = tgrid_entries(n_days, ns);
+    double* tgrid = subh + ns;
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        const int d = k / ns;
+        tgrid[k] = dadd(static_cast<double>(d), dmul(static_cast<double>(k - d * ns), h));
+    }
+    return TimeGrid{K > 0 ? tgrid : nullptr, subh};
+}
+
 // Cooperative copy of a window into shared memory (all threads call; ends
-// with a barrier).  subh[sub] = RN(sub*h), the t offsets of model.cpp:94.
+// with a barrier).
 __device__ __forceinline__ SmemWindow stage_window(const DevWindow* __restrict__ gw, DevWindow* sdesc,
                                                    unsigned char* smem) {
     if (threadIdx.x == 0) *sdesc = *gw;
@@ -46,14 +65,13 @@ __device__ __forceinline__ SmemWindow stage_window(const DevWindow* __restrict__
     const int ns = gw->substeps;
     const int metric = gw->metric;
     ObsDay* obs = reinterpret_cast<ObsDay*>(smem);
-    double* subh = reinterpret_cast<double*>(obs + n);
-    ObsDay* robs = reinterpret_cast<ObsDay*>(subh + ns);
+    double* times = reinterpret_cast<double*>(obs + n);
+    ObsDay* robs = reinterpret_cast<ObsDay*>(times + ns + tgrid_entries(n, ns));
     unsigned char* flag = reinterpret_cast<unsigned char*>(robs + (metric == kMetMAPE ? n : 0));
     const double* src = reinterpret_cast<const double*>(gw->obs);
     double* dst = reinterpret_cast<double*>(obs);
     for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) dst[i] = src[i];
-    const double h = gw->h;
-    for (int i = threadIdx.x; i < ns; i += blockDim.x) subh[i] = dmul(static_cast<double>(i), h);
+    const TimeGrid tg = stage_times(times, n, ns, gw->h);
     if (metric == kMetMAPE) {
         const double* rsrc = reinterpret_cast<const double*>(gw->robs);
         double* rdst = reinterpret_cast<double*>(robs);
@@ -61,13 +79,13 @@ __device__ __forceinline__ SmemWindow stage_window(const DevWindow* __restrict__
         for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) flag[i] = gw->obs_flag[i];
     }
     __syncthreads();
-    return SmemWindow{sdesc, obs, robs, flag, subh};
+    return SmemWindow{sdesc, obs, robs, flag, tg};
 }
 
 // ---- boundary 1 -------------------------------------------------------------
 // positions: row-major n x 6 (the BatchObjective layout, pso.hpp:33-37).
 template <int FAM, int MET, int SUB>
-__global__ void __launch_bounds__(kEvalThreads) eval_costs_kernel(const DevWindow* __restrict__ win,
+__global__ void __launch_bounds__(kEvalThreads, 5) eval_costs_kernel(const DevWindow* __restrict__ win,
                                                                   const double* __restrict__ positions, size_t n,
                                                                   double* __restrict__ costs) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -78,7 +96,7 @@ __global__ void __launch_bounds__(kEvalThreads) eval_costs_kernel(const DevWindo
     double x[6];
 #pragma unroll
     for (int d = 0; d < 6; ++d) x[d] = positions[6 * k + d];
-    costs[k] = eval_particle<FAM, MET, SUB>(x, *sw.w, sw.subh, sw.obs, sw.robs, sw.flag);
+    costs[k] = eval_particle<FAM, MET, SUB>(x, *sw.w, sw.tg, sw.obs, sw.robs, sw.flag);
 }
 
 // ---- trajectories -------------------------------------------------------------
@@ -105,8 +123,7 @@ __global__ void __launch_bounds__(kEvalThreads) integrate_kernel(DevWindow w, co
                                                                  double* __restrict__ states,
                                                                  unsigned char* __restrict__ finite) {
     extern __shared__ __align__(16) unsigned char smem[];
-    double* subh = reinterpret_cast<double*>(smem);
-    for (int i = threadIdx.x; i < w.substeps; i += blockDim.x) subh[i] = dmul(static_cast<double>(i), w.h);
+    const TimeGrid tg = stage_times(reinterpret_cast<double*>(smem), w.n_days, w.substeps, w.h);
     __syncthreads();
     const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k >= n) return;
@@ -128,7 +145,7 @@ __global__ void __launch_bounds__(kEvalThreads) integrate_kernel(DevWindow w, co
     }
     const Particle part = hold_beta2 ? make_particle(p[1], p[1], 0.0, 0.0, p[4], p[5], w)
                                      : make_particle(p[0], p[1], p[2], p[3], p[4], p[5], w);
-    integrate_days<SUB>(part, w, subh, S, I, R, D, sink);
+    integrate_days<SUB>(part, w, tg, S, I, R, D, sink);
     finite[k] = all_finite(S, I, R, D) ? 1 : 0;
 }
 
@@ -237,7 +254,7 @@ __device__ __forceinline__ bool better(double ca, unsigned long long ia, double 
 // best, CTA argmin, and the last CTA of each swarm folds the CTA minima into
 // the global best and writes cost_history[it].
 template <int FAM, int MET, int SUB>
-__global__ void __launch_bounds__(kStepThreads) pso_step_kernel(const DevSwarm* __restrict__ swarms,
+__global__ void __launch_bounds__(kStepThreads, 5) pso_step_kernel(const DevSwarm* __restrict__ swarms,
                                                                 const uint32_t* __restrict__ cta_swarm,
                                                                 const DevWindow* __restrict__ windows,
                                                                 PsoPlanes P, DevSwarmState* __restrict__ state,
@@ -286,7 +303,7 @@ __global__ void __launch_bounds__(kStepThreads) pso_step_kernel(const DevSwarm* 
 #pragma unroll
             for (int d = 0; d < 6; ++d) P.x[d * stride + p] = x[d];
         }
-        const double c = eval_particle<FAM, MET, SUB>(x, *win.w, win.subh, win.obs, win.robs, win.flag);
+        const double c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag);
         P.cost[p] = c;
         double pbc = P.pbc[p];
         if (c < pbc) {  // pso.cpp:83-89
@@ -397,7 +414,7 @@ struct ForecastDSink {
 };
 
 template <int FAM, int MET, int SUB>
-__global__ void __launch_bounds__(kEvalThreads) ensemble_kernel(const DevWindow* __restrict__ win, DevWindow fwin,
+__global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWindow* __restrict__ win, DevWindow fwin,
                                                                 const double* __restrict__ lo,
                                                                 const double* __restrict__ hi, uint64_t seed,
                                                                 size_t n, int horizon, double* __restrict__ costs,
@@ -430,7 +447,7 @@ __global__ void __launch_bounds__(kEvalThreads) ensemble_kernel(const DevWindow*
     double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
     ScoreSink<FAM, MET> score(w, sw.obs, sw.robs, sw.flag);
     score.day(0, S, I, R, D);
-    integrate_days<SUB>(p, w, sw.subh, S, I, R, D, score);
+    integrate_days<SUB>(p, w, sw.tg, S, I, R, D, score);
     const bool fin_w = all_finite(S, I, R, D);
     // forecast_extension re-checks the junction through integrate_euler's
     // isfinite(init.total()) (model.cpp:83).
@@ -444,7 +461,8 @@ __global__ void __launch_bounds__(kEvalThreads) ensemble_kernel(const DevWindow*
     const Particle held = make_particle(x[1], x[1], 0.0, 0.0, x[4], x[5], fwin);
     drow[0] = D;
     ForecastDSink fs{drow};
-    integrate_days<SUB>(held, fwin, sw.subh, S, I, R, D, fs);
+    // held parameters never enter the ramp, so no time table is read
+    integrate_days<SUB>(held, fwin, TimeGrid{nullptr, sw.tg.subh}, S, I, R, D, fs);
     if (!all_finite(S, I, R, D)) {  // calibration.cpp:318-320
         for (int d = 0; d <= horizon; ++d) drow[d] = nan;
     }

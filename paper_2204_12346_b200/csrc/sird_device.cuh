@@ -63,6 +63,12 @@ __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a,
 // std::max(a, b) == (a < b) ? b : a (stl_algobase.h), NaN-preserving order.
 __device__ __forceinline__ double std_max(double a, double b) { return a < b ? b : a; }
 
+// Pin a value in a register: the compiler may not recompute it from its
+// operands.  Without this nvcc sinks the per-particle beta/N divisions into
+// the per-substep regime select (div(sel(b1,b2), N) instead of
+// sel(div(b1,N), div(b2,N))), paying a full division every substep.
+__device__ __forceinline__ void opaque(double& x) { asm volatile("" : "+d"(x)); }
+
 // Biased exponent of a double, from its high word (integer pipe only).
 __device__ __forceinline__ int dexp(double a) {
     return (__double2hiint(a) >> 20) & 0x7FF;
@@ -118,7 +124,20 @@ struct Particle {
     double bp1, bp2;  // beta1/N, beta2/N (model.cpp:67, constant regimes)
     double slope;     // (beta2-beta1)/(t2-t1) (model.cpp:62)
     int k1, k2;       // regime prefix lengths: k<k1 -> beta1; k>=k2 -> beta2; else ramp
+    bool fast;        // every ramp beta admits the 3-op division (see beta_in_fast_range)
 };
+
+// True when every beta the ramp can produce (beta1 + slope*(t - t1) for
+// t in [t1, t2)) is +0 or has magnitude in [2^-700, 2^701), the dividend
+// range of div_exact, so the per-substep exponent test can be skipped:
+// beta1, beta2 each +0 or of magnitude [2^-600, 2^680], t1/t2/slope finite
+// (DESIGN.md §4 bounds the ramp values by these).
+__device__ __forceinline__ bool beta_in_fast_range(double b) {
+    const long long bits = __double_as_longlong(b);
+    if (bits == 0) return true;  // +0 (not -0)
+    const int e = dexp(b);
+    return e >= 1023 - 600 && e <= 1023 + 680;
+}
 
 __device__ __forceinline__ Particle make_particle(double b1, double b2, double t1, double t2, double g, double mu,
                                                   const DevWindow& w) {
@@ -131,12 +150,17 @@ __device__ __forceinline__ Particle make_particle(double b1, double b2, double t
     p.bp1 = ddiv(b1, w.N);
     p.bp2 = ddiv(b2, w.N);
     p.slope = ddiv(dsub(b2, b1), dsub(t2, t1));
+    opaque(p.bp1);
+    opaque(p.bp2);
+    opaque(p.slope);
     const int K = (w.n_days - 1) * w.substeps;
     p.k1 = count_t_below(t1, K, w.substeps, w.h);
     // "t >= t2" is the complement of "t < t2" except for NaN t2, where both
     // comparisons are false and the ramp branch is taken (model.cpp:59-63).
     p.k2 = (t2 != t2) ? K : count_t_below(t2, K, w.substeps, w.h);
     if (p.k2 < p.k1) p.k2 = p.k1;  // t1 > t2: no ramp (k >= k1 implies t >= t2)
+    p.fast = w.fast_N && isfinite(t1) && isfinite(t2) && isfinite(p.slope) && beta_in_fast_range(b1) &&
+             beta_in_fast_range(b2);
     return p;
 }
 
@@ -156,32 +180,75 @@ __device__ __forceinline__ void euler_substep(double bp, double g, double mu, do
     D = dadd(D, dmul(h, mI));
 }
 
-// beta(t_k)/N for a ramp substep (model.cpp:62-63 then model.cpp:67).
-__device__ __forceinline__ double ramp_bp(const Particle& p, double dayf, double subh, const DevWindow& w) {
-    const double t = dadd(dayf, subh);
+// beta(t_k)/N for a ramp substep (model.cpp:62-63 then model.cpp:67); t is
+// the substep time t_k = (day-1) + sub*h (model.cpp:94).
+__device__ __forceinline__ double ramp_bp(const Particle& p, double t, double N, double rN) {
     const double beta = dadd(p.b1, dmul(p.slope, dsub(t, p.t1)));
-    return w.fast_N ? div_exact(beta, w.N, w.rN) : ddiv(beta, w.N);
+    if (p.fast) {  // div_exact without the per-value range test
+        const double q0 = __dmul_rn(beta, rN);
+        const double r = __fma_rn(-q0, N, beta);
+        return __fma_rn(r, rN, q0);
+    }
+    return ddiv(beta, N);
+}
+
+// Substep-time source.  The specialised kernels (SUB == 24, the reference
+// default) read t_k from a per-window table in shared memory (tgrid); the
+// generic kernels (SUB == 0) compute t = RN(RN(day-1) + subh[sub]).
+struct TimeGrid {
+    const double* tgrid;  // (n_days-1)*substeps entries (SUB > 0 only)
+    const double* subh;   // substeps entries: RN(sub*h)
+};
+
+// Largest t_k table kept in shared memory (entries, 16 KB): windows up to 86
+// days at 24 substeps take the specialised path.
+constexpr int kMaxTgrid = 2048;
+
+__host__ __device__ inline bool uses_fast_grid(int n_days, int substeps) {
+    return substeps == 24 && static_cast<long long>(n_days - 1) * substeps <= kMaxTgrid;
 }
 
 // Integrate days 1..n_days-1 (model.cpp:92-106), calling sink.day(day, S, I, R, D)
 // after every day.  SUB > 0 fixes the substep count at compile time
 // (the reference default kDefaultSubsteps = 24, model.hpp:12); SUB == 0 reads
-// it from the window.  `subh` is the table RN(sub*h), sub < substeps.
+// it from the window.
 template <int SUB, class Sink>
-__device__ __forceinline__ void integrate_days(const Particle& p, const DevWindow& w, const double* subh,
+__device__ __forceinline__ void integrate_days(const Particle& p, const DevWindow& w, const TimeGrid& tg,
                                                double& S, double& I, double& R, double& D, Sink& sink) {
     const int nsub = SUB > 0 ? SUB : w.substeps;
     const double h = w.h;
+    const double g = p.g, mu = p.mu;
+    const double N = w.N, rN = w.rN;
     int kbase = 0;
     for (int day = 1; day < w.n_days; ++day) {
-        const double dayf = static_cast<double>(day - 1);
         const int lo = p.k1 - kbase;  // sub < lo  -> beta1
-        const int hi = p.k2 - kbase;  // sub >= hi -> beta2
+        const int hi = p.k2 - kbase;  // sub >= hi -> beta2, else ramp
+        // Warp-uniform day classes (the regime depends only on k, so a day
+        // whose substeps all share one regime in every lane needs no
+        // per-substep select): 2 = some lane ramps today, 1 = some lane
+        // switches beta1 -> beta2 today, 0 = every lane constant all day.
+        const bool ramp_today = lo < hi && lo < nsub && hi > 0;
+        const bool switch_today = lo > 0 && lo < nsub;
+        const unsigned mask = __activemask();
+        if (__any_sync(mask, ramp_today)) {
 #pragma unroll
-        for (int sub = 0; sub < nsub; ++sub) {
-            double bp = sub < lo ? p.bp1 : p.bp2;
-            if (sub >= lo && sub < hi) bp = ramp_bp(p, dayf, subh[sub], w);
-            euler_substep(bp, p.g, p.mu, h, S, I, R, D);
+            for (int sub = 0; sub < nsub; ++sub) {
+                double bp = sub < lo ? p.bp1 : p.bp2;
+                if (sub >= lo && sub < hi) {
+                    double t;
+                    if constexpr (SUB > 0) t = tg.tgrid[kbase + sub];
+                    else t = dadd(static_cast<double>(day - 1), tg.subh[sub]);
+                    bp = ramp_bp(p, t, N, rN);
+                }
+                euler_substep(bp, g, mu, h, S, I, R, D);
+            }
+        } else if (__any_sync(mask, switch_today)) {
+#pragma unroll
+            for (int sub = 0; sub < nsub; ++sub) euler_substep(sub < lo ? p.bp1 : p.bp2, g, mu, h, S, I, R, D);
+        } else {
+            const double bp = lo >= nsub ? p.bp1 : p.bp2;
+#pragma unroll
+            for (int sub = 0; sub < nsub; ++sub) euler_substep(bp, g, mu, h, S, I, R, D);
         }
         kbase += nsub;
         sink.day(day, S, I, R, D);
@@ -260,14 +327,14 @@ struct ScoreSink {
 // Full particle-window evaluation: objective_value(spec, slice,
 // integrate_euler(params)) (calibration.cpp:148-152).
 template <int FAM, int MET, int SUB>
-__device__ __forceinline__ double eval_particle(const double* x, const DevWindow& w, const double* subh,
+__device__ __forceinline__ double eval_particle(const double* x, const DevWindow& w, const TimeGrid& tg,
                                                 const ObsDay* obs, const ObsDay* robs, const unsigned char* flag) {
     if (!w.init_finite) return __longlong_as_double(0x7FF0000000000000LL);
     const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w);
     double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
     ScoreSink<FAM, MET> sink(w, obs, robs, flag);
     sink.day(0, S, I, R, D);  // day 0 is the initial state, bit for bit (model.cpp:85)
-    integrate_days<SUB>(p, w, subh, S, I, R, D, sink);
+    integrate_days<SUB>(p, w, tg, S, I, R, D, sink);
     return sink.finish(all_finite(S, I, R, D));
 }
 

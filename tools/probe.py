@@ -29,12 +29,24 @@ def main():
     print(f"fp64 probe: {rate/1e12:.2f} T lane-ops/s")
     I, R, D = poland()
     # eval kernel
-    for spec in ("ird-mxse", "d-mse", "ird-mape"):
+    for spec, variant in (("ird-mxse", "random"), ("ird-mxse", "noramp"), ("ird-mxse", "sorted_t1"),
+                          ("ird-mxse", "sorted_2d"), ("d-mse", "random"), ("ird-mape", "random")):
         win = window(ctx, I, R, D, 60, spec=spec)
         n = 1 << 20
         g = torch.Generator(device="cuda").manual_seed(1)
         pos = torch.rand((n, 6), dtype=torch.float64, device="cuda", generator=g)
         pos *= torch.tensor([2, 2, 28, 28, 1, 0.1], dtype=torch.float64, device="cuda")
+        t1 = torch.minimum(pos[:, 2], pos[:, 3])
+        t2 = torch.maximum(pos[:, 2], pos[:, 3])
+        pos[:, 2], pos[:, 3] = t1, t2
+        if variant == "noramp":
+            pos[:, 3] = pos[:, 2]
+        elif variant == "sorted_t1":
+            pos = pos[torch.argsort(pos[:, 2])].contiguous()
+        elif variant == "sorted_2d":
+            b1 = (pos[:, 2] / 28 * 32).long().clamp(0, 31)
+            b2 = (pos[:, 3] / 28 * 32).long().clamp(0, 31)
+            pos = pos[torch.argsort(b1 * 64 + b2 * 1.0 + pos[:, 3] / 28)].contiguous()
         costs = torch.empty(n, dtype=torch.float64, device="cuda")
         torch.cuda.synchronize()
         for _ in range(3):
@@ -49,7 +61,7 @@ def main():
         ms = e0.elapsed_time(e1) / 5
         evals = n / (ms * 1e-3)
         A = 35 * 24 * 14 + 36 * 12
-        print(f"eval {spec}: {ms:.3f} ms per 1M particles -> {evals/1e9:.3f} G evals/s; "
+        print(f"eval {spec} {variant}: {ms:.3f} ms per 1M particles -> {evals/1e9:.3f} G evals/s; "
               f"floor ops {A} -> {evals*A/1e12:.2f} T ops/s = {evals*A/rate:.3f} of probe")
     # sweep: 139 windows x 4096 x iters
     for iters in (20, 100):
