@@ -297,10 +297,13 @@ def bench_ours(args):
     total_evals = allreduce_sum(evals_per_step, world)
     value = total_evals / (ms_per_step * 1e-3)
 
-    # roofline: the fused step kernel
-    ops_launch = PARTICLES * n_win * ops_per_eval(TAU + 1)
-    kernel_ms = statistics.mean(step_ms) / (step_launches if step_launches else 1)
-    achieved = ops_launch / (kernel_ms * 1e-3) / 1e12
+    # roofline: the fused step kernel, all its launches of a step (the
+    # partition lanes overlap, so the per-launch figure is the aggregate:
+    # algorithmic ops of every step launch / device time of the step launches)
+    ops_step = evals_per_step * ops_per_eval(TAU + 1)
+    steps_kernel_ms = statistics.mean(step_ms)
+    kernel_ms = steps_kernel_ms / (step_launches if step_launches else 1)
+    achieved = ops_step / (steps_kernel_ms * 1e-3) / 1e12
     traffic, prof = load_profile_traffic()
 
     # ---- e2e through the public calibration C-ABI with host buffers ----
@@ -358,7 +361,8 @@ def bench_ours(args):
                          "kernel": "pso_step_kernel<IRD,MXSE,24> (fused move+integrate+score+argmin)",
                          "ops_per_eval": ops_per_eval(TAU + 1), "ops_note": "FP64 DADD/DMUL ops, no FMA (parity); "
                          "floor count without ramp credit; peak = measured FP64 issue rate (sg_probe_fp64_rate)",
-                         "kernel_ms": kernel_ms, "seed_ms": statistics.mean(seed_ms), "profile": prof},
+                         "kernel_ms_per_launch": kernel_ms, "launches_per_step": step_launches,
+                         "step_kernels_ms": steps_kernel_ms, "seed_ms": statistics.mean(seed_ms), "profile": prof},
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
             "gpu_launches": gpu_launches,

@@ -14,7 +14,10 @@ import numpy as np
 
 from .errors import NoDeviceError, raise_for_status
 
-LIB_PATH = Path(__file__).resolve().parent / "libsirdgpu.so"
+import os
+
+# SG_LIB overrides the library (tuning experiments only; the default is the in-tree build).
+LIB_PATH = Path(os.environ.get("SG_LIB", Path(__file__).resolve().parent / "libsirdgpu.so"))
 
 FAMILY = {"d": 0, "ird": 1}
 METRIC = {"mxse": 0, "mse": 1, "mae": 2, "mape": 3}

@@ -35,14 +35,15 @@ def needs_build() -> bool:
     return any(p.exists() and p.stat().st_mtime > t for p in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: Path = OUT, extra: list | None = None) -> Path:
+    """Compile libsirdgpu.so (`extra`: additional nvcc flags, e.g. tuning -D for experiments)."""
+    if not force and out == OUT and not extra and not needs_build():
         return OUT
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", str(OUT), *[str(s) for s in SOURCES if s.exists()]]
+    cmd = [NVCC, *ARCH, *FLAGS, *(extra or []), "-o", str(out), *[str(s) for s in SOURCES if s.exists()]]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

@@ -22,6 +22,14 @@
 
 using namespace sirdgpu;
 
+// Independent swarm partitions run as separate launch sequences on their own
+// streams so one partition's per-iteration tail overlaps the next
+// partition's iteration (swarms never synchronise with each other).
+#ifndef SG_LANES
+#define SG_LANES 4
+#endif
+constexpr int kMaxLanes = SG_LANES;
+
 struct sg_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -32,6 +40,10 @@ struct sg_ctx {
     double* d_pos = nullptr;
     double* d_cost = nullptr;
     size_t scratch_n = 0;
+    // side streams for concurrent swarm partitions (see step_group)
+    cudaStream_t side[kMaxLanes] = {};
+    cudaEvent_t fork = nullptr;
+    cudaEvent_t join[kMaxLanes] = {};
 };
 
 struct sg_window {
@@ -137,15 +149,15 @@ struct EvalLaunch {
 
 template <int F, int M, int S>
 struct StepLaunch {
-    static void run(unsigned grid, const DevSwarm* sw, const uint32_t* cta_swarm, const DevWindow* wins,
-                    const PsoPlanes& P, DevSwarmState* state, uint64_t it, size_t smem, cudaStream_t st,
-                    cudaError_t* err) {
+    static void run(unsigned grid, uint32_t cta_offset, const DevSwarm* sw, const uint32_t* cta_swarm,
+                    const DevWindow* wins, const PsoPlanes& P, DevSwarmState* state, uint64_t it, size_t smem,
+                    cudaStream_t st, cudaError_t* err) {
         auto k = pso_step_kernel<F, M, S>;
         if (it == 0) {
             *err = prepare_smem(k, smem);
             if (*err != cudaSuccess) return;
         }
-        k<<<grid, kStepThreads, smem, st>>>(sw, cta_swarm, wins, P, state, it);
+        k<<<grid, kStepThreads, smem, st>>>(sw, cta_swarm, wins, P, state, it, cta_offset);
         *err = cudaGetLastError();
     }
 };
@@ -240,6 +252,11 @@ void sg_ctx_destroy(sg_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaFree(ctx->d_pos);
     cudaFree(ctx->d_cost);
+    for (int l = 0; l < kMaxLanes; ++l) {
+        if (ctx->side[l]) cudaStreamDestroy(ctx->side[l]);
+        if (ctx->join[l]) cudaEventDestroy(ctx->join[l]);
+    }
+    if (ctx->fork) cudaEventDestroy(ctx->fork);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -500,6 +517,7 @@ struct SwarmGroup {
     int family = 0, metric = 0, substeps = 24;
     std::vector<size_t> idx;          // positions in the caller's descriptor array
     std::vector<uint64_t> max_iters;  // per swarm
+    std::vector<std::pair<uint32_t, uint32_t>> lanes;  // (first CTA, CTAs) of each swarm partition
     size_t n_total = 0, n_ctas = 0, smem = 0;
     uint64_t iters = 0;               // max over swarms
     DevSwarm* d_sw = nullptr;
@@ -560,6 +578,23 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     }
     g.n_total = offset;
     g.n_ctas = cta_swarm.size();
+    // Partition swarms into up to kMaxLanes lanes of about equal CTA count
+    // (swarm boundaries only).  Small plans stay on one lane.
+    {
+        const int want = g.n_ctas >= 4 * static_cast<size_t>(ctx->sm_count) ? kMaxLanes
+                         : g.n_ctas >= 2 * static_cast<size_t>(ctx->sm_count) ? 2 : 1;
+        const size_t target = (g.n_ctas + want - 1) / want;
+        uint32_t begin = 0, count = 0;
+        for (const DevSwarm& s : sw) {
+            if (count > 0 && count + s.n_ctas > target && static_cast<int>(g.lanes.size()) + 1 < want) {
+                g.lanes.emplace_back(begin, count);
+                begin += count;
+                count = 0;
+            }
+            count += s.n_ctas;
+        }
+        g.lanes.emplace_back(begin, count);
+    }
     if (g.n_ctas > 0x7FFFFFFFu) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "too many particles in one plan");
     std::vector<DevWindow> wtab(wins.size());
     for (size_t k = 0; k < wins.size(); ++k) wtab[k] = wins[k]->host;
@@ -576,8 +611,8 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     SG_CUDA(ctx, b.alloc(&P.pbc, g.n_total));
     SG_CUDA(ctx, b.alloc(&P.cost, g.n_total));
     SG_CUDA(ctx, b.alloc(&P.mt, static_cast<size_t>(kMtN) * g.n_total));
-    SG_CUDA(ctx, b.alloc(&P.part_cost, g.n_ctas));
-    SG_CUDA(ctx, b.alloc(&P.part_idx, g.n_ctas));
+    SG_CUDA(ctx, b.alloc(&P.part_cost, g.n_ctas * kStepWarps));
+    SG_CUDA(ctx, b.alloc(&P.part_idx, g.n_ctas * kStepWarps));
     SG_CUDA(ctx, b.alloc(&P.history, sw.size() * g.iters));
     P.stride = g.n_total;
     P.hist_stride = g.iters;
@@ -597,13 +632,39 @@ int seed_group(sg_ctx* ctx, SwarmGroup& g) {
     return SG_OK;
 }
 
+int ensure_lanes(sg_ctx* ctx) {
+    if (ctx->fork) return SG_OK;
+    SG_CUDA(ctx, cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming));
+    for (int l = 0; l < kMaxLanes; ++l) {
+        SG_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->side[l], cudaStreamNonBlocking));
+        SG_CUDA(ctx, cudaEventCreateWithFlags(&ctx->join[l], cudaEventDisableTiming));
+    }
+    return SG_OK;
+}
+
 int step_group(sg_ctx* ctx, SwarmGroup& g) {
+    const size_t n_lanes = g.lanes.size();
+    if (n_lanes > 1) {
+        const int rc = ensure_lanes(ctx);
+        if (rc) return rc;
+        SG_CUDA(ctx, cudaEventRecord(ctx->fork, ctx->stream));
+        for (size_t l = 0; l < n_lanes; ++l) SG_CUDA(ctx, cudaStreamWaitEvent(ctx->side[l], ctx->fork, 0));
+    }
     for (uint64_t it = 0; it < g.iters; ++it) {
-        cudaError_t err = cudaSuccess;
-        dispatch<StepLaunch>(g.family, g.metric, g.substeps, static_cast<unsigned>(g.n_ctas), g.d_sw, g.d_cta,
-                             g.d_win, g.P, g.d_state, it, g.smem, ctx->stream, &err);
-        ctx->launches += 1;
-        if (err != cudaSuccess) return cuda_fail(ctx, err, "pso_step_kernel");
+        for (size_t l = 0; l < n_lanes; ++l) {
+            cudaError_t err = cudaSuccess;
+            cudaStream_t st = n_lanes > 1 ? ctx->side[l] : ctx->stream;
+            dispatch<StepLaunch>(g.family, g.metric, g.substeps, g.lanes[l].second, g.lanes[l].first, g.d_sw,
+                                 g.d_cta, g.d_win, g.P, g.d_state, it, g.smem, st, &err);
+            ctx->launches += 1;
+            if (err != cudaSuccess) return cuda_fail(ctx, err, "pso_step_kernel");
+        }
+    }
+    if (n_lanes > 1) {
+        for (size_t l = 0; l < n_lanes; ++l) {
+            SG_CUDA(ctx, cudaEventRecord(ctx->join[l], ctx->side[l]));
+            SG_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join[l], 0));
+        }
     }
     return SG_OK;
 }
@@ -713,7 +774,7 @@ int sg_plan_run_timed(sg_plan* plan, double* seed_ms, double* steps_ms) {
 uint64_t sg_plan_step_launches(const sg_plan* plan) {
     uint64_t n = 0;
     if (plan)
-        for (const SwarmGroup* g : plan->groups) n += g->iters;
+        for (const SwarmGroup* g : plan->groups) n += g->iters * g->lanes.size();
     return n;
 }
 

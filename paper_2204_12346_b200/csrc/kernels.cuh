@@ -18,8 +18,15 @@
 
 namespace sirdgpu {
 
+#ifndef SG_STEP_THREADS
+#define SG_STEP_THREADS 128
+#endif
+#ifndef SG_STEP_MIN_BLOCKS
+#define SG_STEP_MIN_BLOCKS 5
+#endif
 constexpr int kEvalThreads = 128;
-constexpr int kStepThreads = 128;
+constexpr int kStepThreads = SG_STEP_THREADS;
+constexpr int kStepWarps = kStepThreads / 32;
 
 // Shared-memory staging of one window: the descriptor in static shared memory,
 // obs, the substep-time tables (+ robs + flags for MAPE) in the dynamic segment.
@@ -181,7 +188,7 @@ struct PsoPlanes {
     double* cost;        // last evaluated cost
     uint64_t* mt;        // 312 planes
     size_t stride;       // total particles (plane length)
-    double* part_cost;   // per CTA
+    double* part_cost;   // per warp of the step kernel
     unsigned long long* part_idx;
     double* history;     // per swarm, max_iters_max entries
     uint64_t hist_stride;
@@ -251,27 +258,24 @@ __device__ __forceinline__ bool better(double ca, unsigned long long ia, double 
 // it > 0 first applies the move of iteration it-1 (move_particles,
 // pso.cpp:103-127), which in the reference closes step it-1; it reads the
 // global best published by the previous launch.  Then evaluate, personal
-// best, CTA argmin, and the last CTA of each swarm folds the CTA minima into
-// the global best and writes cost_history[it].
+// best, warp argmin, and the last warp of each swarm to finish folds the
+// warp minima into the global best and writes cost_history[it].  No
+// CTA-wide barrier after the evaluation: warps retire independently.
 template <int FAM, int MET, int SUB>
-__global__ void __launch_bounds__(kStepThreads, 5) pso_step_kernel(const DevSwarm* __restrict__ swarms,
-                                                                const uint32_t* __restrict__ cta_swarm,
-                                                                const DevWindow* __restrict__ windows,
-                                                                PsoPlanes P, DevSwarmState* __restrict__ state,
-                                                                uint64_t it) {
+__global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
+    pso_step_kernel(const DevSwarm* __restrict__ swarms, const uint32_t* __restrict__ cta_swarm,
+                    const DevWindow* __restrict__ windows, PsoPlanes P, DevSwarmState* __restrict__ state,
+                    uint64_t it, uint32_t cta_offset) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ double red_c[kStepThreads / 32];
-    __shared__ unsigned long long red_i[kStepThreads / 32];
-    __shared__ bool is_last;
-
     __shared__ DevWindow sdesc;
 
-    const int s = static_cast<int>(cta_swarm[blockIdx.x]);
+    const uint32_t cta = blockIdx.x + cta_offset;
+    const int s = static_cast<int>(cta_swarm[cta]);
     const DevSwarm& sw = swarms[s];
     if (it >= sw.max_iters) return;  // CTA-uniform
     const SmemWindow win = stage_window(windows + sw.window, &sdesc, smem);
 
-    const uint64_t i = static_cast<uint64_t>(blockIdx.x - sw.cta_begin) * blockDim.x + threadIdx.x;
+    const uint64_t i = static_cast<uint64_t>(cta - sw.cta_begin) * blockDim.x + threadIdx.x;
     const bool active = i < sw.n;
     const size_t p = sw.offset + (active ? i : 0);
     const size_t stride = P.stride;
@@ -310,13 +314,13 @@ __global__ void __launch_bounds__(kStepThreads, 5) pso_step_kernel(const DevSwar
             pbc = c;
             P.pbc[p] = c;
 #pragma unroll
-            for (int d = 0; d < 6; ++d) P.pb[d * stride + p] = x[d];
+            for (int d = 0; d < 6; ++d) P.pb[d * stride + p] = P.x[d * stride + p];  // this thread's own store
         }
         my_c = pbc;
         my_i = i;
     }
 
-    // CTA argmin of personal-best costs, lowest index on ties.
+    // Warp argmin of personal-best costs, lowest index on ties.
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         const double oc = __shfl_down_sync(0xFFFFFFFFu, my_c, off);
@@ -327,38 +331,28 @@ __global__ void __launch_bounds__(kStepThreads, 5) pso_step_kernel(const DevSwar
         }
     }
     const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
+    const uint32_t wslot = (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5);  // warp within the swarm
+    const uint32_t n_wslots = sw.n_ctas * kStepWarps;
+    unsigned int ticket = 0;
     if (lane == 0) {
-        red_c[warp] = my_c;
-        red_i[warp] = my_i;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double bc = red_c[0];
-        unsigned long long bi = red_i[0];
-        for (int k = 1; k < kStepThreads / 32; ++k)
-            if (better(red_c[k], red_i[k], bc, bi)) {
-                bc = red_c[k];
-                bi = red_i[k];
-            }
-        P.part_cost[blockIdx.x] = bc;
-        P.part_idx[blockIdx.x] = bi;
+        P.part_cost[static_cast<size_t>(sw.cta_begin) * kStepWarps + wslot] = my_c;
+        P.part_idx[static_cast<size_t>(sw.cta_begin) * kStepWarps + wslot] = my_i;
         __threadfence();
-        const unsigned int ticket = atomicAdd(&state[s].arrived, 1u);
-        is_last = (ticket == sw.n_ctas - 1);
+        ticket = atomicAdd(&state[s].arrived, 1u);
     }
-    __syncthreads();
-    if (!is_last) return;
+    ticket = __shfl_sync(0xFFFFFFFFu, ticket, 0);
+    if (ticket != n_wslots - 1) return;
 
-    // Last CTA of the swarm: global-best scan (pso.cpp:90-96) over the CTA
+    // Last warp of the swarm: global-best scan (pso.cpp:90-96) over the warp
     // minima; (cost, index) order makes the parallel fold equal the
     // sequential lowest-index scan.
     __threadfence();
     double bc = __longlong_as_double(0x7FF0000000000000LL);
     unsigned long long bi = ~0ULL;
-    for (uint32_t k = threadIdx.x; k < sw.n_ctas; k += blockDim.x) {
-        const double c = __ldcg(&P.part_cost[sw.cta_begin + k]);
-        const unsigned long long ix = __ldcg(&P.part_idx[sw.cta_begin + k]);
+    const size_t base = static_cast<size_t>(sw.cta_begin) * kStepWarps;
+    for (uint32_t k = lane; k < n_wslots; k += 32) {
+        const double c = __ldcg(&P.part_cost[base + k]);
+        const unsigned long long ix = __ldcg(&P.part_idx[base + k]);
         if (better(c, ix, bc, bi)) {
             bc = c;
             bi = ix;
@@ -373,20 +367,7 @@ __global__ void __launch_bounds__(kStepThreads, 5) pso_step_kernel(const DevSwar
             bi = oi;
         }
     }
-    __syncthreads();  // red_c/red_i reuse
     if (lane == 0) {
-        red_c[warp] = bc;
-        red_i[warp] = bi;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        bc = red_c[0];
-        bi = red_i[0];
-        for (int k = 1; k < kStepThreads / 32; ++k)
-            if (better(red_c[k], red_i[k], bc, bi)) {
-                bc = red_c[k];
-                bi = red_i[k];
-            }
         DevSwarmState& st = state[s];
         if (bc < st.best_cost) {  // strict: an equal later cost never replaces (pso.cpp:91)
             st.best_cost = bc;
