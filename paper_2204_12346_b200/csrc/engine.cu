@@ -163,6 +163,21 @@ struct StepLaunch {
 };
 
 template <int F, int M, int S>
+struct PermEvalLaunch {
+    static void run(unsigned grid, uint32_t cta_offset, const DevSwarm* sw, const uint32_t* cta_swarm,
+                    const DevWindow* wins, const PsoPlanes& P, DevSwarmState* state, const uint32_t* perm,
+                    uint64_t it, size_t smem, cudaStream_t st, cudaError_t* err) {
+        auto k = pso_eval_kernel<F, M, S>;
+        if (it == 0) {
+            *err = prepare_smem(k, smem);
+            if (*err != cudaSuccess) return;
+        }
+        k<<<grid, kStepThreads, smem, st>>>(sw, cta_swarm, wins, P, state, perm, it, cta_offset);
+        *err = cudaGetLastError();
+    }
+};
+
+template <int F, int M, int S>
 struct EnsembleLaunch {
     static void run(const DevWindow* w, const DevWindow& fwin, const double* lo, const double* hi, uint64_t seed,
                     size_t n, int horizon, double* costs, double* params, double* deaths, size_t smem,
@@ -517,7 +532,13 @@ struct SwarmGroup {
     int family = 0, metric = 0, substeps = 24;
     std::vector<size_t> idx;          // positions in the caller's descriptor array
     std::vector<uint64_t> max_iters;  // per swarm
-    std::vector<std::pair<uint32_t, uint32_t>> lanes;  // (first CTA, CTAs) of each swarm partition
+    struct Lane {
+        uint32_t cta_begin, n_ctas, swarm_begin, n_swarms;
+    };
+    std::vector<Lane> lanes;  // swarm partitions launched on separate streams
+    bool sorted = false;      // every swarm <= kSortMax: move+sort / permuted eval
+    uint32_t* d_perm = nullptr;
+    unsigned char* d_keys = nullptr;
     size_t n_total = 0, n_ctas = 0, smem = 0;
     uint64_t iters = 0;               // max over swarms
     DevSwarm* d_sw = nullptr;
@@ -582,20 +603,25 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     // (swarm boundaries only).  Small plans stay on one lane.
     {
         const int want = g.n_ctas >= 4 * static_cast<size_t>(ctx->sm_count) ? kMaxLanes
-                         : g.n_ctas >= 2 * static_cast<size_t>(ctx->sm_count) ? 2 : 1;
+                         : g.n_ctas >= 2 * static_cast<size_t>(ctx->sm_count) ? std::min(2, kMaxLanes) : 1;
         const size_t target = (g.n_ctas + want - 1) / want;
-        uint32_t begin = 0, count = 0;
+        SwarmGroup::Lane cur{0, 0, 0, 0};
         for (const DevSwarm& s : sw) {
-            if (count > 0 && count + s.n_ctas > target && static_cast<int>(g.lanes.size()) + 1 < want) {
-                g.lanes.emplace_back(begin, count);
-                begin += count;
-                count = 0;
+            if (cur.n_ctas > 0 && cur.n_ctas + s.n_ctas > target && static_cast<int>(g.lanes.size()) + 1 < want) {
+                g.lanes.push_back(cur);
+                cur = SwarmGroup::Lane{cur.cta_begin + cur.n_ctas, 0, cur.swarm_begin + cur.n_swarms, 0};
             }
-            count += s.n_ctas;
+            cur.n_ctas += s.n_ctas;
+            cur.n_swarms += 1;
         }
-        g.lanes.emplace_back(begin, count);
+        g.lanes.push_back(cur);
     }
-    if (g.n_ctas > 0x7FFFFFFFu) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "too many particles in one plan");
+#ifndef SG_SORT
+#define SG_SORT 0
+#endif
+    g.sorted = SG_SORT != 0;
+    for (const DevSwarm& s : sw)
+        if (s.n > static_cast<uint64_t>(kSortMax)) g.sorted = false;
     std::vector<DevWindow> wtab(wins.size());
     for (size_t k = 0; k < wins.size(); ++k) wtab[k] = wins[k]->host;
 
@@ -614,6 +640,10 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     SG_CUDA(ctx, b.alloc(&P.part_cost, g.n_ctas * kStepWarps));
     SG_CUDA(ctx, b.alloc(&P.part_idx, g.n_ctas * kStepWarps));
     SG_CUDA(ctx, b.alloc(&P.history, sw.size() * g.iters));
+    if (g.sorted) {
+        SG_CUDA(ctx, b.alloc(&g.d_perm, g.n_total));
+        SG_CUDA(ctx, b.alloc(&g.d_keys, g.n_total));
+    }
     P.stride = g.n_total;
     P.hist_stride = g.iters;
     cudaStream_t st = ctx->stream;
@@ -652,10 +682,22 @@ int step_group(sg_ctx* ctx, SwarmGroup& g) {
     }
     for (uint64_t it = 0; it < g.iters; ++it) {
         for (size_t l = 0; l < n_lanes; ++l) {
-            cudaError_t err = cudaSuccess;
+            const SwarmGroup::Lane& ln = g.lanes[l];
             cudaStream_t st = n_lanes > 1 ? ctx->side[l] : ctx->stream;
-            dispatch<StepLaunch>(g.family, g.metric, g.substeps, g.lanes[l].second, g.lanes[l].first, g.d_sw,
-                                 g.d_cta, g.d_win, g.P, g.d_state, it, g.smem, st, &err);
+            cudaError_t err = cudaSuccess;
+            if (g.sorted) {
+                pso_move_kernel<<<ln.n_ctas, kStepThreads, 0, st>>>(g.d_sw, g.d_cta, g.P, g.d_state, g.d_keys, it,
+                                                                    ln.cta_begin);
+                pso_sort_kernel<<<ln.n_swarms, kSortThreads, 0, st>>>(g.d_sw, g.d_keys, g.d_perm, it, ln.swarm_begin);
+                ctx->launches += 2;
+                err = cudaGetLastError();
+                if (err != cudaSuccess) return cuda_fail(ctx, err, "pso_move_kernel/pso_sort_kernel");
+                dispatch<PermEvalLaunch>(g.family, g.metric, g.substeps, ln.n_ctas, ln.cta_begin, g.d_sw, g.d_cta,
+                                         g.d_win, g.P, g.d_state, g.d_perm, it, g.smem, st, &err);
+            } else {
+                dispatch<StepLaunch>(g.family, g.metric, g.substeps, ln.n_ctas, ln.cta_begin, g.d_sw, g.d_cta,
+                                     g.d_win, g.P, g.d_state, it, g.smem, st, &err);
+            }
             ctx->launches += 1;
             if (err != cudaSuccess) return cuda_fail(ctx, err, "pso_step_kernel");
         }

@@ -254,73 +254,56 @@ __device__ __forceinline__ bool better(double ca, unsigned long long ia, double 
     return ca < cb || (ca == cb && ia < ib);
 }
 
-// One Swarm::step (pso.cpp:77-101) for every swarm, iteration `it`.
-// it > 0 first applies the move of iteration it-1 (move_particles,
-// pso.cpp:103-127), which in the reference closes step it-1; it reads the
-// global best published by the previous launch.  Then evaluate, personal
-// best, warp argmin, and the last warp of each swarm to finish folds the
-// warp minima into the global best and writes cost_history[it].  No
-// CTA-wide barrier after the evaluation: warps retire independently.
-template <int FAM, int MET, int SUB>
-__global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
-    pso_step_kernel(const DevSwarm* __restrict__ swarms, const uint32_t* __restrict__ cta_swarm,
-                    const DevWindow* __restrict__ windows, PsoPlanes P, DevSwarmState* __restrict__ state,
-                    uint64_t it, uint32_t cta_offset) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ DevWindow sdesc;
+// Swarm::move_particles for one particle (pso.cpp:103-127): 12 draws of the
+// particle's engine (r1, r2 per dimension, always both), velocity and
+// clamped position update, repair.  Reads the global best published after
+// iteration it-1 and writes x, v; returns the new position in x.
+__device__ __forceinline__ void move_particle(const DevSwarm& sw, const DevSwarmState& st, const PsoPlanes& P,
+                                              size_t p, uint64_t it, double* x) {
+    const size_t stride = P.stride;
+    const bool have_best = st.best_cost < __longlong_as_double(0x7FF0000000000000LL);  // pso.cpp:106
+    double u[12];
+    mt_draw<12>(P.mt, stride, p, 6 + 12 * (it - 1), u);
+#pragma unroll
+    for (int d = 0; d < 6; ++d) {
+        const double r1 = u[2 * d];
+        const double r2 = u[2 * d + 1];
+        const double vd = P.v[d * stride + p];
+        const double pbd = P.pb[d * stride + p];
+        // vel = w*v + (c1*r1)*(pbest - x)   (pso.cpp:116)
+        double vel = dadd(dmul(sw.w, vd), dmul(dmul(sw.c1, r1), dsub(pbd, x[d])));
+        if (have_best) vel = dadd(vel, dmul(dmul(sw.c2, r2), dsub(st.best[d], x[d])));  // pso.cpp:117-119
+        P.v[d * stride + p] = vel;
+        x[d] = std_clamp(dadd(x[d], vel), sw.lo[d], sw.hi[d]);  // pso.cpp:121
+    }
+    if (sw.repair) repair_order(x);  // pso.cpp:123-125
+#pragma unroll
+    for (int d = 0; d < 6; ++d) P.x[d * stride + p] = x[d];
+}
 
-    const uint32_t cta = blockIdx.x + cta_offset;
-    const int s = static_cast<int>(cta_swarm[cta]);
-    const DevSwarm& sw = swarms[s];
-    if (it >= sw.max_iters) return;  // CTA-uniform
-    const SmemWindow win = stage_window(windows + sw.window, &sdesc, smem);
-
-    const uint64_t i = static_cast<uint64_t>(cta - sw.cta_begin) * blockDim.x + threadIdx.x;
-    const bool active = i < sw.n;
-    const size_t p = sw.offset + (active ? i : 0);
+// Personal best (pso.cpp:83-89), warp argmin of personal-best costs (lowest
+// particle index on ties), and — in the last warp of the swarm to arrive —
+// the global-best scan (pso.cpp:90-96) over the warp minima plus
+// cost_history[it].  (cost, index) order makes the parallel fold equal the
+// sequential lowest-index scan.  No CTA-wide barrier: warps retire on their own.
+__device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& st, const PsoPlanes& P, int s,
+                                            bool active, size_t p, uint64_t i, double c, uint32_t wslot,
+                                            uint64_t it) {
     const size_t stride = P.stride;
     double my_c = __longlong_as_double(0x7FF0000000000000LL);
     unsigned long long my_i = ~0ULL;
-
     if (active) {
-        double x[6];
-#pragma unroll
-        for (int d = 0; d < 6; ++d) x[d] = P.x[d * stride + p];
-        if (it > 0) {
-            const double gbc = state[s].best_cost;
-            const bool have_best = gbc < __longlong_as_double(0x7FF0000000000000LL);  // pso.cpp:106
-            double u[12];
-            mt_draw<12>(P.mt, stride, p, 6 + 12 * (it - 1), u);
-#pragma unroll
-            for (int d = 0; d < 6; ++d) {
-                const double r1 = u[2 * d];
-                const double r2 = u[2 * d + 1];
-                const double vd = P.v[d * stride + p];
-                const double pbd = P.pb[d * stride + p];
-                // vel = w*v + (c1*r1)*(pbest - x)   (pso.cpp:116)
-                double vel = dadd(dmul(sw.w, vd), dmul(dmul(sw.c1, r1), dsub(pbd, x[d])));
-                if (have_best) vel = dadd(vel, dmul(dmul(sw.c2, r2), dsub(state[s].best[d], x[d])));  // 117-119
-                P.v[d * stride + p] = vel;
-                x[d] = std_clamp(dadd(x[d], vel), sw.lo[d], sw.hi[d]);  // pso.cpp:121
-            }
-            if (sw.repair) repair_order(x);  // pso.cpp:123-125
-#pragma unroll
-            for (int d = 0; d < 6; ++d) P.x[d * stride + p] = x[d];
-        }
-        const double c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag);
         P.cost[p] = c;
         double pbc = P.pbc[p];
-        if (c < pbc) {  // pso.cpp:83-89
+        if (c < pbc) {
             pbc = c;
             P.pbc[p] = c;
 #pragma unroll
-            for (int d = 0; d < 6; ++d) P.pb[d * stride + p] = P.x[d * stride + p];  // this thread's own store
+            for (int d = 0; d < 6; ++d) P.pb[d * stride + p] = P.x[d * stride + p];
         }
         my_c = pbc;
         my_i = i;
     }
-
-    // Warp argmin of personal-best costs, lowest index on ties.
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         const double oc = __shfl_down_sync(0xFFFFFFFFu, my_c, off);
@@ -331,30 +314,25 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
         }
     }
     const int lane = threadIdx.x & 31;
-    const uint32_t wslot = (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5);  // warp within the swarm
     const uint32_t n_wslots = sw.n_ctas * kStepWarps;
+    const size_t base = static_cast<size_t>(sw.cta_begin) * kStepWarps;
     unsigned int ticket = 0;
     if (lane == 0) {
-        P.part_cost[static_cast<size_t>(sw.cta_begin) * kStepWarps + wslot] = my_c;
-        P.part_idx[static_cast<size_t>(sw.cta_begin) * kStepWarps + wslot] = my_i;
+        P.part_cost[base + wslot] = my_c;
+        P.part_idx[base + wslot] = my_i;
         __threadfence();
-        ticket = atomicAdd(&state[s].arrived, 1u);
+        ticket = atomicAdd(&st.arrived, 1u);
     }
     ticket = __shfl_sync(0xFFFFFFFFu, ticket, 0);
     if (ticket != n_wslots - 1) return;
-
-    // Last warp of the swarm: global-best scan (pso.cpp:90-96) over the warp
-    // minima; (cost, index) order makes the parallel fold equal the
-    // sequential lowest-index scan.
     __threadfence();
     double bc = __longlong_as_double(0x7FF0000000000000LL);
     unsigned long long bi = ~0ULL;
-    const size_t base = static_cast<size_t>(sw.cta_begin) * kStepWarps;
     for (uint32_t k = lane; k < n_wslots; k += 32) {
-        const double c = __ldcg(&P.part_cost[base + k]);
+        const double cc = __ldcg(&P.part_cost[base + k]);
         const unsigned long long ix = __ldcg(&P.part_idx[base + k]);
-        if (better(c, ix, bc, bi)) {
-            bc = c;
+        if (better(cc, ix, bc, bi)) {
+            bc = cc;
             bi = ix;
         }
     }
@@ -368,7 +346,6 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
         }
     }
     if (lane == 0) {
-        DevSwarmState& st = state[s];
         if (bc < st.best_cost) {  // strict: an equal later cost never replaces (pso.cpp:91)
             st.best_cost = bc;
             const size_t q = sw.offset + bi;
@@ -377,6 +354,161 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
         P.history[static_cast<size_t>(s) * P.hist_stride + it] = st.best_cost;
         st.arrived = 0;
     }
+}
+
+// One Swarm::step (pso.cpp:77-101) for every swarm, iteration `it`, fused:
+// the move of iteration it-1 (which closes step it-1 in the reference), then
+// evaluate, personal best, and the global-best fold.  Thread t of a swarm's
+// CTA range owns particle t for all iterations.  Used for large swarms.
+template <int FAM, int MET, int SUB>
+__global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
+    pso_step_kernel(const DevSwarm* __restrict__ swarms, const uint32_t* __restrict__ cta_swarm,
+                    const DevWindow* __restrict__ windows, PsoPlanes P, DevSwarmState* __restrict__ state,
+                    uint64_t it, uint32_t cta_offset) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ DevWindow sdesc;
+    const uint32_t cta = blockIdx.x + cta_offset;
+    const int s = static_cast<int>(cta_swarm[cta]);
+    const DevSwarm& sw = swarms[s];
+    if (it >= sw.max_iters) return;  // CTA-uniform
+    const SmemWindow win = stage_window(windows + sw.window, &sdesc, smem);
+    const uint64_t i = static_cast<uint64_t>(cta - sw.cta_begin) * blockDim.x + threadIdx.x;
+    const bool active = i < sw.n;
+    const size_t p = sw.offset + (active ? i : 0);
+    double c = 0.0;
+    if (active) {
+        double x[6];
+#pragma unroll
+        for (int d = 0; d < 6; ++d) x[d] = P.x[d * P.stride + p];
+        if (it > 0) move_particle(sw, state[s], P, p, it, x);
+        c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag);
+    }
+    finish_step(sw, state[s], P, s, active, p, i, c, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it);
+}
+
+// ---- ramp-coherent evaluation order (swarms of at most kSortMax particles) ----
+//
+// The cost of a warp-day is set by the union of its lanes' beta ramps
+// [t1, t2) (sird_device.cuh integrate_days), so particles are evaluated in
+// Morton order of their switch times (t1, t2): pso_move_kernel moves every
+// particle (coalesced, particle order) and writes its key, pso_sort_kernel
+// counting-sorts each swarm's particle indices by key into perm, and
+// pso_eval_kernel maps thread slot -> perm[slot].
+// The order only decides which thread evaluates which particle — every
+// result is written to the particle's own slot and ties break on the
+// particle index, so results are identical for any order.
+constexpr int kSortThreads = 256;
+constexpr int kSortMax = 16384;
+constexpr int kSortBits = 4;                       // per coordinate
+constexpr int kSortBuckets = 1 << (2 * kSortBits);  // 256
+
+__device__ __forceinline__ uint32_t morton_key(double t1, double t2, double lo, double hi) {
+    const double span = hi - lo;
+    const float s = span > 0.0 ? static_cast<float>((1 << kSortBits) / span) : 0.0f;
+    int q1 = static_cast<int>(static_cast<float>(t1 - lo) * s);
+    int q2 = static_cast<int>(static_cast<float>(t2 - lo) * s);
+    q1 = min(max(q1, 0), (1 << kSortBits) - 1);  // NaN -> 0 (float->int of NaN is 0 on the device)
+    q2 = min(max(q2, 0), (1 << kSortBits) - 1);
+    uint32_t k = 0;
+#pragma unroll
+    for (int b = 0; b < kSortBits; ++b) k |= (((q1 >> b) & 1u) << (2 * b + 1)) | (((q2 >> b) & 1u) << (2 * b));
+    return k;
+}
+
+// Move phase (it > 0) for every particle of the lane's swarms, in particle
+// order (coalesced engine and state traffic), plus the Morton key of the new
+// switch times.  Same CTA -> swarm map as the evaluation kernels.
+__global__ void __launch_bounds__(kStepThreads) pso_move_kernel(const DevSwarm* __restrict__ swarms,
+                                                                const uint32_t* __restrict__ cta_swarm, PsoPlanes P,
+                                                                const DevSwarmState* __restrict__ state,
+                                                                unsigned char* __restrict__ keys, uint64_t it,
+                                                                uint32_t cta_offset) {
+    const uint32_t cta = blockIdx.x + cta_offset;
+    const int s = static_cast<int>(cta_swarm[cta]);
+    const DevSwarm& sw = swarms[s];
+    if (it >= sw.max_iters) return;
+    const uint64_t i = static_cast<uint64_t>(cta - sw.cta_begin) * blockDim.x + threadIdx.x;
+    if (i >= sw.n) return;
+    const size_t p = sw.offset + i;
+    double x[6];
+#pragma unroll
+    for (int d = 0; d < 6; ++d) x[d] = P.x[d * P.stride + p];
+    if (it > 0) move_particle(sw, state[s], P, p, it, x);
+    const double tlo = sw.lo[2] < sw.lo[3] ? sw.lo[2] : sw.lo[3];
+    const double thi = sw.hi[2] > sw.hi[3] ? sw.hi[2] : sw.hi[3];
+    keys[p] = static_cast<unsigned char>(morton_key(x[2], x[3], tlo, thi));
+}
+
+// Counting sort of one swarm's particle indices by key (one CTA per swarm).
+// Ties keep no particular order: the order never affects results.
+__global__ void __launch_bounds__(kSortThreads) pso_sort_kernel(const DevSwarm* __restrict__ swarms,
+                                                                const unsigned char* __restrict__ keys,
+                                                                uint32_t* __restrict__ perm, uint64_t it,
+                                                                uint32_t swarm_offset) {
+    __shared__ unsigned int hist[kSortBuckets];
+    const int s = static_cast<int>(blockIdx.x + swarm_offset);
+    const DevSwarm& sw = swarms[s];
+    if (it >= sw.max_iters) return;
+    for (int b = threadIdx.x; b < kSortBuckets; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    const uint32_t n = static_cast<uint32_t>(sw.n);
+    const unsigned char* kk = keys + sw.offset;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&hist[kk[i]], 1u);
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of the buckets by one warp
+        const int lane = threadIdx.x;
+        constexpr int per = kSortBuckets / 32;
+        unsigned int local[per];
+        unsigned int sum = 0;
+#pragma unroll
+        for (int j = 0; j < per; ++j) {
+            local[j] = hist[lane * per + j];
+            sum += local[j];
+        }
+        unsigned int incl = sum;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned int v = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+            if (lane >= off) incl += v;
+        }
+        unsigned int run = incl - sum;
+#pragma unroll
+        for (int j = 0; j < per; ++j) {
+            hist[lane * per + j] = run;
+            run += local[j];
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) perm[sw.offset + atomicAdd(&hist[kk[i]], 1u)] = i;
+}
+
+// Evaluation half of Swarm::step in permuted order (see above): thread slot
+// t of the swarm evaluates particle perm[t], already moved by
+// pso_move_sort_kernel, then personal best and the global-best fold.
+template <int FAM, int MET, int SUB>
+__global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
+    pso_eval_kernel(const DevSwarm* __restrict__ swarms, const uint32_t* __restrict__ cta_swarm,
+                    const DevWindow* __restrict__ windows, PsoPlanes P, DevSwarmState* __restrict__ state,
+                    const uint32_t* __restrict__ perm, uint64_t it, uint32_t cta_offset) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ DevWindow sdesc;
+    const uint32_t cta = blockIdx.x + cta_offset;
+    const int s = static_cast<int>(cta_swarm[cta]);
+    const DevSwarm& sw = swarms[s];
+    if (it >= sw.max_iters) return;  // CTA-uniform
+    const SmemWindow win = stage_window(windows + sw.window, &sdesc, smem);
+    const uint64_t slot = static_cast<uint64_t>(cta - sw.cta_begin) * blockDim.x + threadIdx.x;
+    const bool active = slot < sw.n;
+    const uint64_t i = active ? perm[sw.offset + slot] : 0;
+    const size_t p = sw.offset + i;
+    double c = 0.0;
+    if (active) {
+        double x[6];
+#pragma unroll
+        for (int d = 0; d < 6; ++d) x[d] = P.x[d * P.stride + p];
+        c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag);
+    }
+    finish_step(sw, state[s], P, s, active, p, i, c, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it);
 }
 
 // ---- forecast-scenario ensemble ----------------------------------------------------

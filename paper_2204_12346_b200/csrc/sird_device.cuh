@@ -12,6 +12,10 @@
 
 #include <cstdint>
 
+#ifndef SG_RAMP_MODE
+#define SG_RAMP_MODE 1
+#endif
+
 namespace sirdgpu {
 
 constexpr int kFamD = 0;
@@ -219,6 +223,10 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
     const double h = w.h;
     const double g = p.g, mu = p.mu;
     const double N = w.N, rN = w.rN;
+    const unsigned mask = __activemask();
+    // Warp-uniform: every lane's ramp admits the 3-op division, so the ramp
+    // days run without the per-value IEEE-division fallback.
+    const bool warp_fast = __all_sync(mask, p.fast);
     int kbase = 0;
     for (int day = 1; day < w.n_days; ++day) {
         const int lo = p.k1 - kbase;  // sub < lo  -> beta1
@@ -229,18 +237,33 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
         // switches beta1 -> beta2 today, 0 = every lane constant all day.
         const bool ramp_today = lo < hi && lo < nsub && hi > 0;
         const bool switch_today = lo > 0 && lo < nsub;
-        const unsigned mask = __activemask();
         if (__any_sync(mask, ramp_today)) {
+            if (SG_RAMP_MODE >= 1 && SUB > 0 && warp_fast) {
+                // Branch-free ramp day: every lane computes the ramp value
+                // (the warp would issue it anyway once any lane needs it) and
+                // selects; non-FP64 work per substep is two compares and
+                // selects plus the t_k load.
 #pragma unroll
-            for (int sub = 0; sub < nsub; ++sub) {
-                double bp = sub < lo ? p.bp1 : p.bp2;
-                if (sub >= lo && sub < hi) {
-                    double t;
-                    if constexpr (SUB > 0) t = tg.tgrid[kbase + sub];
-                    else t = dadd(static_cast<double>(day - 1), tg.subh[sub]);
-                    bp = ramp_bp(p, t, N, rN);
+                for (int sub = 0; sub < nsub; ++sub) {
+                    const double t = tg.tgrid[kbase + sub];
+                    const double beta = dadd(p.b1, dmul(p.slope, dsub(t, p.t1)));
+                    const double q0 = __dmul_rn(beta, rN);
+                    const double q = __fma_rn(__fma_rn(-q0, N, beta), rN, q0);
+                    const double bp = sub < lo ? p.bp1 : (sub < hi ? q : p.bp2);
+                    euler_substep(bp, g, mu, h, S, I, R, D);
                 }
-                euler_substep(bp, g, mu, h, S, I, R, D);
+            } else {
+#pragma unroll
+                for (int sub = 0; sub < nsub; ++sub) {
+                    double bp = sub < lo ? p.bp1 : p.bp2;
+                    if (sub >= lo && sub < hi) {
+                        double t;
+                        if constexpr (SUB > 0) t = tg.tgrid[kbase + sub];
+                        else t = dadd(static_cast<double>(day - 1), tg.subh[sub]);
+                        bp = ramp_bp(p, t, N, rN);
+                    }
+                    euler_substep(bp, g, mu, h, S, I, R, D);
+                }
             }
         } else if (__any_sync(mask, switch_today)) {
 #pragma unroll
@@ -379,20 +402,37 @@ __device__ __forceinline__ double to_uniform01(uint64_t x) {
     return dmul(static_cast<double>(x >> 11), 0x1.0p-53);
 }
 
-// Draw `n` consecutive values (n <= 312) starting at the uniform stream
+// Draw NDRAW consecutive values (NDRAW <= 12) starting at the uniform stream
 // position `count` (values drawn so far) from the SoA engine of particle p.
+// All 2*NDRAW+1 state words are loaded before any is rewritten: the batch's
+// words are distinct (NDRAW < 156), every "next" word is read before it is
+// twisted (old value, as the sequential twist reads it), and every "far"
+// word lies outside the batch — so the loads are independent and overlap.
 template <int NDRAW>
 __device__ __forceinline__ void mt_draw(uint64_t* __restrict__ st, size_t stride, size_t p, uint64_t count,
                                         double* out) {
+    static_assert(NDRAW >= 1 && NDRAW < kMtM, "batch must not reach its own far words");
+    const int i0 = static_cast<int>(count % kMtN);
+    uint64_t cur[NDRAW + 1];
+    uint64_t far[NDRAW];
+#pragma unroll
+    for (int j = 0; j <= NDRAW; ++j) {
+        int i = i0 + j;
+        if (i >= kMtN) i -= kMtN;
+        cur[j] = st[static_cast<size_t>(i) * stride + p];
+    }
 #pragma unroll
     for (int j = 0; j < NDRAW; ++j) {
-        const int i = static_cast<int>((count + j) % kMtN);
-        const uint64_t cur = st[static_cast<size_t>(i) * stride + p];
-        const int i1 = i + 1 == kMtN ? 0 : i + 1;
-        const uint64_t nxt = st[static_cast<size_t>(i1) * stride + p];
-        const int im = i + kMtM >= kMtN ? i + kMtM - kMtN : i + kMtM;
-        const uint64_t far = st[static_cast<size_t>(im) * stride + p];
-        const uint64_t w = mt_twist_word(cur, nxt, far);
+        int im = i0 + j + kMtM;
+        if (im >= kMtN) im -= kMtN;
+        if (im >= kMtN) im -= kMtN;
+        far[j] = st[static_cast<size_t>(im) * stride + p];
+    }
+#pragma unroll
+    for (int j = 0; j < NDRAW; ++j) {
+        int i = i0 + j;
+        if (i >= kMtN) i -= kMtN;
+        const uint64_t w = mt_twist_word(cur[j], cur[j + 1], far[j]);
         st[static_cast<size_t>(i) * stride + p] = w;
         out[j] = to_uniform01(mt_temper(w));
     }
