@@ -75,9 +75,13 @@ def mix_seed(base, index):
 
 
 def ops_per_eval(n_days, c_score=12, substeps=24):
-    """Algorithmic FP64 ops of one particle-window evaluation,
-    conservative floor without ramp credit: 14 per Euler substep + c_score per day."""
+    """Algorithmic FP64 ops of one particle-window evaluation without ramp credit
+    (SURVEY.md §8d): 14 per Euler substep (model.cpp:66-74, 96-99) + c_score per
+    day (12 for IRD-MXSE: 3 x {sub, mul, mul, max}, objectives.cpp:15-39)."""
     return (n_days - 1) * substeps * 14 + n_days * c_score
+
+
+RAMP_OPS = 5  # per ramp substep: t, t - t1, slope*, beta1+, beta/N (model.cpp:62-63, 67)
 
 
 class ClockSampler:
@@ -174,11 +178,12 @@ def barrier(world):
 
 
 def load_profile_traffic():
-    """dram bytes per launch of the step kernel from the committed ncu summary, if any."""
+    """DRAM bytes per particle-iteration of the step kernel from the committed
+    ncu --set full summary (profiles/ncu_step_kernel_*.json), if any."""
     for p in sorted((ROOT / "profiles").glob("ncu_step_kernel_*.json"), reverse=True):
         try:
             d = json.loads(p.read_text())
-            return d.get("dram_bytes_per_launch"), p.name
+            return d.get("dram_bytes_per_particle"), p.name
         except (OSError, ValueError):
             continue
     return None, None
@@ -186,31 +191,36 @@ def load_profile_traffic():
 
 # ---------------------------------------------------------------------------------------------
 def cpu_reference_sample(I, R, D, budget_s=12.0, threads=None):
-    """The reference C++ (oracle/_ref) or, absent, the C restatement: one
-    window's swarm of PARTICLES particles for as many iterations as fit the
-    budget; returns (evals/s, kind, cores, sample description)."""
+    """The reference C++ (oracle/_ref) or, absent, the C restatement, on the
+    host cores: whole window swarms of the sweep (PARTICLES particles, up to
+    ITERS iterations, the workload's seeds) until the time budget is spent;
+    returns (evals/s, kind, cores, sample description)."""
     from oracle import oracle_py
     kind = "reference" if oracle_py.REF_SO.exists() else "port"
     ora = oracle_py.load(kind)
     threads = threads or os.cpu_count() or 1
-    w = 60
-    a = w * DELTA
-    sl = slice(a, a + TAU + 1)
-    init = [POPULATION - I[a] - R[a] - D[a], I[a], R[a], D[a]]
     lo = [0.0] * 6
 
-    def run(iters):
+    def run(w, iters):
+        a = w * DELTA
+        sl = slice(a, a + TAU + 1)
+        init = [POPULATION - I[a] - R[a] - D[a], I[a], R[a], D[a]]
         t = time.perf_counter()
         ora.fit_swarm(SPEC, I[sl], R[sl], D[sl], init, POPULATION, lo, STAGE2_HI, PARTICLES, iters,
                       seed=mix_seed(BASE_SEED, w), n_threads=threads)
         return time.perf_counter() - t
 
-    t2 = run(2)
+    t2 = run(60, 2)
     iters = int(max(2, min(ITERS, budget_s / max(t2 / 2, 1e-6))))
-    dt = run(iters)
-    evals = PARTICLES * iters
-    return evals / dt, kind, threads, f"window {w} of the sweep, {PARTICLES} particles x {iters} iterations " \
-                                      f"({evals} evals, {dt:.1f} s)"
+    spent, evals, windows = 0.0, 0, []
+    for w in range(0, n_windows(len(I)), 17):
+        spent += run(w, iters)
+        evals += PARTICLES * iters
+        windows.append(w)
+        if spent >= budget_s:
+            break
+    return evals / spent, kind, threads, f"windows {windows} of the sweep, {PARTICLES} particles x {iters} " \
+                                         f"iterations each ({evals} evals, {spent:.1f} s)"
 
 
 def bench_reference(args):
@@ -300,11 +310,16 @@ def bench_ours(args):
     # roofline: the fused step kernel, all its launches of a step (the
     # partition lanes overlap, so the per-launch figure is the aggregate:
     # algorithmic ops of every step launch / device time of the step launches)
-    ops_step = evals_per_step * ops_per_eval(TAU + 1)
+    ramp_substeps = plan.ramp_substeps  # of the last timed run (identical every run)
+    ops_floor = evals_per_step * ops_per_eval(TAU + 1)
+    ops_step = ops_floor + RAMP_OPS * ramp_substeps
     steps_kernel_ms = statistics.mean(step_ms)
     kernel_ms = steps_kernel_ms / (step_launches if step_launches else 1)
     achieved = ops_step / (steps_kernel_ms * 1e-3) / 1e12
-    traffic, prof = load_profile_traffic()
+    achieved_floor = ops_floor / (steps_kernel_ms * 1e-3) / 1e12
+    bytes_per_particle, prof = load_profile_traffic()
+    # one "launch" of the roofline = one iteration of the sweep (all lanes)
+    traffic = bytes_per_particle * n_win * PARTICLES if bytes_per_particle else None
 
     # ---- e2e through the public calibration C-ABI with host buffers ----
     settings = _capi.sg_fit_settings(1, 0, 0.0, 2.0, 0.0, 1.0, 0.0, 0.1, 7, PARTICLES, iters, 0.5, 0.5, 0.5,
@@ -359,8 +374,14 @@ def bench_ours(args):
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
                          "frac": achieved * 1e12 / fp64_peak, "traffic": traffic,
                          "kernel": "pso_step_kernel<IRD,MXSE,24> (fused move+integrate+score+argmin)",
-                         "ops_per_eval": ops_per_eval(TAU + 1), "ops_note": "FP64 DADD/DMUL ops, no FMA (parity); "
-                         "floor count without ramp credit; peak = measured FP64 issue rate (sg_probe_fp64_rate)",
+                         "ops_per_eval_floor": ops_per_eval(TAU + 1),
+                         "ramp_substeps_per_eval": ramp_substeps / evals_per_step,
+                         "ops_per_eval": ops_step / evals_per_step,
+                         "frac_floor": achieved_floor * 1e12 / fp64_peak,
+                         "ops_note": "algorithmic FP64 ops (SURVEY.md §8d: 14/substep + 5/ramp substep + 12/day), "
+                                     "DADD/DMUL without FMA for bit parity; peak = FP64 issue rate measured "
+                                     "on this GPU by sg_probe_fp64_rate (neither MEASURED_PEAKS.json nor "
+                                     "B200_PROFILING.md has an FP64 figure)",
                          "kernel_ms_per_launch": kernel_ms, "launches_per_step": step_launches,
                          "step_kernels_ms": steps_kernel_ms, "seed_ms": statistics.mean(seed_ms), "profile": prof},
             "cpu_baseline": cpu,

@@ -160,6 +160,10 @@ int sg_plan_run_timed(sg_plan* plan, double* seed_ms, double* steps_ms);
 int sg_plan_results(sg_plan* plan, sg_swarm_result* results);
 uint64_t sg_plan_evals(const sg_plan* plan);  /* sum of n_particles * max_iters */
 uint64_t sg_plan_step_launches(const sg_plan* plan);  /* fused step launches per run */
+/* Ramp substeps evaluated by the last run (beta in its linear ramp,
+ * model.cpp:62-63): the R_ramp term of the algorithmic FP64 operation count
+ * (DESIGN.md §5).  Synchronous; 0 before the first run. */
+uint64_t sg_plan_ramp_substeps(sg_plan* plan);
 void sg_plan_destroy(sg_plan* plan);
 
 /* --- forecast ---------------------------------------------------------------

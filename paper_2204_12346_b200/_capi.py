@@ -96,6 +96,7 @@ SIGNATURES = {
     "sg_plan_run": (ctypes.c_int, [ctypes.c_void_p]),
     "sg_plan_run_timed": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp]),
     "sg_plan_step_launches": (ctypes.c_uint64, [ctypes.c_void_p]),
+    "sg_plan_ramp_substeps": (ctypes.c_uint64, [ctypes.c_void_p]),
     "sg_plan_results": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(sg_swarm_result)]),
     "sg_plan_evals": (ctypes.c_uint64, [ctypes.c_void_p]),
     "sg_plan_destroy": (None, [ctypes.c_void_p]),
@@ -347,6 +348,11 @@ class Plan:
         a, b = ctypes.c_double(), ctypes.c_double()
         self.ctx.check(lib().sg_plan_run_timed(self._h, ctypes.byref(a), ctypes.byref(b)))
         return a.value, b.value
+
+    @property
+    def ramp_substeps(self) -> int:
+        """Ramp substeps evaluated by the last run (R_ramp of the algorithmic op count)."""
+        return int(lib().sg_plan_ramp_substeps(self._h))
 
     @property
     def step_launches(self) -> int:

@@ -53,6 +53,7 @@ struct sg_window {
     ObsDay* d_obs = nullptr;
     ObsDay* d_robs = nullptr;
     unsigned char* d_flag = nullptr;
+    unsigned char* d_block = nullptr;  // the one allocation holding desc/obs/robs/flags
     size_t smem = 0;
 };
 
@@ -74,9 +75,12 @@ int cuda_fail(sg_ctx* ctx, cudaError_t e, const char* what) {
         if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
     } while (0)
 
+// Device memory comes from the device's stream-ordered pool (cudaMallocAsync
+// on the context stream; the pool keeps freed blocks, see sg_ctx_create), so
+// repeated calls of the calibration API do not pay cudaMalloc/cudaFree.
 template <class T>
-cudaError_t dalloc(T** p, size_t count) {
-    return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T));
+cudaError_t dalloc(T** p, size_t count, cudaStream_t st) {
+    return cudaMallocAsync(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T), st);
 }
 
 // Divisor admissibility for the 3-op exact division (sird_device.cuh
@@ -209,17 +213,18 @@ int launch_integrate(sg_ctx* ctx, const DevWindow& w, const double* d_params, co
     return SG_OK;
 }
 
-// RAII bundle of device allocations for one call.
+// RAII bundle of device allocations for one call / plan (stream-ordered).
 struct DevBufs {
+    cudaStream_t st = nullptr;
     std::vector<void*> ptrs;
     template <class T>
     cudaError_t alloc(T** p, size_t count) {
-        const cudaError_t e = dalloc(p, count);
+        const cudaError_t e = dalloc(p, count, st);
         if (e == cudaSuccess) ptrs.push_back(*p);
         return e;
     }
     ~DevBufs() {
-        for (void* p : ptrs) cudaFree(p);
+        for (void* p : ptrs) cudaFreeAsync(p, st);
     }
 };
 
@@ -258,6 +263,11 @@ int sg_ctx_create(int device, sg_ctx** out) {
         delete ctx;
         return SG_ERR_CUDA;
     }
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;  // keep freed blocks for the next plan
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     *out = ctx;
     return SG_OK;
 }
@@ -265,8 +275,9 @@ int sg_ctx_create(int device, sg_ctx** out) {
 void sg_ctx_destroy(sg_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
-    cudaFree(ctx->d_pos);
-    cudaFree(ctx->d_cost);
+    cudaFreeAsync(ctx->d_pos, ctx->stream);
+    cudaFreeAsync(ctx->d_cost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
     for (int l = 0; l < kMaxLanes; ++l) {
         if (ctx->side[l]) cudaStreamDestroy(ctx->side[l]);
         if (ctx->join[l]) cudaEventDestroy(ctx->join[l]);
@@ -335,19 +346,31 @@ int sg_window_create(sg_ctx* ctx, const double* infectious, const double* recove
         }
         d.kept[c] = static_cast<double>(kept);
     }
-    cudaError_t e = dalloc(&w->d_obs, n_days);
-    if (e == cudaSuccess) e = dalloc(&w->d_robs, n_days);
-    if (e == cudaSuccess) e = dalloc(&w->d_flag, 3 * static_cast<size_t>(n_days));
-    if (e == cudaSuccess) e = dalloc(&w->d_desc, 1);
+    // One device block: descriptor | obs | robs | flags.
+    const size_t obs_b = sizeof(ObsDay) * static_cast<size_t>(n_days);
+    const size_t off_obs = (sizeof(DevWindow) + 255) & ~size_t(255);
+    const size_t off_robs = off_obs + obs_b;
+    const size_t off_flag = off_robs + obs_b;
+    const size_t total = off_flag + flag.size();
+    unsigned char* block = nullptr;
+    cudaError_t e = dalloc(&block, total, ctx->stream);
     if (e == cudaSuccess) {
+        w->d_block = block;
+        w->d_desc = reinterpret_cast<DevWindow*>(block);
+        w->d_obs = reinterpret_cast<ObsDay*>(block + off_obs);
+        w->d_robs = reinterpret_cast<ObsDay*>(block + off_robs);
+        w->d_flag = block + off_flag;
         d.obs = w->d_obs;
         d.robs = w->d_robs;
         d.obs_flag = w->d_flag;
-        e = cudaMemcpy(w->d_obs, obs.data(), sizeof(ObsDay) * n_days, cudaMemcpyHostToDevice);
+        std::vector<unsigned char> staging(total);
+        std::memcpy(staging.data(), &d, sizeof d);
+        std::memcpy(staging.data() + off_obs, obs.data(), obs_b);
+        std::memcpy(staging.data() + off_robs, robs.data(), obs_b);
+        std::memcpy(staging.data() + off_flag, flag.data(), flag.size());
+        e = cudaMemcpyAsync(block, staging.data(), total, cudaMemcpyHostToDevice, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     }
-    if (e == cudaSuccess) e = cudaMemcpy(w->d_robs, robs.data(), sizeof(ObsDay) * n_days, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(w->d_flag, flag.data(), flag.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(w->d_desc, &d, sizeof d, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         sg_window_destroy(w);
         return cuda_fail(ctx, e, "sg_window_create");
@@ -363,10 +386,7 @@ int sg_window_create(sg_ctx* ctx, const double* infectious, const double* recove
 
 void sg_window_destroy(sg_window* w) {
     if (!w) return;
-    cudaFree(w->d_obs);
-    cudaFree(w->d_robs);
-    cudaFree(w->d_flag);
-    cudaFree(w->d_desc);
+    if (w->d_block) cudaFreeAsync(w->d_block, w->ctx->stream);
     delete w;
 }
 
@@ -393,13 +413,13 @@ int sg_eval_costs(sg_window* w, const double* positions, size_t n, size_t dim, d
     if (!positions || !costs) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null host buffer");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     if (ctx->scratch_n < n) {
-        cudaFree(ctx->d_pos);
-        cudaFree(ctx->d_cost);
+        cudaFreeAsync(ctx->d_pos, ctx->stream);
+        cudaFreeAsync(ctx->d_cost, ctx->stream);
         ctx->d_pos = nullptr;
         ctx->d_cost = nullptr;
         ctx->scratch_n = 0;
-        SG_CUDA(ctx, dalloc(&ctx->d_pos, 6 * n));
-        SG_CUDA(ctx, dalloc(&ctx->d_cost, n));
+        SG_CUDA(ctx, dalloc(&ctx->d_pos, 6 * n, ctx->stream));
+        SG_CUDA(ctx, dalloc(&ctx->d_cost, n, ctx->stream));
         ctx->scratch_n = n;
     }
     SG_CUDA(ctx, cudaMemcpyAsync(ctx->d_pos, positions, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
@@ -420,6 +440,7 @@ int sg_integrate_batch(sg_ctx* ctx, const double* params, size_t n, sg_state ini
     if (!params || !states || !finite) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null host buffer");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     DevBufs b;
+    b.st = ctx->stream;
     double *d_p, *d_init, *d_states;
     unsigned char* d_fin;
     SG_CUDA(ctx, b.alloc(&d_p, 6 * n));
@@ -449,6 +470,7 @@ int sg_integrate_states(sg_ctx* ctx, const double* params, const sg_state* inits
     if (!params || !inits || !states || !finite) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null host buffer");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     DevBufs b;
+    b.st = ctx->stream;
     double *d_p, *d_init, *d_states;
     unsigned char* d_fin;
     SG_CUDA(ctx, b.alloc(&d_p, 6 * n));
@@ -477,6 +499,7 @@ int sg_forecast_batch(sg_ctx* ctx, const double* params, const sg_state* junctio
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     const int n_days = horizon + 1;
     DevBufs b;
+    b.st = ctx->stream;
     double *d_p, *d_init, *d_states;
     unsigned char* d_fin;
     SG_CUDA(ctx, b.alloc(&d_p, 6 * n));
@@ -626,6 +649,7 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     for (size_t k = 0; k < wins.size(); ++k) wtab[k] = wins[k]->host;
 
     DevBufs& b = g.bufs;
+    b.st = ctx->stream;
     PsoPlanes& P = g.P;
     SG_CUDA(ctx, b.alloc(&g.d_sw, sw.size()));
     SG_CUDA(ctx, b.alloc(&g.d_cta, g.n_ctas));
@@ -856,6 +880,21 @@ int sg_plan_results(sg_plan* plan, sg_swarm_result* results) {
 
 uint64_t sg_plan_evals(const sg_plan* plan) { return plan ? plan->evals : 0; }
 
+uint64_t sg_plan_ramp_substeps(sg_plan* plan) {
+    if (!plan || !plan->ran) return 0;
+    sg_ctx* ctx = plan->ctx;
+    uint64_t total = 0;
+    for (SwarmGroup* g : plan->groups) {
+        std::vector<DevSwarmState> state(g->idx.size());
+        if (cudaMemcpyAsync(state.data(), g->d_state, sizeof(DevSwarmState) * state.size(), cudaMemcpyDeviceToHost,
+                            ctx->stream) != cudaSuccess ||
+            cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+            return 0;
+        for (const DevSwarmState& s : state) total += s.ramp_substeps;
+    }
+    return total;
+}
+
 void sg_plan_destroy(sg_plan* plan) {
     if (!plan) return;
     cudaSetDevice(plan->ctx->device);
@@ -906,6 +945,7 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
     if (n == 0) return SG_OK;
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     DevBufs b;
+    b.st = ctx->stream;
     double *d_lo, *d_hi, *d_cost = nullptr, *d_par = nullptr, *d_D;
     SG_CUDA(ctx, b.alloc(&d_lo, 6));
     SG_CUDA(ctx, b.alloc(&d_hi, 6));
@@ -959,6 +999,7 @@ extern "C" int sg_probe_fp64_rate(sg_ctx* ctx, double* ops_per_s) {
     if (!ctx || !ops_per_s) return SG_ERR_INVALID_ARGUMENT;
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     DevBufs b;
+    b.st = ctx->stream;
     double* d_out;
     SG_CUDA(ctx, b.alloc(&d_out, 1));
     const int iters = 4096;

@@ -178,6 +178,7 @@ struct DevSwarmState {
     double best[6];      // Swarm::best_position_ (0 initially, pso.cpp:63)
     unsigned int arrived;
     unsigned int pad;
+    unsigned long long ramp_substeps;  // telemetry: ramp substeps evaluated (roofline op count)
 };
 
 struct PsoPlanes {
@@ -221,6 +222,7 @@ __global__ void __launch_bounds__(kStepThreads) pso_init_kernel(const DevSwarm* 
         state[s].best_cost = __longlong_as_double(0x7FF0000000000000LL);
         for (int d = 0; d < 6; ++d) state[s].best[d] = 0.0;
         state[s].arrived = 0;
+        state[s].ramp_substeps = 0;
     }
     if (i >= sw.n) return;
     const size_t p = sw.offset + i;
@@ -288,8 +290,10 @@ __device__ __forceinline__ void move_particle(const DevSwarm& sw, const DevSwarm
 // sequential lowest-index scan.  No CTA-wide barrier: warps retire on their own.
 __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& st, const PsoPlanes& P, int s,
                                             bool active, size_t p, uint64_t i, double c, uint32_t wslot,
-                                            uint64_t it) {
+                                            uint64_t it, int ramp) {
     const size_t stride = P.stride;
+    const unsigned int wramp = __reduce_add_sync(0xFFFFFFFFu, static_cast<unsigned int>(active ? ramp : 0));
+    if ((threadIdx.x & 31) == 0 && wramp) atomicAdd(&st.ramp_substeps, static_cast<unsigned long long>(wramp));
     double my_c = __longlong_as_double(0x7FF0000000000000LL);
     unsigned long long my_i = ~0ULL;
     if (active) {
@@ -376,14 +380,16 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
     const bool active = i < sw.n;
     const size_t p = sw.offset + (active ? i : 0);
     double c = 0.0;
+    int ramp = 0;
     if (active) {
         double x[6];
 #pragma unroll
         for (int d = 0; d < 6; ++d) x[d] = P.x[d * P.stride + p];
         if (it > 0) move_particle(sw, state[s], P, p, it, x);
-        c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag);
+        c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag, &ramp);
     }
-    finish_step(sw, state[s], P, s, active, p, i, c, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it);
+    finish_step(sw, state[s], P, s, active, p, i, c, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it,
+                ramp);
 }
 
 // ---- ramp-coherent evaluation order (swarms of at most kSortMax particles) ----
@@ -502,13 +508,15 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
     const uint64_t i = active ? perm[sw.offset + slot] : 0;
     const size_t p = sw.offset + i;
     double c = 0.0;
+    int ramp = 0;
     if (active) {
         double x[6];
 #pragma unroll
         for (int d = 0; d < 6; ++d) x[d] = P.x[d * P.stride + p];
-        c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag);
+        c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag, &ramp);
     }
-    finish_step(sw, state[s], P, s, active, p, i, c, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it);
+    finish_step(sw, state[s], P, s, active, p, i, c, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it,
+                ramp);
 }
 
 // ---- forecast-scenario ensemble ----------------------------------------------------

@@ -349,11 +349,18 @@ struct ScoreSink {
 
 // Full particle-window evaluation: objective_value(spec, slice,
 // integrate_euler(params)) (calibration.cpp:148-152).
+// *ramp receives the particle's number of ramp substeps (the R_ramp of the
+// algorithmic operation count).
 template <int FAM, int MET, int SUB>
 __device__ __forceinline__ double eval_particle(const double* x, const DevWindow& w, const TimeGrid& tg,
-                                                const ObsDay* obs, const ObsDay* robs, const unsigned char* flag) {
-    if (!w.init_finite) return __longlong_as_double(0x7FF0000000000000LL);
+                                                const ObsDay* obs, const ObsDay* robs, const unsigned char* flag,
+                                                int* ramp = nullptr) {
+    if (!w.init_finite) {
+        if (ramp) *ramp = 0;
+        return __longlong_as_double(0x7FF0000000000000LL);
+    }
     const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w);
+    if (ramp) *ramp = p.k2 - p.k1;
     double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
     ScoreSink<FAM, MET> sink(w, obs, robs, flag);
     sink.day(0, S, I, R, D);  // day 0 is the initial state, bit for bit (model.cpp:85)
