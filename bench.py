@@ -139,6 +139,12 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# Collective plumbing: NCCL between GPUs.  SG_BENCH_BACKEND=gloo (with ranks
+# sharing a GPU) exists only to exercise the multi-rank code path on a
+# one-GPU box; ranks never wait on each other inside kernels.
+BACKEND = os.environ.get("SG_BENCH_BACKEND", "nccl")
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -146,9 +152,17 @@ def dist_setup():
     if world > 1:
         import torch
         import torch.distributed as dist
+        local = local % max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(BACKEND)
     return world, rank, local
+
+
+def _coll_device():
+    return "cuda" if BACKEND == "nccl" else "cpu"
 
 
 def allreduce_max(x, world):
@@ -156,7 +170,7 @@ def allreduce_max(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([float(x)], dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -166,7 +180,7 @@ def allreduce_sum(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([float(x)], dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 

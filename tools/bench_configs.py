@@ -1,0 +1,123 @@
+"""The other BASELINE.json configs on one GPU (bench.py measures configs[1], C2).
+
+  C1  single 21-day window (tau=20), 256 particles x 500 iterations
+  C3  single 36-day window, one swarm of 1,048,576 particles x --c3-iters iterations
+  C4  parameter-stability restarts: 139 windows x R restarts x 256 particles x 500
+      iterations (R = --c4-restarts; BASELINE's 1024 restarts shard over 8 GPUs)
+  C5  forecast-scenario ensemble: 10^6 sampled parameter sets per window, 21-day
+      forecast, all 139 windows (device time per window; host copy excluded)
+
+Each prints one JSON line (evals/s device-timed with CUDA events; the
+reference CPU path timed on a bounded sample beside it when --cpu).
+"""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import bench  # noqa: E402
+import paper_2204_12346_b200 as eng  # noqa: E402
+
+I, R, D = bench.load_series()
+N = bench.POPULATION
+
+
+def window(ctx, w, tau, spec=bench.SPEC):
+    a = w * bench.DELTA
+    sl = slice(a, a + tau + 1)
+    return eng.Window(ctx, I[sl], R[sl], D[sl], [N - I[a] - R[a] - D[a], I[a], R[a], D[a]], N, spec)
+
+
+def stage2(tau):
+    return [2.0, 2.0, float(tau - 7), float(tau - 7), 1.0, 0.1]
+
+
+def timed_plan(ctx, swarms, reps=2):
+    plan = eng.Plan(ctx, swarms)
+    plan.run_timed()
+    best = min(plan.run_timed()[1] for _ in range(reps))
+    ramp = plan.ramp_substeps
+    res = plan.results()
+    evals = plan.evals
+    plan.close()
+    return best, evals, ramp, res
+
+
+def cpu_sample(w, tau, n, iters):
+    from oracle import oracle_py
+    ora = oracle_py.load("reference" if oracle_py.REF_SO.exists() else "port")
+    a = w * bench.DELTA
+    sl = slice(a, a + tau + 1)
+    import os
+    t = time.perf_counter()
+    ora.fit_swarm(bench.SPEC, I[sl], R[sl], D[sl], [N - I[a] - R[a] - D[a], I[a], R[a], D[a]], N, [0] * 6,
+                  stage2(tau), n, iters, seed=bench.mix_seed(bench.BASE_SEED, w), n_threads=os.cpu_count())
+    dt = time.perf_counter() - t
+    return n * iters / dt, dt
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--c3-iters", type=int, default=100)
+    ap.add_argument("--c4-restarts", type=int, default=32)
+    ap.add_argument("--c5-windows", type=int, default=139)
+    ap.add_argument("--cpu", action="store_true")
+    args = ap.parse_args()
+    ctx = eng.Context(0)
+    peak = eng.probe_fp64_rate(ctx)
+
+    # C1
+    win = window(ctx, 0, 20)
+    ms, evals, ramp, res = timed_plan(ctx, [dict(window=win, lower=[0] * 6, upper=stage2(20), n_particles=256,
+                                                 max_iters=500, seed=bench.mix_seed(bench.BASE_SEED, 0))], reps=5)
+    line = {"config": "C1", "evals": evals, "device_ms": ms, "evals_per_s": evals / ms * 1e3, "best": res[0][2]}
+    if args.cpu:
+        v, dt = cpu_sample(0, 20, 256, 500)
+        line["cpu_reference_evals_per_s"] = v
+        line["cpu_reference_s"] = dt
+    print(json.dumps(line), flush=True)
+
+    # C3
+    win = window(ctx, 60, 35)
+    ms, evals, ramp, res = timed_plan(ctx, [dict(window=win, lower=[0] * 6, upper=stage2(35), n_particles=1 << 20,
+                                                 max_iters=args.c3_iters, seed=7)], reps=1)
+    ops = evals * bench.ops_per_eval(36) + bench.RAMP_OPS * ramp
+    print(json.dumps({"config": "C3", "particles": 1 << 20, "iters": args.c3_iters, "device_ms": ms,
+                      "evals_per_s": evals / ms * 1e3, "fp64_frac": ops / (ms * 1e-3) / peak, "best": res[0][2]}),
+          flush=True)
+
+    # C4 (fraction of the restarts)
+    wins = [window(ctx, w, 35) for w in range(139)]
+    swarms = [dict(window=wins[w], lower=[0] * 6, upper=stage2(35), n_particles=256, max_iters=500,
+                   seed=bench.mix_seed(bench.BASE_SEED + r, w)) for r in range(args.c4_restarts) for w in range(139)]
+    ms, evals, ramp, res = timed_plan(ctx, swarms, reps=1)
+    ops = evals * bench.ops_per_eval(36) + bench.RAMP_OPS * ramp
+    full = 139 * 1024 * 256 * 500
+    print(json.dumps({"config": "C4", "restarts": args.c4_restarts, "swarms": len(swarms), "device_ms": ms,
+                      "evals_per_s": evals / ms * 1e3, "fp64_frac": ops / (ms * 1e-3) / peak,
+                      "full_c4_evals": full, "full_c4_projected_s_1gpu": full / (evals / ms * 1e3),
+                      "full_c4_projected_s_8gpu": full / (evals / ms * 1e3) / 8}), flush=True)
+
+    # C5 ensemble: 1e6 sampled parameter sets per window, 21-day forecast
+    n = 1_000_000
+    tot_ms = 0.0
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    for w in range(args.c5_windows):
+        win = wins[w]
+        t0 = time.perf_counter()
+        costs, params, deaths = win.forecast_ensemble([0] * 6, stage2(35), seed=bench.mix_seed(2204, w), n=n,
+                                                      horizon=21, want_costs=True, want_params=False)
+        tot_ms += (time.perf_counter() - t0) * 1e3
+    print(json.dumps({"config": "C5", "windows": args.c5_windows, "samples_per_window": n, "horizon": 21,
+                      "wall_ms_incl_d2h": tot_ms, "samples_per_s_wall": args.c5_windows * n / tot_ms * 1e3,
+                      "finite_forecasts_last_window": int(np.isfinite(deaths[:, -1]).sum())}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
