@@ -182,6 +182,18 @@ struct PermEvalLaunch {
 };
 
 template <int F, int M, int S>
+struct SwarmLaunch {
+    static void run(unsigned grid, unsigned threads, uint32_t swarm_offset, const DevSwarm* sw, const DevWindow* wins,
+                    const PsoPlanes& P, DevSwarmState* state, size_t smem, cudaStream_t st, cudaError_t* err) {
+        auto k = pso_swarm_kernel<F, M, S>;
+        *err = prepare_smem(k, smem);
+        if (*err != cudaSuccess) return;
+        k<<<grid, threads, smem, st>>>(sw, wins, P, state, swarm_offset);
+        *err = cudaGetLastError();
+    }
+};
+
+template <int F, int M, int S>
 struct EnsembleLaunch {
     static void run(const DevWindow* w, const DevWindow& fwin, const double* lo, const double* hi, uint64_t seed,
                     size_t n, int horizon, double* costs, double* params, double* deaths, size_t smem,
@@ -560,6 +572,8 @@ struct SwarmGroup {
     };
     std::vector<Lane> lanes;  // swarm partitions launched on separate streams
     bool sorted = false;      // every swarm <= kSortMax: move+sort / permuted eval
+    bool persistent = false;  // every swarm <= kPersistMax: one CTA per swarm, one launch
+    unsigned threads = 0;     // persistent CTA size
     uint32_t* d_perm = nullptr;
     unsigned char* d_keys = nullptr;
     size_t n_total = 0, n_ctas = 0, smem = 0;
@@ -642,7 +656,12 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
 #ifndef SG_SORT
 #define SG_SORT 0
 #endif
-    g.sorted = SG_SORT != 0;
+    g.sorted = SG_SORT != 0 && !g.persistent;
+    if (g.persistent) {
+        uint64_t max_n = 0;
+        for (const DevSwarm& s : sw) max_n = std::max(max_n, s.n);
+        g.threads = static_cast<unsigned>(std::min<uint64_t>(kSwarmThreadsMax, (max_n + 31) / 32 * 32));
+    }
     for (const DevSwarm& s : sw)
         if (s.n > static_cast<uint64_t>(kSortMax)) g.sorted = false;
     std::vector<DevWindow> wtab(wins.size());
@@ -679,6 +698,7 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
 }
 
 int seed_group(sg_ctx* ctx, SwarmGroup& g) {
+    if (g.persistent) return SG_OK;  // the persistent kernel seeds its own swarm
     pso_init_kernel<<<static_cast<unsigned>(g.n_ctas), kStepThreads, 0, ctx->stream>>>(g.d_sw, g.d_cta, g.P,
                                                                                       g.d_state);
     ctx->launches += 1;
@@ -697,6 +717,14 @@ int ensure_lanes(sg_ctx* ctx) {
 }
 
 int step_group(sg_ctx* ctx, SwarmGroup& g) {
+    if (g.persistent) {
+        cudaError_t err = cudaSuccess;
+        dispatch<SwarmLaunch>(g.family, g.metric, g.substeps, static_cast<unsigned>(g.idx.size()), g.threads, 0u,
+                              g.d_sw, g.d_win, g.P, g.d_state, g.smem, ctx->stream, &err);
+        ctx->launches += 1;
+        if (err != cudaSuccess) return cuda_fail(ctx, err, "pso_swarm_kernel");
+        return SG_OK;
+    }
     const size_t n_lanes = g.lanes.size();
     if (n_lanes > 1) {
         const int rc = ensure_lanes(ctx);
@@ -750,6 +778,9 @@ int sg_plan_create(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg
     plan->n_desc = n_swarms;
     plan->status.assign(n_swarms, SG_OK);
     std::string why;
+    uint64_t total_particles = 0;
+    for (size_t k = 0; k < n_swarms; ++k) total_particles += swarms[k].n_particles;
+    const bool small_plan = total_particles <= 8 * static_cast<uint64_t>(kStepThreads);
     for (size_t k = 0; k < n_swarms; ++k) {
         if (!swarm_config_valid(swarms[k], &why)) {
             plan->status[k] = SG_ERR_INVALID_ARGUMENT;
@@ -763,9 +794,13 @@ int sg_plan_create(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg
         }
         const DevWindow& w = swarms[k].window->host;
         const int sub = kernel_sub(w.n_days, w.substeps);
+        // Persistent one-CTA-per-swarm mode only pays when the plan cannot fill
+        // the GPU anyway (latency-bound single small swarms, C1); many small
+        // swarms (C4) run faster as flat per-iteration launches.
+        const bool pers = swarms[k].n_particles <= static_cast<uint64_t>(kPersistMax) && small_plan;
         SwarmGroup* g = nullptr;
         for (SwarmGroup* x : plan->groups)
-            if (x->family == w.family && x->metric == w.metric && x->substeps == sub) g = x;
+            if (x->family == w.family && x->metric == w.metric && x->substeps == sub && x->persistent == pers) g = x;
         if (!g) {
             g = new (std::nothrow) SwarmGroup;
             if (!g) {
@@ -775,6 +810,7 @@ int sg_plan_create(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg
             g->family = w.family;
             g->metric = w.metric;
             g->substeps = sub;
+            g->persistent = pers;
             plan->groups.push_back(g);
         }
         g->idx.push_back(k);
@@ -840,7 +876,7 @@ int sg_plan_run_timed(sg_plan* plan, double* seed_ms, double* steps_ms) {
 uint64_t sg_plan_step_launches(const sg_plan* plan) {
     uint64_t n = 0;
     if (plan)
-        for (const SwarmGroup* g : plan->groups) n += g->iters * g->lanes.size();
+        for (const SwarmGroup* g : plan->groups) n += g->persistent ? 1 : g->iters * g->lanes.size();
     return n;
 }
 

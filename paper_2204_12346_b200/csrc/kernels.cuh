@@ -209,23 +209,10 @@ __device__ __forceinline__ double std_clamp(double v, double lo, double hi) {
     return hi < m ? hi : m;
 }
 
-// Swarm::Swarm (pso.cpp:47-75): engine i = mt19937_64(mix_seed(seed, i));
-// x[d] = lo[d] + u*(hi[d]-lo[d]) for d = 0..5 in order; repair; v = 0;
-// pbest = x; pbest cost = +inf.
-__global__ void __launch_bounds__(kStepThreads) pso_init_kernel(const DevSwarm* __restrict__ swarms,
-                                                                const uint32_t* __restrict__ cta_swarm,
-                                                                PsoPlanes P, DevSwarmState* __restrict__ state) {
-    const int s = static_cast<int>(cta_swarm[blockIdx.x]);
-    const DevSwarm& sw = swarms[s];
-    const uint64_t i = static_cast<uint64_t>(blockIdx.x - sw.cta_begin) * blockDim.x + threadIdx.x;
-    if (i == 0) {
-        state[s].best_cost = __longlong_as_double(0x7FF0000000000000LL);
-        for (int d = 0; d < 6; ++d) state[s].best[d] = 0.0;
-        state[s].arrived = 0;
-        state[s].ramp_substeps = 0;
-    }
-    if (i >= sw.n) return;
-    const size_t p = sw.offset + i;
+// Swarm::Swarm (pso.cpp:47-75) for particle i of a swarm (slot p):
+// engine i = mt19937_64(mix_seed(seed, i)); x[d] = lo[d] + u*(hi[d]-lo[d])
+// for d = 0..5 in order; repair; v = 0; pbest = x; pbest cost = +inf.
+__device__ __forceinline__ void init_particle(const DevSwarm& sw, const PsoPlanes& P, size_t p, uint64_t i) {
     const size_t stride = P.stride;
     // seed: mt[0] = seed; mt[j] = f*(mt[j-1] ^ (mt[j-1] >> 62)) + j
     uint64_t m = mix_seed(sw.seed, i);
@@ -249,6 +236,22 @@ __global__ void __launch_bounds__(kStepThreads) pso_init_kernel(const DevSwarm* 
     P.pbc[p] = __longlong_as_double(0x7FF0000000000000LL);
 }
 
+__global__ void __launch_bounds__(kStepThreads) pso_init_kernel(const DevSwarm* __restrict__ swarms,
+                                                                const uint32_t* __restrict__ cta_swarm,
+                                                                PsoPlanes P, DevSwarmState* __restrict__ state) {
+    const int s = static_cast<int>(cta_swarm[blockIdx.x]);
+    const DevSwarm& sw = swarms[s];
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x - sw.cta_begin) * blockDim.x + threadIdx.x;
+    if (i == 0) {
+        state[s].best_cost = __longlong_as_double(0x7FF0000000000000LL);
+        for (int d = 0; d < 6; ++d) state[s].best[d] = 0.0;
+        state[s].arrived = 0;
+        state[s].ramp_substeps = 0;
+    }
+    if (i >= sw.n) return;
+    init_particle(sw, P, sw.offset + i, i);
+}
+
 // (cost, index) ordering of the global-best scan (pso.cpp:90-96): the lowest
 // cost wins, ties go to the lowest index; NaN never wins (pbest costs are never
 // NaN: pbest only takes a cost that compared less, pso.cpp:84).
@@ -260,10 +263,10 @@ __device__ __forceinline__ bool better(double ca, unsigned long long ia, double 
 // particle's engine (r1, r2 per dimension, always both), velocity and
 // clamped position update, repair.  Reads the global best published after
 // iteration it-1 and writes x, v; returns the new position in x.
-__device__ __forceinline__ void move_particle(const DevSwarm& sw, const DevSwarmState& st, const PsoPlanes& P,
-                                              size_t p, uint64_t it, double* x) {
+__device__ __forceinline__ void move_particle(const DevSwarm& sw, double best_cost, const double* best,
+                                              const PsoPlanes& P, size_t p, uint64_t it, double* x) {
     const size_t stride = P.stride;
-    const bool have_best = st.best_cost < __longlong_as_double(0x7FF0000000000000LL);  // pso.cpp:106
+    const bool have_best = best_cost < __longlong_as_double(0x7FF0000000000000LL);  // pso.cpp:106
     double u[12];
     mt_draw<12>(P.mt, stride, p, 6 + 12 * (it - 1), u);
 #pragma unroll
@@ -274,7 +277,7 @@ __device__ __forceinline__ void move_particle(const DevSwarm& sw, const DevSwarm
         const double pbd = P.pb[d * stride + p];
         // vel = w*v + (c1*r1)*(pbest - x)   (pso.cpp:116)
         double vel = dadd(dmul(sw.w, vd), dmul(dmul(sw.c1, r1), dsub(pbd, x[d])));
-        if (have_best) vel = dadd(vel, dmul(dmul(sw.c2, r2), dsub(st.best[d], x[d])));  // pso.cpp:117-119
+        if (have_best) vel = dadd(vel, dmul(dmul(sw.c2, r2), dsub(best[d], x[d])));  // pso.cpp:117-119
         P.v[d * stride + p] = vel;
         x[d] = std_clamp(dadd(x[d], vel), sw.lo[d], sw.hi[d]);  // pso.cpp:121
     }
@@ -385,7 +388,7 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
         double x[6];
 #pragma unroll
         for (int d = 0; d < 6; ++d) x[d] = P.x[d * P.stride + p];
-        if (it > 0) move_particle(sw, state[s], P, p, it, x);
+        if (it > 0) move_particle(sw, state[s].best_cost, state[s].best, P, p, it, x);
         c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag, &ramp);
     }
     finish_step(sw, state[s], P, s, active, p, i, c, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it,
@@ -439,7 +442,7 @@ __global__ void __launch_bounds__(kStepThreads) pso_move_kernel(const DevSwarm* 
     double x[6];
 #pragma unroll
     for (int d = 0; d < 6; ++d) x[d] = P.x[d * P.stride + p];
-    if (it > 0) move_particle(sw, state[s], P, p, it, x);
+    if (it > 0) move_particle(sw, state[s].best_cost, state[s].best, P, p, it, x);
     const double tlo = sw.lo[2] < sw.lo[3] ? sw.lo[2] : sw.lo[3];
     const double thi = sw.hi[2] > sw.hi[3] ? sw.hi[2] : sw.hi[3];
     keys[p] = static_cast<unsigned char>(morton_key(x[2], x[3], tlo, thi));
@@ -517,6 +520,109 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
     }
     finish_step(sw, state[s], P, s, active, p, i, c, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it,
                 ramp);
+}
+
+// ---- small swarms: one persistent CTA per swarm --------------------------------
+//
+// Swarms of at most kPersistMax particles (C1: 256, C4: 256 per restart) run
+// their whole optimize() (pso.cpp:129-143) in one launch: seeding, then every
+// iteration's move -> evaluate -> personal best -> block argmin -> global
+// best, with the global best kept in shared memory and __syncthreads as the
+// iteration barrier.  No per-iteration launches, window staged once.
+constexpr int kSwarmThreadsMax = 256;
+constexpr int kPersistMax = 1024;
+
+template <int FAM, int MET, int SUB>
+__global__ void __launch_bounds__(kSwarmThreadsMax, 2) pso_swarm_kernel(const DevSwarm* __restrict__ swarms,
+                                                                     const DevWindow* __restrict__ windows,
+                                                                     PsoPlanes P, DevSwarmState* __restrict__ state,
+                                                                     uint32_t swarm_offset) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ DevWindow sdesc;
+    __shared__ double red_c[kSwarmThreadsMax / 32];
+    __shared__ unsigned long long red_i[kSwarmThreadsMax / 32];
+    __shared__ double gbest[6];
+    __shared__ double gbest_cost;
+    const int s = static_cast<int>(blockIdx.x + swarm_offset);
+    const DevSwarm& sw = swarms[s];
+    const SmemWindow win = stage_window(windows + sw.window, &sdesc, smem);
+    const uint32_t n = static_cast<uint32_t>(sw.n);
+    const size_t stride = P.stride;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) init_particle(sw, P, sw.offset + i, i);
+    if (threadIdx.x == 0) {
+        gbest_cost = __longlong_as_double(0x7FF0000000000000LL);
+        for (int d = 0; d < 6; ++d) gbest[d] = 0.0;
+    }
+    unsigned long long ramp_acc = 0;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int n_warps = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    for (uint64_t it = 0; it < sw.max_iters; ++it) {
+        double my_c = __longlong_as_double(0x7FF0000000000000LL);
+        unsigned long long my_i = ~0ULL;
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const size_t p = sw.offset + i;
+            double x[6];
+#pragma unroll
+            for (int d = 0; d < 6; ++d) x[d] = P.x[d * stride + p];
+            if (it > 0) move_particle(sw, gbest_cost, gbest, P, p, it, x);
+            int ramp = 0;
+            const double c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag, &ramp);
+            ramp_acc += static_cast<unsigned long long>(ramp);
+            P.cost[p] = c;
+            double pbc = P.pbc[p];
+            if (c < pbc) {  // pso.cpp:83-89
+                pbc = c;
+                P.pbc[p] = c;
+#pragma unroll
+                for (int d = 0; d < 6; ++d) P.pb[d * stride + p] = x[d];
+            }
+            if (better(pbc, i, my_c, my_i)) {
+                my_c = pbc;
+                my_i = i;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double oc = __shfl_down_sync(0xFFFFFFFFu, my_c, off);
+            const unsigned long long oi = __shfl_down_sync(0xFFFFFFFFu, my_i, off);
+            if (better(oc, oi, my_c, my_i)) {
+                my_c = oc;
+                my_i = oi;
+            }
+        }
+        if (lane == 0) {
+            red_c[warp] = my_c;
+            red_i[warp] = my_i;
+        }
+        __syncthreads();  // minima and personal bests of this iteration visible
+        if (threadIdx.x == 0) {
+            double bc = red_c[0];
+            unsigned long long bi = red_i[0];
+            for (int k = 1; k < n_warps; ++k)
+                if (better(red_c[k], red_i[k], bc, bi)) {
+                    bc = red_c[k];
+                    bi = red_i[k];
+                }
+            if (bc < gbest_cost) {  // pso.cpp:90-96: strict, lowest index on ties
+                gbest_cost = bc;
+                for (int d = 0; d < 6; ++d) gbest[d] = P.pb[d * stride + sw.offset + bi];
+            }
+            P.history[static_cast<size_t>(s) * P.hist_stride + it] = gbest_cost;
+        }
+        __syncthreads();  // global best published for the next move
+    }
+    // per-thread count <= iterations * 840 * ceil(n/threads) < 2^32 / 32
+    const unsigned long long wr = __reduce_add_sync(0xFFFFFFFFu, static_cast<unsigned int>(ramp_acc));
+    if (threadIdx.x == 0) {
+        state[s].best_cost = gbest_cost;
+        for (int d = 0; d < 6; ++d) state[s].best[d] = gbest[d];
+        state[s].arrived = 0;
+        state[s].ramp_substeps = 0;
+    }
+    __syncthreads();
+    if (lane == 0) atomicAdd(&state[s].ramp_substeps, wr);
 }
 
 // ---- forecast-scenario ensemble ----------------------------------------------------
