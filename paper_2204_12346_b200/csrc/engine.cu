@@ -1009,6 +1009,18 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
 
 // ---- diagnostics -------------------------------------------------------------------
 
+extern "C" int sg_debug_day_classes(unsigned long long* out3) {
+#if SG_DAY_COUNTERS
+    cudaMemcpyFromSymbol(out3, g_day_class, sizeof(unsigned long long) * 3);
+    unsigned long long zero[3] = {0, 0, 0};
+    cudaMemcpyToSymbol(g_day_class, zero, sizeof zero);
+    return SG_OK;
+#else
+    out3[0] = out3[1] = out3[2] = 0;
+    return SG_ERR_INVALID_ARGUMENT;
+#endif
+}
+
 namespace {
 
 // 8 independent DADD/DMUL chains per thread, alternating, no FMA: the FP64

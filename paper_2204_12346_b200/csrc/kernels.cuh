@@ -367,6 +367,44 @@ __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& s
 // the move of iteration it-1 (which closes step it-1 in the reference), then
 // evaluate, personal best, and the global-best fold.  Thread t of a swarm's
 // CTA range owns particle t for all iterations.  Used for large swarms.
+#ifndef SG_CTA_SORT
+#define SG_CTA_SORT 0
+#endif
+
+// Morton code of the switch times (t1, t2), `bits` per coordinate, over the
+// swarm's time box: particles with close (t1, t2) get close keys.
+__device__ __forceinline__ uint32_t morton_tt(double t1, double t2, double lo, double hi, int bits) {
+    const double span = hi - lo;
+    const float sc = span > 0.0 ? static_cast<float>((1 << bits) / span) : 0.0f;
+    int q1 = static_cast<int>(static_cast<float>(t1 - lo) * sc);
+    int q2 = static_cast<int>(static_cast<float>(t2 - lo) * sc);
+    q1 = min(max(q1, 0), (1 << bits) - 1);  // NaN converts to 0 on the device
+    q2 = min(max(q2, 0), (1 << bits) - 1);
+    uint32_t key = 0;
+    for (int b = 0; b < bits; ++b) key |= (((q1 >> b) & 1u) << (2 * b + 1)) | (((q2 >> b) & 1u) << (2 * b));
+    return key;
+}
+
+// Ascending bitonic sort of kStepThreads 32-bit keys in shared memory.
+__device__ __forceinline__ void cta_bitonic_sort(uint32_t* v) {
+    const int t = threadIdx.x;
+    for (int size = 2; size <= kStepThreads; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            __syncthreads();
+            const int j = t ^ stride;
+            if (j > t) {
+                const uint32_t a = v[t], b = v[j];
+                const bool up = (t & size) == 0;
+                if ((a > b) == up) {
+                    v[t] = b;
+                    v[j] = a;
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
 template <int FAM, int MET, int SUB>
 __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
     pso_step_kernel(const DevSwarm* __restrict__ swarms, const uint32_t* __restrict__ cta_swarm,
@@ -379,18 +417,43 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
     const DevSwarm& sw = swarms[s];
     if (it >= sw.max_iters) return;  // CTA-uniform
     const SmemWindow win = stage_window(windows + sw.window, &sdesc, smem);
-    const uint64_t i = static_cast<uint64_t>(cta - sw.cta_begin) * blockDim.x + threadIdx.x;
-    const bool active = i < sw.n;
-    const size_t p = sw.offset + (active ? i : 0);
-    double c = 0.0;
-    int ramp = 0;
+    const uint64_t first = static_cast<uint64_t>(cta - sw.cta_begin) * blockDim.x;
+    uint64_t i = first + threadIdx.x;
+    bool active = i < sw.n;
+    size_t p = sw.offset + (active ? i : 0);
+    double x[6];
     if (active) {
-        double x[6];
 #pragma unroll
         for (int d = 0; d < 6; ++d) x[d] = P.x[d * P.stride + p];
         if (it > 0) move_particle(sw, state[s].best_cost, state[s].best, P, p, it, x);
-        c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag, &ramp);
     }
+#if SG_CTA_SORT
+    {
+        // Ramp-coherent evaluation order inside the CTA: sort the CTA's
+        // particles by the Morton code of their new (t1, t2) and let thread
+        // slot t evaluate the t-th of them, so a warp's lanes share their
+        // beta-ramp days (the warp pays a ramp substep if any lane ramps).
+        // Positions were written by their movers above; the order only
+        // decides which thread evaluates which particle, never a result.
+        __shared__ uint32_t order[kStepThreads];
+        const double tlo = sw.lo[2] < sw.lo[3] ? sw.lo[2] : sw.lo[3];
+        const double thi = sw.hi[2] > sw.hi[3] ? sw.hi[2] : sw.hi[3];
+        const uint32_t key = active ? morton_tt(x[2], x[3], tlo, thi, 5) : 0x3FFu + 1u;
+        order[threadIdx.x] = (key << 8) | threadIdx.x;
+        cta_bitonic_sort(order);
+        const uint32_t q = order[threadIdx.x] & 0xFFu;
+        i = first + q;
+        active = i < sw.n;
+        p = sw.offset + (active ? i : 0);
+        if (active) {
+#pragma unroll
+            for (int d = 0; d < 6; ++d) x[d] = P.x[d * P.stride + p];
+        }
+    }
+#endif
+    double c = 0.0;
+    int ramp = 0;
+    if (active) c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag, &ramp);
     finish_step(sw, state[s], P, s, active, p, i, c, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it,
                 ramp);
 }

@@ -15,6 +15,13 @@
 #ifndef SG_RAMP_MODE
 #define SG_RAMP_MODE 1
 #endif
+#ifndef SG_DAY_COUNTERS
+#define SG_DAY_COUNTERS 0
+#endif
+#if SG_DAY_COUNTERS
+// Diagnostic build only: warp-days per class (0 constant, 1 switch, 2 ramp).
+__device__ unsigned long long g_day_class[3];
+#endif
 
 namespace sirdgpu {
 
@@ -111,15 +118,17 @@ __device__ __forceinline__ double t_of(int k, int S, double h) {
     return dadd(static_cast<double>(day_m1), dmul(static_cast<double>(sub), h));
 }
 
-// Number of k in [0, K) with t_k < x (x may be NaN -> 0).
+// Number of k in [0, K) with t_k < x (x may be NaN -> 0).  t_k is within a
+// few ulps of k/S, so the search starts at floor(x*S) and walks the exact
+// t_k to the boundary (one or two steps in practice; monotone, so exact).
 __device__ __forceinline__ int count_t_below(double x, int K, int S, double h) {
-    int lo = 0, hi = K;  // answer in [lo, hi]
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (t_of(mid, S, h) < x) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
+    if (!(x > 0.0)) return 0;  // t_0 = 0: nothing below 0, -inf or NaN
+    if (!(x <= static_cast<double>(K))) return K;  // +inf / beyond the window
+    int k = static_cast<int>(x * static_cast<double>(S));  // estimate, any rounding
+    k = k < 0 ? 0 : (k > K ? K : k);
+    while (k < K && t_of(k, S, h) < x) ++k;
+    while (k > 0 && !(t_of(k - 1, S, h) < x)) --k;
+    return k;
 }
 
 // Per-particle constants of the integration.
@@ -237,8 +246,23 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
         // switches beta1 -> beta2 today, 0 = every lane constant all day.
         const bool ramp_today = lo < hi && lo < nsub && hi > 0;
         const bool switch_today = lo > 0 && lo < nsub;
+#if SG_DAY_COUNTERS
+        {
+            const int cls = __any_sync(mask, ramp_today) ? 2 : (__any_sync(mask, switch_today) ? 1 : 0);
+            if ((threadIdx.x & 31) == __ffs(mask) - 1) atomicAdd(&g_day_class[cls], 1ull);
+        }
+#endif
         if (__any_sync(mask, ramp_today)) {
-            if (SG_RAMP_MODE >= 1 && SUB > 0 && warp_fast) {
+            if (SG_RAMP_MODE >= 1 && SUB > 0 && warp_fast && __all_sync(mask, lo <= 0 && hi >= nsub)) {
+                // Every lane ramps through the whole day: no selects at all.
+#pragma unroll
+                for (int sub = 0; sub < nsub; ++sub) {
+                    const double t = tg.tgrid[kbase + sub];
+                    const double beta = dadd(p.b1, dmul(p.slope, dsub(t, p.t1)));
+                    const double q0 = __dmul_rn(beta, rN);
+                    euler_substep(__fma_rn(__fma_rn(-q0, N, beta), rN, q0), g, mu, h, S, I, R, D);
+                }
+            } else if (SG_RAMP_MODE >= 1 && SUB > 0 && warp_fast) {
                 // Branch-free ramp day: every lane computes the ramp value
                 // (the warp would issue it anyway once any lane needs it) and
                 // selects; non-FP64 work per substep is two compares and

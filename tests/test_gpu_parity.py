@@ -147,8 +147,12 @@ def golden_fits():
     return json.loads((GOLDEN / "fits.json").read_text())
 
 
-def test_swarms_match_reference_goldens(ctx, golden_fits):
-    """All golden swarms in ONE sg_fit_swarms call (mixed specs, sizes, windows)."""
+@pytest.mark.parametrize("mode", ["persistent", "flat"])
+def test_swarms_match_reference_goldens(ctx, golden_fits, mode):
+    """All golden swarms in ONE sg_fit_swarms call (mixed specs, sizes, windows).
+    Small plans run one persistent CTA per swarm (pso_swarm_kernel); a
+    2048-particle ballast swarm pushes the same swarms onto the flat
+    per-iteration kernels (pso_step_kernel)."""
     import paper_2204_12346_b200 as eng
     wins, descs = [], []
     for c in golden_fits:
@@ -156,6 +160,8 @@ def test_swarms_match_reference_goldens(ctx, golden_fits):
         wins.append(win)
         descs.append(dict(window=win, lower=c["lower"], upper=c["upper"], n_particles=c["n"], max_iters=c["iters"],
                           inertia=c["w"], cognitive=c["c1"], social=c["c2"], seed=c["seed"]))
+    if mode == "flat":
+        descs.append(dict(descs[1], n_particles=2048, max_iters=3, seed=12345))
     out = ctx.fit_swarms(descs)
     for c, (status, best, cost, hist) in zip(golden_fits, out):
         assert status == c["status"], c["name"]
@@ -173,7 +179,7 @@ def test_swarm_matches_oracle_and_is_reproducible(ctx, port, poland):
     init = [N - I[0] - R[0] - D[0], I[0], R[0], D[0]]
     lo, hi = [0] * 6, [2, 2, 28, 28, 1, 0.1]
     win = eng.Window(ctx, I, R, D, init, N, "ird-mxse")
-    # 700 particles -> 6 CTAs incl. a ragged one; 400 iterations -> engine wraps twice (312 words)
+    # 700 particles -> 6 CTAs incl. a ragged one; 60 iterations -> 714 draws, the engine twists three times
     desc = dict(window=win, lower=lo, upper=hi, n_particles=700, max_iters=60, seed=99)
     (s1, b1, c1, h1), (s2, b2, c2, h2) = ctx.fit_swarms([desc, desc])
     rc, bo, co, ho = port.fit_swarm("ird-mxse", I, R, D, init, N, lo, hi, 700, 60, seed=99)
