@@ -77,8 +77,10 @@ def mix_seed(base, index):
 def ops_per_eval(n_days, c_score=12, substeps=24):
     """Algorithmic FP64 ops of one particle-window evaluation without ramp credit
     (SURVEY.md §8d): 14 per Euler substep (model.cpp:66-74, 96-99) + c_score per
-    day (12 for IRD-MXSE: 3 x {sub, mul, mul, max}, objectives.cpp:15-39)."""
-    return (n_days - 1) * substeps * 14 + n_days * c_score
+    scored day (12 for IRD-MXSE: 3 x {sub, mul, mul, max}, objectives.cpp:15-39).
+    Day 0 scores the initial state, identical for every particle; the engine
+    scores it once per window, so it is not credited per evaluation."""
+    return (n_days - 1) * substeps * 14 + (n_days - 1) * c_score
 
 
 RAMP_OPS = 5  # per ramp substep: t, t - t1, slope*, beta1+, beta/N (model.cpp:62-63, 67)
@@ -392,7 +394,7 @@ def bench_ours(args):
                          "ramp_substeps_per_eval": ramp_substeps / evals_per_step,
                          "ops_per_eval": ops_step / evals_per_step,
                          "frac_floor": achieved_floor * 1e12 / fp64_peak,
-                         "ops_note": "algorithmic FP64 ops (SURVEY.md §8d: 14/substep + 5/ramp substep + 12/day), "
+                         "ops_note": "algorithmic FP64 ops (SURVEY.md §8d: 14/substep + 5/ramp substep + 12/scored day), "
                                      "DADD/DMUL without FMA for bit parity; peak = FP64 issue rate measured "
                                      "on this GPU by sg_probe_fp64_rate (neither MEASURED_PEAKS.json nor "
                                      "B200_PROFILING.md has an FP64 figure)",

@@ -358,6 +358,29 @@ int sg_window_create(sg_ctx* ctx, const double* infectious, const double* recove
         }
         d.kept[c] = static_cast<double>(kept);
     }
+    // Day-0 contribution of objective_value (objectives.cpp:15-55 at k = 0):
+    // the prediction on day 0 is the initial state for every particle
+    // (model.cpp:85), so it is computed once here, with the device's
+    // operation order (e = (obs - pred) * scale; MXSE max(0, e*e); MSE
+    // 0 + e*e; MAE 0 + |e|; MAPE 0 + |(obs - pred) / obs| unless obs == 0).
+    {
+        const double pred[3] = {init.I, init.R, init.D};
+        for (int c = 0; c < 3; ++c) {
+            const double o = series[c][0];
+            double a = 0.0;
+            if (metric == SG_METRIC_MAPE) {
+                if (o != 0.0) a = 0.0 + std::fabs((o - pred[c]) / o);
+            } else {
+                double e = o - pred[c];
+                if (family == SG_FAMILY_IRD_JOINT) e = e * d.scale[c];
+                const double e2 = e * e;
+                if (metric == SG_METRIC_MXSE) a = (0.0 < e2) ? e2 : 0.0;
+                else if (metric == SG_METRIC_MSE) a = 0.0 + e2;
+                else a = 0.0 + std::fabs(e);
+            }
+            d.acc0[c] = a;
+        }
+    }
     // One device block: descriptor | obs | robs | flags.
     const size_t obs_b = sizeof(ObsDay) * static_cast<size_t>(n_days);
     const size_t off_obs = (sizeof(DevWindow) + 255) & ~size_t(255);
@@ -387,7 +410,7 @@ int sg_window_create(sg_ctx* ctx, const double* infectious, const double* recove
         sg_window_destroy(w);
         return cuda_fail(ctx, e, "sg_window_create");
     }
-    w->smem = smem_window_bytes(n_days, substeps, metric);
+    w->smem = kernel_smem_bytes(n_days, substeps, metric, uses_fast_grid(n_days, substeps));
     if (w->smem > 200 * 1024) {
         sg_window_destroy(w);
         return fail(ctx, SG_ERR_INVALID_ARGUMENT, "window too long for shared-memory staging");

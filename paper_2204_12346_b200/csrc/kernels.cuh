@@ -64,22 +64,42 @@ __device__ __forceinline__ TimeGrid stage_times(double* base, int n_days, int ns
 }
 
 // Cooperative copy of a window into shared memory (all threads call; ends
-// with a barrier).
+// with a barrier).  The specialised kernels (SUB > 0, windows of at most
+// kFastDays days) use static shared arrays, so every per-day observation
+// read is an LDS with an immediate base; the generic kernels use the
+// dynamic segment.
+constexpr int kFastDays = kMaxTgrid / 24 + 1;  // 86: uses_fast_grid() bound
+
+template <int MET, int SUB>
 __device__ __forceinline__ SmemWindow stage_window(const DevWindow* __restrict__ gw, DevWindow* sdesc,
                                                    unsigned char* smem) {
     if (threadIdx.x == 0) *sdesc = *gw;
     const int n = gw->n_days;
     const int ns = gw->substeps;
-    const int metric = gw->metric;
-    ObsDay* obs = reinterpret_cast<ObsDay*>(smem);
-    double* times = reinterpret_cast<double*>(obs + n);
-    ObsDay* robs = reinterpret_cast<ObsDay*>(times + ns + tgrid_entries(n, ns));
-    unsigned char* flag = reinterpret_cast<unsigned char*>(robs + (metric == kMetMAPE ? n : 0));
+    ObsDay* obs;
+    double* times;
+    ObsDay* robs;
+    unsigned char* flag;
+    if constexpr (SUB > 0) {
+        __shared__ ObsDay s_obs[kFastDays];
+        __shared__ double s_times[24 + kMaxTgrid];
+        __shared__ ObsDay s_robs[MET == kMetMAPE ? kFastDays : 1];
+        __shared__ unsigned char s_flag[MET == kMetMAPE ? 3 * kFastDays : 1];
+        obs = s_obs;
+        times = s_times;
+        robs = s_robs;
+        flag = s_flag;
+    } else {
+        obs = reinterpret_cast<ObsDay*>(smem);
+        times = reinterpret_cast<double*>(obs + n);
+        robs = reinterpret_cast<ObsDay*>(times + ns + tgrid_entries(n, ns));
+        flag = reinterpret_cast<unsigned char*>(robs + (MET == kMetMAPE ? n : 0));
+    }
     const double* src = reinterpret_cast<const double*>(gw->obs);
     double* dst = reinterpret_cast<double*>(obs);
     for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) dst[i] = src[i];
     const TimeGrid tg = stage_times(times, n, ns, gw->h);
-    if (metric == kMetMAPE) {
+    if (MET == kMetMAPE) {
         const double* rsrc = reinterpret_cast<const double*>(gw->robs);
         double* rdst = reinterpret_cast<double*>(robs);
         for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) rdst[i] = rsrc[i];
@@ -87,6 +107,11 @@ __device__ __forceinline__ SmemWindow stage_window(const DevWindow* __restrict__
     }
     __syncthreads();
     return SmemWindow{sdesc, obs, robs, flag, tg};
+}
+
+// Dynamic shared memory a kernel specialisation needs for a window.
+__host__ __device__ inline size_t kernel_smem_bytes(int n_days, int substeps, int metric, bool fast) {
+    return fast ? 0 : smem_window_bytes(n_days, substeps, metric);
 }
 
 // ---- boundary 1 -------------------------------------------------------------
@@ -97,7 +122,7 @@ __global__ void __launch_bounds__(kEvalThreads, 5) eval_costs_kernel(const DevWi
                                                                   double* __restrict__ costs) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ DevWindow sdesc;
-    const SmemWindow sw = stage_window(win, &sdesc, smem);
+    const SmemWindow sw = stage_window<MET, SUB>(win, &sdesc, smem);
     const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k >= n) return;
     double x[6];
@@ -222,7 +247,7 @@ __device__ __forceinline__ void init_particle(const DevSwarm& sw, const PsoPlane
         P.mt[static_cast<size_t>(j) * stride + p] = m;
     }
     double u[6];
-    mt_draw<6>(P.mt, stride, p, 0, u);
+    mt_draw<6>(P.mt, stride, p, 0, u);  // words 0..5 of the first generation
     double x[6];
 #pragma unroll
     for (int d = 0; d < 6; ++d) x[d] = dadd(sw.lo[d], dmul(u[d], dsub(sw.hi[d], sw.lo[d])));
@@ -268,7 +293,7 @@ __device__ __forceinline__ void move_particle(const DevSwarm& sw, double best_co
     const size_t stride = P.stride;
     const bool have_best = best_cost < __longlong_as_double(0x7FF0000000000000LL);  // pso.cpp:106
     double u[12];
-    mt_draw<12>(P.mt, stride, p, 6 + 12 * (it - 1), u);
+    mt_draw<12>(P.mt, stride, p, move_draw_word(it), u);
 #pragma unroll
     for (int d = 0; d < 6; ++d) {
         const double r1 = u[2 * d];
@@ -416,7 +441,7 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
     const int s = static_cast<int>(cta_swarm[cta]);
     const DevSwarm& sw = swarms[s];
     if (it >= sw.max_iters) return;  // CTA-uniform
-    const SmemWindow win = stage_window(windows + sw.window, &sdesc, smem);
+    const SmemWindow win = stage_window<MET, SUB>(windows + sw.window, &sdesc, smem);
     const uint64_t first = static_cast<uint64_t>(cta - sw.cta_begin) * blockDim.x;
     uint64_t i = first + threadIdx.x;
     bool active = i < sw.n;
@@ -568,7 +593,7 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
     const int s = static_cast<int>(cta_swarm[cta]);
     const DevSwarm& sw = swarms[s];
     if (it >= sw.max_iters) return;  // CTA-uniform
-    const SmemWindow win = stage_window(windows + sw.window, &sdesc, smem);
+    const SmemWindow win = stage_window<MET, SUB>(windows + sw.window, &sdesc, smem);
     const uint64_t slot = static_cast<uint64_t>(cta - sw.cta_begin) * blockDim.x + threadIdx.x;
     const bool active = slot < sw.n;
     const uint64_t i = active ? perm[sw.offset + slot] : 0;
@@ -608,7 +633,7 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 2) pso_swarm_kernel(const De
     __shared__ double gbest_cost;
     const int s = static_cast<int>(blockIdx.x + swarm_offset);
     const DevSwarm& sw = swarms[s];
-    const SmemWindow win = stage_window(windows + sw.window, &sdesc, smem);
+    const SmemWindow win = stage_window<MET, SUB>(windows + sw.window, &sdesc, smem);
     const uint32_t n = static_cast<uint32_t>(sw.n);
     const size_t stride = P.stride;
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) init_particle(sw, P, sw.offset + i, i);
@@ -712,7 +737,7 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
                                                                 double* __restrict__ deaths_out) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ DevWindow sdesc;
-    const SmemWindow sw = stage_window(win, &sdesc, smem);
+    const SmemWindow sw = stage_window<MET, SUB>(win, &sdesc, smem);
     const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (k >= n) return;
     double u[6];
@@ -735,8 +760,7 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
     }
     const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w);
     double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
-    ScoreSink<FAM, MET> score(w, sw.obs, sw.robs, sw.flag);
-    score.day(0, S, I, R, D);
+    ScoreSink<FAM, MET> score(w, sw.obs, sw.robs, sw.flag);  // starts from the day-0 contribution
     integrate_days<SUB>(p, w, sw.tg, S, I, R, D, score);
     const bool fin_w = all_finite(S, I, R, D);
     // forecast_extension re-checks the junction through integrate_euler's

@@ -58,6 +58,8 @@ struct DevWindow {
     int init_finite;      // isfinite(init.total()) (model.cpp:83)
     double init[4];       // S, I, R, D
     double scale[3];      // compartment_cost scale (objectives.cpp:61-69); 1 for D-only
+    double acc0[3];       // day-0 score contribution per compartment: the initial state is
+                          // the same for every particle (model.cpp:85), so it is window-constant
     double kept[3];       // MAPE: number of days with obs != 0 (objectives.cpp:41-55)
     const ObsDay* obs;    // n_days
     const ObsDay* robs;   // RN(1/obs) per day (MAPE)
@@ -323,7 +325,9 @@ struct ScoreSink {
     __device__ __forceinline__ ScoreSink(const DevWindow& win, const ObsDay* o, const ObsDay* ro,
                                          const unsigned char* f)
         : w(win), obs(o), robs(ro), flag(f) {
-        acc[0] = acc[1] = acc[2] = 0.0;
+        acc[0] = w.acc0[0];  // day 0 already scored (sg_window_create)
+        acc[1] = w.acc0[1];
+        acc[2] = w.acc0[2];
     }
 
     __device__ __forceinline__ void one(int c, int day, double pred) {
@@ -386,8 +390,7 @@ __device__ __forceinline__ double eval_particle(const double* x, const DevWindow
     const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w);
     if (ramp) *ramp = p.k2 - p.k1;
     double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
-    ScoreSink<FAM, MET> sink(w, obs, robs, flag);
-    sink.day(0, S, I, R, D);  // day 0 is the initial state, bit for bit (model.cpp:85)
+    ScoreSink<FAM, MET> sink(w, obs, robs, flag);  // starts from the day-0 contribution
     integrate_days<SUB>(p, w, tg, S, I, R, D, sink);
     return sink.finish(all_finite(S, I, R, D));
 }
@@ -433,40 +436,42 @@ __device__ __forceinline__ double to_uniform01(uint64_t x) {
     return dmul(static_cast<double>(x >> 11), 0x1.0p-53);
 }
 
-// Draw NDRAW consecutive values (NDRAW <= 12) starting at the uniform stream
-// position `count` (values drawn so far) from the SoA engine of particle p.
-// All 2*NDRAW+1 state words are loaded before any is rewritten: the batch's
-// words are distinct (NDRAW < 156), every "next" word is read before it is
-// twisted (old value, as the sequential twist reads it), and every "far"
-// word lies outside the batch — so the loads are independent and overlap.
+// Draw NDRAW consecutive values (NDRAW <= 12) from the SoA engine of particle
+// p, starting at state word i0 = (values drawn so far) mod 312 — uniform over
+// a swarm, so callers compute it once.  All 2*NDRAW+1 state words are loaded
+// before any is rewritten: the batch's words are distinct (NDRAW < 156),
+// every "next" word is read before it is twisted (old value, as the
+// sequential twist reads it), and every "far" word lies outside the batch —
+// so the loads are independent and overlap.
 template <int NDRAW>
-__device__ __forceinline__ void mt_draw(uint64_t* __restrict__ st, size_t stride, size_t p, uint64_t count,
-                                        double* out) {
+__device__ __forceinline__ void mt_draw(uint64_t* __restrict__ st, size_t stride, size_t p, int i0, double* out) {
     static_assert(NDRAW >= 1 && NDRAW < kMtM, "batch must not reach its own far words");
-    const int i0 = static_cast<int>(count % kMtN);
+    uint64_t* __restrict__ base = st + p;
     uint64_t cur[NDRAW + 1];
     uint64_t far[NDRAW];
 #pragma unroll
     for (int j = 0; j <= NDRAW; ++j) {
-        int i = i0 + j;
-        if (i >= kMtN) i -= kMtN;
-        cur[j] = st[static_cast<size_t>(i) * stride + p];
+        const int w = i0 + j < kMtN ? i0 + j : i0 + j - kMtN;
+        cur[j] = base[static_cast<size_t>(w) * stride];
     }
 #pragma unroll
     for (int j = 0; j < NDRAW; ++j) {
-        int im = i0 + j + kMtM;
-        if (im >= kMtN) im -= kMtN;
-        if (im >= kMtN) im -= kMtN;
-        far[j] = st[static_cast<size_t>(im) * stride + p];
+        const int w = i0 + j + kMtM < kMtN ? i0 + j + kMtM : i0 + j + kMtM - kMtN;
+        far[j] = base[static_cast<size_t>(w) * stride];
     }
 #pragma unroll
     for (int j = 0; j < NDRAW; ++j) {
-        int i = i0 + j;
-        if (i >= kMtN) i -= kMtN;
-        const uint64_t w = mt_twist_word(cur[j], cur[j + 1], far[j]);
-        st[static_cast<size_t>(i) * stride + p] = w;
-        out[j] = to_uniform01(mt_temper(w));
+        const int w = i0 + j < kMtN ? i0 + j : i0 + j - kMtN;
+        const uint64_t v = mt_twist_word(cur[j], cur[j + 1], far[j]);
+        base[static_cast<size_t>(w) * stride] = v;
+        out[j] = to_uniform01(mt_temper(v));
     }
+}
+
+// Engine word where iteration it's move starts (it >= 1): 6 draws at
+// Swarm::Swarm, then 12 per move_particles (pso.cpp:65-69, 114-115).
+__host__ __device__ __forceinline__ int move_draw_word(uint64_t it) {
+    return static_cast<int>((6 + 12 * ((it - 1) % 26)) % kMtN);
 }
 
 // First `n` (<= 156) outputs of mt19937_64(seed) without materialising the
