@@ -248,6 +248,17 @@ int sg_stability_study_series(sg_ctx* ctx, const double* infectious, const doubl
  * the non-FMA integrate-and-score kernel). */
 int sg_probe_fp64_rate(sg_ctx* ctx, double* ops_per_s);
 
+/* The same ensemble reduced on the device to the per-day quantile bands of
+ * the forecast deaths — build_quantile_bands (calibration.cpp:337-361) over
+ * the n samples of each forecast day, non-finite samples (blown-up sets)
+ * dropped as append_finite_sorted does (calibration.cpp:17-25) — so an
+ * ensemble of 10^6 sets per window never leaves HBM.  bands: 7 x (horizon+1)
+ * doubles, rows median, p50_lo, p50_hi, p90_lo, p90_hi, p95_lo, p95_hi;
+ * counts: finite samples per day (horizon+1); costs: n window costs or NULL.
+ * n must fit in an int (one device radix sort per forecast day). */
+int sg_forecast_ensemble_bands(sg_window* window, const double lower[6], const double upper[6], uint64_t seed,
+                               size_t n, int horizon, double* bands, uint64_t* counts, double* costs);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -361,6 +361,48 @@ def gen_calibration(ref, poland: dict) -> dict:
     return out
 
 
+def gen_ensemble_bands(ref, poland: dict) -> list:
+    """Forecast-scenario ensembles reduced to build_quantile_bands by the
+    reference: sample k = Swarm-init draws of mt19937_64(mix_seed(seed, k))
+    (pso.cpp:55-73) + repair, integrate_euler over the window, then
+    forecast_extension; blown-up samples are NaN rows (dropped)."""
+    out = []
+    dp = op._dp
+    for name, widx, stage, seed, n, horizon in (("poland_w138_stage2", 138, 2, 2204, 3000, 21),
+                                                ("poland_w33_stage1", 33, 1, 77, 2000, 21),
+                                                ("poland_w90_wild", 90, 0, 13, 1500, 14),
+                                                ("poland_w0_h0", 0, 2, 5, 257, 0)):
+        a = 3 * widx
+        I, R, D = poland["I"][a:a + 36], poland["R"][a:a + 36], poland["D"][a:a + 36]
+        init = np.array([POLAND_N - I[0] - R[0] - D[0], I[0], R[0], D[0]])
+        if stage == 0:  # rates up to 60/day: explicit Euler at h = 1/24 blows up for part of the box
+            lo, hi = np.zeros(6), np.array([60.0, 60.0, 28.0, 28.0, 60.0, 60.0])
+        else:
+            lo, hi = (np.array(v, dtype=np.float64) for v in stage_box(stage, 35))
+        rows = np.full((n, horizon + 1), np.nan)
+        for k in range(n):
+            u = ref.uniform01(ref.mix_seed(seed, k), 6)
+            x = lo + u * (hi - lo)
+            if x[2] > x[3]:
+                x[2], x[3] = x[3], x[2]
+            st, fin = ref.integrate(x, init, POLAND_N, 36)
+            if not fin:
+                continue
+            fc, ff = ref.forecast(x, st[-1], POLAND_N, horizon)
+            if ff:
+                rows[k] = fc[:, 3]
+        vals = np.ascontiguousarray(rows)
+        bands = np.zeros(7 * (horizon + 1))
+        counts = np.zeros(horizon + 1, dtype=np.uint64)
+        rc = ref.lib.ref_quantile_bands(vals.ctypes.data_as(dp), n, horizon + 1, bands.ctypes.data_as(dp),
+                                        counts.ctypes.data_as(op._szp))
+        assert rc == 0
+        out.append(dict(name=name, I=_hex(I), R=_hex(R), D=_hex(D), init=_hex(init), N=POLAND_N, stage=stage,
+                        lower=_hex(lo), upper=_hex(hi), seed=seed, n=n, horizon=horizon, bands=_hex(bands),
+                        counts=counts.astype(int).tolist(), blown=int(np.isnan(rows[:, -1]).sum())))
+    return out
+
+
 def ctypes_int():
     import ctypes
     return ctypes.byref(ctypes.c_int(0))
@@ -395,6 +437,7 @@ def main() -> None:
     (GOLDEN / "fits.json").write_text(json.dumps(gen_fits(ref, poland), indent=1))
     np.savez_compressed(GOLDEN / "forecast.npz", **gen_forecast(ref, poland))
     (GOLDEN / "calibration.json").write_text(json.dumps(gen_calibration(ref, poland)))
+    (GOLDEN / "ensemble_bands.json").write_text(json.dumps(gen_ensemble_bands(ref, poland)))
     print("wrote", sorted(p.name for p in GOLDEN.iterdir()))
 
 

@@ -118,6 +118,8 @@ SIGNATURES = {
                                          ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp, _u8p]),
     "sg_forecast_ensemble": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, ctypes.c_uint64, ctypes.c_size_t,
                                             ctypes.c_int, _dp, _dp, _dp]),
+    "sg_forecast_ensemble_bands": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, ctypes.c_uint64, ctypes.c_size_t,
+                                                  ctypes.c_int, _dp, _u64p, _dp]),
 }
 
 _lib = None
@@ -294,6 +296,19 @@ class Window:
                                                   int(horizon), _d(costs) if costs is not None else None,
                                                   _d(params) if params is not None else None, _d(deaths)))
         return costs, params, deaths
+
+    def forecast_ensemble_bands(self, lower, upper, seed: int, n: int, horizon: int, want_costs=False):
+        """Per-day quantile bands of the ensemble's forecast deaths, computed on the device:
+        -> (bands 7 x (horizon+1): median, p50_lo, p50_hi, p90_lo, p90_hi, p95_lo, p95_hi;
+            counts (horizon+1); costs or None)."""
+        lo, hi = _f64(lower), _f64(upper)
+        bands = np.empty((7, horizon + 1))
+        counts = np.empty(horizon + 1, dtype=np.uint64)
+        costs = np.empty(n) if want_costs else None
+        self.ctx.check(lib().sg_forecast_ensemble_bands(self._h, _d(lo), _d(hi), int(seed) & 0xFFFFFFFFFFFFFFFF, n,
+                                                        int(horizon), _d(bands), counts.ctypes.data_as(_u64p),
+                                                        _d(costs) if costs is not None else None))
+        return bands, counts, costs
 
     def close(self):
         if getattr(self, "_h", None):

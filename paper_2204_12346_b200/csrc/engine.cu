@@ -10,6 +10,7 @@
 #include "engine_internal.h"
 #include "kernels.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -196,13 +197,14 @@ struct SwarmLaunch {
 template <int F, int M, int S>
 struct EnsembleLaunch {
     static void run(const DevWindow* w, const DevWindow& fwin, const double* lo, const double* hi, uint64_t seed,
-                    size_t n, int horizon, double* costs, double* params, double* deaths, size_t smem,
-                    cudaStream_t st, cudaError_t* err) {
+                    size_t n, int horizon, double* costs, double* params, double* deaths, size_t sstride,
+                    size_t dstride, size_t smem, cudaStream_t st, cudaError_t* err) {
         auto k = ensemble_kernel<F, M, S>;
         *err = prepare_smem(k, smem);
         if (*err != cudaSuccess) return;
         const unsigned grid = static_cast<unsigned>((n + kEvalThreads - 1) / kEvalThreads);
-        k<<<grid, kEvalThreads, smem, st>>>(w, fwin, lo, hi, seed, n, horizon, costs, params, deaths);
+        k<<<grid, kEvalThreads, smem, st>>>(w, fwin, lo, hi, seed, n, horizon, costs, params, deaths, sstride,
+                                            dstride);
         *err = cudaGetLastError();
     }
 };
@@ -1015,8 +1017,9 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
     SG_CUDA(ctx, cudaMemcpyAsync(d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     DevWindow fwin = integration_window(horizon + 1, w->host.substeps, w->host.N);
     cudaError_t err = cudaSuccess;
-    dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc, fwin, d_lo, d_hi, seed, n,
-                             horizon, d_cost, d_par, d_D, w->smem, ctx->stream, &err);
+    dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc,
+                             fwin, d_lo, d_hi, seed, n, horizon, d_cost, d_par, d_D,
+                             static_cast<size_t>(horizon + 1), size_t(1), w->smem, ctx->stream, &err);
     ctx->launches += 1;
     if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
     if (costs) SG_CUDA(ctx, cudaMemcpyAsync(costs, d_cost, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1024,6 +1027,65 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
         SG_CUDA(ctx, cudaMemcpyAsync(params_out, d_par, 6 * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     SG_CUDA(ctx, cudaMemcpyAsync(deaths_out, d_D, n * (horizon + 1) * sizeof(double), cudaMemcpyDeviceToHost,
                                  ctx->stream));
+    SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SG_OK;
+}
+
+int sg_forecast_ensemble_bands(sg_window* w, const double lower[6], const double upper[6], uint64_t seed, size_t n,
+                               int horizon, double* bands, uint64_t* counts, double* costs) {
+    if (!w) return SG_ERR_INVALID_ARGUMENT;
+    sg_ctx* ctx = w->ctx;
+    if (!lower || !upper || !bands || !counts) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null buffer");
+    if (horizon < 0) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "horizon must be >= 0");
+    for (int k = 0; k < 6; ++k)
+        if (!std::isfinite(lower[k]) || !std::isfinite(upper[k]) || lower[k] > upper[k])
+            return fail(ctx, SG_ERR_INVALID_ARGUMENT, "pso: bound " + std::to_string(k) + " is invalid");
+    if (n > static_cast<size_t>(INT32_MAX))
+        return fail(ctx, SG_ERR_INVALID_ARGUMENT, "ensemble too large for one radix sort");
+    const int n_days = horizon + 1;
+    SG_CUDA(ctx, cudaSetDevice(ctx->device));
+    DevBufs b;
+    b.st = ctx->stream;
+    double *d_lo, *d_hi, *d_cost = nullptr, *d_D, *d_sorted, *d_bands;
+    unsigned long long* d_counts;
+    SG_CUDA(ctx, b.alloc(&d_lo, 6));
+    SG_CUDA(ctx, b.alloc(&d_hi, 6));
+    if (costs) SG_CUDA(ctx, b.alloc(&d_cost, n));
+    SG_CUDA(ctx, b.alloc(&d_D, n * n_days));
+    SG_CUDA(ctx, b.alloc(&d_sorted, n * n_days));
+    SG_CUDA(ctx, b.alloc(&d_bands, 7 * static_cast<size_t>(n_days)));
+    SG_CUDA(ctx, b.alloc(&d_counts, n_days));
+    SG_CUDA(ctx, cudaMemcpyAsync(d_lo, lower, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, cudaMemcpyAsync(d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    if (n > 0) {
+        const DevWindow fwin = integration_window(n_days, w->host.substeps, w->host.N);
+        cudaError_t err = cudaSuccess;
+        dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps),
+                                 w->d_desc, fwin, d_lo, d_hi, seed, n, horizon, d_cost, static_cast<double*>(nullptr),
+                                 d_D, size_t(1), n, w->smem, ctx->stream, &err);  // day-major columns
+        ctx->launches += 1;
+        if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
+        // one sorted column per forecast day (calibration.cpp:17-25: ascending);
+        // a device-wide radix sort per column (columns are large and few)
+        size_t temp_bytes = 0;
+        SG_CUDA(ctx, cub::DeviceRadixSort::SortKeys(nullptr, temp_bytes, d_D, d_sorted, static_cast<int>(n), 0, 64,
+                                                     ctx->stream));
+        unsigned char* d_temp;
+        SG_CUDA(ctx, b.alloc(&d_temp, temp_bytes));
+        for (int d = 0; d < n_days; ++d) {
+            SG_CUDA(ctx, cub::DeviceRadixSort::SortKeys(d_temp, temp_bytes, d_D + static_cast<size_t>(d) * n,
+                                                         d_sorted + static_cast<size_t>(d) * n, static_cast<int>(n),
+                                                         0, 64, ctx->stream));
+            ctx->launches += 1;
+        }
+    }
+    bands_kernel<<<n_days, 32, 0, ctx->stream>>>(d_sorted, n, d_bands, d_counts, n_days);
+    ctx->launches += 1;
+    SG_CUDA(ctx, cudaGetLastError());
+    static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "count width");
+    SG_CUDA(ctx, cudaMemcpyAsync(bands, d_bands, 7 * n_days * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, cudaMemcpyAsync(counts, d_counts, n_days * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    if (costs) SG_CUDA(ctx, cudaMemcpyAsync(costs, d_cost, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SG_OK;
 }

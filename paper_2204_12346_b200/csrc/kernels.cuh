@@ -720,11 +720,12 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 2) pso_swarm_kernel(const De
 // (forecast_extension, calibration.cpp:305-317) and write D per forecast day.
 struct ForecastDSink {
     double* out;
+    size_t dstride;
     __device__ __forceinline__ void day(int d, double S, double I, double R, double D) {
         (void)S;
         (void)I;
         (void)R;
-        out[d] = D;
+        out[d * dstride] = D;
     }
 };
 
@@ -734,7 +735,8 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
                                                                 const double* __restrict__ hi, uint64_t seed,
                                                                 size_t n, int horizon, double* __restrict__ costs,
                                                                 double* __restrict__ params_out,
-                                                                double* __restrict__ deaths_out) {
+                                                                double* __restrict__ deaths_out, size_t sstride,
+                                                                size_t dstride) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ DevWindow sdesc;
     const SmemWindow sw = stage_window<MET, SUB>(win, &sdesc, smem);
@@ -752,10 +754,12 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
     }
     const DevWindow& w = *sw.w;
     const double nan = __longlong_as_double(0x7FF8000000000000LL);
-    double* drow = deaths_out + k * static_cast<size_t>(horizon + 1);
+    // deaths of sample k, forecast day d at deaths_out[k*sstride + d*dstride]
+    // (sample-major rows, or day-major columns for the on-device bands)
+    double* drow = deaths_out + k * sstride;
     if (!w.init_finite) {
         if (costs) costs[k] = __longlong_as_double(0x7FF0000000000000LL);
-        for (int d = 0; d <= horizon; ++d) drow[d] = nan;
+        for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
         return;
     }
     const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w);
@@ -768,18 +772,52 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
     const bool fin_j = fin_w && isfinite(dadd(dadd(dadd(S, I), R), D));
     if (costs) costs[k] = score.finish(fin_w);
     if (!fin_j) {  // forecast_extension throws NonFiniteError (calibration.cpp:301-303, 318-320)
-        for (int d = 0; d <= horizon; ++d) drow[d] = nan;
+        for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
         return;
     }
     // Forecast: fwin carries n_days = horizon + 1 and the same N, h, substeps.
     const Particle held = make_particle(x[1], x[1], 0.0, 0.0, x[4], x[5], fwin);
     drow[0] = D;
-    ForecastDSink fs{drow};
+    ForecastDSink fs{drow, dstride};
     // held parameters never enter the ramp, so no time table is read
     integrate_days<SUB>(held, fwin, TimeGrid{nullptr, sw.tg.subh}, S, I, R, D, fs);
     if (!all_finite(S, I, R, D)) {  // calibration.cpp:318-320
-        for (int d = 0; d <= horizon; ++d) drow[d] = nan;
+        for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
     }
+}
+
+// ---- quantile bands of sorted columns (build_quantile_bands) -------------------------
+//
+// calibration.cpp:324-361 over each forecast day: the column (n samples,
+// sorted ascending by the radix sort, NaN rows of blown-up samples last)
+// is cut at its first NaN — append_finite_sorted drops non-finite values —
+// and quantile_sorted runs with the reference's operation order.
+__device__ __forceinline__ double quantile_sorted_dev(const double* sorted, size_t k, double p) {
+    if (k == 0) return __longlong_as_double(0x7FF8000000000000LL);
+    const double h = dmul(static_cast<double>(k - 1), p);
+    const size_t lo = static_cast<size_t>(h);
+    if (lo + 1 >= k) return sorted[k - 1];
+    const double frac = dsub(h, static_cast<double>(lo));
+    return dadd(sorted[lo], dmul(frac, dsub(sorted[lo + 1], sorted[lo])));
+}
+
+__global__ void bands_kernel(const double* __restrict__ sorted, size_t n, double* __restrict__ bands,
+                             unsigned long long* __restrict__ counts, int n_days) {
+    const int d = blockIdx.x;
+    if (threadIdx.x != 0 || d >= n_days) return;
+    const double* col = sorted + static_cast<size_t>(d) * n;
+    // first non-finite entry (finite values precede NaN after the sort)
+    size_t lo = 0, hi = n;
+    while (lo < hi) {
+        const size_t mid = lo + (hi - lo) / 2;
+        if (isfinite(col[mid])) lo = mid + 1;
+        else hi = mid;
+    }
+    const size_t k = lo;
+    counts[d] = k;
+    const double ps[7] = {0.5, 0.25, 0.75, 0.05, 0.95, 0.025, 0.975};  // calibration.cpp:352-358
+#pragma unroll
+    for (int q = 0; q < 7; ++q) bands[q * n_days + d] = quantile_sorted_dev(col, k, ps[q]);
 }
 
 }  // namespace sirdgpu

@@ -225,3 +225,18 @@ def test_forecast_ensemble_matches_oracle(ctx, port, poland):
                 assert_bitwise(deaths[k], fc[:, 3], f"forecast {k}")
                 continue
         assert np.all(np.isnan(deaths[k]))
+
+
+def test_forecast_ensemble_bands_match_reference(ctx):
+    """Device quantile bands of forecast ensembles == the reference's
+    build_quantile_bands (calibration.cpp:337-361) over the same samples,
+    blown-up samples dropped (tests/golden/ensemble_bands.json)."""
+    import paper_2204_12346_b200 as eng
+    from conftest import GOLDEN
+    for c in json.loads((GOLDEN / "ensemble_bands.json").read_text()):
+        I, R, D = _unhex(c["I"]), _unhex(c["R"]), _unhex(c["D"])
+        win = eng.Window(ctx, I, R, D, _unhex(c["init"]), c["N"], "ird-mxse")
+        bands, counts, _ = win.forecast_ensemble_bands(_unhex(c["lower"]), _unhex(c["upper"]), c["seed"], c["n"],
+                                                       c["horizon"])
+        assert counts.tolist() == c["counts"], c["name"]
+        assert_bitwise(bands.ravel(), _unhex(c["bands"]), c["name"])
