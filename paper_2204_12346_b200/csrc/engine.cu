@@ -645,7 +645,7 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
         s.offset = offset;
         s.max_iters = d.max_iters;
         s.cta_begin = static_cast<uint32_t>(cta_swarm.size());
-        s.n_ctas = static_cast<uint32_t>((d.n_particles + kStepThreads - 1) / kStepThreads);
+        s.n_ctas = static_cast<uint32_t>((d.n_particles + kStepThreads * kNP - 1) / (kStepThreads * kNP));
         for (int k = 0; k < 6; ++k) {
             s.lo[k] = d.lower[k];
             s.hi[k] = d.upper[k];
@@ -681,7 +681,7 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
 #ifndef SG_SORT
 #define SG_SORT 0
 #endif
-    g.sorted = SG_SORT != 0 && !g.persistent;
+    g.sorted = SG_SORT != 0 && !g.persistent && kNP == 1;
     if (g.persistent) {
         uint64_t max_n = 0;
         for (const DevSwarm& s : sw) max_n = std::max(max_n, s.n);

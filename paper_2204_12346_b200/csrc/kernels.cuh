@@ -24,8 +24,12 @@ namespace sirdgpu {
 #ifndef SG_STEP_MIN_BLOCKS
 #define SG_STEP_MIN_BLOCKS 5
 #endif
+#ifndef SG_NP
+#define SG_NP 1
+#endif
 constexpr int kEvalThreads = 128;
 constexpr int kStepThreads = SG_STEP_THREADS;
+constexpr int kNP = SG_NP;  // particles per thread in the flat step kernel
 constexpr int kStepWarps = kStepThreads / 32;
 
 // Shared-memory staging of one window: the descriptor in static shared memory,
@@ -266,15 +270,17 @@ __global__ void __launch_bounds__(kStepThreads) pso_init_kernel(const DevSwarm* 
                                                                 PsoPlanes P, DevSwarmState* __restrict__ state) {
     const int s = static_cast<int>(cta_swarm[blockIdx.x]);
     const DevSwarm& sw = swarms[s];
-    const uint64_t i = static_cast<uint64_t>(blockIdx.x - sw.cta_begin) * blockDim.x + threadIdx.x;
-    if (i == 0) {
+    const uint64_t first = static_cast<uint64_t>(blockIdx.x - sw.cta_begin) * blockDim.x * kNP;
+    if (first + threadIdx.x == 0) {
         state[s].best_cost = __longlong_as_double(0x7FF0000000000000LL);
         for (int d = 0; d < 6; ++d) state[s].best[d] = 0.0;
         state[s].arrived = 0;
         state[s].ramp_substeps = 0;
     }
-    if (i >= sw.n) return;
-    init_particle(sw, P, sw.offset + i, i);
+    for (int q = 0; q < kNP; ++q) {
+        const uint64_t i = first + static_cast<uint64_t>(q) * blockDim.x + threadIdx.x;
+        if (i < sw.n) init_particle(sw, P, sw.offset + i, i);
+    }
 }
 
 // (cost, index) ordering of the global-best scan (pso.cpp:90-96): the lowest
@@ -316,25 +322,33 @@ __device__ __forceinline__ void move_particle(const DevSwarm& sw, double best_co
 // the global-best scan (pso.cpp:90-96) over the warp minima plus
 // cost_history[it].  (cost, index) order makes the parallel fold equal the
 // sequential lowest-index scan.  No CTA-wide barrier: warps retire on their own.
+template <int NPT>
 __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& st, const PsoPlanes& P, int s,
-                                            bool active, size_t p, uint64_t i, double c, uint32_t wslot,
-                                            uint64_t it, int ramp) {
+                                            const bool* active, const size_t* p, const uint64_t* i, const double* c,
+                                            uint32_t wslot, uint64_t it, const int* ramp) {
     const size_t stride = P.stride;
-    const unsigned int wramp = __reduce_add_sync(0xFFFFFFFFu, static_cast<unsigned int>(active ? ramp : 0));
+    unsigned int my_ramp = 0;
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) my_ramp += active[q] ? static_cast<unsigned int>(ramp[q]) : 0u;
+    const unsigned int wramp = __reduce_add_sync(0xFFFFFFFFu, my_ramp);
     if ((threadIdx.x & 31) == 0 && wramp) atomicAdd(&st.ramp_substeps, static_cast<unsigned long long>(wramp));
     double my_c = __longlong_as_double(0x7FF0000000000000LL);
     unsigned long long my_i = ~0ULL;
-    if (active) {
-        P.cost[p] = c;
-        double pbc = P.pbc[p];
-        if (c < pbc) {
-            pbc = c;
-            P.pbc[p] = c;
 #pragma unroll
-            for (int d = 0; d < 6; ++d) P.pb[d * stride + p] = P.x[d * stride + p];
+    for (int q = 0; q < NPT; ++q) {
+        if (!active[q]) continue;
+        P.cost[p[q]] = c[q];
+        double pbc = P.pbc[p[q]];
+        if (c[q] < pbc) {
+            pbc = c[q];
+            P.pbc[p[q]] = c[q];
+#pragma unroll
+            for (int d = 0; d < 6; ++d) P.pb[d * stride + p[q]] = P.x[d * stride + p[q]];
         }
-        my_c = pbc;
-        my_i = i;
+        if (better(pbc, i[q], my_c, my_i)) {
+            my_c = pbc;
+            my_i = i[q];
+        }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -442,17 +456,28 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
     const DevSwarm& sw = swarms[s];
     if (it >= sw.max_iters) return;  // CTA-uniform
     const SmemWindow win = stage_window<MET, SUB>(windows + sw.window, &sdesc, smem);
-    const uint64_t first = static_cast<uint64_t>(cta - sw.cta_begin) * blockDim.x;
-    uint64_t i = first + threadIdx.x;
-    bool active = i < sw.n;
-    size_t p = sw.offset + (active ? i : 0);
-    double x[6];
-    if (active) {
+    // Thread t owns particles first + q*blockDim + t, q < kNP (coalesced per q).
+    const uint64_t first = static_cast<uint64_t>(cta - sw.cta_begin) * blockDim.x * kNP;
+    uint64_t i[kNP];
+    bool active[kNP];
+    size_t p[kNP];
+    double x[kNP][6];
 #pragma unroll
-        for (int d = 0; d < 6; ++d) x[d] = P.x[d * P.stride + p];
-        if (it > 0) move_particle(sw, state[s].best_cost, state[s].best, P, p, it, x);
+    for (int q = 0; q < kNP; ++q) {
+        i[q] = first + static_cast<uint64_t>(q) * blockDim.x + threadIdx.x;
+        active[q] = i[q] < sw.n;
+        p[q] = sw.offset + (active[q] ? i[q] : 0);
+        if (active[q]) {
+#pragma unroll
+            for (int d = 0; d < 6; ++d) x[q][d] = P.x[d * P.stride + p[q]];
+            if (it > 0) move_particle(sw, state[s].best_cost, state[s].best, P, p[q], it, x[q]);
+        } else {
+#pragma unroll
+            for (int d = 0; d < 6; ++d) x[q][d] = x[0][d];  // idle slot mirrors slot 0 (result unused)
+        }
     }
 #if SG_CTA_SORT
+    static_assert(kNP == 1, "CTA-local evaluation order needs one particle per thread");
     {
         // Ramp-coherent evaluation order inside the CTA: sort the CTA's
         // particles by the Morton code of their new (t1, t2) and let thread
@@ -463,24 +488,33 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
         __shared__ uint32_t order[kStepThreads];
         const double tlo = sw.lo[2] < sw.lo[3] ? sw.lo[2] : sw.lo[3];
         const double thi = sw.hi[2] > sw.hi[3] ? sw.hi[2] : sw.hi[3];
-        const uint32_t key = active ? morton_tt(x[2], x[3], tlo, thi, 5) : 0x3FFu + 1u;
+        const uint32_t key = active[0] ? morton_tt(x[0][2], x[0][3], tlo, thi, 5) : 0x3FFu + 1u;
         order[threadIdx.x] = (key << 8) | threadIdx.x;
         cta_bitonic_sort(order);
-        const uint32_t q = order[threadIdx.x] & 0xFFu;
-        i = first + q;
-        active = i < sw.n;
-        p = sw.offset + (active ? i : 0);
-        if (active) {
+        const uint32_t qv = order[threadIdx.x] & 0xFFu;
+        i[0] = first + qv;
+        active[0] = i[0] < sw.n;
+        p[0] = sw.offset + (active[0] ? i[0] : 0);
+        if (active[0]) {
 #pragma unroll
-            for (int d = 0; d < 6; ++d) x[d] = P.x[d * P.stride + p];
+            for (int d = 0; d < 6; ++d) x[0][d] = P.x[d * P.stride + p[0]];
         }
     }
 #endif
-    double c = 0.0;
-    int ramp = 0;
-    if (active) c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag, &ramp);
-    finish_step(sw, state[s], P, s, active, p, i, c, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it,
-                ramp);
+    double c[kNP];
+    int ramp[kNP];
+#pragma unroll
+    for (int q = 0; q < kNP; ++q) {
+        c[q] = 0.0;
+        ramp[q] = 0;
+    }
+    if (active[0]) {
+        if constexpr (kNP == 1) c[0] = eval_particle<FAM, MET, SUB>(x[0], *win.w, win.tg, win.obs, win.robs, win.flag,
+                                                                     &ramp[0]);
+        else eval_particles<FAM, MET, SUB, kNP>(x, *win.w, win.tg, win.obs, win.robs, win.flag, c, ramp);
+    }
+    finish_step<kNP>(sw, state[s], P, s, active, p, i, c, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it,
+                     ramp);
 }
 
 // ---- ramp-coherent evaluation order (swarms of at most kSortMax particles) ----
@@ -606,8 +640,11 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
         for (int d = 0; d < 6; ++d) x[d] = P.x[d * P.stride + p];
         c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag, &ramp);
     }
-    finish_step(sw, state[s], P, s, active, p, i, c, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it,
-                ramp);
+    const bool act[1] = {active};
+    const size_t pp[1] = {p};
+    const uint64_t ii[1] = {i};
+    finish_step<1>(sw, state[s], P, s, act, pp, ii, &c, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it,
+                   &ramp);
 }
 
 // ---- small swarms: one persistent CTA per swarm --------------------------------
