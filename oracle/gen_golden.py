@@ -403,6 +403,108 @@ def gen_ensemble_bands(ref, poland: dict) -> list:
     return out
 
 
+def gen_series(ref) -> dict:
+    """Host data layer pins (tools/main.cpp inputs/outputs): format_double,
+    build_epi_series(+smooth7) on raw series with gaps / dips / outflow caps,
+    and build_envelope, all by the reference."""
+    import ctypes
+    dp = op._dp
+    rng = np.random.default_rng(2204)
+    out = {"format_double": [], "clean": [], "envelope": []}
+    vals = [0.0, -0.0, 1.0, 2.5, 1e-05, 0.0001, 123456789.0, 1.2345678901234567e17, 1e16, 1e15, 1e21, 3.14159,
+            -2.75, 5e-324, 1.7976931348623157e308, 1e-7, 123.456, 0.1 + 0.2, 38000000.0, 85358.31234, float("inf"),
+            -float("inf"), float("nan"), 100.0, 1e22, 12345678.9, 2 ** 53, 0.5, 9.999999999999999e-5]
+    vals += list(rng.standard_normal(40) * 10.0 ** rng.integers(-12, 20, 40))
+    buf = ctypes.create_string_buffer(64)
+    for v in vals:
+        ref.lib.ref_format_double(float(v), buf)
+        out["format_double"].append([float(v).hex(), buf.value.decode()])
+    for case in range(6):
+        n = int(rng.integers(20, 80))
+        days = np.sort(rng.choice(np.arange(n + 20), size=n, replace=False)).astype(np.int32)
+        days -= days[0]
+        base = np.cumsum(rng.uniform(0, 50, size=(n, 3)), axis=0) * np.array([3.0, 1.5, 0.2])
+        if case >= 2:  # reporting dips and outflow spikes
+            base[rng.integers(1, n - 1, 4), 1] *= 0.5
+            base[rng.integers(1, n - 1, 3), 2] *= 0.3
+            base[rng.integers(1, n - 1, 3), 1] += 5000.0
+        raw = base.copy()
+        mask = rng.random((n, 3)) < (0.15 if case % 2 else 0.0)
+        mask[0] = mask[-1] = False
+        raw[mask] = np.nan
+        for smooth in (0, 1):
+            m = int(days[-1]) + 1
+            I, R, D, NEW = (np.zeros(m) for _ in range(4))
+            nout = ctypes.c_size_t()
+            stats = np.zeros(3, dtype=np.uint64)
+            c_, r_, d_ = (np.ascontiguousarray(raw[:, k]) for k in range(3))
+            rc = ref.lib.ref_clean_raw(days.ctypes.data_as(op._ip), c_.ctypes.data_as(dp), r_.ctypes.data_as(dp),
+                                       d_.ctypes.data_as(dp), n, smooth, m, I.ctypes.data_as(dp),
+                                       R.ctypes.data_as(dp), D.ctypes.data_as(dp), NEW.ctypes.data_as(dp),
+                                       ctypes.byref(nout), stats.ctypes.data_as(op._u64p))
+            assert rc == 0, ref.lib.ref_last_error()
+            out["clean"].append(dict(days=days.tolist(), raw=[[None if np.isnan(x) else float(x).hex() for x in row]
+                                                              for row in raw], smooth=smooth, I=_hex(I), R=_hex(R),
+                                     D=_hex(D), new=_hex(NEW), stats=stats.astype(int).tolist()))
+    for case in range(4):
+        ns, nd = int(rng.integers(1, 12)), int(rng.integers(1, 9))
+        v = rng.standard_normal((ns, nd))
+        v[rng.random((ns, nd)) < 0.2] = np.nan
+        bands = np.zeros(7 * nd)
+        cnt = np.zeros(nd, dtype=np.uint64)
+        v = np.ascontiguousarray(v)
+        assert ref.lib.ref_build_envelope(v.ctypes.data_as(dp), ns, nd, bands.ctypes.data_as(dp),
+                                          cnt.ctypes.data_as(op._szp)) == 0
+        out["envelope"].append(dict(values=[[None if np.isnan(x) else float(x).hex() for x in row] for row in v],
+                                    bands=_hex(bands), counts=cnt.astype(int).tolist()))
+    return out
+
+
+def gen_cli(ref) -> dict:
+    """acceptance/main.cpp:180-207 setup: a model trajectory reported as raw
+    cumulative counts (synthetic.hpp:56-69), cleaned by build_epi_series and
+    fitted by fit_all_windows with the CLI's settings; the reference's
+    per-window results for `fit --tau 20 --delta 10 --objective ird-mxse
+    --particles 300 --iters 40 --seed 7`."""
+    import ctypes
+    dp = op._dp
+    N = 1e6
+    st, _ = ref.integrate([0.55, 0.85, 15.0, 30.0, 0.09, 0.012], [N - 100, 100, 0, 0], N, 60)
+    confirmed = st[:, 1] + st[:, 2] + st[:, 3]
+    raw = np.stack([confirmed, st[:, 2], st[:, 3]], axis=1)
+    n = len(raw)
+    days = np.arange(n, dtype=np.int32)
+    I, R, D, NEW = (np.zeros(n) for _ in range(4))
+    nout = ctypes.c_size_t()
+    stats = np.zeros(3, dtype=np.uint64)
+    c_, r_, d_ = (np.ascontiguousarray(raw[:, k]) for k in range(3))
+    assert ref.lib.ref_clean_raw(days.ctypes.data_as(op._ip), c_.ctypes.data_as(dp), r_.ctypes.data_as(dp),
+                                 d_.ctypes.data_as(dp), n, 0, n, I.ctypes.data_as(dp), R.ctypes.data_as(dp),
+                                 D.ctypes.data_as(dp), NEW.ctypes.data_as(dp), ctypes.byref(nout),
+                                 stats.ctypes.data_as(op._u64p)) == 0
+    mw = 16
+    nw, failed = ctypes.c_size_t(), ctypes.c_size_t()
+    ok = np.zeros(mw, dtype=np.int32)
+    best, obj, r2, mean = np.zeros(6 * mw), np.zeros(mw), np.zeros(mw), np.zeros(1)
+    b7 = np.ascontiguousarray(STAGE_BOUNDS7[2], dtype=np.float64)
+    assert ref.lib.ref_fit_all_windows(I.ctypes.data_as(dp), R.ctypes.data_as(dp), D.ctypes.data_as(dp), n, 20, 10,
+                                       1, 0, b7.ctypes.data_as(dp), N, 24, 1, 300, 40, 0.5, 0.5, 0.5, 7, mw, nw,
+                                       ok.ctypes.data_as(op._ip), best.ctypes.data_as(dp), obj.ctypes.data_as(dp),
+                                       r2.ctypes.data_as(dp), mean.ctypes.data_as(dp), failed) == 0
+    k = nw.value
+    buf = ctypes.create_string_buffer(64)
+    cells = []
+    for row in raw:
+        out_row = []
+        for v in row:
+            ref.lib.ref_format_double(float(v), buf)
+            out_row.append(buf.value.decode())
+        cells.append(out_row)
+    return dict(raw_cells=cells, start_date="2020-03-01", n_windows=k, ok=ok[:k].tolist(),
+                params=_hex(best[:6 * k]), objective=_hex(obj[:k]), r2=_hex(r2[:k]), mean_r2=float(mean[0]).hex(),
+                failed=failed.value)
+
+
 def ctypes_int():
     import ctypes
     return ctypes.byref(ctypes.c_int(0))
@@ -438,6 +540,8 @@ def main() -> None:
     np.savez_compressed(GOLDEN / "forecast.npz", **gen_forecast(ref, poland))
     (GOLDEN / "calibration.json").write_text(json.dumps(gen_calibration(ref, poland)))
     (GOLDEN / "ensemble_bands.json").write_text(json.dumps(gen_ensemble_bands(ref, poland)))
+    (GOLDEN / "series.json").write_text(json.dumps(gen_series(ref)))
+    (GOLDEN / "cli_fit.json").write_text(json.dumps(gen_cli(ref)))
     print("wrote", sorted(p.name for p in GOLDEN.iterdir()))
 
 

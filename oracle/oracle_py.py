@@ -87,6 +87,10 @@ class Oracle:
                                                 ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
                                                 ctypes.c_double, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                                 _ip, _dp, _dp, _dp, _u64p, _dp, _u64p, _u64p]
+            lib.ref_format_double.argtypes = [ctypes.c_double, ctypes.c_char_p]
+            lib.ref_clean_raw.argtypes = [_ip, _dp, _dp, _dp, ctypes.c_size_t, ctypes.c_int, ctypes.c_size_t, _dp,
+                                          _dp, _dp, _dp, _szp, _u64p]
+            lib.ref_build_envelope.argtypes = [_dp, ctypes.c_size_t, ctypes.c_size_t, _dp, _szp]
             lib.ref_fit_window_forecast.argtypes = [_dp, _dp, _dp, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_size_t,
                                                     ctypes.c_int, ctypes.c_int, _dp, ctypes.c_double, ctypes.c_int,
                                                     ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,

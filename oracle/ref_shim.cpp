@@ -9,6 +9,7 @@
 #include "oracle.h"
 
 #include "sirdfit/calibration.hpp"
+#include "sirdfit/csv.hpp"
 #include "sirdfit/errors.hpp"
 #include "sirdfit/model.hpp"
 #include "sirdfit/objectives.hpp"
@@ -16,6 +17,7 @@
 #include "sirdfit/timeseries.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <limits>
 #include <random>
@@ -332,6 +334,67 @@ int ref_fit_window_forecast(const double* I, const double* R, const double* D, s
         const FitResult fit = fit_window(epi, Window{.index = 0, .start = start, .length = length}, settings, seed);
         const Forecast fc = forecast_extension(fit, horizon, substeps);
         write_states(fc.trajectory, states);
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// format_double (csv.cpp:84-94) into buf (>= 32 bytes).
+void ref_format_double(double v, char* buf) {
+    const std::string s = format_double(v);
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+}
+
+// build_epi_series (+ smooth7) from raw rows with optional cells (NaN =
+// missing) and day offsets from 2020-03-18; stats = {interpolated,
+// negative, outflow}.  Outputs hold max_days values; *n_out the series length.
+int ref_clean_raw(const int* day_offset, const double* c, const double* r, const double* d, size_t n_rows, int smooth,
+                  size_t max_days, double* I, double* R, double* D, double* new_cases, size_t* n_out,
+                  uint64_t* stats) {
+    try {
+        RawSeries raw;
+        for (std::size_t k = 0; k < n_rows; ++k) {
+            RawRecord rec;
+            rec.date = Date{std::chrono::days(18339 + day_offset[k])};
+            if (!std::isnan(c[k])) rec.confirmed_cum = c[k];
+            if (!std::isnan(r[k])) rec.recovered_cum = r[k];
+            if (!std::isnan(d[k])) rec.deaths_cum = d[k];
+            raw.records.push_back(rec);
+        }
+        CleaningStats st;
+        EpiSeries epi = build_epi_series(raw, &st);
+        if (smooth) epi = smooth7(epi);
+        *n_out = epi.size();
+        if (epi.size() > max_days) return 1;
+        std::copy(epi.infectious.begin(), epi.infectious.end(), I);
+        std::copy(epi.recovered_cum.begin(), epi.recovered_cum.end(), R);
+        std::copy(epi.deaths_cum.begin(), epi.deaths_cum.end(), D);
+        std::copy(epi.new_cases.begin(), epi.new_cases.end(), new_cases);
+        stats[0] = st.interpolated_cells;
+        stats[1] = st.negative_corrections;
+        stats[2] = st.outflow_corrections;
+        return 0;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
+// build_envelope (calibration.cpp:218-245) per day over a row-major
+// n_samples x n_days matrix (NaN = no sample).  out: 7 x n_days (outer_lo,
+// band1_lo, band2_lo, median, band2_hi, band1_hi, outer_hi); count: n_days.
+int ref_build_envelope(const double* values, size_t n_samples, size_t n_days, double* out, size_t* count) {
+    try {
+        std::vector<std::vector<double>> per_day(n_days);
+        for (std::size_t s = 0; s < n_samples; ++s)
+            for (std::size_t d = 0; d < n_days; ++d) per_day[d].push_back(values[s * n_days + d]);
+        const Envelope e = build_envelope(per_day);
+        for (std::size_t d = 0; d < n_days; ++d) {
+            const double v[7] = {e.outer_lo[d], e.band1_lo[d], e.band2_lo[d], e.median[d],
+                                 e.band2_hi[d], e.band1_hi[d], e.outer_hi[d]};
+            for (int k = 0; k < 7; ++k) out[k * n_days + d] = v[k];
+            count[d] = e.count[d];
+        }
         return 0;
     } catch (const std::exception& e) {
         return status_of(e);

@@ -7,9 +7,8 @@ drop-in for the calibration path.  The functions call the C++ host layer
 (csrc/host_api.cpp) through the C-ABI (include/sirdgpu.h); every SIRD
 integration and cost evaluation runs on the GPU.
 
-Out of scope here: the raw-CSV cleaning pipeline behind the
-reference's `load_raw_csv` (timeseries.cpp); `load_epi_csv` reads an already
-cleaned series instead.
+`load_raw_csv` runs the reference's cleaning pipeline (timeseries.cpp),
+restated on the host in paper_2204_12346_b200/series.py.
 """
 from __future__ import annotations
 
@@ -29,7 +28,8 @@ kDefaultSubsteps = 24  # model.hpp:12
 
 __all__ = ["EpiSeries", "FitAllResult", "FitResult", "Forecast", "SirdParams", "SirdState", "Trajectory", "Window",
            "StabilityResult", "QuantileBands", "ScalarBands", "basic_reproduction_number", "beta_at",
-           "fit_all_windows", "fit_window", "forecast_extension", "integrate", "load_epi_csv", "make_windows",
+           "fit_all_windows", "fit_window", "forecast_extension", "integrate", "load_epi_csv", "load_raw_csv",
+           "make_windows",
            "stability_study", "mix_seed", "r_squared_d"]
 
 
@@ -252,6 +252,16 @@ def make_windows(n_days: int, tau: int = 35, delta: int = 3) -> list:
     return [Window(i, i * delta, tau + 1) for i in range(count)]
 
 
+def load_raw_csv(path: str, smooth: bool = False) -> EpiSeries:
+    """module.cpp:151-162: read date,confirmed,recovered,deaths and clean it
+    (build_epi_series, optionally smooth7)."""
+    from . import series as S
+    epi = S.build_epi_series(S.read_raw_csv_file(path))
+    if smooth:
+        epi = S.smooth7(epi)
+    return EpiSeries(epi.infectious, epi.recovered_cum, epi.deaths_cum, epi.new_cases, S.format_date(epi.start_date))
+
+
 def load_epi_csv(path: str) -> EpiSeries:
     """Read a cleaned series (columns infectious, recovered_cum, deaths_cum[, new_cases])."""
     with open(path, newline="") as f:
@@ -293,8 +303,14 @@ def fit_window(data: EpiSeries, window: Window, population: float, objective: st
                cognitive: float = 0.5, social: float = 0.5, seed: int = 0, substeps: int = kDefaultSubsteps,
                threads: int = 1) -> FitResult:
     """fit_window (calibration.cpp:157-188); module.cpp:167-180 signature."""
-    ctx = context()
     s = _settings(population, objective, bounds, particles, iters, inertia, cognitive, social, substeps)
+    return fit_window_settings(data, window, s, seed)
+
+
+def fit_window_settings(data: EpiSeries, window: Window, s, seed: int = 0) -> FitResult:
+    """fit_window with an explicit sg_fit_settings (any bounds, e.g. the CLI's custom box)."""
+    ctx = context()
+    population, substeps = s.population, s.substeps
     I, R, D = _series(data)
     rec = _capi.sg_fit_record()
     traj = np.empty((max(int(window.length), 1), 4))
@@ -314,8 +330,14 @@ def fit_all_windows(data: EpiSeries, population: float, tau: int = 35, delta: in
                     substeps: int = kDefaultSubsteps, threads: int = 1) -> FitAllResult:
     """fit_all_windows (calibration.cpp:190-216); module.cpp:182-196 signature.
     All windows run as concurrent swarms on the device."""
-    ctx = context()
     s = _settings(population, objective, bounds, particles, iters, inertia, cognitive, social, substeps)
+    return fit_all_windows_settings(data, s, tau, delta, seed)
+
+
+def fit_all_windows_settings(data: EpiSeries, s, tau: int = 35, delta: int = 3, seed: int = 0) -> FitAllResult:
+    """fit_all_windows with an explicit sg_fit_settings."""
+    ctx = context()
+    population, substeps = s.population, s.substeps
     I, R, D = _series(data)
     n_max = max(1, 1 + (len(I) - 1 - tau) // max(delta, 1)) if len(I) > tau else 1
     recs = (_capi.sg_fit_record * n_max)()
@@ -352,8 +374,15 @@ def stability_study(data: EpiSeries, window: Window, population: float, repetiti
                     inertia: float = 0.5, cognitive: float = 0.5, social: float = 0.5, seed: int = 0,
                     substeps: int = kDefaultSubsteps) -> StabilityResult:
     """stability_study (calibration.cpp:378-436): repetitions run as concurrent swarms."""
-    ctx = context()
     s = _settings(population, objective, bounds, particles, iters, inertia, cognitive, social, substeps)
+    return stability_study_settings(data, window, s, repetitions, horizon, seed)
+
+
+def stability_study_settings(data: EpiSeries, window: Window, s, repetitions: int, horizon: int,
+                             seed: int = 0) -> StabilityResult:
+    """stability_study with an explicit sg_fit_settings."""
+    ctx = context()
+    population, substeps = s.population, s.substeps
     I, R, D = _series(data)
     L, H = int(window.length), int(horizon)
     reps = max(int(repetitions), 1)
