@@ -5,6 +5,9 @@ arm import this module, as the checker.  The product package never does.
 
     load("port")       -> oracle/libsirdoracle.so (C restatement)
     load("reference")  -> oracle/_ref/libsirdref.so (the reference itself)
+    load("hybrid")     -> oracle/_ref/libsirdhybrid.so: the reference's own
+                          Swarm driving the GPU objective through the C-ABI
+                          (the drop-in under test)
 """
 from __future__ import annotations
 
@@ -18,6 +21,8 @@ import numpy as np
 ORACLE_DIR = Path(__file__).resolve().parent
 PORT_SO = ORACLE_DIR / "libsirdoracle.so"
 REF_SO = ORACLE_DIR / "_ref" / "libsirdref.so"
+HYBRID_SO = ORACLE_DIR / "_ref" / "libsirdhybrid.so"
+ENGINE_SO = ORACLE_DIR.parent / "paper_2204_12346_b200" / "libsirdgpu.so"
 REFERENCE_SRC = Path("/root/reference/proj")
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -42,8 +47,15 @@ def build(kind: str = "all") -> None:
         targets.append("port")
     if kind in ("all", "ref", "reference") and REFERENCE_SRC.exists():
         targets.append("ref")
+    if kind in ("all", "hybrid") and REFERENCE_SRC.exists() and ENGINE_SO.exists():
+        targets.append("hybrid")
     if targets:
         subprocess.run(["make", "-s", "-C", str(ORACLE_DIR), *targets], check=True)
+
+
+_FIT_SWARM_ARGS = [ctypes.c_int, ctypes.c_int, _dp, _dp, _dp, ctypes.c_int, _dp, ctypes.c_double, ctypes.c_int,
+                   ctypes.c_int, _dp, _dp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double, ctypes.c_double,
+                   ctypes.c_double, ctypes.c_uint64, ctypes.c_int, _dp, _dp, _dp]
 
 
 def _d(a):
@@ -56,6 +68,11 @@ class Oracle:
         self.path = path
         lib = ctypes.CDLL(str(path), mode=ctypes.RTLD_LOCAL)
         self.lib = lib
+        if kind == "hybrid":
+            lib.hybrid_fit_swarm.argtypes = _FIT_SWARM_ARGS
+            self._fit_swarm = lib.hybrid_fit_swarm
+            return
+        self._fit_swarm = lib.oracle_fit_swarm
         lib.oracle_mix_seed.restype = ctypes.c_uint64
         lib.oracle_mix_seed.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
         lib.oracle_mt_raw.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_size_t, _u64p]
@@ -63,10 +80,7 @@ class Oracle:
         lib.oracle_integrate.argtypes = [_dp, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp, _ip]
         lib.oracle_eval_costs.argtypes = [ctypes.c_int, ctypes.c_int, _dp, _dp, _dp, ctypes.c_int, _dp,
                                           ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp, ctypes.c_size_t, _dp]
-        lib.oracle_fit_swarm.argtypes = [ctypes.c_int, ctypes.c_int, _dp, _dp, _dp, ctypes.c_int, _dp,
-                                         ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp, _dp, ctypes.c_uint64,
-                                         ctypes.c_uint64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
-                                         ctypes.c_uint64, ctypes.c_int, _dp, _dp, _dp]
+        lib.oracle_fit_swarm.argtypes = _FIT_SWARM_ARGS
         lib.oracle_forecast.argtypes = [_dp, _dp, ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp, _ip]
         if kind == "reference":
             lib.ref_last_error.restype = ctypes.c_char_p
@@ -143,7 +157,7 @@ class Oracle:
         best = np.zeros(6)
         cost = np.zeros(1)
         hist = np.zeros(max_iters)
-        rc = self.lib.oracle_fit_swarm(fam, met, _d(I), _d(R), _d(D), len(I), _d(init), population, substeps,
+        rc = self._fit_swarm(fam, met, _d(I), _d(R), _d(D), len(I), _d(init), population, substeps,
                                        n_threads, _d(lo), _d(hi), n_particles, max_iters, inertia, cognitive,
                                        social, seed, 1 if repair else 0, _d(best), _d(cost), _d(hist))
         return rc, best, float(cost[0]), hist
@@ -165,9 +179,9 @@ _cache: dict[str, Oracle] = {}
 def load(kind: str = "port") -> Oracle:
     """Load an oracle; kind "port" (C restatement) or "reference" (oracle/_ref)."""
     if kind not in _cache:
-        path = PORT_SO if kind == "port" else REF_SO
+        path = {"port": PORT_SO, "reference": REF_SO, "hybrid": HYBRID_SO}[kind]
         if not path.exists():
-            build("port" if kind == "port" else "ref")
+            build({"port": "port", "reference": "ref", "hybrid": "hybrid"}[kind])
         if not path.exists():
             raise FileNotFoundError(f"oracle library {path} is not built")
         _cache[kind] = Oracle(path, kind)

@@ -154,15 +154,14 @@ struct EvalLaunch {
 
 template <int F, int M, int S>
 struct StepLaunch {
-    static void run(unsigned grid, uint32_t cta_offset, const DevSwarm* sw, const uint32_t* cta_swarm,
-                    const DevWindow* wins, const PsoPlanes& P, DevSwarmState* state, uint64_t it, size_t smem,
-                    cudaStream_t st, cudaError_t* err) {
+    static void run(unsigned grid, uint32_t cta_offset, const CtaTask* tasks, const DevSwarm* sw, const PsoPlanes& P,
+                    DevSwarmState* state, uint64_t it, size_t smem, cudaStream_t st, cudaError_t* err) {
         auto k = pso_step_kernel<F, M, S>;
         if (it == 0) {
             *err = prepare_smem(k, smem);
             if (*err != cudaSuccess) return;
         }
-        k<<<grid, kStepThreads, smem, st>>>(sw, cta_swarm, wins, P, state, it, cta_offset);
+        k<<<grid, kStepThreads, smem, st>>>(tasks, sw, P, state, it, cta_offset);
         *err = cudaGetLastError();
     }
 };
@@ -383,12 +382,27 @@ int sg_window_create(sg_ctx* ctx, const double* infectious, const double* recove
             d.acc0[c] = a;
         }
     }
-    // One device block: descriptor | obs | robs | flags.
+    // Substep times, staged by every CTA that evaluates this window:
+    // subh[sub] = RN(sub*h) and t_k = RN(RN(day-1) + subh[sub]) (model.cpp:94),
+    // the same IEEE operations as stage_times on the device.
+    const int n_tgrid = tgrid_entries(n_days, substeps);
+    std::vector<double> times(static_cast<size_t>(substeps) + n_tgrid);
+    for (int i = 0; i < substeps; ++i) times[i] = static_cast<double>(i) * d.h;
+    for (int k = 0; k < n_tgrid; ++k) {
+        const int day = k / substeps;
+        times[substeps + k] = static_cast<double>(day) + static_cast<double>(k - day * substeps) * d.h;
+    }
+    // One device block: descriptor | times | obs | robs | flags.
+    // Every section starts 16-byte aligned and is padded to a 16-byte
+    // multiple: the step kernel stages them with bulk copies (CtaTask).
     const size_t obs_b = sizeof(ObsDay) * static_cast<size_t>(n_days);
-    const size_t off_obs = (sizeof(DevWindow) + 255) & ~size_t(255);
-    const size_t off_robs = off_obs + obs_b;
-    const size_t off_flag = off_robs + obs_b;
-    const size_t total = off_flag + flag.size();
+    const size_t obs_b16 = (obs_b + 15) & ~size_t(15);
+    const size_t off_times = (sizeof(DevWindow) + 255) & ~size_t(255);
+    const size_t times_b = (times.size() * sizeof(double) + 15) & ~size_t(15);
+    const size_t off_obs = off_times + times_b;
+    const size_t off_robs = off_obs + obs_b16;
+    const size_t off_flag = off_robs + obs_b16;
+    const size_t total = off_flag + ((flag.size() + 15) & ~size_t(15));
     unsigned char* block = nullptr;
     cudaError_t e = dalloc(&block, total, ctx->stream);
     if (e == cudaSuccess) {
@@ -400,8 +414,10 @@ int sg_window_create(sg_ctx* ctx, const double* infectious, const double* recove
         d.obs = w->d_obs;
         d.robs = w->d_robs;
         d.obs_flag = w->d_flag;
-        std::vector<unsigned char> staging(total);
+        d.times = reinterpret_cast<const double*>(block + off_times);
+        std::vector<unsigned char> staging(total, 0);
         std::memcpy(staging.data(), &d, sizeof d);
+        std::memcpy(staging.data() + off_times, times.data(), times.size() * sizeof(double));
         std::memcpy(staging.data() + off_obs, obs.data(), obs_b);
         std::memcpy(staging.data() + off_robs, robs.data(), obs_b);
         std::memcpy(staging.data() + off_flag, flag.data(), flag.size());
@@ -605,6 +621,7 @@ struct SwarmGroup {
     uint64_t iters = 0;               // max over swarms
     DevSwarm* d_sw = nullptr;
     uint32_t* d_cta = nullptr;
+    CtaTask* d_task = nullptr;
     DevWindow* d_win = nullptr;
     DevSwarmState* d_state = nullptr;
     PsoPlanes P{};
@@ -698,6 +715,7 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     SG_CUDA(ctx, b.alloc(&g.d_sw, sw.size()));
     SG_CUDA(ctx, b.alloc(&g.d_cta, g.n_ctas));
     SG_CUDA(ctx, b.alloc(&g.d_win, wtab.size()));
+    SG_CUDA(ctx, b.alloc(&g.d_task, g.n_ctas));
     SG_CUDA(ctx, b.alloc(&g.d_state, sw.size()));
     SG_CUDA(ctx, b.alloc(&P.x, 6 * g.n_total));
     SG_CUDA(ctx, b.alloc(&P.v, 6 * g.n_total));
@@ -718,6 +736,26 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     SG_CUDA(ctx, cudaMemcpyAsync(g.d_sw, sw.data(), sizeof(DevSwarm) * sw.size(), cudaMemcpyHostToDevice, st));
     SG_CUDA(ctx, cudaMemcpyAsync(g.d_cta, cta_swarm.data(), sizeof(uint32_t) * g.n_ctas, cudaMemcpyHostToDevice, st));
     SG_CUDA(ctx, cudaMemcpyAsync(g.d_win, wtab.data(), sizeof(DevWindow) * wtab.size(), cudaMemcpyHostToDevice, st));
+    std::vector<CtaTask> tasks(g.n_ctas);
+    for (size_t c = 0; c < g.n_ctas; ++c) {
+        const DevSwarm& s = sw[cta_swarm[c]];
+        const DevWindow& w = wtab[s.window];
+        CtaTask& t = tasks[c];
+        const uint64_t first = static_cast<uint64_t>(c - s.cta_begin) * kStepThreads * kNP;
+        t.swarm = cta_swarm[c];
+        t.n_valid = static_cast<uint32_t>(std::min<uint64_t>(kStepThreads * kNP, s.n - first));
+        t.p0 = s.offset + first;
+        t.i0 = first;
+        t.max_iters = s.max_iters;
+        t.win = g.d_win + s.window;
+        t.times = w.times;
+        t.obs = reinterpret_cast<const double*>(w.obs);
+        t.times_bytes = static_cast<uint32_t>(
+            ((static_cast<size_t>(w.substeps) + tgrid_entries(w.n_days, w.substeps)) * sizeof(double) + 15) &
+            ~size_t(15));
+        t.obs_bytes = static_cast<uint32_t>((sizeof(ObsDay) * static_cast<size_t>(w.n_days) + 15) & ~size_t(15));
+    }
+    SG_CUDA(ctx, cudaMemcpyAsync(g.d_task, tasks.data(), sizeof(CtaTask) * tasks.size(), cudaMemcpyHostToDevice, st));
     SG_CUDA(ctx, cudaStreamSynchronize(st));  // host vectors go out of scope
     return SG_OK;
 }
@@ -772,8 +810,8 @@ int step_group(sg_ctx* ctx, SwarmGroup& g) {
                 dispatch<PermEvalLaunch>(g.family, g.metric, g.substeps, ln.n_ctas, ln.cta_begin, g.d_sw, g.d_cta,
                                          g.d_win, g.P, g.d_state, g.d_perm, it, g.smem, st, &err);
             } else {
-                dispatch<StepLaunch>(g.family, g.metric, g.substeps, ln.n_ctas, ln.cta_begin, g.d_sw, g.d_cta,
-                                     g.d_win, g.P, g.d_state, it, g.smem, st, &err);
+                dispatch<StepLaunch>(g.family, g.metric, g.substeps, ln.n_ctas, ln.cta_begin, g.d_task, g.d_sw, g.P,
+                                     g.d_state, it, g.smem, st, &err);
             }
             ctx->launches += 1;
             if (err != cudaSuccess) return cuda_fail(ctx, err, "pso_step_kernel");

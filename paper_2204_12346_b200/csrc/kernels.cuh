@@ -86,7 +86,7 @@ __device__ __forceinline__ SmemWindow stage_window(const DevWindow* __restrict__
     unsigned char* flag;
     if constexpr (SUB > 0) {
         __shared__ ObsDay s_obs[kFastDays];
-        __shared__ double s_times[24 + kMaxTgrid];
+        __shared__ __align__(16) double s_times[24 + kMaxTgrid];
         __shared__ ObsDay s_robs[MET == kMetMAPE ? kFastDays : 1];
         __shared__ unsigned char s_flag[MET == kMetMAPE ? 3 * kFastDays : 1];
         obs = s_obs;
@@ -102,7 +102,22 @@ __device__ __forceinline__ SmemWindow stage_window(const DevWindow* __restrict__
     const double* src = reinterpret_cast<const double*>(gw->obs);
     double* dst = reinterpret_cast<double*>(obs);
     for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) dst[i] = src[i];
-    const TimeGrid tg = stage_times(times, n, ns, gw->h);
+    TimeGrid tg;
+    if (gw->times) {
+        // Copy the host-built table (16-byte vectors; both ends 16-aligned).
+        const int m = ns + tgrid_entries(n, ns);
+        if constexpr (SUB > 0) {  // static smem table: 16-byte aligned
+            const double2* s2 = reinterpret_cast<const double2*>(gw->times);
+            double2* d2 = reinterpret_cast<double2*>(times);
+            for (int i = threadIdx.x; i < (m >> 1); i += blockDim.x) d2[i] = __ldg(s2 + i);
+            if ((m & 1) && threadIdx.x == 0) times[m - 1] = gw->times[m - 1];
+        } else {
+            for (int i = threadIdx.x; i < m; i += blockDim.x) times[i] = __ldg(gw->times + i);
+        }
+        tg = TimeGrid{m > ns ? times + ns : nullptr, times};
+    } else {
+        tg = stage_times(times, n, ns, gw->h);
+    }
     if (MET == kMetMAPE) {
         const double* rsrc = reinterpret_cast<const double*>(gw->robs);
         double* rdst = reinterpret_cast<double*>(robs);
@@ -325,7 +340,8 @@ __device__ __forceinline__ void move_particle(const DevSwarm& sw, double best_co
 template <int NPT>
 __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& st, const PsoPlanes& P, int s,
                                             const bool* active, const size_t* p, const uint64_t* i, const double* c,
-                                            uint32_t wslot, uint64_t it, const int* ramp) {
+                                            const double (*x)[6], const double* pbc_in, uint32_t wslot, uint64_t it,
+                                            const int* ramp) {
     const size_t stride = P.stride;
     unsigned int my_ramp = 0;
 #pragma unroll
@@ -338,12 +354,12 @@ __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& s
     for (int q = 0; q < NPT; ++q) {
         if (!active[q]) continue;
         P.cost[p[q]] = c[q];
-        double pbc = P.pbc[p[q]];
+        double pbc = pbc_in[q];
         if (c[q] < pbc) {
             pbc = c[q];
             P.pbc[p[q]] = c[q];
 #pragma unroll
-            for (int d = 0; d < 6; ++d) P.pb[d * stride + p[q]] = P.x[d * stride + p[q]];
+            for (int d = 0; d < 6; ++d) P.pb[d * stride + p[q]] = x[q][d];  // the position just evaluated
         }
         if (better(pbc, i[q], my_c, my_i)) {
             my_c = pbc;
@@ -366,9 +382,12 @@ __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& s
     if (lane == 0) {
         P.part_cost[base + wslot] = my_c;
         P.part_idx[base + wslot] = my_i;
-        __threadfence();
-        ticket = atomicAdd(&st.arrived, 1u);
     }
+    // Every lane's personal-best stores and lane 0's partial are ordered
+    // before the arrival (release); the last warp fences before reading (acquire).
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) ticket = atomicAdd(&st.arrived, 1u);
     ticket = __shfl_sync(0xFFFFFFFFu, ticket, 0);
     if (ticket != n_wslots - 1) return;
     __threadfence();
@@ -402,105 +421,132 @@ __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& s
     }
 }
 
+// One CTA's share of a step launch, resolved on the host so that a CTA
+// reaches everything it needs after ONE dependent load: its swarm, its
+// particle range and the window's device block (descriptor, substep times,
+// observations), which the CTA stages with bulk asynchronous copies.
+struct CtaTask {
+    uint32_t swarm;          // index into the group's DevSwarm / DevSwarmState arrays
+    uint32_t n_valid;        // particles of this CTA (<= kStepThreads * kNP)
+    uint64_t p0;             // plane slot of the CTA's first particle
+    uint64_t i0;             // swarm-local index of the CTA's first particle
+    uint64_t max_iters;      // the swarm's iteration count
+    const DevWindow* win;    // window descriptor (device)
+    const double* times;     // its substep-time table (device)
+    const double* obs;       // obs | robs | flags, 16-byte padded sections (device)
+    uint32_t times_bytes;    // 16-byte multiples
+    uint32_t obs_bytes;
+};
+
+// ---- bulk asynchronous global -> shared copies (TMA, non-tensor) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    }
+}
+
+#ifndef SG_PBC_PREFETCH
+#define SG_PBC_PREFETCH 0
+#endif
+#ifndef SG_TMA_STAGE
+#define SG_TMA_STAGE 1
+#endif
+
+// Asynchronous staging of the CTA's window (specialised kernels, static
+// shared arrays): thread 0 arms the barrier and issues the bulk copies; the
+// caller overlaps them with the particle moves and waits with mbar_wait.
+template <int MET>
+__device__ __forceinline__ SmemWindow stage_window_async(const CtaTask& t, DevWindow* sdesc, uint64_t* bar) {
+    __shared__ __align__(16) ObsDay s_obs[kFastDays];
+    __shared__ __align__(16) double s_times[24 + kMaxTgrid];
+    __shared__ __align__(16) ObsDay s_robs[MET == kMetMAPE ? kFastDays : 1];
+    __shared__ __align__(16) unsigned char s_flag[MET == kMetMAPE ? (3 * kFastDays + 15) / 16 * 16 : 16];
+    if (threadIdx.x == 0) {
+        const uint32_t b = smem_u32(bar);
+        mbar_init(b, 1);
+        const uint32_t flag_bytes = MET == kMetMAPE ? (3u * (t.obs_bytes / 24u) + 15u) & ~15u : 0u;
+        // obs_bytes = round16(24 n) is the obs and the robs section size
+        const uint32_t n_days_bytes = t.obs_bytes;
+        mbar_expect_tx(b, static_cast<uint32_t>(sizeof(DevWindow)) + t.times_bytes + n_days_bytes +
+                              (MET == kMetMAPE ? n_days_bytes + flag_bytes : 0u));
+        bulk_g2s(smem_u32(sdesc), t.win, sizeof(DevWindow), b);
+        bulk_g2s(smem_u32(s_times), t.times, t.times_bytes, b);
+        bulk_g2s(smem_u32(s_obs), t.obs, n_days_bytes, b);
+        if (MET == kMetMAPE) {
+            const unsigned char* o = reinterpret_cast<const unsigned char*>(t.obs);
+            bulk_g2s(smem_u32(s_robs), o + n_days_bytes, n_days_bytes, b);
+            bulk_g2s(smem_u32(s_flag), o + 2 * n_days_bytes, flag_bytes, b);
+        }
+    }
+    __syncthreads();  // barrier initialised before anyone waits on it
+    return SmemWindow{sdesc, s_obs, s_robs, s_flag, TimeGrid{s_times + 24, s_times}};
+}
+
 // One Swarm::step (pso.cpp:77-101) for every swarm, iteration `it`, fused:
 // the move of iteration it-1 (which closes step it-1 in the reference), then
 // evaluate, personal best, and the global-best fold.  Thread t of a swarm's
 // CTA range owns particle t for all iterations.  Used for large swarms.
-#ifndef SG_CTA_SORT
-#define SG_CTA_SORT 0
-#endif
-
-// Morton code of the switch times (t1, t2), `bits` per coordinate, over the
-// swarm's time box: particles with close (t1, t2) get close keys.
-__device__ __forceinline__ uint32_t morton_tt(double t1, double t2, double lo, double hi, int bits) {
-    const double span = hi - lo;
-    const float sc = span > 0.0 ? static_cast<float>((1 << bits) / span) : 0.0f;
-    int q1 = static_cast<int>(static_cast<float>(t1 - lo) * sc);
-    int q2 = static_cast<int>(static_cast<float>(t2 - lo) * sc);
-    q1 = min(max(q1, 0), (1 << bits) - 1);  // NaN converts to 0 on the device
-    q2 = min(max(q2, 0), (1 << bits) - 1);
-    uint32_t key = 0;
-    for (int b = 0; b < bits; ++b) key |= (((q1 >> b) & 1u) << (2 * b + 1)) | (((q2 >> b) & 1u) << (2 * b));
-    return key;
-}
-
-// Ascending bitonic sort of kStepThreads 32-bit keys in shared memory.
-__device__ __forceinline__ void cta_bitonic_sort(uint32_t* v) {
-    const int t = threadIdx.x;
-    for (int size = 2; size <= kStepThreads; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            __syncthreads();
-            const int j = t ^ stride;
-            if (j > t) {
-                const uint32_t a = v[t], b = v[j];
-                const bool up = (t & size) == 0;
-                if ((a > b) == up) {
-                    v[t] = b;
-                    v[j] = a;
-                }
-            }
-        }
-    }
-    __syncthreads();
-}
-
 template <int FAM, int MET, int SUB>
 __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
-    pso_step_kernel(const DevSwarm* __restrict__ swarms, const uint32_t* __restrict__ cta_swarm,
-                    const DevWindow* __restrict__ windows, PsoPlanes P, DevSwarmState* __restrict__ state,
-                    uint64_t it, uint32_t cta_offset) {
+    pso_step_kernel(const CtaTask* __restrict__ tasks, const DevSwarm* __restrict__ swarms, PsoPlanes P,
+                    DevSwarmState* __restrict__ state, uint64_t it, uint32_t cta_offset) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ DevWindow sdesc;
+    __shared__ __align__(16) DevWindow sdesc;
+    __shared__ __align__(8) uint64_t bar;
     const uint32_t cta = blockIdx.x + cta_offset;
-    const int s = static_cast<int>(cta_swarm[cta]);
+    const CtaTask task = tasks[cta];
+    if (it >= task.max_iters) return;  // CTA-uniform
+    constexpr bool kAsync = SUB > 0 && SG_TMA_STAGE;
+    SmemWindow win;
+    if constexpr (kAsync) win = stage_window_async<MET>(task, &sdesc, &bar);
+    else win = stage_window<MET, SUB>(task.win, &sdesc, smem);
+    const int s = static_cast<int>(task.swarm);
     const DevSwarm& sw = swarms[s];
-    if (it >= sw.max_iters) return;  // CTA-uniform
-    const SmemWindow win = stage_window<MET, SUB>(windows + sw.window, &sdesc, smem);
-    // Thread t owns particles first + q*blockDim + t, q < kNP (coalesced per q).
-    const uint64_t first = static_cast<uint64_t>(cta - sw.cta_begin) * blockDim.x * kNP;
+    // Thread t owns particles i0 + q*blockDim + t, q < kNP (coalesced per q).
     uint64_t i[kNP];
     bool active[kNP];
     size_t p[kNP];
     double x[kNP][6];
+    double pbc[kNP];
 #pragma unroll
     for (int q = 0; q < kNP; ++q) {
-        i[q] = first + static_cast<uint64_t>(q) * blockDim.x + threadIdx.x;
-        active[q] = i[q] < sw.n;
-        p[q] = sw.offset + (active[q] ? i[q] : 0);
+        const uint32_t local = static_cast<uint32_t>(q) * blockDim.x + threadIdx.x;
+        active[q] = local < task.n_valid;
+        i[q] = task.i0 + local;
+        p[q] = task.p0 + (active[q] ? local : 0);
         if (active[q]) {
+            if (SG_PBC_PREFETCH) pbc[q] = P.pbc[p[q]];
 #pragma unroll
             for (int d = 0; d < 6; ++d) x[q][d] = P.x[d * P.stride + p[q]];
             if (it > 0) move_particle(sw, state[s].best_cost, state[s].best, P, p[q], it, x[q]);
         } else {
+            pbc[q] = 0.0;
 #pragma unroll
             for (int d = 0; d < 6; ++d) x[q][d] = x[0][d];  // idle slot mirrors slot 0 (result unused)
         }
     }
-#if SG_CTA_SORT
-    static_assert(kNP == 1, "CTA-local evaluation order needs one particle per thread");
-    {
-        // Ramp-coherent evaluation order inside the CTA: sort the CTA's
-        // particles by the Morton code of their new (t1, t2) and let thread
-        // slot t evaluate the t-th of them, so a warp's lanes share their
-        // beta-ramp days (the warp pays a ramp substep if any lane ramps).
-        // Positions were written by their movers above; the order only
-        // decides which thread evaluates which particle, never a result.
-        __shared__ uint32_t order[kStepThreads];
-        const double tlo = sw.lo[2] < sw.lo[3] ? sw.lo[2] : sw.lo[3];
-        const double thi = sw.hi[2] > sw.hi[3] ? sw.hi[2] : sw.hi[3];
-        const uint32_t key = active[0] ? morton_tt(x[0][2], x[0][3], tlo, thi, 5) : 0x3FFu + 1u;
-        order[threadIdx.x] = (key << 8) | threadIdx.x;
-        cta_bitonic_sort(order);
-        const uint32_t qv = order[threadIdx.x] & 0xFFu;
-        i[0] = first + qv;
-        active[0] = i[0] < sw.n;
-        p[0] = sw.offset + (active[0] ? i[0] : 0);
-        if (active[0]) {
+    if constexpr (kAsync) mbar_wait(smem_u32(&bar), 0);
+    if (!SG_PBC_PREFETCH) {
 #pragma unroll
-            for (int d = 0; d < 6; ++d) x[0][d] = P.x[d * P.stride + p[0]];
-        }
+        for (int q = 0; q < kNP; ++q) pbc[q] = active[q] ? P.pbc[p[q]] : 0.0;
     }
-#endif
     double c[kNP];
     int ramp[kNP];
 #pragma unroll
@@ -513,8 +559,8 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
                                                                      &ramp[0]);
         else eval_particles<FAM, MET, SUB, kNP>(x, *win.w, win.tg, win.obs, win.robs, win.flag, c, ramp);
     }
-    finish_step<kNP>(sw, state[s], P, s, active, p, i, c, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it,
-                     ramp);
+    finish_step<kNP>(sw, state[s], P, s, active, p, i, c, x, pbc,
+                     (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it, ramp);
 }
 
 // ---- ramp-coherent evaluation order (swarms of at most kSortMax particles) ----
@@ -634,17 +680,18 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
     const size_t p = sw.offset + i;
     double c = 0.0;
     int ramp = 0;
+    double x[1][6] = {};
     if (active) {
-        double x[6];
 #pragma unroll
-        for (int d = 0; d < 6; ++d) x[d] = P.x[d * P.stride + p];
-        c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag, &ramp);
+        for (int d = 0; d < 6; ++d) x[0][d] = P.x[d * P.stride + p];
+        c = eval_particle<FAM, MET, SUB>(x[0], *win.w, win.tg, win.obs, win.robs, win.flag, &ramp);
     }
     const bool act[1] = {active};
     const size_t pp[1] = {p};
     const uint64_t ii[1] = {i};
-    finish_step<1>(sw, state[s], P, s, act, pp, ii, &c, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it,
-                   &ramp);
+    const double pbc0[1] = {active ? P.pbc[p] : 0.0};
+    finish_step<1>(sw, state[s], P, s, act, pp, ii, &c, x, pbc0, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5),
+                   it, &ramp);
 }
 
 // ---- small swarms: one persistent CTA per swarm --------------------------------

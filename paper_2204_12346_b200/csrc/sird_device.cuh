@@ -18,6 +18,18 @@
 #ifndef SG_DAY_COUNTERS
 #define SG_DAY_COUNTERS 0
 #endif
+#ifndef SG_DAY_SPLIT
+#define SG_DAY_SPLIT 1
+#endif
+#ifndef SG_CONST_UNROLL
+#define SG_CONST_UNROLL 8
+#endif
+#ifndef SG_RAMP_UNROLL
+#define SG_RAMP_UNROLL 12
+#endif
+#ifndef SG_OBS_ASM
+#define SG_OBS_ASM 1
+#endif
 #if SG_DAY_COUNTERS
 // Diagnostic build only: warp-days per class (0 constant, 1 switch, 2 ramp).
 __device__ unsigned long long g_day_class[3];
@@ -25,6 +37,8 @@ __device__ unsigned long long g_day_class[3];
 
 namespace sirdgpu {
 
+constexpr int kConstUnroll = SG_CONST_UNROLL;  // substep unroll of constant days
+constexpr int kRampUnroll = SG_RAMP_UNROLL;    // ... of switch and ramp days
 constexpr int kFamD = 0;
 constexpr int kFamIRD = 1;
 constexpr int kMetMXSE = 0;
@@ -46,7 +60,7 @@ struct ObsDay {
 // Window descriptor as the kernels see it (device memory, one per window).
 // Built on the host by sg_window_create from the reference's
 // make_window_objective inputs (calibration.cpp:120-139).
-struct DevWindow {
+struct alignas(16) DevWindow {  // 16-byte multiple: staged by one bulk copy
     int n_days;
     int substeps;
     int family;
@@ -64,6 +78,7 @@ struct DevWindow {
     const ObsDay* obs;    // n_days
     const ObsDay* robs;   // RN(1/obs) per day (MAPE)
     const unsigned char* obs_flag;  // 3 per day (MAPE)
+    const double* times;  // subh[substeps] then tgrid (tgrid_entries), host-built; null: kernels compute them
 };
 
 // ---- exact arithmetic ---------------------------------------------------------
@@ -238,6 +253,14 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
     // Warp-uniform: every lane's ramp admits the 3-op division, so the ramp
     // days run without the per-value IEEE-division fallback.
     const bool warp_fast = __all_sync(mask, p.fast);
+    // Warp-uniform quiet stretches.  A lane is in beta1 for all of day d iff
+    // k1 >= d*nsub, and in beta2 for all of it iff k2 <= (d-1)*nsub
+    // (k2 >= k1).  Days before d_first are beta1 days in every lane, days
+    // after d_last beta2 days in every lane: they skip the class votes.
+#if SG_DAY_SPLIT
+    const int d_first = __reduce_min_sync(mask, p.k1 / nsub + 1);
+    const int d_last = __reduce_max_sync(mask, (p.k2 + nsub - 1) / nsub);
+#endif
     int kbase = 0;
     for (int day = 1; day < w.n_days; ++day) {
         const int lo = p.k1 - kbase;  // sub < lo  -> beta1
@@ -254,10 +277,15 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
             if ((threadIdx.x & 31) == __ffs(mask) - 1) atomicAdd(&g_day_class[cls], 1ull);
         }
 #endif
-        if (__any_sync(mask, ramp_today)) {
+#if SG_DAY_SPLIT
+        const bool quiet = day < d_first || day > d_last;
+#else
+        constexpr bool quiet = false;
+#endif
+        if (!quiet && __any_sync(mask, ramp_today)) {
             if (SG_RAMP_MODE >= 1 && SUB > 0 && warp_fast && __all_sync(mask, lo <= 0 && hi >= nsub)) {
                 // Every lane ramps through the whole day: no selects at all.
-#pragma unroll
+#pragma unroll(SUB > 0 ? kRampUnroll : 4)
                 for (int sub = 0; sub < nsub; ++sub) {
                     const double t = tg.tgrid[kbase + sub];
                     const double beta = dadd(p.b1, dmul(p.slope, dsub(t, p.t1)));
@@ -269,7 +297,7 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
                 // (the warp would issue it anyway once any lane needs it) and
                 // selects; non-FP64 work per substep is two compares and
                 // selects plus the t_k load.
-#pragma unroll
+#pragma unroll(SUB > 0 ? kRampUnroll : 4)
                 for (int sub = 0; sub < nsub; ++sub) {
                     const double t = tg.tgrid[kbase + sub];
                     const double beta = dadd(p.b1, dmul(p.slope, dsub(t, p.t1)));
@@ -279,7 +307,7 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
                     euler_substep(bp, g, mu, h, S, I, R, D);
                 }
             } else {
-#pragma unroll
+#pragma unroll(SUB > 0 ? kRampUnroll : 4)
                 for (int sub = 0; sub < nsub; ++sub) {
                     double bp = sub < lo ? p.bp1 : p.bp2;
                     if (sub >= lo && sub < hi) {
@@ -291,12 +319,12 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
                     euler_substep(bp, g, mu, h, S, I, R, D);
                 }
             }
-        } else if (__any_sync(mask, switch_today)) {
-#pragma unroll
+        } else if (!quiet && __any_sync(mask, switch_today)) {
+#pragma unroll(SUB > 0 ? kRampUnroll : 4)
             for (int sub = 0; sub < nsub; ++sub) euler_substep(sub < lo ? p.bp1 : p.bp2, g, mu, h, S, I, R, D);
         } else {
             const double bp = lo >= nsub ? p.bp1 : p.bp2;
-#pragma unroll
+#pragma unroll(SUB > 0 ? kConstUnroll : 4)
             for (int sub = 0; sub < nsub; ++sub) euler_substep(bp, g, mu, h, S, I, R, D);
         }
         kbase += nsub;
@@ -413,19 +441,28 @@ struct ScoreSink {
     const ObsDay* obs;    // shared memory
     const ObsDay* robs;   // shared memory (MAPE)
     const unsigned char* flag;  // shared memory (MAPE)
+    uint32_t obs_s;       // shared-window address of obs
     double acc[3];
 
     ScoreSink() = default;
     __device__ __forceinline__ ScoreSink(const DevWindow& win, const ObsDay* o, const ObsDay* ro,
                                          const unsigned char* f)
-        : w(&win), obs(o), robs(ro), flag(f) {
+        : w(&win), obs(o), robs(ro), flag(f), obs_s(static_cast<uint32_t>(__cvta_generic_to_shared(o))) {
         acc[0] = win.acc0[0];  // day 0 already scored (sg_window_create)
         acc[1] = win.acc0[1];
         acc[2] = win.acc0[2];
     }
 
     __device__ __forceinline__ void one(int c, int day, double pred) {
-        const double o = obs[day].v[c];
+        double o;
+        if (MET == kMetMAPE || !SG_OBS_ASM) {
+            o = obs[day].v[c];
+        } else {
+            // 32-bit shared address + immediate offset (a generic pointer
+            // makes nvcc rebuild the shared-window base every day)
+            const uint32_t a = obs_s + static_cast<uint32_t>(day) * sizeof(ObsDay) + 8u * c;
+            asm("ld.shared.f64 %0, [%1];" : "=d"(o) : "r"(a));
+        }
         if (MET == kMetMAPE) {
             const unsigned char f = flag[3 * day + c];
             if (f == kObsSkip) return;  // objectives.cpp:46-48
