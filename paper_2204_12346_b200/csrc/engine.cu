@@ -717,12 +717,12 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     SG_CUDA(ctx, b.alloc(&g.d_win, wtab.size()));
     SG_CUDA(ctx, b.alloc(&g.d_task, g.n_ctas));
     SG_CUDA(ctx, b.alloc(&g.d_state, sw.size()));
-    SG_CUDA(ctx, b.alloc(&P.x, 6 * g.n_total));
-    SG_CUDA(ctx, b.alloc(&P.v, 6 * g.n_total));
-    SG_CUDA(ctx, b.alloc(&P.pb, 6 * g.n_total));
+    SG_CUDA(ctx, b.alloc(&P.x, pblock_elems(g.n_total, 6)));
+    SG_CUDA(ctx, b.alloc(&P.v, pblock_elems(g.n_total, 6)));
+    SG_CUDA(ctx, b.alloc(&P.pb, pblock_elems(g.n_total, 6)));
     SG_CUDA(ctx, b.alloc(&P.pbc, g.n_total));
     SG_CUDA(ctx, b.alloc(&P.cost, g.n_total));
-    SG_CUDA(ctx, b.alloc(&P.mt, static_cast<size_t>(kMtN) * g.n_total));
+    SG_CUDA(ctx, b.alloc(&P.mt, pblock_elems(g.n_total, kMtN)));
     SG_CUDA(ctx, b.alloc(&P.part_cost, g.n_ctas * kStepWarps));
     SG_CUDA(ctx, b.alloc(&P.part_idx, g.n_ctas * kStepWarps));
     SG_CUDA(ctx, b.alloc(&P.history, sw.size() * g.iters));

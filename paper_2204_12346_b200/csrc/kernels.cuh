@@ -225,13 +225,24 @@ struct DevSwarmState {
     unsigned long long ramp_substeps;  // telemetry: ramp substeps evaluated (roofline op count)
 };
 
+// Particle-block layout: particles come in blocks of 32 (one warp's worth);
+// a block stores each field's 32 values contiguously, so a warp's access to
+// one field is one 256-byte segment and every field of a particle sits at a
+// compile-time offset (field * 32 elements) from the particle's base.
+__host__ __device__ __forceinline__ size_t pblock_base(size_t p, int fields) {
+    return (p >> 5) * (32 * static_cast<size_t>(fields)) + (p & 31);
+}
+__host__ __device__ inline size_t pblock_elems(size_t n, int fields) {
+    return (n + 31) / 32 * 32 * static_cast<size_t>(fields);
+}
+
 struct PsoPlanes {
-    double* x;           // 6 planes of `stride` doubles
+    double* x;           // particle blocks of 6 fields (pblock_base(p, 6) + d*32)
     double* v;
     double* pb;
     double* pbc;         // personal-best cost
     double* cost;        // last evaluated cost
-    uint64_t* mt;        // 312 planes
+    uint64_t* mt;        // particle blocks of 312 engine words (pblock_base(p, 312) + w*32)
     size_t stride;       // total particles (plane length)
     double* part_cost;   // per warp of the step kernel
     unsigned long long* part_idx;
@@ -257,25 +268,26 @@ __device__ __forceinline__ double std_clamp(double v, double lo, double hi) {
 // engine i = mt19937_64(mix_seed(seed, i)); x[d] = lo[d] + u*(hi[d]-lo[d])
 // for d = 0..5 in order; repair; v = 0; pbest = x; pbest cost = +inf.
 __device__ __forceinline__ void init_particle(const DevSwarm& sw, const PsoPlanes& P, size_t p, uint64_t i) {
-    const size_t stride = P.stride;
     // seed: mt[0] = seed; mt[j] = f*(mt[j-1] ^ (mt[j-1] >> 62)) + j
+    uint64_t* const mt = P.mt + pblock_base(p, kMtN);
     uint64_t m = mix_seed(sw.seed, i);
-    P.mt[p] = m;
+    mt[0] = m;
     for (int j = 1; j < kMtN; ++j) {
         m = kMtF * (m ^ (m >> 62)) + static_cast<uint64_t>(j);
-        P.mt[static_cast<size_t>(j) * stride + p] = m;
+        mt[32 * j] = m;
     }
     double u[6];
-    mt_draw<6>(P.mt, stride, p, 0, u);  // words 0..5 of the first generation
+    mt_draw<6>(mt, 0, u);  // words 0..5 of the first generation
     double x[6];
 #pragma unroll
     for (int d = 0; d < 6; ++d) x[d] = dadd(sw.lo[d], dmul(u[d], dsub(sw.hi[d], sw.lo[d])));
     if (sw.repair) repair_order(x);
+    const size_t b = pblock_base(p, 6);
 #pragma unroll
     for (int d = 0; d < 6; ++d) {
-        P.x[d * stride + p] = x[d];
-        P.v[d * stride + p] = 0.0;
-        P.pb[d * stride + p] = x[d];
+        P.x[b + 32 * d] = x[d];
+        P.v[b + 32 * d] = 0.0;
+        P.pb[b + 32 * d] = x[d];
     }
     P.pbc[p] = __longlong_as_double(0x7FF0000000000000LL);
 }
@@ -311,25 +323,27 @@ __device__ __forceinline__ bool better(double ca, unsigned long long ia, double 
 // iteration it-1 and writes x, v; returns the new position in x.
 __device__ __forceinline__ void move_particle(const DevSwarm& sw, double best_cost, const double* best,
                                               const PsoPlanes& P, size_t p, uint64_t it, double* x) {
-    const size_t stride = P.stride;
     const bool have_best = best_cost < __longlong_as_double(0x7FF0000000000000LL);  // pso.cpp:106
     double u[12];
-    mt_draw<12>(P.mt, stride, p, move_draw_word(it), u);
+    mt_draw<12>(P.mt + pblock_base(p, kMtN), move_draw_word(it), u);
+    double* const vb = P.v + pblock_base(p, 6);
+    const double* const pbb = P.pb + pblock_base(p, 6);
+    double* const xb = P.x + pblock_base(p, 6);
 #pragma unroll
     for (int d = 0; d < 6; ++d) {
         const double r1 = u[2 * d];
         const double r2 = u[2 * d + 1];
-        const double vd = P.v[d * stride + p];
-        const double pbd = P.pb[d * stride + p];
+        const double vd = vb[32 * d];
+        const double pbd = pbb[32 * d];
         // vel = w*v + (c1*r1)*(pbest - x)   (pso.cpp:116)
         double vel = dadd(dmul(sw.w, vd), dmul(dmul(sw.c1, r1), dsub(pbd, x[d])));
         if (have_best) vel = dadd(vel, dmul(dmul(sw.c2, r2), dsub(best[d], x[d])));  // pso.cpp:117-119
-        P.v[d * stride + p] = vel;
+        vb[32 * d] = vel;
         x[d] = std_clamp(dadd(x[d], vel), sw.lo[d], sw.hi[d]);  // pso.cpp:121
     }
     if (sw.repair) repair_order(x);  // pso.cpp:123-125
 #pragma unroll
-    for (int d = 0; d < 6; ++d) P.x[d * stride + p] = x[d];
+    for (int d = 0; d < 6; ++d) xb[32 * d] = x[d];
 }
 
 // Personal best (pso.cpp:83-89), warp argmin of personal-best costs (lowest
@@ -342,7 +356,6 @@ __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& s
                                             const bool* active, const size_t* p, const uint64_t* i, const double* c,
                                             const double (*x)[6], const double* pbc_in, uint32_t wslot, uint64_t it,
                                             const int* ramp) {
-    const size_t stride = P.stride;
     unsigned int my_ramp = 0;
 #pragma unroll
     for (int q = 0; q < NPT; ++q) my_ramp += active[q] ? static_cast<unsigned int>(ramp[q]) : 0u;
@@ -359,7 +372,7 @@ __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& s
             pbc = c[q];
             P.pbc[p[q]] = c[q];
 #pragma unroll
-            for (int d = 0; d < 6; ++d) P.pb[d * stride + p[q]] = x[q][d];  // the position just evaluated
+            for (int d = 0; d < 6; ++d) P.pb[pblock_base(p[q], 6) + 32 * d] = x[q][d];  // the position just evaluated
         }
         if (better(pbc, i[q], my_c, my_i)) {
             my_c = pbc;
@@ -414,7 +427,7 @@ __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& s
         if (bc < st.best_cost) {  // strict: an equal later cost never replaces (pso.cpp:91)
             st.best_cost = bc;
             const size_t q = sw.offset + bi;
-            for (int d = 0; d < 6; ++d) st.best[d] = __ldcg(&P.pb[d * stride + q]);
+            for (int d = 0; d < 6; ++d) st.best[d] = __ldcg(&P.pb[pblock_base(q, 6) + 32 * d]);
         }
         P.history[static_cast<size_t>(s) * P.hist_stride + it] = st.best_cost;
         st.arrived = 0;
@@ -534,7 +547,7 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
         if (active[q]) {
             if (SG_PBC_PREFETCH) pbc[q] = P.pbc[p[q]];
 #pragma unroll
-            for (int d = 0; d < 6; ++d) x[q][d] = P.x[d * P.stride + p[q]];
+            for (int d = 0; d < 6; ++d) x[q][d] = P.x[pblock_base(p[q], 6) + 32 * d];
             if (it > 0) move_particle(sw, state[s].best_cost, state[s].best, P, p[q], it, x[q]);
         } else {
             pbc[q] = 0.0;
@@ -609,7 +622,7 @@ __global__ void __launch_bounds__(kStepThreads) pso_move_kernel(const DevSwarm* 
     const size_t p = sw.offset + i;
     double x[6];
 #pragma unroll
-    for (int d = 0; d < 6; ++d) x[d] = P.x[d * P.stride + p];
+    for (int d = 0; d < 6; ++d) x[d] = P.x[pblock_base(p, 6) + 32 * d];
     if (it > 0) move_particle(sw, state[s].best_cost, state[s].best, P, p, it, x);
     const double tlo = sw.lo[2] < sw.lo[3] ? sw.lo[2] : sw.lo[3];
     const double thi = sw.hi[2] > sw.hi[3] ? sw.hi[2] : sw.hi[3];
@@ -683,7 +696,7 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
     double x[1][6] = {};
     if (active) {
 #pragma unroll
-        for (int d = 0; d < 6; ++d) x[0][d] = P.x[d * P.stride + p];
+        for (int d = 0; d < 6; ++d) x[0][d] = P.x[pblock_base(p, 6) + 32 * d];
         c = eval_particle<FAM, MET, SUB>(x[0], *win.w, win.tg, win.obs, win.robs, win.flag, &ramp);
     }
     const bool act[1] = {active};
@@ -719,7 +732,6 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 2) pso_swarm_kernel(const De
     const DevSwarm& sw = swarms[s];
     const SmemWindow win = stage_window<MET, SUB>(windows + sw.window, &sdesc, smem);
     const uint32_t n = static_cast<uint32_t>(sw.n);
-    const size_t stride = P.stride;
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) init_particle(sw, P, sw.offset + i, i);
     if (threadIdx.x == 0) {
         gbest_cost = __longlong_as_double(0x7FF0000000000000LL);
@@ -737,7 +749,7 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 2) pso_swarm_kernel(const De
             const size_t p = sw.offset + i;
             double x[6];
 #pragma unroll
-            for (int d = 0; d < 6; ++d) x[d] = P.x[d * stride + p];
+            for (int d = 0; d < 6; ++d) x[d] = P.x[pblock_base(p, 6) + 32 * d];
             if (it > 0) move_particle(sw, gbest_cost, gbest, P, p, it, x);
             int ramp = 0;
             const double c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag, &ramp);
@@ -748,7 +760,7 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 2) pso_swarm_kernel(const De
                 pbc = c;
                 P.pbc[p] = c;
 #pragma unroll
-                for (int d = 0; d < 6; ++d) P.pb[d * stride + p] = x[d];
+                for (int d = 0; d < 6; ++d) P.pb[pblock_base(p, 6) + 32 * d] = x[d];
             }
             if (better(pbc, i, my_c, my_i)) {
                 my_c = pbc;
@@ -779,7 +791,7 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 2) pso_swarm_kernel(const De
                 }
             if (bc < gbest_cost) {  // pso.cpp:90-96: strict, lowest index on ties
                 gbest_cost = bc;
-                for (int d = 0; d < 6; ++d) gbest[d] = P.pb[d * stride + sw.offset + bi];
+                for (int d = 0; d < 6; ++d) gbest[d] = P.pb[pblock_base(sw.offset + bi, 6) + 32 * d];
             }
             P.history[static_cast<size_t>(s) * P.hist_stride + it] = gbest_cost;
         }

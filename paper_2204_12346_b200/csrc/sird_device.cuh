@@ -561,8 +561,8 @@ __device__ __forceinline__ void eval_particles(const double (*x)[6], const DevWi
 // ---- std::mt19937_64, structure-of-arrays ---------------------------------
 //
 // Each particle owns one engine (pso.hpp:79) seeded mix_seed(seed, i)
-// (pso.cpp:55-57).  State word j of particle p lives at st[j*stride + p] so a
-// warp touches 32 consecutive words.  Every particle of a swarm has drawn the
+// (pso.cpp:55-57).  State word j of particle p lives at
+// mt[pblock_base(p, 312) + 32*j], so a warp touches 32 consecutive words.  Every particle of a swarm has drawn the
 // same number of values at any time, so the generation position `count` is
 // uniform and the standard in-place twist is evaluated lazily, one word per
 // draw: word i of the next generation depends on words i, i+1 (old) and
@@ -599,34 +599,35 @@ __device__ __forceinline__ double to_uniform01(uint64_t x) {
     return dmul(static_cast<double>(x >> 11), 0x1.0p-53);
 }
 
-// Draw NDRAW consecutive values (NDRAW <= 12) from the SoA engine of particle
-// p, starting at state word i0 = (values drawn so far) mod 312 — uniform over
-// a swarm, so callers compute it once.  All 2*NDRAW+1 state words are loaded
-// before any is rewritten: the batch's words are distinct (NDRAW < 156),
-// every "next" word is read before it is twisted (old value, as the
-// sequential twist reads it), and every "far" word lies outside the batch —
-// so the loads are independent and overlap.
+// Draw NDRAW consecutive values (NDRAW <= 12) from the engine whose word w
+// lives at mt[32*w] (particle-block layout), starting at state word
+// i0 = (values drawn so far) mod 312 — uniform over a swarm, so callers
+// compute it once.  All 2*NDRAW+1 state words are loaded before any is
+// rewritten: the batch's words are distinct (NDRAW < 156), every "next" word
+// is read before it is twisted (old value, as the sequential twist reads
+// it), and every "far" word lies outside the batch — so the loads are
+// independent and overlap.  Word addresses are a row pointer plus a
+// compile-time offset; the (warp-uniform) wrap past word 311 switches rows.
 template <int NDRAW>
-__device__ __forceinline__ void mt_draw(uint64_t* __restrict__ st, size_t stride, size_t p, int i0, double* out) {
+__device__ __forceinline__ void mt_draw(uint64_t* __restrict__ mt, int i0, double* out) {
     static_assert(NDRAW >= 1 && NDRAW < kMtM, "batch must not reach its own far words");
-    uint64_t* __restrict__ base = st + p;
+    uint64_t* const row = mt + 32 * i0;            // word i0 + j at row[32*j] ...
+    uint64_t* const row_w = row - 32 * kMtN;       // ... or, past word 311, at row_w[32*j]
+    const int wrap = kMtN - i0;                    // first j that wraps
+    const int f0 = i0 + kMtM < kMtN ? i0 + kMtM : i0 + kMtM - kMtN;  // far word of j = 0
+    uint64_t* const frow = mt + 32 * f0;
+    uint64_t* const frow_w = frow - 32 * kMtN;
+    const int fwrap = kMtN - f0;
     uint64_t cur[NDRAW + 1];
     uint64_t far[NDRAW];
 #pragma unroll
-    for (int j = 0; j <= NDRAW; ++j) {
-        const int w = i0 + j < kMtN ? i0 + j : i0 + j - kMtN;
-        cur[j] = base[static_cast<size_t>(w) * stride];
-    }
+    for (int j = 0; j <= NDRAW; ++j) cur[j] = (j < wrap ? row : row_w)[32 * j];
+#pragma unroll
+    for (int j = 0; j < NDRAW; ++j) far[j] = (j < fwrap ? frow : frow_w)[32 * j];
 #pragma unroll
     for (int j = 0; j < NDRAW; ++j) {
-        const int w = i0 + j + kMtM < kMtN ? i0 + j + kMtM : i0 + j + kMtM - kMtN;
-        far[j] = base[static_cast<size_t>(w) * stride];
-    }
-#pragma unroll
-    for (int j = 0; j < NDRAW; ++j) {
-        const int w = i0 + j < kMtN ? i0 + j : i0 + j - kMtN;
         const uint64_t v = mt_twist_word(cur[j], cur[j + 1], far[j]);
-        base[static_cast<size_t>(w) * stride] = v;
+        (j < wrap ? row : row_w)[32 * j] = v;
         out[j] = to_uniform01(mt_temper(v));
     }
 }
