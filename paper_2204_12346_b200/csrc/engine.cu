@@ -14,6 +14,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -1004,14 +1007,31 @@ void sg_plan_destroy(sg_plan* plan) {
 // engine words) — used to split oversized calls into sequential plans.
 static constexpr size_t kBytesPerParticle = (18 + 2 + kMtN) * sizeof(double);
 
+void sg_trace_phase(const char* what) {
+    static const bool on = std::getenv("SG_TRACE") != nullptr;
+    if (!on) return;
+    static auto last = std::chrono::steady_clock::now();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[sg] %-28s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
+
 int sg_fit_swarms(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg_swarm_result* results) {
     if (!ctx) return SG_ERR_INVALID_ARGUMENT;
     if (n_swarms == 0) return SG_OK;
     if (!swarms || !results) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null swarm arrays");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
-    size_t free_b = 0, total_b = 0;
-    SG_CUDA(ctx, cudaMemGetInfo(&free_b, &total_b));
-    const size_t budget = std::max<size_t>(free_b / 10 * 7, size_t(1) << 28);
+    // Split oversized calls into sequential plans that fit in 70% of the
+    // free memory; the (slow, driver-locking) memory query only runs when
+    // the call could come near the 180 GB of a B200.
+    size_t want = 0;
+    for (size_t k = 0; k < n_swarms; ++k) want += swarms[k].n_particles * kBytesPerParticle;
+    size_t budget = want;
+    if (want > (size_t(16) << 30)) {
+        size_t free_b = 0, total_b = 0;
+        SG_CUDA(ctx, cudaMemGetInfo(&free_b, &total_b));
+        budget = std::max<size_t>(free_b / 10 * 7, size_t(1) << 28);
+    }
     size_t begin = 0;
     while (begin < n_swarms) {
         size_t end = begin, bytes = 0;
@@ -1022,10 +1042,15 @@ int sg_fit_swarms(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg_
             ++end;
         }
         sg_plan* plan = nullptr;
+        sg_trace_phase("fit_swarms: chunk");
         int rc = sg_plan_create(ctx, swarms + begin, end - begin, &plan);
+        sg_trace_phase("plan_create");
         if (!rc) rc = sg_plan_run(plan);
+        sg_trace_phase("plan_run");
         if (!rc) rc = sg_plan_results(plan, results + begin);
+        sg_trace_phase("plan_results");
         sg_plan_destroy(plan);
+        sg_trace_phase("plan_destroy");
         if (rc) return rc;
         begin = end;
     }

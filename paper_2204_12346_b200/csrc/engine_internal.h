@@ -8,3 +8,6 @@
 
 // Sets the text sg_last_error(ctx) returns.
 void sg_set_last_error(sg_ctx* ctx, const std::string& message);
+
+// SG_TRACE=1: host-phase timestamps on stderr (diagnostics only).
+extern "C" void sg_trace_phase(const char* what);

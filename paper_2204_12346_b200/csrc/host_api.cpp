@@ -381,6 +381,7 @@ std::vector<JobOutcome> fit_jobs(const EpiSeries& data, const std::vector<Job>& 
             fail_job(o, status_of(e), e.what());
         }
     }
+    sg_trace_phase("fit_jobs: windows built");
     if (descs.empty()) return out;
     std::vector<sg_swarm_result> res(descs.size());
     for (std::size_t k = 0; k < descs.size(); ++k) {
@@ -388,6 +389,7 @@ std::vector<JobOutcome> fit_jobs(const EpiSeries& data, const std::vector<Job>& 
         res[k].cost_history = histories[desc_job[k]].data();
     }
     check(ctx, sg_fit_swarms(ctx, descs.data(), descs.size(), res.data()));
+    sg_trace_phase("fit_jobs: swarms done");
     // Re-integrate every successful best fit (calibration.cpp:175-176).
     std::vector<std::size_t> done;
     std::vector<double> params;
@@ -439,6 +441,7 @@ std::vector<JobOutcome> fit_jobs(const EpiSeries& data, const std::vector<Job>& 
             o.fit.ok = true;
         }
     }
+    sg_trace_phase("fit_jobs: re-integrated");
     return out;
 }
 
@@ -755,6 +758,7 @@ int sg_fit_all_windows_series(sg_ctx* ctx, const double* I, const double* R, con
     if (!ctx || !I || !R || !D || !s || !n_windows || !records || !mean_r2_d || !failed_count)
         return SG_ERR_INVALID_ARGUMENT;
     return guarded(ctx, [&] {
+        sg_trace_phase("fit_all_windows_series: in");
         const EpiSeries data = series_of(I, R, D, n_series);
         const WindowScheme scheme{static_cast<std::size_t>(tau), static_cast<std::size_t>(delta)};
         *n_windows = make_windows(data.size(), scheme).size();
@@ -769,6 +773,7 @@ int sg_fit_all_windows_series(sg_ctx* ctx, const double* I, const double* R, con
         }
         *mean_r2_d = all.mean_r2_d;
         *failed_count = all.failed_count;
+        sg_trace_phase("fit_all_windows_series: out");
     });
 }
 
