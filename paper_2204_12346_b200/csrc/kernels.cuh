@@ -203,17 +203,17 @@ __global__ void __launch_bounds__(kEvalThreads) integrate_kernel(DevWindow w, co
 // ---- particle swarm ---------------------------------------------------------------
 
 // One swarm as the kernels see it (pso.hpp:14-32 config + bounds).
-struct DevSwarm {
-    int window;          // index into the window table
-    int repair;          // repair_time_order hook (calibration.cpp:89-93)
+struct alignas(16) DevSwarm {  // bounds and coefficients first: 16-byte vector loads
+    double lo[6], hi[6];
+    double w, c1, c2;    // w, c1 adjacent and 16-byte aligned
+    uint64_t seed;
     uint64_t n;          // particles
     uint64_t offset;     // first particle in the flattened SoA planes
     uint64_t max_iters;
     uint32_t cta_begin;  // first CTA of this swarm in pso_step_kernel's grid
     uint32_t n_ctas;
-    double lo[6], hi[6];
-    double w, c1, c2;
-    uint64_t seed;
+    int window;          // index into the window table
+    int repair;          // repair_time_order hook (calibration.cpp:89-93)
 };
 
 // Swarm-global state updated by the last CTA of every iteration.
@@ -324,6 +324,17 @@ __device__ __forceinline__ bool better(double ca, unsigned long long ia, double 
 __device__ __forceinline__ void move_particle(const DevSwarm& sw, double best_cost, const double* best,
                                               const PsoPlanes& P, size_t p, uint64_t it, double* x) {
     const bool have_best = best_cost < __longlong_as_double(0x7FF0000000000000LL);  // pso.cpp:106
+    double lo[6], hi[6];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {  // 16-byte loads of the swarm's bounds
+        const double2 l = reinterpret_cast<const double2*>(sw.lo)[k];
+        const double2 h = reinterpret_cast<const double2*>(sw.hi)[k];
+        lo[2 * k] = l.x;
+        lo[2 * k + 1] = l.y;
+        hi[2 * k] = h.x;
+        hi[2 * k + 1] = h.y;
+    }
+    const double2 wc1 = *reinterpret_cast<const double2*>(&sw.w);
     double u[12];
     mt_draw<12>(P.mt + pblock_base(p, kMtN), move_draw_word(it), u);
     double* const vb = P.v + pblock_base(p, 6);
@@ -336,10 +347,10 @@ __device__ __forceinline__ void move_particle(const DevSwarm& sw, double best_co
         const double vd = vb[32 * d];
         const double pbd = pbb[32 * d];
         // vel = w*v + (c1*r1)*(pbest - x)   (pso.cpp:116)
-        double vel = dadd(dmul(sw.w, vd), dmul(dmul(sw.c1, r1), dsub(pbd, x[d])));
+        double vel = dadd(dmul(wc1.x, vd), dmul(dmul(wc1.y, r1), dsub(pbd, x[d])));
         if (have_best) vel = dadd(vel, dmul(dmul(sw.c2, r2), dsub(best[d], x[d])));  // pso.cpp:117-119
         vb[32 * d] = vel;
-        x[d] = std_clamp(dadd(x[d], vel), sw.lo[d], sw.hi[d]);  // pso.cpp:121
+        x[d] = std_clamp(dadd(x[d], vel), lo[d], hi[d]);  // pso.cpp:121
     }
     if (sw.repair) repair_order(x);  // pso.cpp:123-125
 #pragma unroll
@@ -858,7 +869,7 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
         for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
         return;
     }
-    const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w);
+    const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w, SUB > 0 ? sw.tg.tgrid : nullptr);
     double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
     ScoreSink<FAM, MET> score(w, sw.obs, sw.robs, sw.flag);  // starts from the day-0 contribution
     integrate_days<SUB>(p, w, sw.tg, S, I, R, D, score);

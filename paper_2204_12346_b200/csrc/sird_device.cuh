@@ -138,11 +138,18 @@ __device__ __forceinline__ double t_of(int k, int S, double h) {
 // Number of k in [0, K) with t_k < x (x may be NaN -> 0).  t_k is within a
 // few ulps of k/S, so the search starts at floor(x*S) and walks the exact
 // t_k to the boundary (one or two steps in practice; monotone, so exact).
-__device__ __forceinline__ int count_t_below(double x, int K, int S, double h) {
+// With a substep-time table (tgrid[k] == t_of(k), k < K) the walk reads it
+// instead of recomputing t_k.
+__device__ __forceinline__ int count_t_below(double x, int K, int S, double h, const double* tgrid = nullptr) {
     if (!(x > 0.0)) return 0;  // t_0 = 0: nothing below 0, -inf or NaN
     if (!(x <= static_cast<double>(K))) return K;  // +inf / beyond the window
     int k = static_cast<int>(x * static_cast<double>(S));  // estimate, any rounding
     k = k < 0 ? 0 : (k > K ? K : k);
+    if (tgrid) {
+        while (k < K && tgrid[k] < x) ++k;
+        while (k > 0 && !(tgrid[k - 1] < x)) --k;
+        return k;
+    }
     while (k < K && t_of(k, S, h) < x) ++k;
     while (k > 0 && !(t_of(k - 1, S, h) < x)) --k;
     return k;
@@ -170,7 +177,7 @@ __device__ __forceinline__ bool beta_in_fast_range(double b) {
 }
 
 __device__ __forceinline__ Particle make_particle(double b1, double b2, double t1, double t2, double g, double mu,
-                                                  const DevWindow& w) {
+                                                  const DevWindow& w, const double* tgrid = nullptr) {
     Particle p;
     p.b1 = b1;
     p.b2 = b2;
@@ -184,10 +191,10 @@ __device__ __forceinline__ Particle make_particle(double b1, double b2, double t
     opaque(p.bp2);
     opaque(p.slope);
     const int K = (w.n_days - 1) * w.substeps;
-    p.k1 = count_t_below(t1, K, w.substeps, w.h);
+    p.k1 = count_t_below(t1, K, w.substeps, w.h, tgrid);
     // "t >= t2" is the complement of "t < t2" except for NaN t2, where both
     // comparisons are false and the ramp branch is taken (model.cpp:59-63).
-    p.k2 = (t2 != t2) ? K : count_t_below(t2, K, w.substeps, w.h);
+    p.k2 = (t2 != t2) ? K : count_t_below(t2, K, w.substeps, w.h, tgrid);
     if (p.k2 < p.k1) p.k2 = p.k1;  // t1 > t2: no ramp (k >= k1 implies t >= t2)
     p.fast = w.fast_N && isfinite(t1) && isfinite(t2) && isfinite(p.slope) && beta_in_fast_range(b1) &&
              beta_in_fast_range(b2);
@@ -518,7 +525,7 @@ __device__ __forceinline__ double eval_particle(const double* x, const DevWindow
         if (ramp) *ramp = 0;
         return __longlong_as_double(0x7FF0000000000000LL);
     }
-    const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w);
+    const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w, SUB > 0 ? tg.tgrid : nullptr);
     if (ramp) *ramp = p.k2 - p.k1;
     double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
     ScoreSink<FAM, MET> sink(w, obs, robs, flag);  // starts from the day-0 contribution
@@ -545,7 +552,7 @@ __device__ __forceinline__ void eval_particles(const double (*x)[6], const DevWi
     ScoreSink<FAM, MET> sink[NP];
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
-        p[q] = make_particle(x[q][0], x[q][1], x[q][2], x[q][3], x[q][4], x[q][5], w);
+        p[q] = make_particle(x[q][0], x[q][1], x[q][2], x[q][3], x[q][4], x[q][5], w, SUB > 0 ? tg.tgrid : nullptr);
         ramp[q] = p[q].k2 - p[q].k1;
         S[q] = w.init[0];
         I[q] = w.init[1];
