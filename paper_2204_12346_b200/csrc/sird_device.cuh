@@ -19,7 +19,7 @@
 #define SG_DAY_COUNTERS 0
 #endif
 #ifndef SG_DAY_SPLIT
-#define SG_DAY_SPLIT 1
+#define SG_DAY_SPLIT 2
 #endif
 #ifndef SG_CONST_UNROLL
 #define SG_CONST_UNROLL 8
@@ -268,8 +268,8 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
     const int d_first = __reduce_min_sync(mask, p.k1 / nsub + 1);
     const int d_last = __reduce_max_sync(mask, (p.k2 + nsub - 1) / nsub);
 #endif
-    int kbase = 0;
-    for (int day = 1; day < w.n_days; ++day) {
+    // One classified day (class votes, then the matching substep loop).
+    auto classified_day = [&](int day, int kbase) {
         const int lo = p.k1 - kbase;  // sub < lo  -> beta1
         const int hi = p.k2 - kbase;  // sub >= hi -> beta2, else ramp
         // Warp-uniform day classes (the regime depends only on k, so a day
@@ -284,10 +284,10 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
             if ((threadIdx.x & 31) == __ffs(mask) - 1) atomicAdd(&g_day_class[cls], 1ull);
         }
 #endif
-#if SG_DAY_SPLIT
+#if SG_DAY_SPLIT == 1
         const bool quiet = day < d_first || day > d_last;
 #else
-        constexpr bool quiet = false;
+        constexpr bool quiet = false;  // SG_DAY_SPLIT 2: quiet days never reach here
 #endif
         if (!quiet && __any_sync(mask, ramp_today)) {
             if (SG_RAMP_MODE >= 1 && SUB > 0 && warp_fast && __all_sync(mask, lo <= 0 && hi >= nsub)) {
@@ -334,9 +334,37 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
 #pragma unroll(SUB > 0 ? kConstUnroll : 4)
             for (int sub = 0; sub < nsub; ++sub) euler_substep(bp, g, mu, h, S, I, R, D);
         }
-        kbase += nsub;
+    };
+#if SG_DAY_SPLIT >= 2
+    // Three segments: quiet beta1 days, classified days, quiet beta2 days.
+    // The quiet loop body exists once in the code (instruction-cache
+    // footprint) and runs without votes or regime selects.
+    const int n_days = w.n_days;
+    int day = 1;
+#pragma unroll 1
+    for (int seg = 0; seg < 3; ++seg) {
+        if (seg == 1) {
+            const int end = d_last + 1 < n_days ? d_last + 1 : n_days;
+            for (; day < end; ++day) {
+                classified_day(day, (day - 1) * nsub);
+                sink.day(day, S, I, R, D);
+            }
+            continue;
+        }
+        const int end = seg == 0 ? (d_first < n_days ? d_first : n_days) : n_days;
+        const double bpq = seg == 0 ? p.bp1 : p.bp2;
+        for (; day < end; ++day) {
+#pragma unroll(SUB > 0 ? kConstUnroll : 4)
+            for (int sub = 0; sub < nsub; ++sub) euler_substep(bpq, g, mu, h, S, I, R, D);
+            sink.day(day, S, I, R, D);
+        }
+    }
+#else
+    for (int day = 1; day < w.n_days; ++day) {
+        classified_day(day, (day - 1) * nsub);
         sink.day(day, S, I, R, D);
     }
+#endif
 }
 
 // NP particles per thread, interleaved: NP independent Euler chains give the
@@ -448,13 +476,13 @@ struct ScoreSink {
     const ObsDay* obs;    // shared memory
     const ObsDay* robs;   // shared memory (MAPE)
     const unsigned char* flag;  // shared memory (MAPE)
-    uint32_t obs_s;       // shared-window address of obs
+    uint32_t obs_s;       // shared-window address of obs[next day] (days arrive as 1, 2, ... in order)
     double acc[3];
 
     ScoreSink() = default;
     __device__ __forceinline__ ScoreSink(const DevWindow& win, const ObsDay* o, const ObsDay* ro,
                                          const unsigned char* f)
-        : w(&win), obs(o), robs(ro), flag(f), obs_s(static_cast<uint32_t>(__cvta_generic_to_shared(o))) {
+        : w(&win), obs(o), robs(ro), flag(f), obs_s(static_cast<uint32_t>(__cvta_generic_to_shared(o + 1))) {
         acc[0] = win.acc0[0];  // day 0 already scored (sg_window_create)
         acc[1] = win.acc0[1];
         acc[2] = win.acc0[2];
@@ -467,7 +495,7 @@ struct ScoreSink {
         } else {
             // 32-bit shared address + immediate offset (a generic pointer
             // makes nvcc rebuild the shared-window base every day)
-            const uint32_t a = obs_s + static_cast<uint32_t>(day) * sizeof(ObsDay) + 8u * c;
+            const uint32_t a = obs_s + 8u * c;
             asm("ld.shared.f64 %0, [%1];" : "=d"(o) : "r"(a));
         }
         if (MET == kMetMAPE) {
@@ -492,6 +520,7 @@ struct ScoreSink {
             one(1, d, R);
         }
         one(2, d, D);
+        obs_s += sizeof(ObsDay);
     }
 
     __device__ __forceinline__ double finish_one(int c) const {
