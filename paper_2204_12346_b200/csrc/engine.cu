@@ -186,13 +186,26 @@ struct PermEvalLaunch {
 
 template <int F, int M, int S>
 struct SwarmLaunch {
-    static void run(unsigned grid, unsigned threads, uint32_t swarm_offset, const DevSwarm* sw, const DevWindow* wins,
-                    const PsoPlanes& P, DevSwarmState* state, size_t smem, cudaStream_t st, cudaError_t* err) {
+    // n_swarms clusters of `cluster` CTAs (thread-block clusters, one swarm each)
+    static void run(unsigned n_swarms, unsigned cluster, unsigned threads, uint32_t swarm_offset, const DevSwarm* sw,
+                    const DevWindow* wins, const PsoPlanes& P, DevSwarmState* state, size_t smem, cudaStream_t st,
+                    cudaError_t* err) {
         auto k = pso_swarm_kernel<F, M, S>;
         *err = prepare_smem(k, smem);
         if (*err != cudaSuccess) return;
-        k<<<grid, threads, smem, st>>>(sw, wins, P, state, swarm_offset);
-        *err = cudaGetLastError();
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(n_swarms * cluster);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr{};
+        attr.id = cudaLaunchAttributeClusterDimension;
+        attr.val.clusterDim.x = cluster;
+        attr.val.clusterDim.y = 1;
+        attr.val.clusterDim.z = 1;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        *err = cudaLaunchKernelEx(&cfg, k, sw, wins, P, state, swarm_offset);
     }
 };
 
@@ -618,6 +631,7 @@ struct SwarmGroup {
     bool sorted = false;      // every swarm <= kSortMax: move+sort / permuted eval
     bool persistent = false;  // every swarm <= kPersistMax: one CTA per swarm, one launch
     unsigned threads = 0;     // persistent CTA size
+    unsigned cluster = 1;     // persistent CTAs per swarm (thread-block cluster)
     uint32_t* d_perm = nullptr;
     unsigned char* d_keys = nullptr;
     size_t n_total = 0, n_ctas = 0, smem = 0;
@@ -705,7 +719,12 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     if (g.persistent) {
         uint64_t max_n = 0;
         for (const DevSwarm& s : sw) max_n = std::max(max_n, s.n);
-        g.threads = static_cast<unsigned>(std::min<uint64_t>(kSwarmThreadsMax, (max_n + 31) / 32 * 32));
+        // At most one warp per SM sub-partition: spread the swarm over
+        // ceil(n / 128) SMs (<= 8, a portable cluster).
+        g.cluster = static_cast<unsigned>(
+            std::min<uint64_t>(kSwarmClusterMax, std::max<uint64_t>(1, (max_n + kSwarmThreadsMax - 1) / kSwarmThreadsMax)));
+        const uint64_t per_cta = (max_n + g.cluster - 1) / g.cluster;
+        g.threads = static_cast<unsigned>(std::min<uint64_t>(kSwarmThreadsMax, (per_cta + 31) / 32 * 32));
     }
     for (const DevSwarm& s : sw)
         if (s.n > static_cast<uint64_t>(kSortMax)) g.sorted = false;
@@ -785,8 +804,8 @@ int ensure_lanes(sg_ctx* ctx) {
 int step_group(sg_ctx* ctx, SwarmGroup& g) {
     if (g.persistent) {
         cudaError_t err = cudaSuccess;
-        dispatch<SwarmLaunch>(g.family, g.metric, g.substeps, static_cast<unsigned>(g.idx.size()), g.threads, 0u,
-                              g.d_sw, g.d_win, g.P, g.d_state, g.smem, ctx->stream, &err);
+        dispatch<SwarmLaunch>(g.family, g.metric, g.substeps, static_cast<unsigned>(g.idx.size()), g.cluster,
+                              g.threads, 0u, g.d_sw, g.d_win, g.P, g.d_state, g.smem, ctx->stream, &err);
         ctx->launches += 1;
         if (err != cudaSuccess) return cuda_fail(ctx, err, "pso_swarm_kernel");
         return SG_OK;

@@ -16,6 +16,8 @@
 
 #include "sird_device.cuh"
 
+#include <cooperative_groups.h>
+
 namespace sirdgpu {
 
 #ifndef SG_STEP_THREADS
@@ -718,45 +720,69 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
                    it, &ramp);
 }
 
-// ---- small swarms: one persistent CTA per swarm --------------------------------
+// ---- small swarms: one persistent thread-block cluster per swarm ---------------
 //
-// Swarms of at most kPersistMax particles (C1: 256, C4: 256 per restart) run
-// their whole optimize() (pso.cpp:129-143) in one launch: seeding, then every
-// iteration's move -> evaluate -> personal best -> block argmin -> global
-// best, with the global best kept in shared memory and __syncthreads as the
-// iteration barrier.  No per-iteration launches, window staged once.
-constexpr int kSwarmThreadsMax = 256;
-constexpr int kPersistMax = 1024;
+// Swarms of at most kPersistMax particles (C1: 256, tests) run their whole
+// optimize() (pso.cpp:129-143) in one launch: seeding, then every
+// iteration's move -> evaluate -> personal best -> argmin -> global best.
+// Such a plan cannot fill the GPU, so the time per iteration is the Euler
+// dependency chain of one particle (6 dependent FP64 ops per substep): the
+// swarm is spread over a cluster of up to 8 CTAs (one per SM, at most one
+// warp per SM sub-partition) instead of stacking warps on one SM.  CTA r of
+// the cluster owns particles r*blockDim + t (+ k*cluster*blockDim).  Per
+// iteration each CTA folds its warps' minima into a partial (cost, index,
+// personal-best position) in its shared memory; after one cluster barrier
+// every CTA folds the partials of all ranks in rank order through
+// distributed shared memory, so all CTAs hold the same global best.  The
+// partials are double-buffered by iteration parity, which makes one cluster
+// barrier per iteration enough.
+constexpr int kSwarmThreadsMax = 128;
+constexpr int kSwarmClusterMax = 8;
+constexpr int kPersistMax = kSwarmThreadsMax * kSwarmClusterMax;  // 1024
+
+struct SwarmPartial {
+    double cost;
+    unsigned long long idx;
+    double pos[6];
+};
 
 template <int FAM, int MET, int SUB>
-__global__ void __launch_bounds__(kSwarmThreadsMax, 2) pso_swarm_kernel(const DevSwarm* __restrict__ swarms,
+__global__ void __launch_bounds__(kSwarmThreadsMax, 4) pso_swarm_kernel(const DevSwarm* __restrict__ swarms,
                                                                      const DevWindow* __restrict__ windows,
                                                                      PsoPlanes P, DevSwarmState* __restrict__ state,
                                                                      uint32_t swarm_offset) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ DevWindow sdesc;
     __shared__ double red_c[kSwarmThreadsMax / 32];
     __shared__ unsigned long long red_i[kSwarmThreadsMax / 32];
+    __shared__ SwarmPartial part[2];
     __shared__ double gbest[6];
     __shared__ double gbest_cost;
-    const int s = static_cast<int>(blockIdx.x + swarm_offset);
+    const unsigned rank = cluster.block_rank();
+    const unsigned n_ranks = cluster.num_blocks();
+    const int s = static_cast<int>(blockIdx.x / n_ranks + swarm_offset);
     const DevSwarm& sw = swarms[s];
     const SmemWindow win = stage_window<MET, SUB>(windows + sw.window, &sdesc, smem);
     const uint32_t n = static_cast<uint32_t>(sw.n);
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) init_particle(sw, P, sw.offset + i, i);
+    const uint32_t first = rank * blockDim.x + threadIdx.x;
+    const uint32_t step = n_ranks * blockDim.x;
+    for (uint32_t i = first; i < n; i += step) init_particle(sw, P, sw.offset + i, i);
     if (threadIdx.x == 0) {
         gbest_cost = __longlong_as_double(0x7FF0000000000000LL);
         for (int d = 0; d < 6; ++d) gbest[d] = 0.0;
+        if (rank == 0) state[s].ramp_substeps = 0;
     }
     unsigned long long ramp_acc = 0;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int n_warps = (blockDim.x + 31) >> 5;
-    __syncthreads();
+    cluster.sync();  // ramp counter cleared before any CTA adds to it; gbest initialised
     for (uint64_t it = 0; it < sw.max_iters; ++it) {
         double my_c = __longlong_as_double(0x7FF0000000000000LL);
         unsigned long long my_i = ~0ULL;
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        for (uint32_t i = first; i < n; i += step) {
             const size_t p = sw.offset + i;
             double x[6];
 #pragma unroll
@@ -791,7 +817,8 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 2) pso_swarm_kernel(const De
             red_c[warp] = my_c;
             red_i[warp] = my_i;
         }
-        __syncthreads();  // minima and personal bests of this iteration visible
+        __syncthreads();  // warp minima and this CTA's personal bests visible in the CTA
+        SwarmPartial& mine = part[it & 1];
         if (threadIdx.x == 0) {
             double bc = red_c[0];
             unsigned long long bi = red_i[0];
@@ -800,24 +827,38 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 2) pso_swarm_kernel(const De
                     bc = red_c[k];
                     bi = red_i[k];
                 }
-            if (bc < gbest_cost) {  // pso.cpp:90-96: strict, lowest index on ties
-                gbest_cost = bc;
-                for (int d = 0; d < 6; ++d) gbest[d] = P.pb[pblock_base(sw.offset + bi, 6) + 32 * d];
+            mine.cost = bc;
+            mine.idx = bi;
+            if (bi != ~0ULL)
+                for (int d = 0; d < 6; ++d) mine.pos[d] = P.pb[pblock_base(sw.offset + bi, 6) + 32 * d];
+        }
+        cluster.sync();  // every rank's partial of iteration `it` visible cluster-wide
+        if (threadIdx.x == 0) {
+            // Global-best scan (pso.cpp:90-96) over the ranks' partials in
+            // rank order: identical in every CTA.
+            const SwarmPartial* best = nullptr;
+            for (unsigned r = 0; r < n_ranks; ++r) {
+                const SwarmPartial* q = cluster.map_shared_rank(&part[it & 1], r);
+                if (!best || better(q->cost, q->idx, best->cost, best->idx)) best = q;
             }
-            P.history[static_cast<size_t>(s) * P.hist_stride + it] = gbest_cost;
+            const double bc = best->cost;
+            if (bc < gbest_cost) {  // strict: an equal later cost never replaces
+                gbest_cost = bc;
+                for (int d = 0; d < 6; ++d) gbest[d] = best->pos[d];
+            }
+            if (rank == 0) P.history[static_cast<size_t>(s) * P.hist_stride + it] = gbest_cost;
         }
         __syncthreads();  // global best published for the next move
     }
     // per-thread count <= iterations * 840 * ceil(n/threads) < 2^32 / 32
     const unsigned long long wr = __reduce_add_sync(0xFFFFFFFFu, static_cast<unsigned int>(ramp_acc));
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && rank == 0) {
         state[s].best_cost = gbest_cost;
         for (int d = 0; d < 6; ++d) state[s].best[d] = gbest[d];
         state[s].arrived = 0;
-        state[s].ramp_substeps = 0;
     }
-    __syncthreads();
     if (lane == 0) atomicAdd(&state[s].ramp_substeps, wr);
+    cluster.sync();  // no CTA leaves while another may still read its partials
 }
 
 // ---- forecast-scenario ensemble ----------------------------------------------------
