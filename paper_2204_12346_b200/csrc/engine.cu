@@ -101,6 +101,18 @@ bool divisor_admits_fast_path(double b) {
     return m < (1ULL << 53) / 3;
 }
 
+// The ramp's 2-op division q = fma(a, y, RN(a*y_lo)) needs the
+// divisor's odd part below 2^50 on top of the 3-op conditions.
+bool divisor_admits_two_op(double b) {
+    if (!divisor_admits_fast_path(b)) return false;
+    const double a = std::fabs(b);
+    uint64_t bits;
+    std::memcpy(&bits, &a, sizeof bits);
+    uint64_t m = (bits & ((1ULL << 52) - 1)) | (1ULL << 52);
+    while ((m & 1ULL) == 0) m >>= 1;
+    return m < (1ULL << 50);
+}
+
 // objectives.cpp:61-69 — scale of one compartment's residuals.
 double compartment_scale(const double* obs, int n) {
     const double* lo = std::min_element(obs, obs + n);
@@ -263,8 +275,10 @@ DevWindow integration_window(int n_days, int substeps, double N) {
     w.substeps = substeps;
     w.N = N;
     w.h = 1.0 / static_cast<double>(substeps);  // model.cpp:90
-    w.fast_N = divisor_admits_fast_path(N) ? 1 : 0;
+    w.fast_N = divisor_admits_two_op(N) ? 1 : 0;
     w.rN = 1.0 / N;
+    // 1/N = rN + e/N exactly with e = 1 - rN*N (exact by fma); rN_lo = RN(e/N)
+    w.rN_lo = std::fma(-w.rN, N, 1.0) / N;
     w.init_finite = 1;
     return w;
 }

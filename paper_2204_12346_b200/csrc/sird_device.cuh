@@ -66,9 +66,10 @@ struct alignas(16) DevWindow {  // 16-byte multiple: staged by one bulk copy
     int family;
     int metric;
     double N;             // population
-    double rN;            // RN(1/N), valid when fast_N
+    double rN;            // RN(1/N)
+    double rN_lo;         // RN(1/N - rN): rN + rN_lo is 1/N to ~2^-106 (ramp division, when fast_N)
     double h;             // 1.0 / substeps (model.cpp:90)
-    int fast_N;           // divisor N admits the 3-op exact division
+    int fast_N;           // N admits the exact 2-op ramp division
     int init_finite;      // isfinite(init.total()) (model.cpp:83)
     double init[4];       // S, I, R, D
     double scale[3];      // compartment_cost scale (objectives.cpp:61-69); 1 for D-only
@@ -219,13 +220,16 @@ __device__ __forceinline__ void euler_substep(double bp, double g, double mu, do
 
 // beta(t_k)/N for a ramp substep (model.cpp:62-63 then model.cpp:67); t is
 // the substep time t_k = (day-1) + sub*h (model.cpp:94).
-__device__ __forceinline__ double ramp_bp(const Particle& p, double t, double N, double rN) {
+// RN(beta/N) in two operations for an admissible N and beta:
+// beta*(rN + rN_lo) is within 2^-105 relative of beta/N, closer than any
+// rounding boundary of the quotient.
+__device__ __forceinline__ double div_by_N(double beta, double rN, double rN_lo) {
+    return __fma_rn(beta, rN, __dmul_rn(beta, rN_lo));
+}
+
+__device__ __forceinline__ double ramp_bp(const Particle& p, double t, double N, double rN, double rN_lo) {
     const double beta = dadd(p.b1, dmul(p.slope, dsub(t, p.t1)));
-    if (p.fast) {  // div_exact without the per-value range test
-        const double q0 = __dmul_rn(beta, rN);
-        const double r = __fma_rn(-q0, N, beta);
-        return __fma_rn(r, rN, q0);
-    }
+    if (p.fast) return div_by_N(beta, rN, rN_lo);  // no per-value range test needed
     return ddiv(beta, N);
 }
 
@@ -255,7 +259,7 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
     const int nsub = SUB > 0 ? SUB : w.substeps;
     const double h = w.h;
     const double g = p.g, mu = p.mu;
-    const double N = w.N, rN = w.rN;
+    const double N = w.N, rN = w.rN, rN_lo = w.rN_lo;
     const unsigned mask = __activemask();
     // Warp-uniform: every lane's ramp admits the 3-op division, so the ramp
     // days run without the per-value IEEE-division fallback.
@@ -296,8 +300,7 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
                 for (int sub = 0; sub < nsub; ++sub) {
                     const double t = tg.tgrid[kbase + sub];
                     const double beta = dadd(p.b1, dmul(p.slope, dsub(t, p.t1)));
-                    const double q0 = __dmul_rn(beta, rN);
-                    euler_substep(__fma_rn(__fma_rn(-q0, N, beta), rN, q0), g, mu, h, S, I, R, D);
+                    euler_substep(div_by_N(beta, rN, rN_lo), g, mu, h, S, I, R, D);
                 }
             } else if (SG_RAMP_MODE >= 1 && SUB > 0 && warp_fast) {
                 // Branch-free ramp day: every lane computes the ramp value
@@ -308,8 +311,7 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
                 for (int sub = 0; sub < nsub; ++sub) {
                     const double t = tg.tgrid[kbase + sub];
                     const double beta = dadd(p.b1, dmul(p.slope, dsub(t, p.t1)));
-                    const double q0 = __dmul_rn(beta, rN);
-                    const double q = __fma_rn(__fma_rn(-q0, N, beta), rN, q0);
+                    const double q = div_by_N(beta, rN, rN_lo);
                     const double bp = sub < lo ? p.bp1 : (sub < hi ? q : p.bp2);
                     euler_substep(bp, g, mu, h, S, I, R, D);
                 }
@@ -321,7 +323,7 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
                         double t;
                         if constexpr (SUB > 0) t = tg.tgrid[kbase + sub];
                         else t = dadd(static_cast<double>(day - 1), tg.subh[sub]);
-                        bp = ramp_bp(p, t, N, rN);
+                        bp = ramp_bp(p, t, N, rN, rN_lo);
                     }
                     euler_substep(bp, g, mu, h, S, I, R, D);
                 }
@@ -377,7 +379,7 @@ __device__ __forceinline__ void integrate_days_n(const Particle* p, const DevWin
                                                  double* S, double* I, double* R, double* D, Sink* sink) {
     const int nsub = SUB > 0 ? SUB : w.substeps;
     const double h = w.h;
-    const double N = w.N, rN = w.rN;
+    const double N = w.N, rN = w.rN, rN_lo = w.rN_lo;
     const unsigned mask = __activemask();
     bool fast = true;
 #pragma unroll
@@ -403,9 +405,7 @@ __device__ __forceinline__ void integrate_days_n(const Particle* p, const DevWin
 #pragma unroll
                     for (int q = 0; q < NP; ++q) {
                         const double beta = dadd(p[q].b1, dmul(p[q].slope, dsub(t, p[q].t1)));
-                        const double q0 = __dmul_rn(beta, rN);
-                        euler_substep(__fma_rn(__fma_rn(-q0, N, beta), rN, q0), p[q].g, p[q].mu, h, S[q], I[q], R[q],
-                                      D[q]);
+                        euler_substep(div_by_N(beta, rN, rN_lo), p[q].g, p[q].mu, h, S[q], I[q], R[q], D[q]);
                     }
                 }
             } else if (SUB > 0 && warp_fast) {
@@ -415,8 +415,7 @@ __device__ __forceinline__ void integrate_days_n(const Particle* p, const DevWin
 #pragma unroll
                     for (int q = 0; q < NP; ++q) {
                         const double beta = dadd(p[q].b1, dmul(p[q].slope, dsub(t, p[q].t1)));
-                        const double q0 = __dmul_rn(beta, rN);
-                        const double qv = __fma_rn(__fma_rn(-q0, N, beta), rN, q0);
+                        const double qv = div_by_N(beta, rN, rN_lo);
                         const double bp = sub < lo[q] ? p[q].bp1 : (sub < hi[q] ? qv : p[q].bp2);
                         euler_substep(bp, p[q].g, p[q].mu, h, S[q], I[q], R[q], D[q]);
                     }
@@ -431,7 +430,7 @@ __device__ __forceinline__ void integrate_days_n(const Particle* p, const DevWin
                             double t;
                             if constexpr (SUB > 0) t = tg.tgrid[kbase + sub];
                             else t = dadd(static_cast<double>(day - 1), tg.subh[sub]);
-                            bp = ramp_bp(p[q], t, N, rN);
+                            bp = ramp_bp(p[q], t, N, rN, rN_lo);
                         }
                         euler_substep(bp, p[q].g, p[q].mu, h, S[q], I[q], R[q], D[q]);
                     }
