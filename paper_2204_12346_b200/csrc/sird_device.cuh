@@ -177,6 +177,13 @@ __device__ __forceinline__ bool beta_in_fast_range(double b) {
     return e >= 1023 - 600 && e <= 1023 + 680;
 }
 
+// RN(beta/N) in two operations for an admissible N and beta (DESIGN.md §4):
+// beta*(rN + rN_lo) is within 2^-105 relative of beta/N, closer than any
+// rounding boundary of the quotient.
+__device__ __forceinline__ double div_by_N(double beta, double rN, double rN_lo) {
+    return __fma_rn(beta, rN, __dmul_rn(beta, rN_lo));
+}
+
 __device__ __forceinline__ Particle make_particle(double b1, double b2, double t1, double t2, double g, double mu,
                                                   const DevWindow& w, const double* tgrid = nullptr) {
     Particle p;
@@ -185,8 +192,10 @@ __device__ __forceinline__ Particle make_particle(double b1, double b2, double t
     p.t1 = t1;
     p.g = g;
     p.mu = mu;
-    p.bp1 = ddiv(b1, w.N);
-    p.bp2 = ddiv(b2, w.N);
+    const bool fast1 = w.fast_N && beta_in_fast_range(b1);
+    const bool fast2 = w.fast_N && beta_in_fast_range(b2);
+    p.bp1 = fast1 ? div_by_N(b1, w.rN, w.rN_lo) : ddiv(b1, w.N);
+    p.bp2 = fast2 ? div_by_N(b2, w.rN, w.rN_lo) : ddiv(b2, w.N);
     p.slope = ddiv(dsub(b2, b1), dsub(t2, t1));
     opaque(p.bp1);
     opaque(p.bp2);
@@ -197,8 +206,7 @@ __device__ __forceinline__ Particle make_particle(double b1, double b2, double t
     // comparisons are false and the ramp branch is taken (model.cpp:59-63).
     p.k2 = (t2 != t2) ? K : count_t_below(t2, K, w.substeps, w.h, tgrid);
     if (p.k2 < p.k1) p.k2 = p.k1;  // t1 > t2: no ramp (k >= k1 implies t >= t2)
-    p.fast = w.fast_N && isfinite(t1) && isfinite(t2) && isfinite(p.slope) && beta_in_fast_range(b1) &&
-             beta_in_fast_range(b2);
+    p.fast = fast1 && fast2 && isfinite(t1) && isfinite(t2) && isfinite(p.slope);
     return p;
 }
 
@@ -220,13 +228,6 @@ __device__ __forceinline__ void euler_substep(double bp, double g, double mu, do
 
 // beta(t_k)/N for a ramp substep (model.cpp:62-63 then model.cpp:67); t is
 // the substep time t_k = (day-1) + sub*h (model.cpp:94).
-// RN(beta/N) in two operations for an admissible N and beta (DESIGN.md §4):
-// beta*(rN + rN_lo) is within 2^-105 relative of beta/N, closer than any
-// rounding boundary of the quotient.
-__device__ __forceinline__ double div_by_N(double beta, double rN, double rN_lo) {
-    return __fma_rn(beta, rN, __dmul_rn(beta, rN_lo));
-}
-
 __device__ __forceinline__ double ramp_bp(const Particle& p, double t, double N, double rN, double rN_lo) {
     const double beta = dadd(p.b1, dmul(p.slope, dsub(t, p.t1)));
     if (p.fast) return div_by_N(beta, rN, rN_lo);  // no per-value range test needed
