@@ -1,0 +1,101 @@
+"""Plan-level parity: the launch machinery around the step kernels.
+
+Every swarm of a mixed plan (all 8 objective specs, window lengths on both
+sides of the shared-memory time-table limit, substep counts 24/7/1,
+different particle counts, iteration counts, coefficients, repair on/off)
+must follow the C restatement's optimize() bit for bit — which exercises the
+CTA task table, the lane partition, the generic-substep kernels, CTAs whose
+swarm has finished early, and the cluster kernel at every cluster size.
+Mirrors test_pso.cpp:78-131 (reproducibility, first iteration, best-so-far
+monotone) at the plan level.
+"""
+import numpy as np
+import pytest
+
+from helpers import assert_bitwise
+
+pytestmark = pytest.mark.gpu
+
+SPECS = [f"{f}-{m}" for f in ("d", "ird") for m in ("mxse", "mse", "mae", "mape")]
+
+
+def _window(eng, ctx, poland, start, n_days, spec, substeps=24):
+    I, R, D = (poland[k][start:start + n_days] for k in ("I", "R", "D"))
+    N = poland["N"]
+    init = [N - I[0] - R[0] - D[0], I[0], R[0], D[0]]
+    return eng.Window(ctx, I, R, D, init, N, spec, substeps=substeps), (I, R, D, init, N)
+
+
+def _check(port, swarms, data, out):
+    for k, (s, (I, R, D, init, N, substeps)) in enumerate(zip(swarms, data)):
+        rc, best, cost, hist = port.fit_swarm((s["window"].family, s["window"].metric), I, R, D, init, N, s["lower"],
+                                              s["upper"], s["n_particles"], s["max_iters"],
+                                              inertia=s.get("inertia", 0.5), cognitive=s.get("cognitive", 0.5),
+                                              social=s.get("social", 0.5), seed=s["seed"],
+                                              repair=s.get("repair", True), substeps=substeps)
+        status, gbest, gcost, ghist = out[k]
+        assert status == rc, k
+        assert_bitwise(ghist, hist, f"swarm {k} history")
+        if rc == 0:
+            assert_bitwise(gbest, best, f"swarm {k} best")
+            assert gcost == cost
+        assert np.all(np.diff(ghist) <= 0) or not np.all(np.isfinite(ghist))
+
+
+def test_mixed_plan_matches_oracle(ctx, port, poland):
+    import paper_2204_12346_b200 as eng
+    rng = np.random.default_rng(2204)
+    cases = [  # (start, n_days, spec, substeps, particles, iters)
+        (0, 8, "ird-mxse", 24, 300, 17), (30, 36, "d-mse", 24, 1500, 9), (90, 100, "ird-mae", 24, 257, 6),
+        (120, 21, "ird-mape", 7, 640, 12), (200, 36, "d-mxse", 1, 129, 25), (260, 15, "d-mae", 24, 33, 40),
+        (300, 36, "ird-mse", 24, 2048, 5), (400, 30, "d-mape", 24, 700, 11),
+    ]
+    swarms, data, keep = [], [], []
+    for k, (a, n, spec, sub, n_p, iters) in enumerate(cases):
+        win, (I, R, D, init, N) = _window(eng, ctx, poland, a, n, spec, sub)
+        keep.append(win)
+        tau = n - 1
+        hi = [2.0, 2.0, float(tau), float(tau), 1.0, 0.1] if k % 2 else [0.9, 0.9, 0.8 * tau, 0.8 * tau, 0.3, 0.05]
+        swarms.append(dict(window=win, lower=[0.0] * 6, upper=hi, n_particles=n_p, max_iters=iters,
+                           inertia=float(rng.uniform(0.2, 0.9)), cognitive=float(rng.uniform(0.2, 1.5)),
+                           social=float(rng.uniform(0.2, 1.5)), seed=int(rng.integers(1 << 62)),
+                           repair=k != 3))
+        data.append((I, R, D, init, N, sub))
+    out = ctx.fit_swarms(swarms)
+    _check(port, swarms, data, out)
+
+
+@pytest.mark.parametrize("n_particles", [1, 31, 33, 128, 129, 257, 600, 1024])
+def test_cluster_kernel_every_cluster_size(ctx, port, poland, n_particles):
+    """Plans of <= 1024 particles run as one thread-block cluster per swarm
+    (cluster size ceil(n/128)); two swarms per plan when they still fit."""
+    import paper_2204_12346_b200 as eng
+    win, (I, R, D, init, N) = _window(eng, ctx, poland, 150, 21, "ird-mxse")
+    swarms, data = [], []
+    for j in range(2 if 2 * n_particles <= 1024 else 1):
+        swarms.append(dict(window=win, lower=[0.0] * 6, upper=[2, 2, 13, 13, 1, 0.1], n_particles=n_particles,
+                           max_iters=30, seed=77 + j))
+        data.append((I, R, D, init, N, 24))
+    plan = eng.Plan(ctx, swarms)
+    assert plan.step_launches == 1  # one persistent launch
+    plan.run()
+    _check(port, swarms, data, plan.results())
+
+
+def test_plan_reruns_are_identical(ctx, poland):
+    import paper_2204_12346_b200 as eng
+    wins = [_window(eng, ctx, poland, 3 * w, 36, "ird-mxse")[0] for w in range(12)]
+    swarms = [dict(window=w, lower=[0.0] * 6, upper=[2, 2, 28, 28, 1, 0.1], n_particles=500, max_iters=20, seed=k)
+              for k, w in enumerate(wins)]
+    plan = eng.Plan(ctx, swarms)
+    assert plan.step_launches > 1  # flat per-iteration kernels
+    plan.run()
+    a = plan.results()
+    plan.run()
+    b = plan.results()
+    c = ctx.fit_swarms(swarms)
+    for x, y, z in zip(a, b, c):
+        assert x[0] == y[0] == z[0] == 0
+        assert_bitwise(x[3], y[3], "rerun history")
+        assert_bitwise(x[3], z[3], "fresh plan history")
+        assert_bitwise(x[1], z[1], "fresh plan best")
