@@ -24,6 +24,12 @@
 #ifndef SG_CONST_UNROLL
 #define SG_CONST_UNROLL 8
 #endif
+#ifndef SG_QUIET_UNROLL
+#define SG_QUIET_UNROLL 8
+#endif
+#ifndef SG_SLOW_UNROLL
+#define SG_SLOW_UNROLL 12
+#endif
 #ifndef SG_RAMP_UNROLL
 #define SG_RAMP_UNROLL 12
 #endif
@@ -39,6 +45,8 @@ namespace sirdgpu {
 
 constexpr int kConstUnroll = SG_CONST_UNROLL;  // substep unroll of constant days
 constexpr int kRampUnroll = SG_RAMP_UNROLL;    // ... of switch and ramp days
+constexpr int kQuietUnroll = SG_QUIET_UNROLL;  // ... of the quiet-stretch loop
+constexpr int kSlowUnroll = SG_SLOW_UNROLL;    // ... of ramp days with IEEE divisions
 constexpr int kFamD = 0;
 constexpr int kFamIRD = 1;
 constexpr int kMetMXSE = 0;
@@ -317,7 +325,7 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
                     euler_substep(bp, g, mu, h, S, I, R, D);
                 }
             } else {
-#pragma unroll(SUB > 0 ? kRampUnroll : 4)
+#pragma unroll(SUB > 0 ? kSlowUnroll : 4)  // rare path (a lane outside the 2-op division range)
                 for (int sub = 0; sub < nsub; ++sub) {
                     double bp = sub < lo ? p.bp1 : p.bp2;
                     if (sub >= lo && sub < hi) {
@@ -357,7 +365,7 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
         const int end = seg == 0 ? (d_first < n_days ? d_first : n_days) : n_days;
         const double bpq = seg == 0 ? p.bp1 : p.bp2;
         for (; day < end; ++day) {
-#pragma unroll(SUB > 0 ? kConstUnroll : 4)
+#pragma unroll(SUB > 0 ? kQuietUnroll : 4)
             for (int sub = 0; sub < nsub; ++sub) euler_substep(bpq, g, mu, h, S, I, R, D);
             sink.day(day, S, I, R, D);
         }
