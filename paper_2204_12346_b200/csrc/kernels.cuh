@@ -359,6 +359,21 @@ __device__ __forceinline__ void move_particle(const DevSwarm& sw, double best_co
     for (int d = 0; d < 6; ++d) xb[32 * d] = x[d];
 }
 
+// move_particle on register-resident state (the persistent cluster kernel):
+// u holds the 12 draws of this move, drawn ahead of time.
+__device__ __forceinline__ void move_particle_regs(const DevSwarm& sw, double best_cost, const double* best,
+                                                   const double* u, double* x, double* v, const double* pb) {
+    const bool have_best = best_cost < __longlong_as_double(0x7FF0000000000000LL);  // pso.cpp:106
+#pragma unroll
+    for (int d = 0; d < 6; ++d) {
+        double vel = dadd(dmul(sw.w, v[d]), dmul(dmul(sw.c1, u[2 * d]), dsub(pb[d], x[d])));  // pso.cpp:116
+        if (have_best) vel = dadd(vel, dmul(dmul(sw.c2, u[2 * d + 1]), dsub(best[d], x[d])));  // pso.cpp:117-119
+        v[d] = vel;
+        x[d] = std_clamp(dadd(x[d], vel), sw.lo[d], sw.hi[d]);  // pso.cpp:121
+    }
+    if (sw.repair) repair_order(x);  // pso.cpp:123-125
+}
+
 // Personal best (pso.cpp:83-89), warp argmin of personal-best costs (lowest
 // particle index on ties), and — in the last warp of the swarm to arrive —
 // the global-best scan (pso.cpp:90-96) over the warp minima plus
@@ -747,7 +762,7 @@ struct SwarmPartial {
 };
 
 template <int FAM, int MET, int SUB>
-__global__ void __launch_bounds__(kSwarmThreadsMax, 4) pso_swarm_kernel(const DevSwarm* __restrict__ swarms,
+__global__ void __launch_bounds__(kSwarmThreadsMax, 1) pso_swarm_kernel(const DevSwarm* __restrict__ swarms,
                                                                      const DevWindow* __restrict__ windows,
                                                                      PsoPlanes P, DevSwarmState* __restrict__ state,
                                                                      uint32_t swarm_offset) {
@@ -757,6 +772,7 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 4) pso_swarm_kernel(const De
     __shared__ DevWindow sdesc;
     __shared__ double red_c[kSwarmThreadsMax / 32];
     __shared__ unsigned long long red_i[kSwarmThreadsMax / 32];
+    __shared__ double red_pos[kSwarmThreadsMax / 32][6];
     __shared__ SwarmPartial part[2];
     __shared__ double gbest[6];
     __shared__ double gbest_cost;
@@ -766,9 +782,24 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 4) pso_swarm_kernel(const De
     const DevSwarm& sw = swarms[s];
     const SmemWindow win = stage_window<MET, SUB>(windows + sw.window, &sdesc, smem);
     const uint32_t n = static_cast<uint32_t>(sw.n);
-    const uint32_t first = rank * blockDim.x + threadIdx.x;
-    const uint32_t step = n_ranks * blockDim.x;
-    for (uint32_t i = first; i < n; i += step) init_particle(sw, P, sw.offset + i, i);
+    // The host sizes the cluster so that every thread owns at most one
+    // particle (cluster * blockDim >= n): its state lives in registers for
+    // the whole optimize() and goes back to the planes at the end.
+    const uint32_t i = rank * blockDim.x + threadIdx.x;
+    const bool active = i < n;
+    const size_t p = sw.offset + (active ? i : 0);
+    double x[6], v[6], pb[6], pbc = __longlong_as_double(0x7FF0000000000000LL), c = pbc;
+    double u[12];  // the next move's draws, taken one iteration ahead
+    if (active) {
+        init_particle(sw, P, p, i);
+#pragma unroll
+        for (int d = 0; d < 6; ++d) {
+            x[d] = P.x[pblock_base(p, 6) + 32 * d];
+            v[d] = 0.0;
+            pb[d] = x[d];
+        }
+        if (sw.max_iters > 1) mt_draw<12>(P.mt + pblock_base(p, kMtN), move_draw_word(1), u);
+    }
     if (threadIdx.x == 0) {
         gbest_cost = __longlong_as_double(0x7FF0000000000000LL);
         for (int d = 0; d < 6; ++d) gbest[d] = 0.0;
@@ -782,55 +813,53 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 4) pso_swarm_kernel(const De
     for (uint64_t it = 0; it < sw.max_iters; ++it) {
         double my_c = __longlong_as_double(0x7FF0000000000000LL);
         unsigned long long my_i = ~0ULL;
-        for (uint32_t i = first; i < n; i += step) {
-            const size_t p = sw.offset + i;
-            double x[6];
-#pragma unroll
-            for (int d = 0; d < 6; ++d) x[d] = P.x[pblock_base(p, 6) + 32 * d];
-            if (it > 0) move_particle(sw, gbest_cost, gbest, P, p, it, x);
+        if (active) {
+            if (it > 0) {
+                move_particle_regs(sw, gbest_cost, gbest, u, x, v, pb);
+                // draws of the next move, overlapped with this evaluation
+                if (it + 1 < sw.max_iters) mt_draw<12>(P.mt + pblock_base(p, kMtN), move_draw_word(it + 1), u);
+            }
             int ramp = 0;
-            const double c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag, &ramp);
+            c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag, &ramp);
             ramp_acc += static_cast<unsigned long long>(ramp);
-            P.cost[p] = c;
-            double pbc = P.pbc[p];
             if (c < pbc) {  // pso.cpp:83-89
                 pbc = c;
-                P.pbc[p] = c;
 #pragma unroll
-                for (int d = 0; d < 6; ++d) P.pb[pblock_base(p, 6) + 32 * d] = x[d];
+                for (int d = 0; d < 6; ++d) pb[d] = x[d];
             }
-            if (better(pbc, i, my_c, my_i)) {
-                my_c = pbc;
-                my_i = i;
-            }
+            my_c = pbc;
+            my_i = i;
         }
+        unsigned long long w_i = my_i;  // warp argmin (cost, index)
+        double w_c = my_c;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
-            const double oc = __shfl_down_sync(0xFFFFFFFFu, my_c, off);
-            const unsigned long long oi = __shfl_down_sync(0xFFFFFFFFu, my_i, off);
-            if (better(oc, oi, my_c, my_i)) {
-                my_c = oc;
-                my_i = oi;
+            const double oc = __shfl_xor_sync(0xFFFFFFFFu, w_c, off);
+            const unsigned long long oi = __shfl_xor_sync(0xFFFFFFFFu, w_i, off);
+            if (better(oc, oi, w_c, w_i)) {
+                w_c = oc;
+                w_i = oi;
             }
         }
-        if (lane == 0) {
-            red_c[warp] = my_c;
-            red_i[warp] = my_i;
+        if (active && my_i == w_i) {  // the warp's winner publishes its personal best
+            red_c[warp] = w_c;
+            red_i[warp] = w_i;
+#pragma unroll
+            for (int d = 0; d < 6; ++d) red_pos[warp][d] = pb[d];
+        } else if (lane == 0 && w_i == ~0ULL) {
+            red_c[warp] = w_c;
+            red_i[warp] = w_i;
         }
-        __syncthreads();  // warp minima and this CTA's personal bests visible in the CTA
+        __syncthreads();  // warp minima visible in the CTA
         SwarmPartial& mine = part[it & 1];
         if (threadIdx.x == 0) {
-            double bc = red_c[0];
-            unsigned long long bi = red_i[0];
+            int bw = 0;
             for (int k = 1; k < n_warps; ++k)
-                if (better(red_c[k], red_i[k], bc, bi)) {
-                    bc = red_c[k];
-                    bi = red_i[k];
-                }
-            mine.cost = bc;
-            mine.idx = bi;
-            if (bi != ~0ULL)
-                for (int d = 0; d < 6; ++d) mine.pos[d] = P.pb[pblock_base(sw.offset + bi, 6) + 32 * d];
+                if (better(red_c[k], red_i[k], red_c[bw], red_i[bw])) bw = k;
+            mine.cost = red_c[bw];
+            mine.idx = red_i[bw];
+            if (red_i[bw] != ~0ULL)
+                for (int d = 0; d < 6; ++d) mine.pos[d] = red_pos[bw][d];
         }
         cluster.sync();  // every rank's partial of iteration `it` visible cluster-wide
         if (threadIdx.x == 0) {
@@ -850,7 +879,17 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 4) pso_swarm_kernel(const De
         }
         __syncthreads();  // global best published for the next move
     }
-    // per-thread count <= iterations * 840 * ceil(n/threads) < 2^32 / 32
+    if (active) {  // final particle state back to the planes
+#pragma unroll
+        for (int d = 0; d < 6; ++d) {
+            P.x[pblock_base(p, 6) + 32 * d] = x[d];
+            P.v[pblock_base(p, 6) + 32 * d] = v[d];
+            P.pb[pblock_base(p, 6) + 32 * d] = pb[d];
+        }
+        P.pbc[p] = pbc;
+        P.cost[p] = c;
+    }
+    // per-thread count <= iterations * 840 < 2^32 / 32
     const unsigned long long wr = __reduce_add_sync(0xFFFFFFFFu, static_cast<unsigned int>(ramp_acc));
     if (threadIdx.x == 0 && rank == 0) {
         state[s].best_cost = gbest_cost;
