@@ -11,6 +11,7 @@
 #include "kernels.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -225,13 +226,14 @@ template <int F, int M, int S>
 struct EnsembleLaunch {
     static void run(const DevWindow* w, const DevWindow& fwin, const double* lo, const double* hi, uint64_t seed,
                     size_t n, int horizon, double* costs, double* params, double* deaths, size_t sstride,
-                    size_t dstride, size_t smem, cudaStream_t st, cudaError_t* err) {
+                    size_t dstride, const uint32_t* perm, const double* planes, int out_by_slot, size_t smem,
+                    cudaStream_t st, cudaError_t* err) {
         auto k = ensemble_kernel<F, M, S>;
         *err = prepare_smem(k, smem);
         if (*err != cudaSuccess) return;
         const unsigned grid = static_cast<unsigned>((n + kEvalThreads - 1) / kEvalThreads);
         k<<<grid, kEvalThreads, smem, st>>>(w, fwin, lo, hi, seed, n, horizon, costs, params, deaths, sstride,
-                                            dstride);
+                                            dstride, perm, planes, out_by_slot);
         *err = cudaGetLastError();
     }
 };
@@ -1090,6 +1092,34 @@ int sg_fit_swarms(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg_
     return SG_OK;
 }
 
+// Ramp-coherent evaluation order of an ensemble (ens_sample_kernel + a
+// 16-bit radix sort of the (day t1, day t2) keys): returns perm and planes.
+static cudaError_t ensemble_order(sg_ctx* ctx, DevBufs& b, const double* d_lo, const double* d_hi, uint64_t seed,
+                                  size_t n, uint32_t** perm, double** planes) {
+    uint32_t *keys, *keys_sorted, *idx, *idx_sorted;
+    cudaError_t e;
+    if ((e = b.alloc(planes, 6 * n)) != cudaSuccess) return e;
+    if ((e = b.alloc(&keys, n)) != cudaSuccess) return e;
+    if ((e = b.alloc(&keys_sorted, n)) != cudaSuccess) return e;
+    if ((e = b.alloc(&idx, n)) != cudaSuccess) return e;
+    if ((e = b.alloc(&idx_sorted, n)) != cudaSuccess) return e;
+    ens_sample_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(d_lo, d_hi, seed, n, *planes,
+                                                                                     keys, idx);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    size_t temp_bytes = 0;
+    if ((e = cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, keys_sorted, idx, idx_sorted,
+                                             static_cast<int>(n), 0, 16, ctx->stream)) != cudaSuccess)
+        return e;
+    unsigned char* temp;
+    if ((e = b.alloc(&temp, std::max<size_t>(temp_bytes, 16))) != cudaSuccess) return e;
+    if ((e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys_sorted, idx, idx_sorted,
+                                             static_cast<int>(n), 0, 16, ctx->stream)) != cudaSuccess)
+        return e;
+    ctx->launches += 2;
+    *perm = idx_sorted;
+    return cudaSuccess;
+}
+
 int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper[6], uint64_t seed, size_t n,
                          int horizon, double* costs, double* params_out, double* deaths_out) {
     if (!w) return SG_ERR_INVALID_ARGUMENT;
@@ -1112,10 +1142,14 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
     SG_CUDA(ctx, cudaMemcpyAsync(d_lo, lower, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     SG_CUDA(ctx, cudaMemcpyAsync(d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     DevWindow fwin = integration_window(horizon + 1, w->host.substeps, w->host.N);
+    uint32_t* perm = nullptr;
+    double* planes = nullptr;
+    if (n <= static_cast<size_t>(INT32_MAX)) SG_CUDA(ctx, ensemble_order(ctx, b, d_lo, d_hi, seed, n, &perm, &planes));
     cudaError_t err = cudaSuccess;
     dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc,
                              fwin, d_lo, d_hi, seed, n, horizon, d_cost, d_par, d_D,
-                             static_cast<size_t>(horizon + 1), size_t(1), w->smem, ctx->stream, &err);
+                             static_cast<size_t>(horizon + 1), size_t(1), perm, planes, 0, w->smem, ctx->stream,
+                             &err);
     ctx->launches += 1;
     if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
     if (costs) SG_CUDA(ctx, cudaMemcpyAsync(costs, d_cost, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1136,9 +1170,9 @@ int sg_forecast_ensemble_bands(sg_window* w, const double lower[6], const double
     for (int k = 0; k < 6; ++k)
         if (!std::isfinite(lower[k]) || !std::isfinite(upper[k]) || lower[k] > upper[k])
             return fail(ctx, SG_ERR_INVALID_ARGUMENT, "pso: bound " + std::to_string(k) + " is invalid");
-    if (n > static_cast<size_t>(INT32_MAX))
-        return fail(ctx, SG_ERR_INVALID_ARGUMENT, "ensemble too large for one radix sort");
     const int n_days = horizon + 1;
+    if (n * static_cast<size_t>(n_days) > static_cast<size_t>(INT32_MAX))
+        return fail(ctx, SG_ERR_INVALID_ARGUMENT, "ensemble too large for one device selection (n x days > 2^31)");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     DevBufs b;
     b.st = ctx->stream;
@@ -1155,28 +1189,55 @@ int sg_forecast_ensemble_bands(sg_window* w, const double lower[6], const double
     SG_CUDA(ctx, cudaMemcpyAsync(d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     if (n > 0) {
         const DevWindow fwin = integration_window(n_days, w->host.substeps, w->host.N);
+        uint32_t* perm = nullptr;
+        double* planes = nullptr;
+        SG_CUDA(ctx, ensemble_order(ctx, b, d_lo, d_hi, seed, n, &perm, &planes));
         cudaError_t err = cudaSuccess;
+        // day-major columns in evaluation order: the bands only need each day's multiset
         dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps),
                                  w->d_desc, fwin, d_lo, d_hi, seed, n, horizon, d_cost, static_cast<double*>(nullptr),
-                                 d_D, size_t(1), n, w->smem, ctx->stream, &err);  // day-major columns
+                                 d_D, size_t(1), n, perm, planes, 1, w->smem, ctx->stream, &err);
         ctx->launches += 1;
         if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
-        // one sorted column per forecast day (calibration.cpp:17-25: ascending);
-        // a device-wide radix sort per column (columns are large and few)
+        // per forecast day: k and the order statistics quantile_sorted reads
+        // (calibration.cpp:17-25, 324-361), by bin selection (kernels.cuh)
+        SelDay* d_days;
+        unsigned int* d_hist;
+        int *d_beg, *d_end;
+        SG_CUDA(ctx, b.alloc(&d_days, n_days));
+        SG_CUDA(ctx, b.alloc(&d_hist, static_cast<size_t>(n_days) * kSelBins));
+        SG_CUDA(ctx, b.alloc(&d_beg, static_cast<size_t>(n_days) * kBandRanks));
+        SG_CUDA(ctx, b.alloc(&d_end, static_cast<size_t>(n_days) * kBandRanks));
+        SG_CUDA(ctx, cudaMemsetAsync(d_hist, 0, sizeof(unsigned int) * n_days * kSelBins, ctx->stream));
+        const unsigned small = static_cast<unsigned>((n_days + 127) / 128);
+        sel_init_kernel<<<small, 128, 0, ctx->stream>>>(d_days, n_days);
+        const unsigned chunks = static_cast<unsigned>(std::min<size_t>(64, (n + 4095) / 4096));
+        const dim3 grid(chunks, static_cast<unsigned>(n_days));
+        sel_range_kernel<<<grid, 256, 0, ctx->stream>>>(d_D, n, d_days);
+        const dim3 hgrid(static_cast<unsigned>(std::min<size_t>(16, (n + 16383) / 16384)), static_cast<unsigned>(n_days));
+        sel_hist_kernel<<<hgrid, 1024, 0, ctx->stream>>>(d_D, n, d_days, d_hist);
+        sel_locate_kernel<<<static_cast<unsigned>(n_days), 1024, 0, ctx->stream>>>(d_hist, d_days);
+        sel_gather_kernel<<<grid, 256, 0, ctx->stream>>>(d_D, n, d_days, d_sorted);
+        const int n_seg = n_days * kBandRanks;
+        sel_segments_kernel<<<static_cast<unsigned>((n_seg + 127) / 128), 128, 0, ctx->stream>>>(d_days, n, n_days,
+                                                                                            d_beg, d_end);
+        ctx->launches += 6;
+        SG_CUDA(ctx, cudaGetLastError());
         size_t temp_bytes = 0;
-        SG_CUDA(ctx, cub::DeviceRadixSort::SortKeys(nullptr, temp_bytes, d_D, d_sorted, static_cast<int>(n), 0, 64,
-                                                     ctx->stream));
+        const int n_items = static_cast<int>(n * n_days);
+        SG_CUDA(ctx, cub::DeviceSegmentedSort::SortKeys(nullptr, temp_bytes, d_sorted, d_D, n_items, n_seg, d_beg,
+                                                         d_end, ctx->stream));
         unsigned char* d_temp;
-        SG_CUDA(ctx, b.alloc(&d_temp, temp_bytes));
-        for (int d = 0; d < n_days; ++d) {
-            SG_CUDA(ctx, cub::DeviceRadixSort::SortKeys(d_temp, temp_bytes, d_D + static_cast<size_t>(d) * n,
-                                                         d_sorted + static_cast<size_t>(d) * n, static_cast<int>(n),
-                                                         0, 64, ctx->stream));
-            ctx->launches += 1;
-        }
+        SG_CUDA(ctx, b.alloc(&d_temp, std::max<size_t>(temp_bytes, 16)));
+        SG_CUDA(ctx, cub::DeviceSegmentedSort::SortKeys(d_temp, temp_bytes, d_sorted, d_D, n_items, n_seg, d_beg,
+                                                         d_end, ctx->stream));
+        ctx->launches += 1;
+        sel_bands_kernel<<<small, 128, 0, ctx->stream>>>(d_days, d_D, n, d_bands, d_counts, n_days);
+        ctx->launches += 1;
+    } else {
+        bands_kernel<<<n_days, 32, 0, ctx->stream>>>(d_sorted, 0, d_bands, d_counts, n_days);  // k = 0: NaN bands
+        ctx->launches += 1;
     }
-    bands_kernel<<<n_days, 32, 0, ctx->stream>>>(d_sorted, n, d_bands, d_counts, n_days);
-    ctx->launches += 1;
     SG_CUDA(ctx, cudaGetLastError());
     static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "count width");
     SG_CUDA(ctx, cudaMemcpyAsync(bands, d_bands, 7 * n_days * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));

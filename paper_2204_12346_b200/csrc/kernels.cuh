@@ -17,6 +17,7 @@
 #include "sird_device.cuh"
 
 #include <cooperative_groups.h>
+#include <cstring>
 
 namespace sirdgpu {
 
@@ -916,6 +917,37 @@ struct ForecastDSink {
     }
 };
 
+// Sample k of an ensemble: the first 6 draws of mt19937_64(mix_seed(seed, k))
+// mapped into the box like Swarm::Swarm (pso.cpp:65-72), then repaired.
+__device__ __forceinline__ void x_of_sample(const double* lo, const double* hi, uint64_t seed, size_t k, double* x) {
+    double u[6];
+    mt_first_uniforms<6>(mix_seed(seed, k), u);
+#pragma unroll
+    for (int d = 0; d < 6; ++d) x[d] = dadd(lo[d], dmul(u[d], dsub(hi[d], lo[d])));
+    repair_order(x);
+}
+
+// Evaluation order of an ensemble: every sample's parameters into SoA
+// planes and a key (day of t1, day of t2) — samples with equal keys ramp on
+// the same days, so sorting by it makes a warp's lanes ramp together (the
+// warp pays a ramp substep if any lane ramps).  The order never changes a
+// result: every sample is evaluated by the same code into its own slot.
+__global__ void __launch_bounds__(256) ens_sample_kernel(const double* __restrict__ lo, const double* __restrict__ hi,
+                                                         uint64_t seed, size_t n, double* __restrict__ planes,
+                                                         uint32_t* __restrict__ keys, uint32_t* __restrict__ idx) {
+    const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double x[6];
+    x_of_sample(lo, hi, seed, k, x);
+#pragma unroll
+    for (int d = 0; d < 6; ++d) planes[d * n + k] = x[d];
+    auto day = [](double t) -> uint32_t {  // NaN and negatives -> 0, capped at 255
+        return t > 0.0 ? static_cast<uint32_t>(fmin(floor(t), 255.0)) : 0u;
+    };
+    keys[k] = (day(x[2]) << 8) | day(x[3]);
+    idx[k] = static_cast<uint32_t>(k);
+}
+
 template <int FAM, int MET, int SUB>
 __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWindow* __restrict__ win, DevWindow fwin,
                                                                 const double* __restrict__ lo,
@@ -923,18 +955,25 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
                                                                 size_t n, int horizon, double* __restrict__ costs,
                                                                 double* __restrict__ params_out,
                                                                 double* __restrict__ deaths_out, size_t sstride,
-                                                                size_t dstride) {
+                                                                size_t dstride, const uint32_t* __restrict__ perm,
+                                                                const double* __restrict__ planes, int out_by_slot) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ DevWindow sdesc;
     const SmemWindow sw = stage_window<MET, SUB>(win, &sdesc, smem);
-    const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    double u[6];
-    mt_first_uniforms<6>(mix_seed(seed, k), u);
+    // Thread slot -> sample k: identity, or the ramp-coherent order of
+    // ens_sample_kernel + sort (perm), with the sample's parameters read from
+    // its planes.  Costs and parameters always land at k; the deaths row at k,
+    // or at the slot when the caller only needs the per-day multiset (bands).
+    const size_t slot = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (slot >= n) return;
+    const size_t k = perm ? perm[slot] : slot;
     double x[6];
+    if (planes) {
 #pragma unroll
-    for (int d = 0; d < 6; ++d) x[d] = dadd(lo[d], dmul(u[d], dsub(hi[d], lo[d])));
-    repair_order(x);
+        for (int d = 0; d < 6; ++d) x[d] = planes[d * n + k];
+    } else {
+        x_of_sample(lo, hi, seed, k, x);
+    }
     if (params_out) {
 #pragma unroll
         for (int d = 0; d < 6; ++d) params_out[6 * k + d] = x[d];
@@ -943,7 +982,7 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
     const double nan = __longlong_as_double(0x7FF8000000000000LL);
     // deaths of sample k, forecast day d at deaths_out[k*sstride + d*dstride]
     // (sample-major rows, or day-major columns for the on-device bands)
-    double* drow = deaths_out + k * sstride;
+    double* drow = deaths_out + (out_by_slot ? slot : k) * sstride;
     if (!w.init_finite) {
         if (costs) costs[k] = __longlong_as_double(0x7FF0000000000000LL);
         for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
@@ -973,12 +1012,324 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
     }
 }
 
-// ---- quantile bands of sorted columns (build_quantile_bands) -------------------------
+// ---- quantile bands by selection (C5) ------------------------------------------
 //
-// calibration.cpp:324-361 over each forecast day: the column (n samples,
-// sorted ascending by the radix sort, NaN rows of blown-up samples last)
-// is cut at its first NaN — append_finite_sorted drops non-finite values —
-// and quantile_sorted runs with the reference's operation order.
+// build_quantile_bands (calibration.cpp:337-361) needs, per forecast day, the
+// count k of finite values and the order statistics at ranks lo and lo+1 of
+// h = (k-1)*p for 7 probabilities — at most 14 ranks out of 10^6.  Instead of
+// sorting every day column, the values are mapped to order-preserving 64-bit
+// keys, bucketed into 2^12 bins over each day's key range (monotone, so rank
+// intervals of bins are exact), only the bins holding a wanted rank are
+// gathered and sorted (segmented sort), and the ranks are read from there.
+// The order statistics are values of the data, so the bands are the full
+// sort's to the bit (ties between -0 and +0 keep the radix order, as CUB's
+// sort of the whole column does).
+constexpr int kBandP = 7;
+constexpr int kBandRanks = 2 * kBandP;  // lo and lo+1 per probability
+constexpr int kSelBinBits = 12;
+constexpr int kSelBins = 1 << kSelBinBits;  // per day; a CTA histogram fits in shared memory
+__device__ __constant__ double kBandProbs[kBandP] = {0.5, 0.25, 0.75, 0.05, 0.95, 0.025, 0.975};  // 352-358
+
+__host__ __device__ __forceinline__ uint64_t order_key(double x) {
+#ifdef __CUDA_ARCH__
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(x));
+#else
+    uint64_t b;
+    std::memcpy(&b, &x, sizeof b);
+#endif
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+
+struct SelDay {                   // per forecast day, device memory
+    unsigned long long kmin, kmax, count;  // finite values: key range and k
+    int shift;                    // bin = (key - kmin) >> shift
+    int n_seg;                    // distinct bins holding wanted ranks
+    uint32_t seg_bin[kBandRanks];
+    uint64_t seg_rank0[kBandRanks];   // rank of the bin's first value
+    uint32_t seg_count[kBandRanks];
+    uint32_t seg_fill[kBandRanks];
+};
+
+__global__ void sel_init_kernel(SelDay* __restrict__ days, int n_days) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= n_days) return;
+    days[d].kmin = ~0ULL;
+    days[d].kmax = 0;
+    days[d].count = 0;
+    days[d].n_seg = 0;
+}
+
+// k and the key range of every day (grid: chunks x days).
+__global__ void sel_range_kernel(const double* __restrict__ col, size_t n, SelDay* __restrict__ days) {
+    const int d = blockIdx.y;
+    const double* c = col + static_cast<size_t>(d) * n;
+    unsigned long long lo = ~0ULL, hi = 0, cnt = 0;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const double x = c[i];
+        if (!isfinite(x)) continue;
+        const unsigned long long k = order_key(x);
+        lo = k < lo ? k : lo;
+        hi = k > hi ? k : hi;
+        ++cnt;
+    }
+    // 64-bit warp reductions by shuffles
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long olo = __shfl_xor_sync(0xFFFFFFFFu, lo, off);
+        const unsigned long long ohi = __shfl_xor_sync(0xFFFFFFFFu, hi, off);
+        lo = olo < lo ? olo : lo;
+        hi = ohi > hi ? ohi : hi;
+        cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, off);
+    }
+    if ((threadIdx.x & 31) == 0 && cnt) {
+        atomicMin(&days[d].kmin, lo);
+        atomicMax(&days[d].kmax, hi);
+        atomicAdd(&days[d].count, cnt);
+    }
+}
+
+__device__ __forceinline__ int sel_shift(unsigned long long range) {
+    const int bits = range ? 64 - __clzll(static_cast<long long>(range)) : 0;
+    return bits > kSelBinBits ? bits - kSelBinBits : 0;
+}
+
+// Histogram of every day's finite values over its bins: per CTA in shared
+// memory, then one global add per non-empty bin.
+__global__ void __launch_bounds__(1024) sel_hist_kernel(const double* __restrict__ col, size_t n,
+                                                        const SelDay* __restrict__ days,
+                                                        unsigned int* __restrict__ hist) {
+    __shared__ unsigned int sh[kSelBins];
+    const int d = blockIdx.y;
+    const SelDay& sd = days[d];
+    if (sd.count == 0) return;
+    for (int b = threadIdx.x; b < kSelBins; b += blockDim.x) sh[b] = 0;
+    __syncthreads();
+    const int shift = sel_shift(sd.kmax - sd.kmin);
+    const unsigned long long kmin = sd.kmin;
+    const double* c = col + static_cast<size_t>(d) * n;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const double x = c[i];
+        if (!isfinite(x)) continue;
+        atomicAdd(&sh[static_cast<unsigned>((order_key(x) - kmin) >> shift)], 1u);
+    }
+    __syncthreads();
+    unsigned int* h = hist + static_cast<size_t>(d) * kSelBins;
+    for (int b = threadIdx.x; b < kSelBins; b += blockDim.x)
+        if (sh[b]) atomicAdd(&h[b], sh[b]);
+}
+
+// One CTA (1024 threads) per day: exclusive scan of the bins, then the bins
+// holding the wanted ranks (deduplicated, ascending) and their rank offsets.
+__global__ void __launch_bounds__(1024) sel_locate_kernel(const unsigned int* __restrict__ hist,
+                                                          SelDay* __restrict__ days) {
+    const int d = blockIdx.x;
+    SelDay& sd = days[d];
+    const unsigned long long k = sd.count;
+    if (threadIdx.x == 0) {
+        sd.shift = sel_shift(sd.kmax - sd.kmin);
+        sd.n_seg = 0;
+    }
+    if (k == 0) return;
+    const unsigned int* h = hist + static_cast<size_t>(d) * kSelBins;
+    constexpr int kPer = kSelBins / 1024;
+    uint32_t mine = 0;
+    for (int j = 0; j < kPer; ++j) mine += h[threadIdx.x * kPer + j];
+    __shared__ uint32_t warp_sum[32];
+    __shared__ uint64_t ranks[kBandRanks];
+    __shared__ int n_ranks;
+    __shared__ uint32_t bins[kBandRanks];
+    __shared__ uint64_t bin_rank0[kBandRanks];
+    __shared__ uint32_t bin_count[kBandRanks];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t incl = mine;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    if (lane == 31) warp_sum[warp] = incl;
+    if (threadIdx.x == 0) {
+        // the ranks quantile_sorted reads (calibration.cpp:324-335)
+        int m = 0;
+        for (int q = 0; q < kBandP; ++q) {
+            const double hq = dmul(static_cast<double>(k - 1), kBandProbs[q]);
+            const uint64_t lo = static_cast<uint64_t>(hq);
+            if (lo + 1 >= k) {
+                ranks[m++] = k - 1;
+            } else {
+                ranks[m++] = lo;
+                ranks[m++] = lo + 1;
+            }
+        }
+        n_ranks = m;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = warp_sum[lane];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, w, off);
+            if (lane >= off) w += o;
+        }
+        warp_sum[lane] = w - warp_sum[lane];  // exclusive over warps
+    }
+    __syncthreads();
+    uint64_t base = warp_sum[warp] + (incl - mine);  // values before this thread's bins
+    // the thread whose bins cover a wanted rank finds the exact bin
+    for (int r = 0; r < n_ranks; ++r) {
+        const uint64_t want = ranks[r];
+        if (want >= base && want < base + mine) {
+            uint64_t acc = base;
+            for (int j = 0; j < kPer; ++j) {
+                const uint32_t c = h[threadIdx.x * kPer + j];
+                if (want < acc + c) {
+                    bins[r] = threadIdx.x * kPer + j;
+                    bin_rank0[r] = acc;
+                    bin_count[r] = c;
+                    break;
+                }
+                acc += c;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // distinct bins in ascending order (ranks were produced unordered)
+        int ns = 0;
+        for (int r = 0; r < n_ranks; ++r) {
+            bool seen = false;
+            for (int t = 0; t < ns; ++t) seen = seen || sd.seg_bin[t] == bins[r];
+            if (seen) continue;
+            int at = ns++;
+            while (at > 0 && sd.seg_bin[at - 1] > bins[r]) {
+                sd.seg_bin[at] = sd.seg_bin[at - 1];
+                sd.seg_rank0[at] = sd.seg_rank0[at - 1];
+                sd.seg_count[at] = sd.seg_count[at - 1];
+                --at;
+            }
+            sd.seg_bin[at] = bins[r];
+            sd.seg_rank0[at] = bin_rank0[r];
+            sd.seg_count[at] = bin_count[r];
+        }
+        for (int t = 0; t < ns; ++t) sd.seg_fill[t] = 0;
+        sd.n_seg = ns;
+    }
+}
+
+// Segment j of day d occupies cand[d*n + seg_rank0[j] - seg_rank0[0] + ...]:
+// the day's segments are packed in bin order at the start of its slice.
+__device__ __forceinline__ uint64_t sel_seg_offset(const SelDay& sd, int j) {
+    uint64_t off = 0;
+    for (int t = 0; t < j; ++t) off += sd.seg_count[t];
+    return off;
+}
+
+// Copy the values of the wanted bins into their segments (a shared-memory
+// bin -> segment table, warp-aggregated slot reservation).
+__global__ void __launch_bounds__(256) sel_gather_kernel(const double* __restrict__ col, size_t n,
+                                                         SelDay* __restrict__ days, double* __restrict__ cand) {
+    __shared__ unsigned char seg_of[kSelBins];
+    __shared__ uint64_t seg_off[kBandRanks];
+    const int d = blockIdx.y;
+    SelDay& sd = days[d];
+    if (sd.count == 0) return;
+    for (int b = threadIdx.x; b < kSelBins; b += blockDim.x) seg_of[b] = 0xFF;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t off = 0;
+        for (int j = 0; j < sd.n_seg; ++j) {
+            seg_of[sd.seg_bin[j]] = static_cast<unsigned char>(j);
+            seg_off[j] = off;
+            off += sd.seg_count[j];
+        }
+    }
+    __syncthreads();
+    const unsigned long long kmin = sd.kmin;
+    const int shift = sd.shift;
+    const double* c = col + static_cast<size_t>(d) * n;
+    double* out = cand + static_cast<size_t>(d) * n;
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t end = (n + stride - 1) / stride * stride;  // whole warps iterate together
+    const unsigned lane = threadIdx.x & 31;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < end; i += stride) {
+        const double x = i < n ? c[i] : __longlong_as_double(0x7FF8000000000000LL);
+        int seg = -1;
+        if (isfinite(x)) {
+            const unsigned char j = seg_of[static_cast<uint32_t>((order_key(x) - kmin) >> shift)];
+            if (j != 0xFF) seg = j;
+        }
+        const unsigned want = __ballot_sync(0xFFFFFFFFu, seg >= 0);
+        if (want == 0) continue;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, seg);
+        if (seg < 0) continue;
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (static_cast<int>(lane) == leader) base = atomicAdd(&sd.seg_fill[seg], static_cast<unsigned>(__popc(peers)));
+        base = __shfl_sync(peers, base, leader);
+        out[seg_off[seg] + base + __popc(peers & ((1u << lane) - 1u))] = x;
+    }
+}
+
+// Segment boundaries for the segmented sort: day d, slot j < kBandRanks.
+__global__ void sel_segments_kernel(const SelDay* __restrict__ days, size_t n, int n_days,
+                                    int* __restrict__ begin, int* __restrict__ end) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_days * kBandRanks) return;
+    const int d = t / kBandRanks, j = t % kBandRanks;
+    const SelDay& sd = days[d];
+    const int base = d * static_cast<int>(n);  // n_days * n <= INT_MAX (host check)
+    if (sd.count == 0 || j >= sd.n_seg) {
+        begin[t] = end[t] = base;
+        return;
+    }
+    const int off = static_cast<int>(sel_seg_offset(sd, j));
+    begin[t] = base + off;
+    end[t] = base + off + static_cast<int>(sd.seg_count[j]);
+}
+
+// Order statistic of rank r of day d from its sorted segments.
+__device__ __forceinline__ double sel_rank(const SelDay& sd, const double* sorted_day, uint64_t r) {
+    uint64_t off = 0;
+    for (int j = 0; j < sd.n_seg; ++j) {
+        if (r >= sd.seg_rank0[j] && r < sd.seg_rank0[j] + sd.seg_count[j]) return sorted_day[off + (r - sd.seg_rank0[j])];
+        off += sd.seg_count[j];
+    }
+    return __longlong_as_double(0x7FF8000000000000LL);  // unreachable: every wanted rank has a segment
+}
+
+// quantile_sorted (calibration.cpp:324-335) on the selected order statistics.
+__global__ void sel_bands_kernel(const SelDay* __restrict__ days, const double* __restrict__ sorted, size_t n,
+                                 double* __restrict__ bands, unsigned long long* __restrict__ counts, int n_days) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= n_days) return;
+    const SelDay& sd = days[d];
+    const uint64_t k = sd.count;
+    counts[d] = k;
+    const double* s = sorted + static_cast<size_t>(d) * n;
+    for (int q = 0; q < kBandP; ++q) {
+        double v;
+        if (k == 0) {
+            v = __longlong_as_double(0x7FF8000000000000LL);
+        } else {
+            const double h = dmul(static_cast<double>(k - 1), kBandProbs[q]);
+            const uint64_t lo = static_cast<uint64_t>(h);
+            if (lo + 1 >= k) {
+                v = sel_rank(sd, s, k - 1);
+            } else {
+                const double a = sel_rank(sd, s, lo), b = sel_rank(sd, s, lo + 1);
+                v = dadd(a, dmul(dsub(h, static_cast<double>(lo)), dsub(b, a)));
+            }
+        }
+        bands[q * n_days + d] = v;
+    }
+}
+
+// ---- quantile bands of a sorted column (n == 0 path) ------------------------------
+//
+// quantile_sorted (calibration.cpp:324-335) with the reference's operation
+// order; bands_kernel cuts each column at its first non-finite entry.
 __device__ __forceinline__ double quantile_sorted_dev(const double* sorted, size_t k, double p) {
     if (k == 0) return __longlong_as_double(0x7FF8000000000000LL);
     const double h = dmul(static_cast<double>(k - 1), p);

@@ -240,3 +240,59 @@ def test_forecast_ensemble_bands_match_reference(ctx):
                                                        c["horizon"])
         assert counts.tolist() == c["counts"], c["name"]
         assert_bitwise(bands.ravel(), _unhex(c["bands"]), c["name"])
+
+
+def _host_bands(deaths):
+    """build_quantile_bands (calibration.cpp:337-361) on the host: per day,
+    the finite values sorted ascending, then quantile_sorted (324-335)."""
+    ps = [0.5, 0.25, 0.75, 0.05, 0.95, 0.025, 0.975]
+    n_days = deaths.shape[1]
+    bands = np.full((7, n_days), np.nan)
+    counts = []
+    for d in range(n_days):
+        col = np.sort(deaths[:, d][np.isfinite(deaths[:, d])])
+        k = col.size
+        counts.append(k)
+        for q, p in enumerate(ps):
+            if k == 0:
+                continue
+            h = float(k - 1) * p
+            lo = int(h)
+            if lo + 1 >= k:
+                bands[q, d] = col[k - 1]
+            else:
+                a, b = float(col[lo]), float(col[lo + 1])
+                bands[q, d] = a + (h - lo) * (b - a)
+    return bands, counts
+
+
+@pytest.mark.parametrize("case", ["wide", "narrow", "identical", "tiny", "blowups"])
+def test_ensemble_band_selection_equals_full_sort(ctx, poland, case):
+    """The device bands select 14 order statistics per day through key bins
+    instead of sorting; they must equal sorting the same ensemble's deaths
+    (sg_forecast_ensemble) on the host, for wide and narrow spreads, all
+    samples identical (one bin holds everything), tiny ensembles and
+    ensembles with many non-finite forecasts."""
+    import paper_2204_12346_b200 as eng
+    a = 120
+    I, R, D = poland["I"][a:a + 36], poland["R"][a:a + 36], poland["D"][a:a + 36]
+    N = poland["N"]
+    init = [N - I[0] - R[0] - D[0], I[0], R[0], D[0]]
+    win = eng.Window(ctx, I, R, D, init, N, "ird-mxse")
+    lo, hi, n = [0.0] * 6, [2.0, 2.0, 28.0, 28.0, 1.0, 0.1], 300_000
+    if case == "narrow":
+        lo, hi = [0.2, 0.1, 10.0, 20.0, 0.1, 0.002], [0.2000001, 0.1000001, 10.0, 20.0, 0.1, 0.002]
+    elif case == "identical":
+        lo = hi = [0.2, 0.1, 10.0, 20.0, 0.1, 0.002]
+        n = 50_000
+    elif case == "tiny":
+        n = 3
+    elif case == "blowups":
+        hi = [1e150, 1e150, 28.0, 28.0, 1e150, 1e150]
+        n = 100_000
+    horizon = 21
+    bands, counts, _ = win.forecast_ensemble_bands(lo, hi, seed=99, n=n, horizon=horizon)
+    _, _, deaths = win.forecast_ensemble(lo, hi, seed=99, n=n, horizon=horizon, want_costs=False, want_params=False)
+    want, want_counts = _host_bands(deaths)
+    assert counts.tolist() == want_counts
+    assert_bitwise(bands.ravel(), want.ravel(), case)
