@@ -664,6 +664,19 @@ __device__ __forceinline__ void mt_draw(uint64_t* __restrict__ mt, int i0, doubl
     const int fwrap = kMtN - f0;
     uint64_t cur[NDRAW + 1];
     uint64_t far[NDRAW];
+    if (wrap > NDRAW && fwrap >= NDRAW) {  // warp-uniform: no word of the batch wraps (24 moves in 26)
+#pragma unroll
+        for (int j = 0; j <= NDRAW; ++j) cur[j] = row[32 * j];
+#pragma unroll
+        for (int j = 0; j < NDRAW; ++j) far[j] = frow[32 * j];
+#pragma unroll
+        for (int j = 0; j < NDRAW; ++j) {
+            const uint64_t v = mt_twist_word(cur[j], cur[j + 1], far[j]);
+            row[32 * j] = v;
+            out[j] = to_uniform01(mt_temper(v));
+        }
+        return;
+    }
 #pragma unroll
     for (int j = 0; j <= NDRAW; ++j) cur[j] = (j < wrap ? row : row_w)[32 * j];
 #pragma unroll
