@@ -682,6 +682,7 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     std::vector<DevSwarm> sw(g.idx.size());
     std::vector<uint32_t> cta_swarm;
     uint64_t offset = 0;
+    uint32_t n_groups_total = 0;
     for (size_t j = 0; j < g.idx.size(); ++j) {
         const sg_swarm_desc& d = descs[g.idx[j]];
         auto it = std::find(wins.begin(), wins.end(), d.window);
@@ -696,6 +697,9 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
         s.max_iters = d.max_iters;
         s.cta_begin = static_cast<uint32_t>(cta_swarm.size());
         s.n_ctas = static_cast<uint32_t>((d.n_particles + kStepThreads * kNP - 1) / (kStepThreads * kNP));
+        s.n_groups = (s.n_ctas + kFoldGroupCtas - 1) / kFoldGroupCtas;
+        s.group_begin = n_groups_total;
+        n_groups_total += s.n_groups;
         for (int k = 0; k < 6; ++k) {
             s.lo[k] = d.lower[k];
             s.hi[k] = d.upper[k];
@@ -763,6 +767,11 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     SG_CUDA(ctx, b.alloc(&P.mt, pblock_elems(g.n_total, kMtN)));
     SG_CUDA(ctx, b.alloc(&P.part_cost, g.n_ctas * kStepWarps));
     SG_CUDA(ctx, b.alloc(&P.part_idx, g.n_ctas * kStepWarps));
+    SG_CUDA(ctx, b.alloc(&P.gpart_cost, std::max<uint32_t>(n_groups_total, 1)));
+    SG_CUDA(ctx, b.alloc(&P.gpart_idx, std::max<uint32_t>(n_groups_total, 1)));
+    SG_CUDA(ctx, b.alloc(&P.group_arrived, std::max<uint32_t>(n_groups_total, 1)));
+    SG_CUDA(ctx, cudaMemsetAsync(P.group_arrived, 0, sizeof(unsigned int) * std::max<uint32_t>(n_groups_total, 1),
+                                 ctx->stream));
     SG_CUDA(ctx, b.alloc(&P.history, sw.size() * g.iters));
     if (g.sorted) {
         SG_CUDA(ctx, b.alloc(&g.d_perm, g.n_total));

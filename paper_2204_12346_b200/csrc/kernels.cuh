@@ -217,7 +217,15 @@ struct alignas(16) DevSwarm {  // bounds and coefficients first: 16-byte vector 
     uint32_t n_ctas;
     int window;          // index into the window table
     int repair;          // repair_time_order hook (calibration.cpp:89-93)
+    uint32_t group_begin;  // first fold group of this swarm (kFoldGroupCtas CTAs each)
+    uint32_t n_groups;     // 1: the last warp folds every warp partial itself
 };
+
+// Swarms of more than kFoldGroupCtas CTAs fold their warp minima in two
+// levels: the last warp of each group of CTAs folds the group's warps, the
+// last group folds the groups (C3: 32768 warp partials would otherwise be
+// read by one warp on the critical path of every iteration).
+constexpr uint32_t kFoldGroupCtas = 32;
 
 // Swarm-global state updated by the last CTA of every iteration.
 struct DevSwarmState {
@@ -249,6 +257,9 @@ struct PsoPlanes {
     size_t stride;       // total particles (plane length)
     double* part_cost;   // per warp of the step kernel
     unsigned long long* part_idx;
+    double* gpart_cost;  // per fold group (swarms of n_groups > 1)
+    unsigned long long* gpart_idx;
+    unsigned int* group_arrived;  // per fold group: warps arrived this iteration
     double* history;     // per swarm, max_iters_max entries
     uint64_t hist_stride;
 };
@@ -420,7 +431,6 @@ __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& s
     const int lane = threadIdx.x & 31;
     const uint32_t n_wslots = sw.n_ctas * kStepWarps;
     const size_t base = static_cast<size_t>(sw.cta_begin) * kStepWarps;
-    unsigned int ticket = 0;
     if (lane == 0) {
         P.part_cost[base + wslot] = my_c;
         P.part_idx[base + wslot] = my_i;
@@ -429,15 +439,60 @@ __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& s
     // before the arrival (release); the last warp fences before reading (acquire).
     __threadfence();
     __syncwarp();
+    uint32_t fold_begin = 0, fold_n = n_wslots;  // warp partials the last warp folds
+    const double* fold_cost = P.part_cost + base;
+    const unsigned long long* fold_idx = P.part_idx + base;
+    if (sw.n_groups > 1) {
+        constexpr uint32_t kGroupWarps = kFoldGroupCtas * kStepWarps;
+        const uint32_t g = wslot / kGroupWarps;
+        const uint32_t g_first = g * kGroupWarps;
+        const uint32_t g_n = min(kGroupWarps, n_wslots - g_first);
+        unsigned int t = 0;
+        if (lane == 0) t = atomicAdd(&P.group_arrived[sw.group_begin + g], 1u);
+        t = __shfl_sync(0xFFFFFFFFu, t, 0);
+        if (t != g_n - 1) return;
+        __threadfence();
+        double gc = __longlong_as_double(0x7FF0000000000000LL);
+        unsigned long long gi = ~0ULL;
+        for (uint32_t k = lane; k < g_n; k += 32) {
+            const double cc = __ldcg(&P.part_cost[base + g_first + k]);
+            const unsigned long long ix = __ldcg(&P.part_idx[base + g_first + k]);
+            if (better(cc, ix, gc, gi)) {
+                gc = cc;
+                gi = ix;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double oc = __shfl_down_sync(0xFFFFFFFFu, gc, off);
+            const unsigned long long oi = __shfl_down_sync(0xFFFFFFFFu, gi, off);
+            if (better(oc, oi, gc, gi)) {
+                gc = oc;
+                gi = oi;
+            }
+        }
+        if (lane == 0) {
+            P.gpart_cost[sw.group_begin + g] = gc;
+            P.gpart_idx[sw.group_begin + g] = gi;
+            P.group_arrived[sw.group_begin + g] = 0;  // every warp of the group has arrived
+        }
+        __threadfence();
+        __syncwarp();
+        fold_begin = 0;
+        fold_n = sw.n_groups;
+        fold_cost = P.gpart_cost + sw.group_begin;
+        fold_idx = P.gpart_idx + sw.group_begin;
+    }
+    unsigned int ticket = 0;
     if (lane == 0) ticket = atomicAdd(&st.arrived, 1u);
     ticket = __shfl_sync(0xFFFFFFFFu, ticket, 0);
-    if (ticket != n_wslots - 1) return;
+    if (ticket != fold_n - 1) return;
     __threadfence();
     double bc = __longlong_as_double(0x7FF0000000000000LL);
     unsigned long long bi = ~0ULL;
-    for (uint32_t k = lane; k < n_wslots; k += 32) {
-        const double cc = __ldcg(&P.part_cost[base + k]);
-        const unsigned long long ix = __ldcg(&P.part_idx[base + k]);
+    for (uint32_t k = fold_begin + lane; k < fold_n; k += 32) {
+        const double cc = __ldcg(&fold_cost[k]);
+        const unsigned long long ix = __ldcg(&fold_idx[k]);
         if (better(cc, ix, bc, bi)) {
             bc = cc;
             bi = ix;

@@ -99,3 +99,21 @@ def test_plan_reruns_are_identical(ctx, poland):
         assert_bitwise(x[3], y[3], "rerun history")
         assert_bitwise(x[3], z[3], "fresh plan history")
         assert_bitwise(x[1], z[1], "fresh plan best")
+
+
+def test_two_level_fold_for_large_swarms(ctx, port, poland):
+    """Swarms of more than 32 CTAs (4096 particles) fold their warp minima
+    per group of 32 CTAs, then across groups; 10,000 particles = 79 CTAs =
+    3 groups (the last ragged), next to a 4,097-particle swarm (2 groups)."""
+    import paper_2204_12346_b200 as eng
+    w1, (I1, R1, D1, init1, N) = _window(eng, ctx, poland, 210, 36, "ird-mxse")
+    w2, (I2, R2, D2, init2, _) = _window(eng, ctx, poland, 330, 21, "d-mae")
+    swarms = [dict(window=w1, lower=[0.0] * 6, upper=[2, 2, 28, 28, 1, 0.1], n_particles=10_000, max_iters=8, seed=5),
+              dict(window=w2, lower=[0.0] * 6, upper=[2, 2, 13, 13, 1, 0.1], n_particles=4_097, max_iters=12,
+                   seed=6)]
+    data = [(I1, R1, D1, init1, N, 24), (I2, R2, D2, init2, N, 24)]
+    plan = eng.Plan(ctx, swarms)
+    plan.run()
+    _check(port, swarms, data, plan.results())
+    plan.run()  # group counters are reset by their last warp: a rerun must match again
+    _check(port, swarms, data, plan.results())
