@@ -149,7 +149,9 @@ int sg_fit_swarms(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg_
  * allocate, upload descriptors), an asynchronous device run on the context
  * stream (engine seeding + max_iters fused step launches, no host round
  * trips), and result collection.  Lets callers time or graph the device part
- * alone; a plan may be run repeatedly (each run restarts from the seeds). */
+ * alone; a plan may be run repeatedly (each run restarts from the seeds).
+ * The plan reads its windows' device data at every run: destroy a plan
+ * before the windows it was created from (and both before the context). */
 typedef struct sg_plan sg_plan;
 int sg_plan_create(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg_plan** out);
 int sg_plan_run(sg_plan* plan);

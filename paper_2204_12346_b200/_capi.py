@@ -8,6 +8,7 @@ immediately — there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import weakref
 from pathlib import Path
 
 import numpy as np
@@ -180,6 +181,11 @@ class Context:
         raise_for_status(rc, "sg_ctx_create failed")
         self._h = h
         self.device = device
+        # windows and plans of this context: destroyed before it (include/sirdgpu.h rule)
+        self._children = weakref.WeakSet()
+
+    def _adopt(self, child) -> None:
+        self._children.add(child)
 
     @property
     def handle(self):
@@ -199,6 +205,8 @@ class Context:
 
     def close(self) -> None:
         if getattr(self, "_h", None):
+            for child in list(getattr(self, "_children", ())):
+                child.close()
             lib().sg_ctx_destroy(self._h)
             self._h = None
 
@@ -269,6 +277,7 @@ class Window:
                                          sg_state(*self.init), self.population, self.substeps, self.family,
                                          self.metric, ctypes.byref(h)))
         self._h = h
+        ctx._adopt(self)
 
     @property
     def handle(self):
@@ -350,6 +359,7 @@ class Plan:
         h = ctypes.c_void_p()
         ctx.check(lib().sg_plan_create(ctx.handle, self._descs, len(swarms), ctypes.byref(h)))
         self._h = h
+        ctx._adopt(self)
 
     @property
     def evals(self) -> int:

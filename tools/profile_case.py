@@ -13,6 +13,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=8)
     ap.add_argument("--spec", default=bench.SPEC)
+    ap.add_argument("--reps", type=int, default=1, help="timed runs (the first includes lazy module loading)")
     args = ap.parse_args()
     I, R, D = bench.load_series()
     ctx = eng.Context(0)
@@ -25,10 +26,11 @@ def main():
     swarms = [dict(window=w, lower=[0.0] * 6, upper=bench.STAGE2_HI, n_particles=bench.PARTICLES,
                    max_iters=args.iters, seed=bench.mix_seed(bench.BASE_SEED, k)) for k, w in enumerate(wins)]
     plan = eng.Plan(ctx, swarms)
-    seed_ms, steps_ms = plan.run_timed()
-    res = plan.results()
-    print(f"seed {seed_ms:.3f} ms, steps {steps_ms:.3f} ms ({steps_ms / args.iters:.3f} ms/launch), "
-          f"best w0 {res[0][2]!r}, launches {ctx.launch_count}")
+    for _ in range(args.reps):
+        seed_ms, steps_ms = plan.run_timed()
+        res = plan.results()
+        print(f"seed {seed_ms:.3f} ms, steps {steps_ms:.3f} ms ({steps_ms / args.iters:.3f} ms/launch), "
+              f"best w0 {res[0][2]!r}, launches {ctx.launch_count}")
 
 
 if __name__ == "__main__":
