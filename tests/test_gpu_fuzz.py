@@ -1,0 +1,98 @@
+"""Seeded fuzz of the whole path against the C restatement: random series
+(zeros, flat stretches, huge and tiny counts), random populations (integer,
+fractional, tiny, huge), all 8 objective specs, random boxes (negative lower
+bounds, inverted time boxes, zero-width dimensions), random PSO coefficients,
+24 and odd substep counts.  Every case must follow the oracle's optimize()
+bit for bit — this is where the exact-division fast paths and the regime
+prefixes meet inputs nobody chose on purpose."""
+import numpy as np
+import pytest
+
+from helpers import assert_bitwise
+
+pytestmark = pytest.mark.gpu
+
+SPECS = [f"{f}-{m}" for f in ("d", "ird") for m in ("mxse", "mse", "mae", "mape")]
+
+
+def _case(rng):
+    n_days = int(rng.integers(2, 60)) if rng.random() < 0.85 else int(rng.integers(60, 130))
+    kind = rng.integers(0, 4)
+    base = 10.0 ** rng.uniform(-2, 7)
+    if kind == 0:      # smooth growth
+        t = np.arange(n_days)
+        D = base * np.exp(rng.uniform(0, 0.1) * t)
+    elif kind == 1:    # noisy with zeros
+        D = np.maximum(0.0, base * rng.uniform(-0.5, 1.5, n_days)).cumsum()
+    elif kind == 2:    # flat
+        D = np.full(n_days, base)
+    else:              # integer counts
+        D = np.floor(rng.uniform(0, base, n_days)).cumsum()
+    I = np.abs(D * rng.uniform(0.5, 3.0) + rng.normal(0, base * 0.1, n_days))
+    R = np.sort(np.abs(D * rng.uniform(1, 10)))
+    if rng.random() < 0.2:
+        I[: n_days // 2] = 0.0
+    pop_kind = rng.integers(0, 4)
+    N = [38e6, float(rng.integers(10 ** 5, 10 ** 9)) + 0.5, 1e3 * rng.uniform(1, 9), 1e12][pop_kind]
+    N = max(N, float(I[0] + R[0] + D[0]) * 1.01 + 1.0)
+    init = [N - I[0] - R[0] - D[0], I[0], R[0], D[0]]
+    tau = n_days - 1
+    lo = [0.0, 0.0, 0.0, 0.0, 0.0, 0.0]
+    hi = [float(rng.uniform(0.1, 5)), float(rng.uniform(0.1, 5)), float(tau), float(tau),
+          float(rng.uniform(0.01, 2)), float(rng.uniform(0.001, 0.3))]
+    if rng.random() < 0.3:
+        lo[0] = -float(rng.uniform(0, 0.5))     # negative beta allowed by the box
+    if rng.random() < 0.2:
+        lo[4] = hi[4] = float(rng.uniform(0, 1))  # zero-width dimension
+    if rng.random() < 0.2:
+        lo[2], hi[2] = float(tau) * 0.6, float(tau)  # t1 late, t2 anywhere: repairs and t1 > t2
+    sub = int(rng.choice([24, 24, 24, 7, 1, 48]))
+    spec = SPECS[int(rng.integers(0, 8))]
+    coeffs = dict(inertia=float(rng.uniform(0, 1.2)), cognitive=float(rng.uniform(0, 2)),
+                  social=float(rng.uniform(0, 2)))
+    return dict(I=I, R=R, D=D, init=init, N=N, lo=lo, hi=hi, sub=sub, spec=spec, coeffs=coeffs,
+                n=int(rng.integers(1, 200)), iters=int(rng.integers(1, 12)), seed=int(rng.integers(1 << 62)),
+                repair=bool(rng.random() < 0.8))
+
+
+@pytest.mark.parametrize("batch", range(4))
+def test_fuzz_plans_match_oracle(ctx, port, batch):
+    import paper_2204_12346_b200 as eng
+    rng = np.random.default_rng(20240 + batch)
+    cases = [_case(rng) for _ in range(16)]
+    wins, swarms = [], []
+    for c in cases:
+        w = eng.Window(ctx, c["I"], c["R"], c["D"], c["init"], c["N"], c["spec"], substeps=c["sub"])
+        wins.append(w)
+        swarms.append(dict(window=w, lower=c["lo"], upper=c["hi"], n_particles=c["n"], max_iters=c["iters"],
+                           seed=c["seed"], repair=c["repair"], **c["coeffs"]))
+    # two shapes of the same work: one plan (flat kernels: > 1024 particles in
+    # total with the ballast) and one swarm per call (cluster kernel)
+    ballast = dict(swarms[0], n_particles=1100, max_iters=1, seed=1)
+    flat = ctx.fit_swarms(swarms + [ballast])[:-1]
+    for k, c in enumerate(cases):
+        rc, best, cost, hist = port.fit_swarm(c["spec"], c["I"], c["R"], c["D"], c["init"], c["N"], c["lo"], c["hi"],
+                                              c["n"], c["iters"], seed=c["seed"], repair=c["repair"],
+                                              substeps=c["sub"], **c["coeffs"])
+        single = ctx.fit_swarms([swarms[k]])[0]
+        for name, got in (("flat", flat[k]), ("cluster", single)):
+            assert got[0] == rc, (batch, k, name)
+            assert_bitwise(got[3], hist, f"batch {batch} case {k} {name} {c['spec']} sub {c['sub']}")
+            if rc == 0:
+                assert_bitwise(got[1], best, f"batch {batch} case {k} {name} best")
+
+
+def test_fuzz_costs_match_oracle(ctx, port):
+    import paper_2204_12346_b200 as eng
+    rng = np.random.default_rng(777)
+    for _ in range(30):
+        c = _case(rng)
+        w = eng.Window(ctx, c["I"], c["R"], c["D"], c["init"], c["N"], c["spec"], substeps=c["sub"])
+        pos = rng.uniform(np.array(c["lo"]) - 0.1, np.array(c["hi"]) * 1.5 + 0.1, (257, 6))
+        pos[::7, 2], pos[::7, 3] = pos[::7, 3], pos[::7, 2]      # some t1 > t2
+        pos[::11, 0] = 0.0
+        pos[::13, 1] = -0.0
+        pos[5, 2] = np.nan
+        pos[6, 3] = np.inf
+        assert_bitwise(w.eval_costs(pos), port.eval_costs(c["spec"], c["I"], c["R"], c["D"], c["init"], c["N"], pos,
+                                                          substeps=c["sub"]), c["spec"])
