@@ -183,21 +183,6 @@ struct StepLaunch {
 };
 
 template <int F, int M, int S>
-struct PermEvalLaunch {
-    static void run(unsigned grid, uint32_t cta_offset, const DevSwarm* sw, const uint32_t* cta_swarm,
-                    const DevWindow* wins, const PsoPlanes& P, DevSwarmState* state, const uint32_t* perm,
-                    uint64_t it, size_t smem, cudaStream_t st, cudaError_t* err) {
-        auto k = pso_eval_kernel<F, M, S>;
-        if (it == 0) {
-            *err = prepare_smem(k, smem);
-            if (*err != cudaSuccess) return;
-        }
-        k<<<grid, kStepThreads, smem, st>>>(sw, cta_swarm, wins, P, state, perm, it, cta_offset);
-        *err = cudaGetLastError();
-    }
-};
-
-template <int F, int M, int S>
 struct SwarmLaunch {
     // n_swarms clusters of `cluster` CTAs (thread-block clusters, one swarm each)
     static void run(unsigned n_swarms, unsigned cluster, unsigned threads, uint32_t swarm_offset, const DevSwarm* sw,
@@ -644,12 +629,9 @@ struct SwarmGroup {
         uint32_t cta_begin, n_ctas, swarm_begin, n_swarms;
     };
     std::vector<Lane> lanes;  // swarm partitions launched on separate streams
-    bool sorted = false;      // every swarm <= kSortMax: move+sort / permuted eval
     bool persistent = false;  // every swarm <= kPersistMax: one CTA per swarm, one launch
     unsigned threads = 0;     // persistent CTA size
     unsigned cluster = 1;     // persistent CTAs per swarm (thread-block cluster)
-    uint32_t* d_perm = nullptr;
-    unsigned char* d_keys = nullptr;
     size_t n_total = 0, n_ctas = 0, smem = 0;
     uint64_t iters = 0;               // max over swarms
     DevSwarm* d_sw = nullptr;
@@ -732,10 +714,6 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
         }
         g.lanes.push_back(cur);
     }
-#ifndef SG_SORT
-#define SG_SORT 0
-#endif
-    g.sorted = SG_SORT != 0 && !g.persistent && kNP == 1;
     if (g.persistent) {
         uint64_t max_n = 0;
         for (const DevSwarm& s : sw) max_n = std::max(max_n, s.n);
@@ -746,8 +724,6 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
         const uint64_t per_cta = (max_n + g.cluster - 1) / g.cluster;
         g.threads = static_cast<unsigned>(std::min<uint64_t>(kSwarmThreadsMax, (per_cta + 31) / 32 * 32));
     }
-    for (const DevSwarm& s : sw)
-        if (s.n > static_cast<uint64_t>(kSortMax)) g.sorted = false;
     std::vector<DevWindow> wtab(wins.size());
     for (size_t k = 0; k < wins.size(); ++k) wtab[k] = wins[k]->host;
 
@@ -773,10 +749,6 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     SG_CUDA(ctx, cudaMemsetAsync(P.group_arrived, 0, sizeof(unsigned int) * std::max<uint32_t>(n_groups_total, 1),
                                  ctx->stream));
     SG_CUDA(ctx, b.alloc(&P.history, sw.size() * g.iters));
-    if (g.sorted) {
-        SG_CUDA(ctx, b.alloc(&g.d_perm, g.n_total));
-        SG_CUDA(ctx, b.alloc(&g.d_keys, g.n_total));
-    }
     P.stride = g.n_total;
     P.hist_stride = g.iters;
     cudaStream_t st = ctx->stream;
@@ -847,19 +819,8 @@ int step_group(sg_ctx* ctx, SwarmGroup& g) {
             const SwarmGroup::Lane& ln = g.lanes[l];
             cudaStream_t st = n_lanes > 1 ? ctx->side[l] : ctx->stream;
             cudaError_t err = cudaSuccess;
-            if (g.sorted) {
-                pso_move_kernel<<<ln.n_ctas, kStepThreads, 0, st>>>(g.d_sw, g.d_cta, g.P, g.d_state, g.d_keys, it,
-                                                                    ln.cta_begin);
-                pso_sort_kernel<<<ln.n_swarms, kSortThreads, 0, st>>>(g.d_sw, g.d_keys, g.d_perm, it, ln.swarm_begin);
-                ctx->launches += 2;
-                err = cudaGetLastError();
-                if (err != cudaSuccess) return cuda_fail(ctx, err, "pso_move_kernel/pso_sort_kernel");
-                dispatch<PermEvalLaunch>(g.family, g.metric, g.substeps, ln.n_ctas, ln.cta_begin, g.d_sw, g.d_cta,
-                                         g.d_win, g.P, g.d_state, g.d_perm, it, g.smem, st, &err);
-            } else {
-                dispatch<StepLaunch>(g.family, g.metric, g.substeps, ln.n_ctas, ln.cta_begin, g.d_task, g.d_sw, g.P,
-                                     g.d_state, it, g.smem, st, &err);
-            }
+            dispatch<StepLaunch>(g.family, g.metric, g.substeps, ln.n_ctas, ln.cta_begin, g.d_task, g.d_sw, g.P,
+                                 g.d_state, it, g.smem, st, &err);
             ctx->launches += 1;
             if (err != cudaSuccess) return cuda_fail(ctx, err, "pso_step_kernel");
         }

@@ -27,12 +27,10 @@ namespace sirdgpu {
 #ifndef SG_STEP_MIN_BLOCKS
 #define SG_STEP_MIN_BLOCKS 5
 #endif
-#ifndef SG_NP
-#define SG_NP 1
-#endif
+
 constexpr int kEvalThreads = 128;
 constexpr int kStepThreads = SG_STEP_THREADS;
-constexpr int kNP = SG_NP;  // particles per thread in the flat step kernel
+constexpr int kNP = 1;  // particles per thread in the flat step kernel (2, interleaved, measured slower)
 constexpr int kStepWarps = kStepThreads / 32;
 
 // Shared-memory staging of one window: the descriptor in static shared memory,
@@ -651,144 +649,9 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
         c[q] = 0.0;
         ramp[q] = 0;
     }
-    if (active[0]) {
-        if constexpr (kNP == 1) c[0] = eval_particle<FAM, MET, SUB>(x[0], *win.w, win.tg, win.obs, win.robs, win.flag,
-                                                                     &ramp[0]);
-        else eval_particles<FAM, MET, SUB, kNP>(x, *win.w, win.tg, win.obs, win.robs, win.flag, c, ramp);
-    }
+    if (active[0]) c[0] = eval_particle<FAM, MET, SUB>(x[0], *win.w, win.tg, win.obs, win.robs, win.flag, &ramp[0]);
     finish_step<kNP>(sw, state[s], P, s, active, p, i, c, x, pbc,
                      (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it, ramp);
-}
-
-// ---- ramp-coherent evaluation order (swarms of at most kSortMax particles) ----
-//
-// The cost of a warp-day is set by the union of its lanes' beta ramps
-// [t1, t2) (sird_device.cuh integrate_days), so particles are evaluated in
-// Morton order of their switch times (t1, t2): pso_move_kernel moves every
-// particle (coalesced, particle order) and writes its key, pso_sort_kernel
-// counting-sorts each swarm's particle indices by key into perm, and
-// pso_eval_kernel maps thread slot -> perm[slot].
-// The order only decides which thread evaluates which particle — every
-// result is written to the particle's own slot and ties break on the
-// particle index, so results are identical for any order.
-constexpr int kSortThreads = 256;
-constexpr int kSortMax = 16384;
-constexpr int kSortBits = 4;                       // per coordinate
-constexpr int kSortBuckets = 1 << (2 * kSortBits);  // 256
-
-__device__ __forceinline__ uint32_t morton_key(double t1, double t2, double lo, double hi) {
-    const double span = hi - lo;
-    const float s = span > 0.0 ? static_cast<float>((1 << kSortBits) / span) : 0.0f;
-    int q1 = static_cast<int>(static_cast<float>(t1 - lo) * s);
-    int q2 = static_cast<int>(static_cast<float>(t2 - lo) * s);
-    q1 = min(max(q1, 0), (1 << kSortBits) - 1);  // NaN -> 0 (float->int of NaN is 0 on the device)
-    q2 = min(max(q2, 0), (1 << kSortBits) - 1);
-    uint32_t k = 0;
-#pragma unroll
-    for (int b = 0; b < kSortBits; ++b) k |= (((q1 >> b) & 1u) << (2 * b + 1)) | (((q2 >> b) & 1u) << (2 * b));
-    return k;
-}
-
-// Move phase (it > 0) for every particle of the lane's swarms, in particle
-// order (coalesced engine and state traffic), plus the Morton key of the new
-// switch times.  Same CTA -> swarm map as the evaluation kernels.
-__global__ void __launch_bounds__(kStepThreads) pso_move_kernel(const DevSwarm* __restrict__ swarms,
-                                                                const uint32_t* __restrict__ cta_swarm, PsoPlanes P,
-                                                                const DevSwarmState* __restrict__ state,
-                                                                unsigned char* __restrict__ keys, uint64_t it,
-                                                                uint32_t cta_offset) {
-    const uint32_t cta = blockIdx.x + cta_offset;
-    const int s = static_cast<int>(cta_swarm[cta]);
-    const DevSwarm& sw = swarms[s];
-    if (it >= sw.max_iters) return;
-    const uint64_t i = static_cast<uint64_t>(cta - sw.cta_begin) * blockDim.x + threadIdx.x;
-    if (i >= sw.n) return;
-    const size_t p = sw.offset + i;
-    double x[6];
-#pragma unroll
-    for (int d = 0; d < 6; ++d) x[d] = P.x[pblock_base(p, 6) + 32 * d];
-    if (it > 0) move_particle(sw, state[s].best_cost, state[s].best, P, p, it, x);
-    const double tlo = sw.lo[2] < sw.lo[3] ? sw.lo[2] : sw.lo[3];
-    const double thi = sw.hi[2] > sw.hi[3] ? sw.hi[2] : sw.hi[3];
-    keys[p] = static_cast<unsigned char>(morton_key(x[2], x[3], tlo, thi));
-}
-
-// Counting sort of one swarm's particle indices by key (one CTA per swarm).
-// Ties keep no particular order: the order never affects results.
-__global__ void __launch_bounds__(kSortThreads) pso_sort_kernel(const DevSwarm* __restrict__ swarms,
-                                                                const unsigned char* __restrict__ keys,
-                                                                uint32_t* __restrict__ perm, uint64_t it,
-                                                                uint32_t swarm_offset) {
-    __shared__ unsigned int hist[kSortBuckets];
-    const int s = static_cast<int>(blockIdx.x + swarm_offset);
-    const DevSwarm& sw = swarms[s];
-    if (it >= sw.max_iters) return;
-    for (int b = threadIdx.x; b < kSortBuckets; b += blockDim.x) hist[b] = 0;
-    __syncthreads();
-    const uint32_t n = static_cast<uint32_t>(sw.n);
-    const unsigned char* kk = keys + sw.offset;
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&hist[kk[i]], 1u);
-    __syncthreads();
-    if (threadIdx.x < 32) {  // exclusive scan of the buckets by one warp
-        const int lane = threadIdx.x;
-        constexpr int per = kSortBuckets / 32;
-        unsigned int local[per];
-        unsigned int sum = 0;
-#pragma unroll
-        for (int j = 0; j < per; ++j) {
-            local[j] = hist[lane * per + j];
-            sum += local[j];
-        }
-        unsigned int incl = sum;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const unsigned int v = __shfl_up_sync(0xFFFFFFFFu, incl, off);
-            if (lane >= off) incl += v;
-        }
-        unsigned int run = incl - sum;
-#pragma unroll
-        for (int j = 0; j < per; ++j) {
-            hist[lane * per + j] = run;
-            run += local[j];
-        }
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) perm[sw.offset + atomicAdd(&hist[kk[i]], 1u)] = i;
-}
-
-// Evaluation half of Swarm::step in permuted order (see above): thread slot
-// t of the swarm evaluates particle perm[t], already moved by
-// pso_move_sort_kernel, then personal best and the global-best fold.
-template <int FAM, int MET, int SUB>
-__global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
-    pso_eval_kernel(const DevSwarm* __restrict__ swarms, const uint32_t* __restrict__ cta_swarm,
-                    const DevWindow* __restrict__ windows, PsoPlanes P, DevSwarmState* __restrict__ state,
-                    const uint32_t* __restrict__ perm, uint64_t it, uint32_t cta_offset) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ DevWindow sdesc;
-    const uint32_t cta = blockIdx.x + cta_offset;
-    const int s = static_cast<int>(cta_swarm[cta]);
-    const DevSwarm& sw = swarms[s];
-    if (it >= sw.max_iters) return;  // CTA-uniform
-    const SmemWindow win = stage_window<MET, SUB>(windows + sw.window, &sdesc, smem);
-    const uint64_t slot = static_cast<uint64_t>(cta - sw.cta_begin) * blockDim.x + threadIdx.x;
-    const bool active = slot < sw.n;
-    const uint64_t i = active ? perm[sw.offset + slot] : 0;
-    const size_t p = sw.offset + i;
-    double c = 0.0;
-    int ramp = 0;
-    double x[1][6] = {};
-    if (active) {
-#pragma unroll
-        for (int d = 0; d < 6; ++d) x[0][d] = P.x[pblock_base(p, 6) + 32 * d];
-        c = eval_particle<FAM, MET, SUB>(x[0], *win.w, win.tg, win.obs, win.robs, win.flag, &ramp);
-    }
-    const bool act[1] = {active};
-    const size_t pp[1] = {p};
-    const uint64_t ii[1] = {i};
-    const double pbc0[1] = {active ? P.pbc[p] : 0.0};
-    finish_step<1>(sw, state[s], P, s, act, pp, ii, &c, x, pbc0, (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5),
-                   it, &ramp);
 }
 
 // ---- small swarms: one persistent thread-block cluster per swarm ---------------

@@ -378,96 +378,6 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
 #endif
 }
 
-// NP particles per thread, interleaved: NP independent Euler chains give the
-// scheduler independent FP64 work to hide the 8-cycle dependency latency,
-// and the per-day control (votes, class selection, loop) is paid once per
-// NP particles.  The day class is decided over all NP particles of all
-// lanes.  Same arithmetic per particle as integrate_days.
-template <int SUB, int NP, class Sink>
-__device__ __forceinline__ void integrate_days_n(const Particle* p, const DevWindow& w, const TimeGrid& tg,
-                                                 double* S, double* I, double* R, double* D, Sink* sink) {
-    const int nsub = SUB > 0 ? SUB : w.substeps;
-    const double h = w.h;
-    const double N = w.N, rN = w.rN, rN_lo = w.rN_lo;
-    const unsigned mask = __activemask();
-    bool fast = true;
-#pragma unroll
-    for (int q = 0; q < NP; ++q) fast = fast && p[q].fast;
-    const bool warp_fast = __all_sync(mask, fast);
-    int kbase = 0;
-    for (int day = 1; day < w.n_days; ++day) {
-        int lo[NP], hi[NP];
-        bool ramp_today = false, switch_today = false, full = true;
-#pragma unroll
-        for (int q = 0; q < NP; ++q) {
-            lo[q] = p[q].k1 - kbase;
-            hi[q] = p[q].k2 - kbase;
-            ramp_today = ramp_today || (lo[q] < hi[q] && lo[q] < nsub && hi[q] > 0);
-            switch_today = switch_today || (lo[q] > 0 && lo[q] < nsub);
-            full = full && lo[q] <= 0 && hi[q] >= nsub;
-        }
-        if (__any_sync(mask, ramp_today)) {
-            if (SUB > 0 && warp_fast && __all_sync(mask, full)) {
-#pragma unroll
-                for (int sub = 0; sub < nsub; ++sub) {
-                    const double t = tg.tgrid[kbase + sub];
-#pragma unroll
-                    for (int q = 0; q < NP; ++q) {
-                        const double beta = dadd(p[q].b1, dmul(p[q].slope, dsub(t, p[q].t1)));
-                        euler_substep(div_by_N(beta, rN, rN_lo), p[q].g, p[q].mu, h, S[q], I[q], R[q], D[q]);
-                    }
-                }
-            } else if (SUB > 0 && warp_fast) {
-#pragma unroll
-                for (int sub = 0; sub < nsub; ++sub) {
-                    const double t = tg.tgrid[kbase + sub];
-#pragma unroll
-                    for (int q = 0; q < NP; ++q) {
-                        const double beta = dadd(p[q].b1, dmul(p[q].slope, dsub(t, p[q].t1)));
-                        const double qv = div_by_N(beta, rN, rN_lo);
-                        const double bp = sub < lo[q] ? p[q].bp1 : (sub < hi[q] ? qv : p[q].bp2);
-                        euler_substep(bp, p[q].g, p[q].mu, h, S[q], I[q], R[q], D[q]);
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int sub = 0; sub < nsub; ++sub) {
-#pragma unroll
-                    for (int q = 0; q < NP; ++q) {
-                        double bp = sub < lo[q] ? p[q].bp1 : p[q].bp2;
-                        if (sub >= lo[q] && sub < hi[q]) {
-                            double t;
-                            if constexpr (SUB > 0) t = tg.tgrid[kbase + sub];
-                            else t = dadd(static_cast<double>(day - 1), tg.subh[sub]);
-                            bp = ramp_bp(p[q], t, N, rN, rN_lo);
-                        }
-                        euler_substep(bp, p[q].g, p[q].mu, h, S[q], I[q], R[q], D[q]);
-                    }
-                }
-            }
-        } else if (__any_sync(mask, switch_today)) {
-#pragma unroll
-            for (int sub = 0; sub < nsub; ++sub) {
-#pragma unroll
-                for (int q = 0; q < NP; ++q)
-                    euler_substep(sub < lo[q] ? p[q].bp1 : p[q].bp2, p[q].g, p[q].mu, h, S[q], I[q], R[q], D[q]);
-            }
-        } else {
-            double bp[NP];
-#pragma unroll
-            for (int q = 0; q < NP; ++q) bp[q] = lo[q] >= nsub ? p[q].bp1 : p[q].bp2;
-#pragma unroll
-            for (int sub = 0; sub < nsub; ++sub) {
-#pragma unroll
-                for (int q = 0; q < NP; ++q) euler_substep(bp[q], p[q].g, p[q].mu, h, S[q], I[q], R[q], D[q]);
-            }
-        }
-        kbase += nsub;
-#pragma unroll
-        for (int q = 0; q < NP; ++q) sink[q].day(day, S[q], I[q], R[q], D[q]);
-    }
-}
-
 __device__ __forceinline__ bool all_finite(double S, double I, double R, double D) {
     return isfinite(S) && isfinite(I) && isfinite(R) && isfinite(D);
 }
@@ -568,38 +478,6 @@ __device__ __forceinline__ double eval_particle(const double* x, const DevWindow
     ScoreSink<FAM, MET> sink(w, obs, robs, flag);  // starts from the day-0 contribution
     integrate_days<SUB>(p, w, tg, S, I, R, D, sink);
     return sink.finish(all_finite(S, I, R, D));
-}
-
-// NP particle-window evaluations per thread (integrate_days_n); x[q] are the
-// positions, costs[q]/ramp[q] receive the results.
-template <int FAM, int MET, int SUB, int NP>
-__device__ __forceinline__ void eval_particles(const double (*x)[6], const DevWindow& w, const TimeGrid& tg,
-                                               const ObsDay* obs, const ObsDay* robs, const unsigned char* flag,
-                                               double* costs, int* ramp) {
-    if (!w.init_finite) {
-#pragma unroll
-        for (int q = 0; q < NP; ++q) {
-            ramp[q] = 0;
-            costs[q] = __longlong_as_double(0x7FF0000000000000LL);
-        }
-        return;
-    }
-    Particle p[NP];
-    double S[NP], I[NP], R[NP], D[NP];
-    ScoreSink<FAM, MET> sink[NP];
-#pragma unroll
-    for (int q = 0; q < NP; ++q) {
-        p[q] = make_particle(x[q][0], x[q][1], x[q][2], x[q][3], x[q][4], x[q][5], w, SUB > 0 ? tg.tgrid : nullptr);
-        ramp[q] = p[q].k2 - p[q].k1;
-        S[q] = w.init[0];
-        I[q] = w.init[1];
-        R[q] = w.init[2];
-        D[q] = w.init[3];
-        sink[q] = ScoreSink<FAM, MET>(w, obs, robs, flag);
-    }
-    integrate_days_n<SUB, NP>(p, w, tg, S, I, R, D, sink);
-#pragma unroll
-    for (int q = 0; q < NP; ++q) costs[q] = sink[q].finish(all_finite(S[q], I[q], R[q], D[q]));
 }
 
 // ---- std::mt19937_64, structure-of-arrays ---------------------------------
