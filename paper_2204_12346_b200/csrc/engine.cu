@@ -849,9 +849,23 @@ int sg_plan_create(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg
     plan->n_desc = n_swarms;
     plan->status.assign(n_swarms, SG_OK);
     std::string why;
-    uint64_t total_particles = 0;
-    for (size_t k = 0; k < n_swarms; ++k) total_particles += swarms[k].n_particles;
-    const bool small_plan = total_particles <= 8 * static_cast<uint64_t>(kStepThreads);
+    // Swarms of <= kPersistMax particles run as persistent clusters (one
+    // launch, state in registers) when all of them fit in one wave of
+    // cluster CTAs (2 per SM at the kernel's register use); a plan too large
+    // for that fills the GPU better with the flat per-iteration kernels
+    // (measured: 148 swarms x 256 particles 1.45x faster persistent, 296
+    // even, C4's 4448 swarms flat).  SG_PERSIST_CTAS (diagnostic) overrides
+    // the CTA budget.
+    uint64_t n_small = 0, max_small = 0;
+    for (size_t k = 0; k < n_swarms; ++k)
+        if (swarms[k].n_particles <= static_cast<uint64_t>(kPersistMax)) {
+            ++n_small;
+            max_small = std::max<uint64_t>(max_small, swarms[k].n_particles);
+        }
+    static const char* persist_env = std::getenv("SG_PERSIST_CTAS");
+    const uint64_t persist_budget = persist_env ? std::strtoull(persist_env, nullptr, 10)
+                                                : 2 * static_cast<uint64_t>(ctx->sm_count);
+    const bool small_plan = n_small * ((max_small + kSwarmThreadsMax - 1) / kSwarmThreadsMax) <= persist_budget;
     for (size_t k = 0; k < n_swarms; ++k) {
         if (!swarm_config_valid(swarms[k], &why)) {
             plan->status[k] = SG_ERR_INVALID_ARGUMENT;
@@ -865,9 +879,6 @@ int sg_plan_create(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg
         }
         const DevWindow& w = swarms[k].window->host;
         const int sub = kernel_sub(w.n_days, w.substeps);
-        // Persistent one-CTA-per-swarm mode only pays when the plan cannot fill
-        // the GPU anyway (latency-bound single small swarms, C1); many small
-        // swarms (C4) run faster as flat per-iteration launches.
         const bool pers = swarms[k].n_particles <= static_cast<uint64_t>(kPersistMax) && small_plan;
         SwarmGroup* g = nullptr;
         for (SwarmGroup* x : plan->groups)

@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
 // barrier per iteration enough.
 constexpr int kSwarmThreadsMax = 128;
 constexpr int kSwarmClusterMax = 8;
-constexpr int kPersistMax = kSwarmThreadsMax * kSwarmClusterMax;  // 1024
+constexpr int kPersistMax = kSwarmThreadsMax * kSwarmClusterMax;  // 1024 particles per swarm
 
 struct SwarmPartial {
     double cost;

@@ -66,10 +66,11 @@ def test_fuzz_plans_match_oracle(ctx, port, batch):
         wins.append(w)
         swarms.append(dict(window=w, lower=c["lo"], upper=c["hi"], n_particles=c["n"], max_iters=c["iters"],
                            seed=c["seed"], repair=c["repair"], **c["coeffs"]))
-    # two shapes of the same work: one plan (flat kernels: > 1024 particles in
-    # total with the ballast) and one swarm per call (cluster kernel)
-    ballast = dict(swarms[0], n_particles=1100, max_iters=1, seed=1)
-    flat = ctx.fit_swarms(swarms + [ballast])[:-1]
+    # two shapes of the same work: one plan (flat kernels: more small swarms
+    # with the ballast than one wave of persistent clusters) and one swarm
+    # per call (cluster kernel)
+    ballast = [dict(swarms[0], n_particles=1, max_iters=1, seed=j) for j in range(300)]
+    flat = ctx.fit_swarms(swarms + ballast)[:len(swarms)]
     for k, c in enumerate(cases):
         rc, best, cost, hist = port.fit_swarm(c["spec"], c["I"], c["R"], c["D"], c["init"], c["N"], c["lo"], c["hi"],
                                               c["n"], c["iters"], seed=c["seed"], repair=c["repair"],

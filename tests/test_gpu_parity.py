@@ -150,8 +150,8 @@ def golden_fits():
 @pytest.mark.parametrize("mode", ["persistent", "flat"])
 def test_swarms_match_reference_goldens(ctx, golden_fits, mode):
     """All golden swarms in ONE sg_fit_swarms call (mixed specs, sizes, windows).
-    Small plans run one persistent CTA per swarm (pso_swarm_kernel); a
-    2048-particle ballast swarm pushes the same swarms onto the flat
+    Small plans run one persistent cluster per swarm (pso_swarm_kernel); 300
+    one-particle ballast swarms push the same swarms onto the flat
     per-iteration kernels (pso_step_kernel)."""
     import paper_2204_12346_b200 as eng
     wins, descs = [], []
@@ -161,7 +161,8 @@ def test_swarms_match_reference_goldens(ctx, golden_fits, mode):
         descs.append(dict(window=win, lower=c["lower"], upper=c["upper"], n_particles=c["n"], max_iters=c["iters"],
                           inertia=c["w"], cognitive=c["c1"], social=c["c2"], seed=c["seed"]))
     if mode == "flat":
-        descs.append(dict(descs[1], n_particles=2048, max_iters=3, seed=12345))
+        # more small swarms than one wave of persistent clusters: flat kernels
+        descs += [dict(descs[1], n_particles=1, max_iters=1, seed=12345 + j) for j in range(300)]
     out = ctx.fit_swarms(descs)
     for c, (status, best, cost, hist) in zip(golden_fits, out):
         assert status == c["status"], c["name"]

@@ -85,7 +85,7 @@ def test_cluster_kernel_every_cluster_size(ctx, port, poland, n_particles):
 def test_plan_reruns_are_identical(ctx, poland):
     import paper_2204_12346_b200 as eng
     wins = [_window(eng, ctx, poland, 3 * w, 36, "ird-mxse")[0] for w in range(12)]
-    swarms = [dict(window=w, lower=[0.0] * 6, upper=[2, 2, 28, 28, 1, 0.1], n_particles=500, max_iters=20, seed=k)
+    swarms = [dict(window=w, lower=[0.0] * 6, upper=[2, 2, 28, 28, 1, 0.1], n_particles=1100, max_iters=20, seed=k)
               for k, w in enumerate(wins)]
     plan = eng.Plan(ctx, swarms)
     assert plan.step_launches > 1  # flat per-iteration kernels
