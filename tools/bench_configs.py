@@ -77,6 +77,18 @@ def main():
     ms, evals, ramp, res = timed_plan(ctx, [dict(window=win, lower=[0] * 6, upper=stage2(20), n_particles=256,
                                                  max_iters=500, seed=bench.mix_seed(bench.BASE_SEED, 0))], reps=5)
     line = {"config": "C1", "evals": evals, "device_ms": ms, "evals_per_s": evals / ms * 1e3, "best": res[0][2]}
+    # C1 end to end through the public fit_window (host series in, FitResult
+    # out: window setup, swarm, re-integration, R^2)
+    import paper_2204_12346_b200.sirdfit as sf
+    data = sf.EpiSeries(infectious=list(I), recovered_cum=list(R), deaths_cum=list(D), new_cases=[0.0] * len(I))
+    win0 = sf.Window(index=0, start=0, length=21)
+    kw = dict(objective=bench.SPEC, particles=256, iters=500, seed=bench.mix_seed(bench.BASE_SEED, 0))
+    sf.fit_window(data, win0, N, **kw)  # warm
+    t0 = time.perf_counter()
+    for _ in range(5):
+        fit = sf.fit_window(data, win0, N, **kw)
+    line["e2e_ms"] = (time.perf_counter() - t0) / 5 * 1e3
+    line["e2e_objective_matches"] = fit.objective == res[0][2]
     if args.cpu:
         v, dt = cpu_sample(0, 20, 256, 500)
         line["cpu_reference_evals_per_s"] = v
