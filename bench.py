@@ -334,6 +334,10 @@ def bench_ours(args):
     achieved = ops_step / (steps_kernel_ms * 1e-3) / 1e12
     achieved_floor = ops_floor / (steps_kernel_ms * 1e-3) / 1e12
     bytes_per_particle, prof = load_profile_traffic()
+    # nominal FP64 lane-op rate: SMs x 64 lanes x max SM clock
+    clk = clocks.summary() if hasattr(clocks, "summary") else {}
+    sm_max = (clk or {}).get("sm_max_mhz") or 0.0
+    nominal_peak = torch.cuda.get_device_properties(local).multi_processor_count * 64 * sm_max * 1e6
     # one "launch" of the roofline = one iteration of the sweep (all lanes)
     traffic = bytes_per_particle * n_win * PARTICLES if bytes_per_particle else None
 
@@ -398,6 +402,10 @@ def bench_ours(args):
                                      "DADD/DMUL without FMA for bit parity; peak = FP64 issue rate measured "
                                      "on this GPU by sg_probe_fp64_rate (neither MEASURED_PEAKS.json nor "
                                      "B200_PROFILING.md has an FP64 figure)",
+                         "peak_nominal": nominal_peak / 1e12,
+                         "frac_nominal": achieved * 1e12 / nominal_peak if nominal_peak else None,
+                         "peak_nominal_note": "SMs x 64 FP64 lanes x max SM clock (the probe reaches "
+                                              f"{fp64_peak / nominal_peak:.3f} of it)" if nominal_peak else None,
                          "kernel_ms_per_launch": kernel_ms, "launches_per_step": step_launches,
                          "step_kernels_ms": steps_kernel_ms, "seed_ms": statistics.mean(seed_ms), "profile": prof},
             "cpu_baseline": cpu,
