@@ -399,7 +399,9 @@ def bench_ours(args):
                          "ops_per_eval": ops_step / evals_per_step,
                          "frac_floor": achieved_floor * 1e12 / fp64_peak,
                          "ops_note": "algorithmic FP64 ops (SURVEY.md §8d: 14/substep + 5/ramp substep + 12/scored day), "
-                                     "DADD/DMUL without FMA for bit parity; peak = FP64 issue rate measured "
+                                     "DADD/DMUL without FMA for bit parity (the kernel scores MXSE with 2 of the "
+                                     "credited 4 ops per compartment-day, exactly, DESIGN.md §3); peak = FP64 issue "
+                                     "rate measured "
                                      "on this GPU by sg_probe_fp64_rate (neither MEASURED_PEAKS.json nor "
                                      "B200_PROFILING.md has an FP64 figure)",
                          "peak_nominal": nominal_peak / 1e12,

@@ -381,6 +381,12 @@ int sg_window_create(sg_ctx* ctx, const double* infectious, const double* recove
     // (model.cpp:85), so it is computed once here, with the device's
     // operation order (e = (obs - pred) * scale; MXSE max(0, e*e); MSE
     // 0 + e*e; MAE 0 + |e|; MAPE 0 + |(obs - pred) / obs| unless obs == 0).
+    // MXSE by largest |obs - pred|: exact when every scale is
+    // finite and positive (always for D-only, scale 1).
+    d.mxse_abs = 1;
+    if (family == SG_FAMILY_IRD_JOINT)
+        for (int c = 0; c < 3; ++c)
+            if (!(std::isfinite(d.scale[c]) && d.scale[c] > 0.0)) d.mxse_abs = 0;
     {
         const double pred[3] = {init.I, init.R, init.D};
         for (int c = 0; c < 3; ++c) {
@@ -392,7 +398,7 @@ int sg_window_create(sg_ctx* ctx, const double* infectious, const double* recove
                 double e = o - pred[c];
                 if (family == SG_FAMILY_IRD_JOINT) e = e * d.scale[c];
                 const double e2 = e * e;
-                if (metric == SG_METRIC_MXSE) a = (0.0 < e2) ? e2 : 0.0;
+                if (metric == SG_METRIC_MXSE) a = d.mxse_abs ? std::fabs(o - pred[c]) : ((0.0 < e2) ? e2 : 0.0);
                 else if (metric == SG_METRIC_MSE) a = 0.0 + e2;
                 else a = 0.0 + std::fabs(e);
             }

@@ -81,6 +81,7 @@ struct alignas(16) DevWindow {  // 16-byte multiple: staged by one bulk copy
     int init_finite;      // isfinite(init.total()) (model.cpp:83)
     double init[4];       // S, I, R, D
     double scale[3];      // compartment_cost scale (objectives.cpp:61-69); 1 for D-only
+    int mxse_abs;         // MXSE tracks max |obs - pred| (scale and square once at the end)
     double acc0[3];       // day-0 score contribution per compartment: the initial state is
                           // the same for every particle (model.cpp:85), so it is window-constant
     double kept[3];       // MAPE: number of days with obs != 0 (objectives.cpp:41-55)
@@ -395,12 +396,14 @@ struct ScoreSink {
     const ObsDay* robs;   // shared memory (MAPE)
     const unsigned char* flag;  // shared memory (MAPE)
     uint32_t obs_s;       // shared-window address of obs[next day] (days arrive as 1, 2, ... in order)
+    bool abs_max;         // MXSE on max |obs - pred| (DevWindow::mxse_abs)
     double acc[3];
 
     ScoreSink() = default;
     __device__ __forceinline__ ScoreSink(const DevWindow& win, const ObsDay* o, const ObsDay* ro,
                                          const unsigned char* f)
-        : w(&win), obs(o), robs(ro), flag(f), obs_s(static_cast<uint32_t>(__cvta_generic_to_shared(o + 1))) {
+        : w(&win), obs(o), robs(ro), flag(f), obs_s(static_cast<uint32_t>(__cvta_generic_to_shared(o + 1))),
+          abs_max(MET == kMetMXSE && win.mxse_abs) {
         acc[0] = win.acc0[0];  // day 0 already scored (sg_window_create)
         acc[1] = win.acc0[1];
         acc[2] = win.acc0[2];
@@ -422,6 +425,12 @@ struct ScoreSink {
             const double num = dsub(o, pred);
             const double q = f == kObsFast ? div_exact(num, o, robs[day].v[c]) : ddiv(num, o);
             acc[c] = dadd(acc[c], fabs(q));
+            return;
+        }
+        if (MET == kMetMXSE && abs_max) {
+            // max_d RN(RN(d*s)^2) = RN(RN(max_d |d| * s)^2) for s > 0 finite:
+            // both roundings are monotone in |d| (objectives.cpp:22-26)
+            acc[c] = std_max(acc[c], fabs(dsub(o, pred)));
             return;
         }
         double e = dsub(o, pred);
@@ -447,6 +456,10 @@ struct ScoreSink {
             return ddiv(dmul(100.0, acc[c]), w->kept[c]);
         }
         if (MET == kMetMSE || MET == kMetMAE) return ddiv(acc[c], static_cast<double>(w->n_days));
+        if (abs_max) {
+            const double e = FAM == kFamIRD ? dmul(acc[c], w->scale[c]) : acc[c];
+            return dmul(e, e);
+        }
         return acc[c];
     }
 

@@ -97,3 +97,30 @@ def test_fuzz_costs_match_oracle(ctx, port):
         pos[6, 3] = np.inf
         assert_bitwise(w.eval_costs(pos), port.eval_costs(c["spec"], c["I"], c["R"], c["D"], c["init"], c["N"], pos,
                                                           substeps=c["sub"]), c["spec"])
+
+
+@pytest.mark.parametrize("edge", ["subnormal_range", "inf_obs", "nan_obs", "flat_zero", "plain"])
+def test_mxse_largest_residual_shortcut_edges(ctx, port, poland, edge):
+    """MXSE keeps max |obs - pred| and scales/squares once (exact for finite
+    positive scales); windows whose scale is +inf (subnormal range) or 0
+    (infinite observation) take the per-day path — both must equal the
+    reference's per-day max of squared scaled residuals."""
+    import paper_2204_12346_b200 as eng
+    a = 70
+    I, R, D = (poland[k][a:a + 30].copy() for k in ("I", "R", "D"))
+    if edge == "subnormal_range":
+        I[:] = 0.0
+        I[3] = 1e-310             # I's range subnormal: scale = 1/range = inf
+    elif edge == "inf_obs":
+        D[11] = np.inf            # range inf: scale 0
+    elif edge == "nan_obs":
+        R[5] = np.nan
+    elif edge == "flat_zero":
+        I[:] = 0.0
+    N = poland["N"]
+    init = [N - I[0] - R[0] - D[0], I[0], R[0], D[0]]
+    rng = np.random.default_rng(9)
+    pos = rng.uniform([0, 0, 0, 0, 0, 0], [2, 2, 28, 28, 1, 0.1], (300, 6))
+    for spec in ("ird-mxse", "d-mxse", "ird-mse"):
+        w = eng.Window(ctx, I, R, D, init, N, spec)
+        assert_bitwise(w.eval_costs(pos), port.eval_costs(spec, I, R, D, init, N, pos), f"{edge} {spec}")
