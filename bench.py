@@ -194,15 +194,16 @@ def barrier(world):
 
 
 def load_profile_traffic():
-    """DRAM bytes per particle-iteration of the step kernel from the committed
-    ncu --set full summary (profiles/ncu_step_kernel_*.json), if any."""
+    """DRAM bytes and executed FP64 ops per particle-iteration of the step
+    kernel from the committed ncu --set full summary
+    (profiles/ncu_step_kernel_*.json), if any."""
     for p in sorted((ROOT / "profiles").glob("ncu_step_kernel_*.json"), reverse=True):
         try:
             d = json.loads(p.read_text())
-            return d.get("dram_bytes_per_particle"), p.name
+            return d.get("dram_bytes_per_particle"), p.name, d.get("fp64_ops_per_particle_executed")
         except (OSError, ValueError):
             continue
-    return None, None
+    return None, None, None
 
 
 # ---------------------------------------------------------------------------------------------
@@ -333,7 +334,7 @@ def bench_ours(args):
     kernel_ms = steps_kernel_ms / (step_launches if step_launches else 1)
     achieved = ops_step / (steps_kernel_ms * 1e-3) / 1e12
     achieved_floor = ops_floor / (steps_kernel_ms * 1e-3) / 1e12
-    bytes_per_particle, prof = load_profile_traffic()
+    bytes_per_particle, prof, fp64_exec = load_profile_traffic()
     # nominal FP64 lane-op rate: SMs x 64 lanes x max SM clock
     clk = clocks.summary() if hasattr(clocks, "summary") else {}
     sm_max = (clk or {}).get("sm_max_mhz") or 0.0
@@ -397,6 +398,7 @@ def bench_ours(args):
                          "ops_per_eval_floor": ops_per_eval(TAU + 1),
                          "ramp_substeps_per_eval": ramp_substeps / evals_per_step,
                          "ops_per_eval": ops_step / evals_per_step,
+                         "fp64_ops_per_eval_executed": fp64_exec,  # ncu SASS counts (profile), incl. PSO move/setup
                          "frac_floor": achieved_floor * 1e12 / fp64_peak,
                          "ops_note": "algorithmic FP64 ops (SURVEY.md §8d: 14/substep + 5/ramp substep + 12/scored day), "
                                      "DADD/DMUL without FMA for bit parity (the kernel scores MXSE with 2 of the "

@@ -53,8 +53,26 @@ def raw_metrics(rep):
     return out  # SI units (bytes, seconds, Hz)
 
 
+def opcode_mix(rep):
+    """Executed warp-level instructions per opcode from the SASS source page."""
+    import re
+    txt = subprocess.run(["ncu", "-i", str(rep), "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(txt.splitlines()))
+    hdr = rows[1]
+    ia, isrc = hdr.index("Instructions Executed"), hdr.index("Source")
+    ops = collections.Counter()
+    for r in rows[2:]:
+        n = int(r[ia] or 0)
+        mt = re.match(r"(@!?U?P\w+\s+)?([A-Z0-9_]+)", r[isrc].strip())
+        if n and mt:
+            ops[mt.group(2)] += n
+    return ops
+
+
 def step(rep, tag, cmd, note, kernel):
     m = raw_metrics(rep)
+    ops = opcode_mix(rep)
 
     def f(k):
         return m.get(k)
@@ -75,7 +93,12 @@ def step(rep, tag, cmd, note, kernel):
          "instructions_executed": f("smsp__inst_executed.sum"),
          "sm_clock_ghz": (f("smsp__cycles_elapsed.avg.per_second") or 0) / 1e9,
          "stall_samples": dict(sorted(stalls.items())),
-         "dram_bytes_per_particle": (rd + wr) / particles, "note": note}
+         "dram_bytes_per_particle": (rd + wr) / particles,
+         # each warp instruction is one op per lane: per-particle op counts
+         "fp64_ops_per_particle_executed": 32.0 * sum(ops[k] for k in ("DADD", "DMUL", "DFMA", "DSETP")) / particles,
+         "other_ops_per_particle_executed": 32.0 * sum(v for k, v in ops.items()
+                                                       if k not in ("DADD", "DMUL", "DFMA", "DSETP")) / particles,
+         "note": note}
     out = PROF / f"ncu_step_kernel_{tag}.json"
     out.write_text(json.dumps(d, indent=1) + "\n")
     print(json.dumps(d, indent=1))
