@@ -647,6 +647,14 @@ struct SwarmGroup {
     DevSwarmState* d_state = nullptr;
     PsoPlanes P{};
     DevBufs bufs;
+    // The flat step launches of a run (all lanes, all iterations) as one
+    // CUDA graph, captured at the second run of the plan (a plan run once —
+    // every calibration call — never pays the instantiation).
+    int runs = 0;
+    cudaGraphExec_t steps_exec = nullptr;
+    ~SwarmGroup() {
+        if (steps_exec) cudaGraphExecDestroy(steps_exec);
+    }
 };
 
 }  // namespace
@@ -804,7 +812,47 @@ int ensure_lanes(sg_ctx* ctx) {
     return SG_OK;
 }
 
+int enqueue_steps(sg_ctx* ctx, SwarmGroup& g);
+
+bool graphs_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SG_GRAPH");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 int step_group(sg_ctx* ctx, SwarmGroup& g) {
+    if (!g.persistent && graphs_enabled() && g.runs++ >= 1) {
+        if (!g.steps_exec) {
+            const int rc0 = g.lanes.size() > 1 ? ensure_lanes(ctx) : SG_OK;
+            if (rc0) return rc0;
+            SG_CUDA(ctx, cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+            const uint64_t before = ctx->launches;
+            const int rc = enqueue_steps(ctx, g);
+            ctx->launches = before;  // counted when the graph runs
+            cudaGraph_t graph = nullptr;
+            const cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+            if (rc) {
+                if (graph) cudaGraphDestroy(graph);
+                return rc;
+            }
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "plan graph capture");
+            const cudaError_t ei = cudaGraphInstantiate(&g.steps_exec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (ei != cudaSuccess) {
+                g.steps_exec = nullptr;
+                return cuda_fail(ctx, ei, "plan graph instantiate");
+            }
+        }
+        SG_CUDA(ctx, cudaGraphLaunch(g.steps_exec, ctx->stream));
+        ctx->launches += g.iters * g.lanes.size();
+        return SG_OK;
+    }
+    return enqueue_steps(ctx, g);
+}
+
+int enqueue_steps(sg_ctx* ctx, SwarmGroup& g) {
     if (g.persistent) {
         cudaError_t err = cudaSuccess;
         dispatch<SwarmLaunch>(g.family, g.metric, g.substeps, static_cast<unsigned>(g.idx.size()), g.cluster,
