@@ -115,6 +115,15 @@ int sg_integrate_batch(sg_ctx* ctx, const double* params, size_t n, sg_state ini
 int sg_integrate_states(sg_ctx* ctx, const double* params, const sg_state* inits, size_t n, double population,
                         int n_days, int substeps, double* states, uint8_t* finite);
 
+/* fit_window's finish for n fits on the device (calibration.cpp:175-185):
+ * the re-integration of sg_integrate_states plus r_squared_d of the
+ * trajectory's D against the observed deaths (objectives.cpp:122-144,
+ * observed_d: n x n_days), r2[k] = NaN where the observed series is
+ * constant (the ConstantObservedError branch). */
+int sg_integrate_states_r2(sg_ctx* ctx, const double* params, const sg_state* inits, const double* observed_d,
+                           size_t n, double population, int n_days, int substeps, double* states, uint8_t* finite,
+                           double* r2);
+
 /* --- boundary 2: the particle swarm --------------------------------------
  * One descriptor per independent swarm (Swarm::Swarm + optimize,
  * pso.cpp:47-143).  Swarms may use different windows, sizes and seeds;

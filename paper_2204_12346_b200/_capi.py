@@ -104,6 +104,8 @@ SIGNATURES = {
     "sg_probe_fp64_rate": (ctypes.c_int, [ctypes.c_void_p, _dp]),
     "sg_integrate_states": (ctypes.c_int, [ctypes.c_void_p, _dp, ctypes.POINTER(sg_state), ctypes.c_size_t,
                                            ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp, _u8p]),
+    "sg_integrate_states_r2": (ctypes.c_int, [ctypes.c_void_p, _dp, ctypes.POINTER(sg_state), _dp, ctypes.c_size_t,
+                                              ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp, _u8p, _dp]),
     "sg_fit_window_series": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, ctypes.c_size_t, ctypes.c_uint64,
                                             ctypes.c_uint64, ctypes.POINTER(sg_fit_settings), ctypes.c_uint64,
                                             ctypes.POINTER(sg_fit_record), _dp, _dp]),

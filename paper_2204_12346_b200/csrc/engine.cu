@@ -565,6 +565,44 @@ int sg_integrate_states(sg_ctx* ctx, const double* params, const sg_state* inits
     return SG_OK;
 }
 
+int sg_integrate_states_r2(sg_ctx* ctx, const double* params, const sg_state* inits, const double* observed_d,
+                           size_t n, double population, int n_days, int substeps, double* states, uint8_t* finite,
+                           double* r2) {
+    if (!ctx) return SG_ERR_INVALID_ARGUMENT;
+    if (n_days < 1 || substeps < 1 || !(population > 0.0))
+        return fail(ctx, SG_ERR_INVALID_ARGUMENT,
+                    "integrate_euler needs n_days >= 1, substeps >= 1 and a positive population");
+    if (n == 0) return SG_OK;
+    if (!params || !inits || !observed_d || !states || !finite || !r2)
+        return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null host buffer");
+    SG_CUDA(ctx, cudaSetDevice(ctx->device));
+    DevBufs b;
+    b.st = ctx->stream;
+    double *d_p, *d_init, *d_states, *d_obs, *d_r2;
+    unsigned char* d_fin;
+    const size_t nd = n * static_cast<size_t>(n_days);
+    SG_CUDA(ctx, b.alloc(&d_p, 6 * n));
+    SG_CUDA(ctx, b.alloc(&d_init, 4 * n));
+    SG_CUDA(ctx, b.alloc(&d_states, nd * 4));
+    SG_CUDA(ctx, b.alloc(&d_fin, n));
+    SG_CUDA(ctx, b.alloc(&d_obs, nd));
+    SG_CUDA(ctx, b.alloc(&d_r2, n));
+    SG_CUDA(ctx, cudaMemcpyAsync(d_p, params, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, cudaMemcpyAsync(d_init, inits, sizeof(double) * 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, cudaMemcpyAsync(d_obs, observed_d, sizeof(double) * nd, cudaMemcpyHostToDevice, ctx->stream));
+    const DevWindow w = integration_window(n_days, substeps, population);
+    const int rc = launch_integrate(ctx, w, d_p, d_init, 4, 0, n, d_states, d_fin);
+    if (rc) return rc;
+    r2_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, ctx->stream>>>(d_states, d_obs, n, n_days, d_r2);
+    ctx->launches += 1;
+    SG_CUDA(ctx, cudaGetLastError());
+    SG_CUDA(ctx, cudaMemcpyAsync(states, d_states, sizeof(double) * nd * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, cudaMemcpyAsync(finite, d_fin, n, cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, cudaMemcpyAsync(r2, d_r2, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SG_OK;
+}
+
 int sg_forecast_batch(sg_ctx* ctx, const double* params, const sg_state* junction, size_t n, double population,
                       int horizon, int substeps, double* states, uint8_t* finite) {
     if (!ctx) return SG_ERR_INVALID_ARGUMENT;

@@ -424,20 +424,20 @@ std::vector<JobOutcome> fit_jobs(const EpiSeries& data, const std::vector<Job>& 
         }
         std::vector<double> states(qs.size() * len * 4);
         std::vector<uint8_t> fin(qs.size());
-        check(ctx, sg_integrate_states(ctx, p.data(), st.data(), qs.size(), settings.population, static_cast<int>(len),
-                                       settings.substeps, states.data(), fin.data()));
+        std::vector<double> obs_d(qs.size() * len), r2(qs.size());
+        for (std::size_t i = 0; i < qs.size(); ++i) {
+            const WindowSlice observed = slice_window(data, out[done[qs[i]]].fit.window);
+            std::copy(observed.deaths_cum.begin(), observed.deaths_cum.end(), obs_d.begin() + i * len);
+        }
+        // re-integration (calibration.cpp:175-176) and R^2 (182-185) on the device
+        check(ctx, sg_integrate_states_r2(ctx, p.data(), st.data(), obs_d.data(), qs.size(), settings.population,
+                                          static_cast<int>(len), settings.substeps, states.data(), fin.data(),
+                                          r2.data()));
         for (std::size_t i = 0; i < qs.size(); ++i) {
             JobOutcome& o = out[done[qs[i]]];
             states_to_trajectory(states.data() + i * len * 4, static_cast<int>(len), fin[i] != 0, settings.population,
                                  o.fit.trajectory);
-            const WindowSlice observed = slice_window(data, o.fit.window);
-            std::vector<double> predicted_d(len);
-            for (std::size_t k = 0; k < len; ++k) predicted_d[k] = o.fit.trajectory.states[k].D;
-            try {
-                o.fit.r2_d = r_squared_d(observed.deaths_cum, predicted_d);
-            } catch (const ConstantObservedError&) {
-                o.fit.r2_d = kNaN;  // calibration.cpp:183-185
-            }
+            o.fit.r2_d = r2[i];  // NaN for a constant observed series (ConstantObservedError)
             o.fit.ok = true;
         }
     }

@@ -819,6 +819,31 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 1) pso_swarm_kernel(const De
     cluster.sync();  // no CTA leaves while another may still read its partials
 }
 
+// ---- R^2 of the re-integrated deaths (fit_window's finish) ------------------------
+//
+// r_squared_d (objectives.cpp:122-144) per fit, one thread each, with the
+// reference's sequential sums: mean of the observed series, then
+// ss_res += e*e and ss_tot += c*c day by day; NaN where ss_tot == 0
+// (ConstantObservedError, calibration.cpp:183-185).  states: n x n_days x 4.
+__global__ void r2_kernel(const double* __restrict__ states, const double* __restrict__ obs_d, size_t n, int n_days,
+                          double* __restrict__ r2) {
+    const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double* y = obs_d + k * static_cast<size_t>(n_days);
+    const double* st = states + k * static_cast<size_t>(n_days) * 4;
+    double mean = 0.0;
+    for (int d = 0; d < n_days; ++d) mean = dadd(mean, y[d]);
+    mean = ddiv(mean, static_cast<double>(n_days));
+    double ss_res = 0.0, ss_tot = 0.0;
+    for (int d = 0; d < n_days; ++d) {
+        const double e = dsub(y[d], st[4 * d + 3]);
+        ss_res = dadd(ss_res, dmul(e, e));
+        const double c = dsub(y[d], mean);
+        ss_tot = dadd(ss_tot, dmul(c, c));
+    }
+    r2[k] = ss_tot == 0.0 ? __longlong_as_double(0x7FF8000000000000LL) : dsub(1.0, ddiv(ss_res, ss_tot));
+}
+
 // ---- forecast-scenario ensemble ----------------------------------------------------
 // Sample k: 6 uniform01 draws of mt19937_64(mix_seed(seed, k)) mapped into the
 // box like Swarm::Swarm (pso.cpp:65-72) + repair; score it on the window

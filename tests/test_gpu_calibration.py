@@ -172,3 +172,35 @@ def golden_costs_case():
     I, R, D = g["boundary_fixture/obs"]
     return (I, R, D, g["boundary_fixture/init"], float(g["boundary_fixture/N"][0]),
             g["boundary_fixture/special/positions"][:3], g["boundary_fixture/special/ird-mxse"][:3])
+
+
+def test_device_r2_matches_reference_formula_and_flat_series(sirdfit):
+    """R^2(D) is computed on the device with the reference's sequential sums
+    (objectives.cpp:122-144); a constant observed series gives NaN instead of
+    ConstantObservedError (calibration.cpp:183-185)."""
+    import numpy as np
+    from conftest import GOLDEN
+    a = np.genfromtxt(GOLDEN / "poland_like.csv", delimiter=",", names=True)
+    I, R, D = list(a["infectious"]), list(a["recovered_cum"]), list(a["deaths_cum"])
+    D_flat = D[:]
+    for k in range(200, 221):
+        D_flat[k] = 1000.0  # its mean is exact, so ss_tot == 0 exactly
+    for deaths, want_nan in ((D, False), (D_flat, True)):
+        data = sirdfit.EpiSeries(infectious=I, recovered_cum=R, deaths_cum=deaths, new_cases=[0.0] * len(I))
+        fit = sirdfit.fit_window(data, sirdfit.Window(0, 200, 21), 38e6, "ird-mse", particles=120, iters=15, seed=4)
+        assert fit.ok
+        if want_nan:
+            assert np.isnan(fit.r2_d)
+        else:
+            obs = np.array(deaths[200:221])
+            pred = np.array([s.D for s in fit.trajectory.states])
+            mean = 0.0
+            for y in obs:
+                mean += float(y)
+            mean /= len(obs)
+            ss_res = ss_tot = 0.0
+            for y, p in zip(obs, pred):
+                e, c = float(y) - float(p), float(y) - mean
+                ss_res += e * e
+                ss_tot += c * c
+            assert fit.r2_d == 1.0 - ss_res / ss_tot
