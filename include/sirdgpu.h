@@ -270,6 +270,14 @@ int sg_probe_fp64_rate(sg_ctx* ctx, double* ops_per_s);
 int sg_forecast_ensemble_bands(sg_window* window, const double lower[6], const double upper[6], uint64_t seed,
                                size_t n, int horizon, double* bands, uint64_t* counts, double* costs);
 
+/* The same for many windows in one call (C5: every window of the sweep):
+ * window k uses seeds[k]; bands: n_windows x 7 x (horizon + 1), counts:
+ * n_windows x (horizon + 1).  Windows are pipelined on two streams, so one
+ * window's band selection overlaps the next window's evaluation. */
+int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows, const double lower[6],
+                                     const double upper[6], const uint64_t* seeds, size_t n, int horizon,
+                                     double* bands, uint64_t* counts);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

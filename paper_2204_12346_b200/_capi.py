@@ -123,6 +123,8 @@ SIGNATURES = {
                                             ctypes.c_int, _dp, _dp, _dp]),
     "sg_forecast_ensemble_bands": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, ctypes.c_uint64, ctypes.c_size_t,
                                                   ctypes.c_int, _dp, _u64p, _dp]),
+    "sg_forecast_ensemble_bands_batch": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_size_t, _dp, _dp,
+                                                        _u64p, ctypes.c_size_t, ctypes.c_int, _dp, _u64p]),
 }
 
 _lib = None
@@ -243,6 +245,19 @@ class Context:
         return states, fin.astype(bool)
 
     # -- swarms -------------------------------------------------------------------
+    def forecast_ensemble_bands_batch(self, windows, lower, upper, seeds, n: int, horizon: int):
+        """sg_forecast_ensemble_bands for many windows in one pipelined call:
+        -> (bands n_windows x 7 x (horizon+1), counts n_windows x (horizon+1))."""
+        w = len(windows)
+        handles = (ctypes.c_void_p * w)(*[x.handle.value for x in windows])
+        lo, hi = _f64(lower), _f64(upper)
+        sd = np.ascontiguousarray([int(x) & 0xFFFFFFFFFFFFFFFF for x in seeds], dtype=np.uint64)
+        bands = np.empty((w, 7, horizon + 1))
+        counts = np.empty((w, horizon + 1), dtype=np.uint64)
+        self.check(lib().sg_forecast_ensemble_bands_batch(handles, w, _d(lo), _d(hi), sd.ctypes.data_as(_u64p), n,
+                                                          int(horizon), _d(bands), counts.ctypes.data_as(_u64p)))
+        return bands, counts
+
     def fit_swarms(self, swarms: list[dict]):
         """sg_fit_swarms: each dict has window, lower, upper, n_particles, max_iters,
         inertia, cognitive, social, seed, repair.  Returns list of

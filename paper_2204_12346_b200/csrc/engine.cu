@@ -1168,7 +1168,8 @@ int sg_fit_swarms(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg_
 // Ramp-coherent evaluation order of an ensemble (ens_sample_kernel + a
 // 16-bit radix sort of the (day t1, day t2) keys): returns perm and planes.
 static cudaError_t ensemble_order(sg_ctx* ctx, DevBufs& b, const double* d_lo, const double* d_hi, uint64_t seed,
-                                  size_t n, uint32_t** perm, double** planes) {
+                                  size_t n, uint32_t** perm, double** planes, cudaStream_t st = nullptr) {
+    if (!st) st = ctx->stream;
     uint32_t *keys, *keys_sorted, *idx, *idx_sorted;
     cudaError_t e;
     if ((e = b.alloc(planes, 6 * n)) != cudaSuccess) return e;
@@ -1176,17 +1177,17 @@ static cudaError_t ensemble_order(sg_ctx* ctx, DevBufs& b, const double* d_lo, c
     if ((e = b.alloc(&keys_sorted, n)) != cudaSuccess) return e;
     if ((e = b.alloc(&idx, n)) != cudaSuccess) return e;
     if ((e = b.alloc(&idx_sorted, n)) != cudaSuccess) return e;
-    ens_sample_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(d_lo, d_hi, seed, n, *planes,
+    ens_sample_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(d_lo, d_hi, seed, n, *planes,
                                                                                      keys, idx);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     size_t temp_bytes = 0;
     if ((e = cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, keys_sorted, idx, idx_sorted,
-                                             static_cast<int>(n), 0, 16, ctx->stream)) != cudaSuccess)
+                                             static_cast<int>(n), 0, 16, st)) != cudaSuccess)
         return e;
     unsigned char* temp;
     if ((e = b.alloc(&temp, std::max<size_t>(temp_bytes, 16))) != cudaSuccess) return e;
     if ((e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys_sorted, idx, idx_sorted,
-                                             static_cast<int>(n), 0, 16, ctx->stream)) != cudaSuccess)
+                                             static_cast<int>(n), 0, 16, st)) != cudaSuccess)
         return e;
     ctx->launches += 2;
     *perm = idx_sorted;
@@ -1234,88 +1235,158 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
     return SG_OK;
 }
 
+// The whole C5 pipeline of one window on stream `st` (buffers from `b`,
+// whose allocations and frees are ordered on `st`): ensemble order,
+// evaluation, band selection; bands (7 x n_days) and counts land in device
+// memory.
+static int enqueue_bands(sg_ctx* ctx, sg_window* w, DevBufs& b, cudaStream_t st, const double* d_lo,
+                         const double* d_hi, uint64_t seed, size_t n, int horizon, double* d_cost, double* d_bands,
+                         unsigned long long* d_counts) {
+    const int n_days = horizon + 1;
+    if (n == 0) {
+        bands_kernel<<<n_days, 32, 0, st>>>(nullptr, 0, d_bands, d_counts, n_days);  // k = 0: NaN bands
+        ctx->launches += 1;
+        SG_CUDA(ctx, cudaGetLastError());
+        return SG_OK;
+    }
+    double *d_D, *d_sorted;
+    SG_CUDA(ctx, b.alloc(&d_D, n * n_days));
+    SG_CUDA(ctx, b.alloc(&d_sorted, n * n_days));
+    const DevWindow fwin = integration_window(n_days, w->host.substeps, w->host.N);
+    uint32_t* perm = nullptr;
+    double* planes = nullptr;
+    SG_CUDA(ctx, ensemble_order(ctx, b, d_lo, d_hi, seed, n, &perm, &planes, st));
+    cudaError_t err = cudaSuccess;
+    // day-major columns in evaluation order: the bands only need each day's multiset
+    dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc,
+                             fwin, d_lo, d_hi, seed, n, horizon, d_cost, static_cast<double*>(nullptr), d_D, size_t(1),
+                             n, perm, planes, 1, w->smem, st, &err);
+    ctx->launches += 1;
+    if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
+    // per forecast day: k and the order statistics quantile_sorted reads
+    // (calibration.cpp:17-25, 324-361), by bin selection (kernels.cuh)
+    SelDay* d_days;
+    unsigned int* d_hist;
+    int *d_beg, *d_end;
+    SG_CUDA(ctx, b.alloc(&d_days, n_days));
+    SG_CUDA(ctx, b.alloc(&d_hist, static_cast<size_t>(n_days) * kSelBins));
+    SG_CUDA(ctx, b.alloc(&d_beg, static_cast<size_t>(n_days) * kBandRanks));
+    SG_CUDA(ctx, b.alloc(&d_end, static_cast<size_t>(n_days) * kBandRanks));
+    SG_CUDA(ctx, cudaMemsetAsync(d_hist, 0, sizeof(unsigned int) * n_days * kSelBins, st));
+    const unsigned small = static_cast<unsigned>((n_days + 127) / 128);
+    sel_init_kernel<<<small, 128, 0, st>>>(d_days, n_days);
+    const unsigned chunks = static_cast<unsigned>(std::min<size_t>(64, (n + 4095) / 4096));
+    const dim3 grid(chunks, static_cast<unsigned>(n_days));
+    sel_range_kernel<<<grid, 256, 0, st>>>(d_D, n, d_days);
+    const dim3 hgrid(static_cast<unsigned>(std::min<size_t>(16, (n + 16383) / 16384)), static_cast<unsigned>(n_days));
+    sel_hist_kernel<<<hgrid, 1024, 0, st>>>(d_D, n, d_days, d_hist);
+    sel_locate_kernel<<<static_cast<unsigned>(n_days), 1024, 0, st>>>(d_hist, d_days);
+    sel_gather_kernel<<<grid, 256, 0, st>>>(d_D, n, d_days, d_sorted);
+    const int n_seg = n_days * kBandRanks;
+    sel_segments_kernel<<<static_cast<unsigned>((n_seg + 127) / 128), 128, 0, st>>>(d_days, n, n_days, d_beg, d_end);
+    ctx->launches += 6;
+    SG_CUDA(ctx, cudaGetLastError());
+    size_t temp_bytes = 0;
+    const int n_items = static_cast<int>(n * n_days);
+    SG_CUDA(ctx, cub::DeviceSegmentedSort::SortKeys(nullptr, temp_bytes, d_sorted, d_D, n_items, n_seg, d_beg, d_end,
+                                                     st));
+    unsigned char* d_temp;
+    SG_CUDA(ctx, b.alloc(&d_temp, std::max<size_t>(temp_bytes, 16)));
+    SG_CUDA(ctx, cub::DeviceSegmentedSort::SortKeys(d_temp, temp_bytes, d_sorted, d_D, n_items, n_seg, d_beg, d_end,
+                                                     st));
+    ctx->launches += 1;
+    sel_bands_kernel<<<small, 128, 0, st>>>(d_days, d_D, n, d_bands, d_counts, n_days);
+    ctx->launches += 1;
+    SG_CUDA(ctx, cudaGetLastError());
+    return SG_OK;
+}
+
+static int check_bands_args(sg_ctx* ctx, const double* lower, const double* upper, size_t n, int horizon) {
+    if (horizon < 0) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "horizon must be >= 0");
+    for (int k = 0; k < 6; ++k)
+        if (!std::isfinite(lower[k]) || !std::isfinite(upper[k]) || lower[k] > upper[k])
+            return fail(ctx, SG_ERR_INVALID_ARGUMENT, "pso: bound " + std::to_string(k) + " is invalid");
+    if (n * static_cast<size_t>(horizon + 1) > static_cast<size_t>(INT32_MAX))
+        return fail(ctx, SG_ERR_INVALID_ARGUMENT, "ensemble too large for one device selection (n x days > 2^31)");
+    return SG_OK;
+}
+
 int sg_forecast_ensemble_bands(sg_window* w, const double lower[6], const double upper[6], uint64_t seed, size_t n,
                                int horizon, double* bands, uint64_t* counts, double* costs) {
     if (!w) return SG_ERR_INVALID_ARGUMENT;
     sg_ctx* ctx = w->ctx;
     if (!lower || !upper || !bands || !counts) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null buffer");
-    if (horizon < 0) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "horizon must be >= 0");
-    for (int k = 0; k < 6; ++k)
-        if (!std::isfinite(lower[k]) || !std::isfinite(upper[k]) || lower[k] > upper[k])
-            return fail(ctx, SG_ERR_INVALID_ARGUMENT, "pso: bound " + std::to_string(k) + " is invalid");
+    if (const int rc = check_bands_args(ctx, lower, upper, n, horizon)) return rc;
     const int n_days = horizon + 1;
-    if (n * static_cast<size_t>(n_days) > static_cast<size_t>(INT32_MAX))
-        return fail(ctx, SG_ERR_INVALID_ARGUMENT, "ensemble too large for one device selection (n x days > 2^31)");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     DevBufs b;
     b.st = ctx->stream;
-    double *d_lo, *d_hi, *d_cost = nullptr, *d_D, *d_sorted, *d_bands;
+    double *d_lo, *d_hi, *d_cost = nullptr, *d_bands;
     unsigned long long* d_counts;
     SG_CUDA(ctx, b.alloc(&d_lo, 6));
     SG_CUDA(ctx, b.alloc(&d_hi, 6));
-    if (costs) SG_CUDA(ctx, b.alloc(&d_cost, n));
-    SG_CUDA(ctx, b.alloc(&d_D, n * n_days));
-    SG_CUDA(ctx, b.alloc(&d_sorted, n * n_days));
+    if (costs && n) SG_CUDA(ctx, b.alloc(&d_cost, n));
     SG_CUDA(ctx, b.alloc(&d_bands, 7 * static_cast<size_t>(n_days)));
     SG_CUDA(ctx, b.alloc(&d_counts, n_days));
     SG_CUDA(ctx, cudaMemcpyAsync(d_lo, lower, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     SG_CUDA(ctx, cudaMemcpyAsync(d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    if (n > 0) {
-        const DevWindow fwin = integration_window(n_days, w->host.substeps, w->host.N);
-        uint32_t* perm = nullptr;
-        double* planes = nullptr;
-        SG_CUDA(ctx, ensemble_order(ctx, b, d_lo, d_hi, seed, n, &perm, &planes));
-        cudaError_t err = cudaSuccess;
-        // day-major columns in evaluation order: the bands only need each day's multiset
-        dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps),
-                                 w->d_desc, fwin, d_lo, d_hi, seed, n, horizon, d_cost, static_cast<double*>(nullptr),
-                                 d_D, size_t(1), n, perm, planes, 1, w->smem, ctx->stream, &err);
-        ctx->launches += 1;
-        if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
-        // per forecast day: k and the order statistics quantile_sorted reads
-        // (calibration.cpp:17-25, 324-361), by bin selection (kernels.cuh)
-        SelDay* d_days;
-        unsigned int* d_hist;
-        int *d_beg, *d_end;
-        SG_CUDA(ctx, b.alloc(&d_days, n_days));
-        SG_CUDA(ctx, b.alloc(&d_hist, static_cast<size_t>(n_days) * kSelBins));
-        SG_CUDA(ctx, b.alloc(&d_beg, static_cast<size_t>(n_days) * kBandRanks));
-        SG_CUDA(ctx, b.alloc(&d_end, static_cast<size_t>(n_days) * kBandRanks));
-        SG_CUDA(ctx, cudaMemsetAsync(d_hist, 0, sizeof(unsigned int) * n_days * kSelBins, ctx->stream));
-        const unsigned small = static_cast<unsigned>((n_days + 127) / 128);
-        sel_init_kernel<<<small, 128, 0, ctx->stream>>>(d_days, n_days);
-        const unsigned chunks = static_cast<unsigned>(std::min<size_t>(64, (n + 4095) / 4096));
-        const dim3 grid(chunks, static_cast<unsigned>(n_days));
-        sel_range_kernel<<<grid, 256, 0, ctx->stream>>>(d_D, n, d_days);
-        const dim3 hgrid(static_cast<unsigned>(std::min<size_t>(16, (n + 16383) / 16384)), static_cast<unsigned>(n_days));
-        sel_hist_kernel<<<hgrid, 1024, 0, ctx->stream>>>(d_D, n, d_days, d_hist);
-        sel_locate_kernel<<<static_cast<unsigned>(n_days), 1024, 0, ctx->stream>>>(d_hist, d_days);
-        sel_gather_kernel<<<grid, 256, 0, ctx->stream>>>(d_D, n, d_days, d_sorted);
-        const int n_seg = n_days * kBandRanks;
-        sel_segments_kernel<<<static_cast<unsigned>((n_seg + 127) / 128), 128, 0, ctx->stream>>>(d_days, n, n_days,
-                                                                                            d_beg, d_end);
-        ctx->launches += 6;
-        SG_CUDA(ctx, cudaGetLastError());
-        size_t temp_bytes = 0;
-        const int n_items = static_cast<int>(n * n_days);
-        SG_CUDA(ctx, cub::DeviceSegmentedSort::SortKeys(nullptr, temp_bytes, d_sorted, d_D, n_items, n_seg, d_beg,
-                                                         d_end, ctx->stream));
-        unsigned char* d_temp;
-        SG_CUDA(ctx, b.alloc(&d_temp, std::max<size_t>(temp_bytes, 16)));
-        SG_CUDA(ctx, cub::DeviceSegmentedSort::SortKeys(d_temp, temp_bytes, d_sorted, d_D, n_items, n_seg, d_beg,
-                                                         d_end, ctx->stream));
-        ctx->launches += 1;
-        sel_bands_kernel<<<small, 128, 0, ctx->stream>>>(d_days, d_D, n, d_bands, d_counts, n_days);
-        ctx->launches += 1;
-    } else {
-        bands_kernel<<<n_days, 32, 0, ctx->stream>>>(d_sorted, 0, d_bands, d_counts, n_days);  // k = 0: NaN bands
-        ctx->launches += 1;
-    }
-    SG_CUDA(ctx, cudaGetLastError());
+    if (const int rc = enqueue_bands(ctx, w, b, ctx->stream, d_lo, d_hi, seed, n, horizon, d_cost, d_bands, d_counts))
+        return rc;
     static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "count width");
     SG_CUDA(ctx, cudaMemcpyAsync(bands, d_bands, 7 * n_days * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     SG_CUDA(ctx, cudaMemcpyAsync(counts, d_counts, n_days * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
-    if (costs) SG_CUDA(ctx, cudaMemcpyAsync(costs, d_cost, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (costs && n)
+        SG_CUDA(ctx, cudaMemcpyAsync(costs, d_cost, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SG_OK;
+}
+
+int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows, const double lower[6],
+                                     const double upper[6], const uint64_t* seeds, size_t n, int horizon,
+                                     double* bands, uint64_t* counts) {
+    if (!windows || n_windows == 0) return n_windows == 0 ? SG_OK : SG_ERR_INVALID_ARGUMENT;
+    if (!windows[0]) return SG_ERR_INVALID_ARGUMENT;
+    sg_ctx* ctx = windows[0]->ctx;
+    if (!lower || !upper || !seeds || !bands || !counts) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null buffer");
+    for (size_t k = 0; k < n_windows; ++k)
+        if (!windows[k] || windows[k]->ctx != ctx)
+            return fail(ctx, SG_ERR_INVALID_ARGUMENT, "windows must be non-null and share one context");
+    if (const int rc = check_bands_args(ctx, lower, upper, n, horizon)) return rc;
+    const int n_days = horizon + 1;
+    SG_CUDA(ctx, cudaSetDevice(ctx->device));
+    if (const int rc = ensure_lanes(ctx)) return rc;
+    DevBufs b;
+    b.st = ctx->stream;
+    double *d_lo, *d_hi, *d_bands;
+    unsigned long long* d_counts;
+    SG_CUDA(ctx, b.alloc(&d_lo, 6));
+    SG_CUDA(ctx, b.alloc(&d_hi, 6));
+    SG_CUDA(ctx, b.alloc(&d_bands, 7 * static_cast<size_t>(n_days) * n_windows));
+    SG_CUDA(ctx, b.alloc(&d_counts, static_cast<size_t>(n_days) * n_windows));
+    SG_CUDA(ctx, cudaMemcpyAsync(d_lo, lower, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, cudaMemcpyAsync(d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    // Windows alternate between two side streams, so one window's band
+    // selection (small kernels) overlaps the next window's evaluation.
+    constexpr int kBandStreams = 2;
+    SG_CUDA(ctx, cudaEventRecord(ctx->fork, ctx->stream));
+    for (int l = 0; l < kBandStreams; ++l) SG_CUDA(ctx, cudaStreamWaitEvent(ctx->side[l], ctx->fork, 0));
+    for (size_t k = 0; k < n_windows; ++k) {
+        cudaStream_t st = ctx->side[k % kBandStreams];
+        DevBufs wb;  // per-window scratch, freed in stream order on st
+        wb.st = st;
+        const int rc = enqueue_bands(ctx, windows[k], wb, st, d_lo, d_hi, seeds[k], n, horizon, nullptr,
+                                     d_bands + 7 * static_cast<size_t>(n_days) * k,
+                                     d_counts + static_cast<size_t>(n_days) * k);
+        if (rc) return rc;
+    }
+    for (int l = 0; l < kBandStreams; ++l) {
+        SG_CUDA(ctx, cudaEventRecord(ctx->join[l], ctx->side[l]));
+        SG_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join[l], 0));
+    }
+    SG_CUDA(ctx, cudaMemcpyAsync(bands, d_bands, 7 * n_days * n_windows * sizeof(double), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    SG_CUDA(ctx, cudaMemcpyAsync(counts, d_counts, n_days * n_windows * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                 ctx->stream));
     SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SG_OK;
 }

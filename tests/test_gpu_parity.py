@@ -297,3 +297,20 @@ def test_ensemble_band_selection_equals_full_sort(ctx, poland, case):
     want, want_counts = _host_bands(deaths)
     assert counts.tolist() == want_counts
     assert_bitwise(bands.ravel(), want.ravel(), case)
+
+
+def test_ensemble_bands_batch_equals_per_window_calls(ctx, poland):
+    """The pipelined many-window call gives each window exactly its
+    single-window bands."""
+    import paper_2204_12346_b200 as eng
+    N = poland["N"]
+    wins = []
+    for a in (0, 33, 66, 99, 132):
+        I, R, D = poland["I"][a:a + 36], poland["R"][a:a + 36], poland["D"][a:a + 36]
+        wins.append(eng.Window(ctx, I, R, D, [N - I[0] - R[0] - D[0], I[0], R[0], D[0]], N, "ird-mxse"))
+    lo, hi, seeds = [0.0] * 6, [2.0, 2.0, 28.0, 28.0, 1.0, 0.1], [11, 12, 13, 14, 15]
+    bands, counts = ctx.forecast_ensemble_bands_batch(wins, lo, hi, seeds, 50_000, 21)
+    for k, w in enumerate(wins):
+        b1, c1, _ = w.forecast_ensemble_bands(lo, hi, seeds[k], 50_000, 21)
+        assert counts[k].tolist() == c1.tolist()
+        assert_bitwise(bands[k].ravel(), b1.ravel(), f"window {k}")

@@ -123,19 +123,31 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stream = torch.cuda.ExternalStream(ctx.stream)
     wins[0].forecast_ensemble_bands([0] * 6, stage2(35), seed=1, n=n, horizon=21)  # warm
+    seeds = [bench.mix_seed(2204, w) for w in range(args.c5_windows)]
     t0 = time.perf_counter()
     with torch.cuda.stream(stream):
         e0.record(stream)
         for w in range(args.c5_windows):
-            bands, counts, _ = wins[w].forecast_ensemble_bands([0] * 6, stage2(35), seed=bench.mix_seed(2204, w), n=n,
-                                                               horizon=21)
+            bands, counts, _ = wins[w].forecast_ensemble_bands([0] * 6, stage2(35), seed=seeds[w], n=n, horizon=21)
+        e1.record(stream)
+    e1.synchronize()
+    wall_single = time.perf_counter() - t0
+    single_ms = e0.elapsed_time(e1)
+    # the same work through the pipelined many-window call
+    t0 = time.perf_counter()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        all_bands, all_counts = ctx.forecast_ensemble_bands_batch(wins[:args.c5_windows], [0] * 6, stage2(35), seeds,
+                                                                  n, 21)
         e1.record(stream)
     e1.synchronize()
     wall = time.perf_counter() - t0
     dev_ms = e0.elapsed_time(e1)
+    assert np.array_equal(all_bands[-1], bands, equal_nan=True)
     ops = (35 * 24 * 14 + 21 * 24 * 14)  # window + forecast substeps per sample, no ramp credit
     print(json.dumps({"config": "C5", "windows": args.c5_windows, "samples_per_window": n, "horizon": 21,
-                      "device_ms": dev_ms, "wall_ms": wall * 1e3,
+                      "device_ms": dev_ms, "wall_ms": wall * 1e3, "per_window_calls_device_ms": single_ms,
+                      "per_window_calls_wall_ms": wall_single * 1e3,
                       "samples_per_s": args.c5_windows * n / (dev_ms * 1e-3),
                       "fp64_frac_floor": args.c5_windows * n * ops / (dev_ms * 1e-3) / peak,
                       "last_window_day21_median_deaths": float(bands[0, -1]), "finite_last": int(counts[-1])}),
