@@ -34,3 +34,23 @@ def merge_by_index(parts: list[list[tuple[int, object]]]) -> list[object]:
     if idx != list(range(len(idx))):
         raise ValueError("shards do not cover the units exactly once")
     return [v for _, v in flat]
+
+
+def run_sharded(n_units: int, compute, group=None, dst: int = 0):
+    """Run `n_units` independent units across the ranks of a torch.distributed
+    process group (one process per GPU) and merge the results in unit order
+    on rank `dst` (None elsewhere).  `compute(indices)` evaluates one rank's
+    contiguous share in one call — e.g. one engine plan holding all of the
+    rank's swarms — and returns one picklable result per index.  The only
+    collective is the final gather of the (small) results: nothing crosses
+    GPUs on the compute path.  Without an initialised process group this is
+    a single-process run."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return compute(list(range(n_units)))
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    mine = list(partition(n_units, world, rank))
+    part = list(zip(mine, compute(mine))) if mine else []
+    parts = [None] * world if rank == dst else None
+    dist.gather_object(part, parts, dst=dst, group=group)
+    return merge_by_index(parts) if rank == dst else None

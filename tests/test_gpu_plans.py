@@ -117,3 +117,26 @@ def test_two_level_fold_for_large_swarms(ctx, port, poland):
     _check(port, swarms, data, plan.results())
     plan.run()  # group counters are reset by their last warp: a rerun must match again
     _check(port, swarms, data, plan.results())
+
+
+def test_sharded_stability_study_matches_single_process(tmp_path):
+    """tools/shard_c4.py under torchrun, two ranks sharing the one GPU
+    (gloo): the merged shards equal the single-process run bit for bit."""
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), str(root / "tools" / "shard_c4.py"), "--windows", "12",
+           "--restarts", "3", "--iters", "15", "--backend", "gloo", "--check"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1]
+    import json
+    d = json.loads(line)
+    assert d["ranks"] == 2 and d["units"] == 36 and d["identical_to_single_process"] is True

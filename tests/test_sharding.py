@@ -58,16 +58,14 @@ def _worker(rank, world, port, series, out_q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     units = sharding.units(6, 2)
-    mine = [(i, _unit_result(w, r, series)) for i in sharding.partition(len(units), world, rank)
-            for (w, r) in [units[i]]]
-    gathered = [None] * world
-    dist.all_gather_object(gathered, mine)
+    # the library's runner: each rank computes its contiguous share in one call
+    merged = sharding.run_sharded(len(units), lambda idx: [_unit_result(*units[i], series) for i in idx])
     # max-over-ranks timing reduction, as bench.py does over NCCL
     import torch
     t = torch.tensor([float(rank + 1)])
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     if rank == 0:
-        out_q.put((sharding.merge_by_index(gathered), float(t.item())))
+        out_q.put((merged, float(t.item())))
     dist.destroy_process_group()
 
 
