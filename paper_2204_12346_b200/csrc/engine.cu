@@ -686,8 +686,9 @@ struct SwarmGroup {
     PsoPlanes P{};
     DevBufs bufs;
     // The flat step launches of a run (all lanes, all iterations) as one
-    // CUDA graph, captured at the second run of the plan (a plan run once —
-    // every calibration call — never pays the instantiation).
+    // CUDA graph, captured at the third run of the plan: instantiating a
+    // 4000-node graph costs tens of ms, so plans run once or twice (every
+    // calibration call, timing loops with one warm-up) never pay it.
     int runs = 0;
     cudaGraphExec_t steps_exec = nullptr;
     ~SwarmGroup() {
@@ -861,7 +862,7 @@ bool graphs_enabled() {
 }
 
 int step_group(sg_ctx* ctx, SwarmGroup& g) {
-    if (!g.persistent && graphs_enabled() && g.runs++ >= 1) {
+    if (!g.persistent && graphs_enabled() && g.runs++ >= 2) {
         if (!g.steps_exec) {
             const int rc0 = g.lanes.size() > 1 ? ensure_lanes(ctx) : SG_OK;
             if (rc0) return rc0;

@@ -89,16 +89,17 @@ def test_plan_reruns_are_identical(ctx, poland):
               for k, w in enumerate(wins)]
     plan = eng.Plan(ctx, swarms)
     assert plan.step_launches > 1  # flat per-iteration kernels
-    plan.run()
-    a = plan.results()
-    plan.run()
-    b = plan.results()
+    runs = []
+    for _ in range(4):  # the third run captures the CUDA graph, the fourth replays it
+        plan.run()
+        runs.append(plan.results())
     c = ctx.fit_swarms(swarms)
-    for x, y, z in zip(a, b, c):
-        assert x[0] == y[0] == z[0] == 0
-        assert_bitwise(x[3], y[3], "rerun history")
-        assert_bitwise(x[3], z[3], "fresh plan history")
-        assert_bitwise(x[1], z[1], "fresh plan best")
+    for k, z in enumerate(c):
+        assert z[0] == 0
+        for r in runs:
+            assert r[k][0] == 0
+            assert_bitwise(r[k][3], z[3], "rerun history")
+            assert_bitwise(r[k][1], z[1], "rerun best")
 
 
 def test_two_level_fold_for_large_swarms(ctx, port, poland):
