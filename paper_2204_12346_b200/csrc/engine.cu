@@ -229,6 +229,7 @@ int launch_integrate(sg_ctx* ctx, const DevWindow& w, const double* d_params, co
     const unsigned grid = static_cast<unsigned>((n + kEvalThreads - 1) / kEvalThreads);
     const size_t smem = static_cast<size_t>(w.substeps + tgrid_entries(w.n_days, w.substeps)) * sizeof(double);
     if (uses_fast_grid(w.n_days, w.substeps)) {
+        SG_CUDA(ctx, prepare_smem(integrate_kernel<24>, smem));
         integrate_kernel<24><<<grid, kEvalThreads, smem, ctx->stream>>>(w, d_params, d_init, init_stride, hold, n,
                                                                         d_states, d_fin);
     } else {

@@ -47,11 +47,28 @@ __host__ __device__ inline int tgrid_entries(int n_days, int substeps) {
     return uses_fast_grid(n_days, substeps) ? (n_days - 1) * substeps : 0;
 }
 
+// Shared-memory image of a window (dynamic segment, every section 16-byte
+// aligned and padded): subh[substeps] + tgrid | obs | robs | flags (MAPE).
+// The device block of a window (sg_window_create) uses the same section
+// sizes from its times table on, so the step kernel stages it with one bulk
+// copy per section.
+struct WindowLayout {
+    size_t times_bytes, obs_bytes, obs, robs, flag, total;
+};
+
+__host__ __device__ inline WindowLayout window_layout(int n_days, int substeps, int metric) {
+    WindowLayout L;
+    L.times_bytes = (static_cast<size_t>(substeps + tgrid_entries(n_days, substeps)) * sizeof(double) + 15) & ~size_t(15);
+    L.obs_bytes = (static_cast<size_t>(n_days) * sizeof(ObsDay) + 15) & ~size_t(15);
+    L.obs = L.times_bytes;
+    L.robs = L.obs + L.obs_bytes;
+    L.flag = L.robs + L.obs_bytes;
+    L.total = metric == kMetMAPE ? L.flag + ((3 * static_cast<size_t>(n_days) + 15) & ~size_t(15)) : L.robs;
+    return L;
+}
+
 __host__ __device__ inline size_t smem_window_bytes(int n_days, int substeps, int metric) {
-    size_t b = static_cast<size_t>(n_days) * sizeof(ObsDay) +
-               static_cast<size_t>(substeps + tgrid_entries(n_days, substeps)) * sizeof(double);
-    if (metric == kMetMAPE) b += static_cast<size_t>(n_days) * (sizeof(ObsDay) + 3);
-    return (b + 15) & ~size_t(15);
+    return window_layout(n_days, substeps, metric).total;
 }
 
 // Fill subh[sub] = RN(sub*h) and, when it fits, tgrid[k] = RN(RN(day-1) +
@@ -69,37 +86,18 @@ __device__ __forceinline__ TimeGrid stage_times(double* base, int n_days, int ns
 }
 
 // Cooperative copy of a window into shared memory (all threads call; ends
-// with a barrier).  The specialised kernels (SUB > 0, windows of at most
-// kFastDays days) use static shared arrays, so every per-day observation
-// read is an LDS with an immediate base; the generic kernels use the
-// dynamic segment.
-constexpr int kFastDays = kMaxTgrid / 24 + 1;  // 86: uses_fast_grid() bound
-
+// with a barrier), in the WindowLayout of the dynamic segment.
 template <int MET, int SUB>
 __device__ __forceinline__ SmemWindow stage_window(const DevWindow* __restrict__ gw, DevWindow* sdesc,
                                                    unsigned char* smem) {
     if (threadIdx.x == 0) *sdesc = *gw;
     const int n = gw->n_days;
     const int ns = gw->substeps;
-    ObsDay* obs;
-    double* times;
-    ObsDay* robs;
-    unsigned char* flag;
-    if constexpr (SUB > 0) {
-        __shared__ ObsDay s_obs[kFastDays];
-        __shared__ __align__(16) double s_times[24 + kMaxTgrid];
-        __shared__ ObsDay s_robs[MET == kMetMAPE ? kFastDays : 1];
-        __shared__ unsigned char s_flag[MET == kMetMAPE ? 3 * kFastDays : 1];
-        obs = s_obs;
-        times = s_times;
-        robs = s_robs;
-        flag = s_flag;
-    } else {
-        obs = reinterpret_cast<ObsDay*>(smem);
-        times = reinterpret_cast<double*>(obs + n);
-        robs = reinterpret_cast<ObsDay*>(times + ns + tgrid_entries(n, ns));
-        flag = reinterpret_cast<unsigned char*>(robs + (MET == kMetMAPE ? n : 0));
-    }
+    const WindowLayout L = window_layout(n, ns, MET);
+    double* times = reinterpret_cast<double*>(smem);
+    ObsDay* obs = reinterpret_cast<ObsDay*>(smem + L.obs);
+    ObsDay* robs = reinterpret_cast<ObsDay*>(smem + L.robs);
+    unsigned char* flag = smem + L.flag;
     const double* src = reinterpret_cast<const double*>(gw->obs);
     double* dst = reinterpret_cast<double*>(obs);
     for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) dst[i] = src[i];
@@ -107,14 +105,10 @@ __device__ __forceinline__ SmemWindow stage_window(const DevWindow* __restrict__
     if (gw->times) {
         // Copy the host-built table (16-byte vectors; both ends 16-aligned).
         const int m = ns + tgrid_entries(n, ns);
-        if constexpr (SUB > 0) {  // static smem table: 16-byte aligned
-            const double2* s2 = reinterpret_cast<const double2*>(gw->times);
-            double2* d2 = reinterpret_cast<double2*>(times);
-            for (int i = threadIdx.x; i < (m >> 1); i += blockDim.x) d2[i] = __ldg(s2 + i);
-            if ((m & 1) && threadIdx.x == 0) times[m - 1] = gw->times[m - 1];
-        } else {
-            for (int i = threadIdx.x; i < m; i += blockDim.x) times[i] = __ldg(gw->times + i);
-        }
+        const double2* s2 = reinterpret_cast<const double2*>(gw->times);
+        double2* d2 = reinterpret_cast<double2*>(times);
+        for (int i = threadIdx.x; i < (m >> 1); i += blockDim.x) d2[i] = __ldg(s2 + i);
+        if ((m & 1) && threadIdx.x == 0) times[m - 1] = gw->times[m - 1];
         tg = TimeGrid{m > ns ? times + ns : nullptr, times};
     } else {
         tg = stage_times(times, n, ns, gw->h);
@@ -131,7 +125,8 @@ __device__ __forceinline__ SmemWindow stage_window(const DevWindow* __restrict__
 
 // Dynamic shared memory a kernel specialisation needs for a window.
 __host__ __device__ inline size_t kernel_smem_bytes(int n_days, int substeps, int metric, bool fast) {
-    return fast ? 0 : smem_window_bytes(n_days, substeps, metric);
+    (void)fast;
+    return smem_window_bytes(n_days, substeps, metric);
 }
 
 // ---- boundary 1 -------------------------------------------------------------
@@ -568,16 +563,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // shared arrays): thread 0 arms the barrier and issues the bulk copies; the
 // caller overlaps them with the particle moves and waits with mbar_wait.
 template <int MET>
-__device__ __forceinline__ SmemWindow stage_window_async(const CtaTask& t, DevWindow* sdesc, uint64_t* bar) {
-    __shared__ __align__(16) ObsDay s_obs[kFastDays];
-    __shared__ __align__(16) double s_times[24 + kMaxTgrid];
-    __shared__ __align__(16) ObsDay s_robs[MET == kMetMAPE ? kFastDays : 1];
-    __shared__ __align__(16) unsigned char s_flag[MET == kMetMAPE ? (3 * kFastDays + 15) / 16 * 16 : 16];
+__device__ __forceinline__ SmemWindow stage_window_async(const CtaTask& t, DevWindow* sdesc, uint64_t* bar,
+                                                         unsigned char* smem) {
+    // WindowLayout: times | obs | robs | flags, the section sizes in the task
+    double* s_times = reinterpret_cast<double*>(smem);
+    ObsDay* s_obs = reinterpret_cast<ObsDay*>(smem + t.times_bytes);
+    ObsDay* s_robs = reinterpret_cast<ObsDay*>(smem + t.times_bytes + t.obs_bytes);
+    unsigned char* s_flag = smem + t.times_bytes + 2 * t.obs_bytes;
     if (threadIdx.x == 0) {
         const uint32_t b = smem_u32(bar);
         mbar_init(b, 1);
-        const uint32_t flag_bytes = MET == kMetMAPE ? (3u * (t.obs_bytes / 24u) + 15u) & ~15u : 0u;
         // obs_bytes = round16(24 n) is the obs and the robs section size
+        const uint32_t flag_bytes = MET == kMetMAPE ? (3u * (t.obs_bytes / 24u) + 15u) & ~15u : 0u;
         const uint32_t n_days_bytes = t.obs_bytes;
         mbar_expect_tx(b, static_cast<uint32_t>(sizeof(DevWindow)) + t.times_bytes + n_days_bytes +
                               (MET == kMetMAPE ? n_days_bytes + flag_bytes : 0u));
@@ -610,7 +607,7 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
     if (it >= task.max_iters) return;  // CTA-uniform
     constexpr bool kAsync = SUB > 0 && SG_TMA_STAGE;
     SmemWindow win;
-    if constexpr (kAsync) win = stage_window_async<MET>(task, &sdesc, &bar);
+    if constexpr (kAsync) win = stage_window_async<MET>(task, &sdesc, &bar, smem);
     else win = stage_window<MET, SUB>(task.win, &sdesc, smem);
     const int s = static_cast<int>(task.swarm);
     const DevSwarm& sw = swarms[s];

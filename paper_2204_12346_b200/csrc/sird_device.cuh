@@ -251,9 +251,10 @@ struct TimeGrid {
     const double* subh;   // substeps entries: RN(sub*h)
 };
 
-// Largest t_k table kept in shared memory (entries, 16 KB): windows up to 86
-// days at 24 substeps take the specialised path.
-constexpr int kMaxTgrid = 2048;
+// Largest t_k table kept in shared memory (entries, 37.5 KB): windows up to
+// 201 days at 24 substeps take the specialised path (5 CTAs of the step
+// kernel still fit in shared memory with the observations).
+constexpr int kMaxTgrid = 4800;
 
 __host__ __device__ inline bool uses_fast_grid(int n_days, int substeps) {
     return substeps == 24 && static_cast<long long>(n_days - 1) * substeps <= kMaxTgrid;

@@ -49,6 +49,7 @@ def test_mixed_plan_matches_oracle(ctx, port, poland):
         (0, 8, "ird-mxse", 24, 300, 17), (30, 36, "d-mse", 24, 1500, 9), (90, 100, "ird-mae", 24, 257, 6),
         (120, 21, "ird-mape", 7, 640, 12), (200, 36, "d-mxse", 1, 129, 25), (260, 15, "d-mae", 24, 33, 40),
         (300, 36, "ird-mse", 24, 2048, 5), (400, 30, "d-mape", 24, 700, 11),
+        (150, 230, "ird-mxse", 24, 300, 4),  # past the 201-day time table: the generic kernels
     ]
     swarms, data, keep = [], [], []
     for k, (a, n, spec, sub, n_p, iters) in enumerate(cases):

@@ -1,0 +1,30 @@
+"""Throughput vs window length (tau): 40 windows x 4096 particles x 100 iterations, ird-mxse, stage2 box."""
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import bench  # noqa: E402
+import paper_2204_12346_b200 as eng  # noqa: E402
+from tools.bench_configs import stage2, window  # noqa: E402
+
+
+def main():
+    ctx = eng.Context(0)
+    peak = eng.probe_fp64_rate(ctx)
+    for tau in [int(x) for x in sys.argv[1:]] or [20, 35, 60, 85, 86, 100, 150, 200]:
+        n_win = min(40, (450 - tau - 1) // bench.DELTA)
+        wins = [window(ctx, w, tau) for w in range(n_win)]
+        swarms = [dict(window=wins[w], lower=[0] * 6, upper=stage2(tau), n_particles=4096, max_iters=100,
+                       seed=bench.mix_seed(5, w)) for w in range(n_win)]
+        plan = eng.Plan(ctx, swarms)
+        plan.run_timed()
+        s, k = plan.run_timed()
+        ops = plan.evals * bench.ops_per_eval(tau + 1) + bench.RAMP_OPS * plan.ramp_substeps
+        print(f"tau={tau:4d} days={tau + 1:4d} evals/s={plan.evals / (s + k) * 1e3:.3e} frac={ops / ((s + k) * 1e-3) / peak:.3f}",
+              flush=True)
+        plan.close()
+
+
+if __name__ == "__main__":
+    main()
