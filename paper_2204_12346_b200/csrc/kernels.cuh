@@ -2,16 +2,22 @@
 //
 //   eval_costs_kernel     boundary 1: BatchObjective body (calibration.cpp:140-154)
 //   integrate_kernel      integrate_batch / forecast_extension trajectories
+//   r2_kernel             fit_window's R^2(D) of the re-integrated fits
 //   pso_init_kernel       Swarm::Swarm (pso.cpp:47-75) for many swarms
 //   pso_step_kernel       Swarm::step (pso.cpp:77-101) fused: move -> evaluate ->
-//                         personal best -> block argmin -> last-block global best
-//   ensemble_kernel       forecast-scenario ensemble (sample, score, forecast)
+//                         personal best -> warp argmin -> last-warp global best
+//                         (two-level for swarms over 32 CTAs)
+//   pso_swarm_kernel      whole optimize() of small swarms, one thread-block
+//                         cluster per swarm (global best through DSMEM)
+//   ens_sample_kernel,    forecast-scenario ensemble (sample in ramp-coherent
+//   ensemble_kernel       order, score, forecast)
+//   sel_*_kernel          quantile bands by order-statistic selection
 //
-// Layout in HBM: particle state is structure-of-arrays (six planes of n
-// doubles for positions, velocities and personal bests; 312 planes for the
-// MT19937-64 engines), so each warp's loads and stores are 256 B coalesced
-// segments.  Observed windows (3 doubles per day) are staged in shared
-// memory once per CTA and read as broadcasts.
+// Layout in HBM: particle state in particle blocks (32 particles x fields,
+// so each warp's access to a field is one 256 B segment and a particle's
+// fields sit at immediate offsets; the MT19937-64 engines the same with 312
+// words).  Windows are staged in shared memory per CTA (bulk async copies in
+// the step kernel) and read as broadcasts; trajectories stay in registers.
 #pragma once
 
 #include "sird_device.cuh"
@@ -34,7 +40,8 @@ constexpr int kNP = 1;  // particles per thread in the flat step kernel (2, inte
 constexpr int kStepWarps = kStepThreads / 32;
 
 // Shared-memory staging of one window: the descriptor in static shared memory,
-// obs, the substep-time tables (+ robs + flags for MAPE) in the dynamic segment.
+// the substep-time tables, obs (+ robs + flags for MAPE) in the dynamic
+// segment (WindowLayout).
 struct SmemWindow {
     const DevWindow* w;  // shared memory
     const ObsDay* obs;
