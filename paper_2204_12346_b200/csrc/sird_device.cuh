@@ -5,9 +5,10 @@
 // code contains no FMA, SURVEY.md §0 key finding 2).  The file is compiled
 // with -fmad=false and additionally spells every rounded operation with an
 // explicit __dmul_rn/__dadd_rn/__dsub_rn intrinsic, so no contraction can
-// ever be introduced.  The only fma() uses are the exact-division sequence
-// in div_exact(), whose result is proven equal to the correctly rounded
-// quotient.
+// ever be introduced.  The only fma() uses are the exact-division sequences
+// div_exact() (3 ops) and div_by_N() (2 ops), whose results are proven equal
+// to the correctly rounded quotient for the inputs that reach them
+// (DESIGN.md §4).
 #pragma once
 
 #include <cstdint>
