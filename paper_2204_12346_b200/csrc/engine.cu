@@ -907,23 +907,23 @@ int enqueue_steps(sg_ctx* ctx, SwarmGroup& g) {
         SG_CUDA(ctx, cudaEventRecord(ctx->fork, ctx->stream));
         for (size_t l = 0; l < n_lanes; ++l) SG_CUDA(ctx, cudaStreamWaitEvent(ctx->side[l], ctx->fork, 0));
     }
-    for (uint64_t it = 0; it < g.iters; ++it) {
-        for (size_t l = 0; l < n_lanes; ++l) {
+    cudaError_t err = cudaSuccess;
+    for (uint64_t it = 0; it < g.iters && err == cudaSuccess; ++it) {
+        for (size_t l = 0; l < n_lanes && err == cudaSuccess; ++l) {
             const SwarmGroup::Lane& ln = g.lanes[l];
             cudaStream_t st = n_lanes > 1 ? ctx->side[l] : ctx->stream;
-            cudaError_t err = cudaSuccess;
             dispatch<StepLaunch>(g.family, g.metric, g.substeps, ln.n_ctas, ln.cta_begin, g.d_task, g.d_sw, g.P,
                                  g.d_state, it, g.smem, st, &err);
             ctx->launches += 1;
-            if (err != cudaSuccess) return cuda_fail(ctx, err, "pso_step_kernel");
         }
     }
-    if (n_lanes > 1) {
+    if (n_lanes > 1) {  // join the lanes even after a failed launch (capture and buffer order need it)
         for (size_t l = 0; l < n_lanes; ++l) {
             SG_CUDA(ctx, cudaEventRecord(ctx->join[l], ctx->side[l]));
             SG_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join[l], 0));
         }
     }
+    if (err != cudaSuccess) return cuda_fail(ctx, err, "pso_step_kernel");
     return SG_OK;
 }
 
@@ -1371,19 +1371,21 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
     constexpr int kBandStreams = 2;
     SG_CUDA(ctx, cudaEventRecord(ctx->fork, ctx->stream));
     for (int l = 0; l < kBandStreams; ++l) SG_CUDA(ctx, cudaStreamWaitEvent(ctx->side[l], ctx->fork, 0));
-    for (size_t k = 0; k < n_windows; ++k) {
+    int rc = SG_OK;
+    for (size_t k = 0; k < n_windows && !rc; ++k) {
         cudaStream_t st = ctx->side[k % kBandStreams];
         DevBufs wb;  // per-window scratch, freed in stream order on st
         wb.st = st;
-        const int rc = enqueue_bands(ctx, windows[k], wb, st, d_lo, d_hi, seeds[k], n, horizon, nullptr,
-                                     d_bands + 7 * static_cast<size_t>(n_days) * k,
-                                     d_counts + static_cast<size_t>(n_days) * k);
-        if (rc) return rc;
+        rc = enqueue_bands(ctx, windows[k], wb, st, d_lo, d_hi, seeds[k], n, horizon, nullptr,
+                           d_bands + 7 * static_cast<size_t>(n_days) * k, d_counts + static_cast<size_t>(n_days) * k);
     }
+    // join the side streams even after a failure: the shared buffers are
+    // released in ctx->stream order
     for (int l = 0; l < kBandStreams; ++l) {
         SG_CUDA(ctx, cudaEventRecord(ctx->join[l], ctx->side[l]));
         SG_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join[l], 0));
     }
+    if (rc) return rc;
     SG_CUDA(ctx, cudaMemcpyAsync(bands, d_bands, 7 * n_days * n_windows * sizeof(double), cudaMemcpyDeviceToHost,
                                  ctx->stream));
     SG_CUDA(ctx, cudaMemcpyAsync(counts, d_counts, n_days * n_windows * sizeof(uint64_t), cudaMemcpyDeviceToHost,
