@@ -197,7 +197,7 @@ def load_profile_traffic():
     """DRAM bytes and executed FP64 ops per particle-iteration of the step
     kernel from the committed ncu --set full summary
     (profiles/ncu_step_kernel_*.json), if any."""
-    for p in sorted((ROOT / "profiles").glob("ncu_step_kernel_*.json"), reverse=True):
+    for p in sorted((ROOT / "profiles").glob("ncu_step_kernel_r*.json"), reverse=True):
         try:
             d = json.loads(p.read_text())
             return d.get("dram_bytes_per_particle"), p.name, d.get("fp64_ops_per_particle_executed")
