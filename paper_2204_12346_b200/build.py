@@ -11,21 +11,29 @@ travels to the GPU box as one file.
 from __future__ import annotations
 
 import os
+import shutil
 import subprocess
 import sys
+import tempfile
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-SOURCES = [CSRC / "engine.cu", CSRC / "host_api.cpp"]
-HEADERS = [CSRC / "sird_device.cuh", CSRC / "kernels.cuh", CSRC / "engine_internal.h", ROOT / "include" / "sirdgpu.h",
-           ROOT / "include" / "sirdfit_b200.hpp"]
+SOURCES = [CSRC / "engine.cu", CSRC / "family.cu", CSRC / "cub_sorts.cu", CSRC / "host_api.cpp"]
+HEADERS = [CSRC / "sird_device.cuh", CSRC / "kernels.cuh", CSRC / "launchers.cuh", CSRC / "engine_internal.h",
+           ROOT / "include" / "sirdgpu.h", ROOT / "include" / "sirdfit_b200.hpp"]
 OUT = PKG / "libsirdgpu.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++20", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
-         "-shared", f"-I{ROOT / 'include'}", "-cudart", "static"]
+         f"-I{ROOT / 'include'}"]
+# translation units compiled in parallel: the templated kernels per
+# objective family and substep specialisation (family.cu four times), the
+# rest of the engine, the C++ API
+UNITS = [("engine", CSRC / "engine.cu", []), ("cub_sorts", CSRC / "cub_sorts.cu", []),
+         ("host_api", CSRC / "host_api.cpp", [])] + [
+    (f"family{f}_s{sub}", CSRC / "family.cu", [f"-DSG_FAMILY={f}", f"-DSG_SUB={sub}"]) for f in (0, 1) for sub in (24, 0)]
 
 
 def needs_build() -> bool:
@@ -39,10 +47,25 @@ def build(force: bool = False, verbose: bool = False, out: Path = OUT, extra: li
     """Compile libsirdgpu.so (`extra`: additional nvcc flags, e.g. tuning -D for experiments)."""
     if not force and out == OUT and not extra and not needs_build():
         return OUT
-    cmd = [NVCC, *ARCH, *FLAGS, *(extra or []), "-o", str(out), *[str(s) for s in SOURCES if s.exists()]]
-    if verbose:
-        print(" ".join(cmd), flush=True)
-    subprocess.run(cmd, check=True)
+    out = Path(out)
+    objdir = Path(tempfile.mkdtemp(prefix="sirdgpu_build_"))
+    try:
+        procs = []
+        for name, src, defs in UNITS:
+            obj = objdir / f"{name}.o"
+            cmd = [NVCC, *ARCH, *FLAGS, *defs, *(extra or []), "-c", "-o", str(obj), str(src)]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            procs.append((cmd, obj, subprocess.Popen(cmd)))
+        failed = [cmd for cmd, _, p in procs if p.wait() != 0]
+        if failed:
+            raise subprocess.CalledProcessError(1, failed[0])
+        link = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(out), *[str(o) for _, o, _ in procs]]
+        if verbose:
+            print(" ".join(link), flush=True)
+        subprocess.run(link, check=True)
+    finally:
+        shutil.rmtree(objdir, ignore_errors=True)
     return out
 
 

@@ -8,10 +8,8 @@
 #include "sirdgpu.h"
 
 #include "engine_internal.h"
-#include "kernels.cuh"
+#include "launchers.cuh"
 
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_segmented_sort.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -25,6 +23,13 @@
 #include <vector>
 
 using namespace sirdgpu;
+
+// The launchers of the templated kernels are instantiated in family.cu (one
+// object per objective family, compiled in parallel by build.py).
+namespace sirdgpu {
+SG_LAUNCH_FAMILY(extern, 0)
+SG_LAUNCH_FAMILY(extern, 1)
+}  // namespace sirdgpu
 
 // Independent swarm partitions run as separate launch sequences on their own
 // streams so one partition's per-iteration tail overlaps the next
@@ -146,81 +151,6 @@ void dispatch(int family, int metric, int substeps, Args&&... args) {
     SG_CASE(1, 0) SG_CASE(1, 1) SG_CASE(1, 2) SG_CASE(1, 3)
 #undef SG_CASE
 }
-
-template <class KernelPtr>
-cudaError_t prepare_smem(KernelPtr k, size_t smem) {
-    if (smem > 48 * 1024)
-        return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    return cudaSuccess;
-}
-
-template <int F, int M, int S>
-struct EvalLaunch {
-    static void run(const DevWindow* w, const double* pos, size_t n, double* costs, size_t smem, cudaStream_t st,
-                    cudaError_t* err) {
-        auto k = eval_costs_kernel<F, M, S>;
-        *err = prepare_smem(k, smem);
-        if (*err != cudaSuccess) return;
-        const unsigned grid = static_cast<unsigned>((n + kEvalThreads - 1) / kEvalThreads);
-        k<<<grid, kEvalThreads, smem, st>>>(w, pos, n, costs);
-        *err = cudaGetLastError();
-    }
-};
-
-template <int F, int M, int S>
-struct StepLaunch {
-    static void run(unsigned grid, uint32_t cta_offset, const CtaTask* tasks, const DevSwarm* sw, const PsoPlanes& P,
-                    DevSwarmState* state, uint64_t it, size_t smem, cudaStream_t st, cudaError_t* err) {
-        auto k = pso_step_kernel<F, M, S>;
-        if (it == 0) {
-            *err = prepare_smem(k, smem);
-            if (*err != cudaSuccess) return;
-        }
-        k<<<grid, kStepThreads, smem, st>>>(tasks, sw, P, state, it, cta_offset);
-        *err = cudaGetLastError();
-    }
-};
-
-template <int F, int M, int S>
-struct SwarmLaunch {
-    // n_swarms clusters of `cluster` CTAs (thread-block clusters, one swarm each)
-    static void run(unsigned n_swarms, unsigned cluster, unsigned threads, uint32_t swarm_offset, const DevSwarm* sw,
-                    const DevWindow* wins, const PsoPlanes& P, DevSwarmState* state, size_t smem, cudaStream_t st,
-                    cudaError_t* err) {
-        auto k = pso_swarm_kernel<F, M, S>;
-        *err = prepare_smem(k, smem);
-        if (*err != cudaSuccess) return;
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(n_swarms * cluster);
-        cfg.blockDim = dim3(threads);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = st;
-        cudaLaunchAttribute attr{};
-        attr.id = cudaLaunchAttributeClusterDimension;
-        attr.val.clusterDim.x = cluster;
-        attr.val.clusterDim.y = 1;
-        attr.val.clusterDim.z = 1;
-        cfg.attrs = &attr;
-        cfg.numAttrs = 1;
-        *err = cudaLaunchKernelEx(&cfg, k, sw, wins, P, state, swarm_offset);
-    }
-};
-
-template <int F, int M, int S>
-struct EnsembleLaunch {
-    static void run(const DevWindow* w, const DevWindow& fwin, const double* lo, const double* hi, uint64_t seed,
-                    size_t n, int horizon, double* costs, double* params, double* deaths, size_t sstride,
-                    size_t dstride, const uint32_t* perm, const double* planes, int out_by_slot, size_t smem,
-                    cudaStream_t st, cudaError_t* err) {
-        auto k = ensemble_kernel<F, M, S>;
-        *err = prepare_smem(k, smem);
-        if (*err != cudaSuccess) return;
-        const unsigned grid = static_cast<unsigned>((n + kEvalThreads - 1) / kEvalThreads);
-        k<<<grid, kEvalThreads, smem, st>>>(w, fwin, lo, hi, seed, n, horizon, costs, params, deaths, sstride,
-                                            dstride, perm, planes, out_by_slot);
-        *err = cudaGetLastError();
-    }
-};
 
 // Trajectory launcher shared by sg_integrate_batch and sg_forecast_batch.
 int launch_integrate(sg_ctx* ctx, const DevWindow& w, const double* d_params, const double* d_init, int init_stride,
@@ -1182,12 +1112,12 @@ static cudaError_t ensemble_order(sg_ctx* ctx, DevBufs& b, const double* d_lo, c
                                                                                      keys, idx);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     size_t temp_bytes = 0;
-    if ((e = cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, keys_sorted, idx, idx_sorted,
+    if ((e = sg_sort_pairs_u32(nullptr, temp_bytes, keys, keys_sorted, idx, idx_sorted,
                                              static_cast<int>(n), 0, 16, st)) != cudaSuccess)
         return e;
     unsigned char* temp;
     if ((e = b.alloc(&temp, std::max<size_t>(temp_bytes, 16))) != cudaSuccess) return e;
-    if ((e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys_sorted, idx, idx_sorted,
+    if ((e = sg_sort_pairs_u32(temp, temp_bytes, keys, keys_sorted, idx, idx_sorted,
                                              static_cast<int>(n), 0, 16, st)) != cudaSuccess)
         return e;
     ctx->launches += 2;
@@ -1289,11 +1219,11 @@ static int enqueue_bands(sg_ctx* ctx, sg_window* w, DevBufs& b, cudaStream_t st,
     SG_CUDA(ctx, cudaGetLastError());
     size_t temp_bytes = 0;
     const int n_items = static_cast<int>(n * n_days);
-    SG_CUDA(ctx, cub::DeviceSegmentedSort::SortKeys(nullptr, temp_bytes, d_sorted, d_D, n_items, n_seg, d_beg, d_end,
+    SG_CUDA(ctx, sg_segmented_sort_f64(nullptr, temp_bytes, d_sorted, d_D, n_items, n_seg, d_beg, d_end,
                                                      st));
     unsigned char* d_temp;
     SG_CUDA(ctx, b.alloc(&d_temp, std::max<size_t>(temp_bytes, 16)));
-    SG_CUDA(ctx, cub::DeviceSegmentedSort::SortKeys(d_temp, temp_bytes, d_sorted, d_D, n_items, n_seg, d_beg, d_end,
+    SG_CUDA(ctx, sg_segmented_sort_f64(d_temp, temp_bytes, d_sorted, d_D, n_items, n_seg, d_beg, d_end,
                                                      st));
     ctx->launches += 1;
     sel_bands_kernel<<<small, 128, 0, st>>>(d_days, d_D, n, d_bands, d_counts, n_days);
@@ -1398,11 +1328,23 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
 
 // ---- diagnostics -------------------------------------------------------------------
 
+#if SG_DAY_COUNTERS
+extern "C" int sg_day_classes_f0_s24(unsigned long long* out3);
+extern "C" int sg_day_classes_f1_s24(unsigned long long* out3);
+extern "C" int sg_day_classes_f0_s0(unsigned long long* out3);
+extern "C" int sg_day_classes_f1_s0(unsigned long long* out3);
+#endif
+
 extern "C" int sg_debug_day_classes(unsigned long long* out3) {
 #if SG_DAY_COUNTERS
-    cudaMemcpyFromSymbol(out3, g_day_class, sizeof(unsigned long long) * 3);
-    unsigned long long zero[3] = {0, 0, 0};
-    cudaMemcpyToSymbol(g_day_class, zero, sizeof zero);
+    int (*parts[4])(unsigned long long*) = {sg_day_classes_f0_s24, sg_day_classes_f1_s24, sg_day_classes_f0_s0,
+                                            sg_day_classes_f1_s0};
+    for (int k = 0; k < 3; ++k) out3[k] = 0;
+    for (auto f : parts) {
+        unsigned long long a[3];
+        f(a);
+        for (int k = 0; k < 3; ++k) out3[k] += a[k];
+    }
     return SG_OK;
 #else
     out3[0] = out3[1] = out3[2] = 0;

@@ -306,6 +306,7 @@ __device__ __forceinline__ void init_particle(const DevSwarm& sw, const PsoPlane
     P.pbc[p] = __longlong_as_double(0x7FF0000000000000LL);
 }
 
+#ifndef SG_FAMILY_TU  // engine.cu only (family.cu holds the templated kernels)
 __global__ void __launch_bounds__(kStepThreads) pso_init_kernel(const DevSwarm* __restrict__ swarms,
                                                                 const uint32_t* __restrict__ cta_swarm,
                                                                 PsoPlanes P, DevSwarmState* __restrict__ state) {
@@ -323,6 +324,8 @@ __global__ void __launch_bounds__(kStepThreads) pso_init_kernel(const DevSwarm* 
         if (i < sw.n) init_particle(sw, P, sw.offset + i, i);
     }
 }
+
+#endif  // SG_FAMILY_TU
 
 // (cost, index) ordering of the global-best scan (pso.cpp:90-96): the lowest
 // cost wins, ties go to the lowest index; NaN never wins (pbest costs are never
@@ -823,6 +826,7 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 1) pso_swarm_kernel(const De
     cluster.sync();  // no CTA leaves while another may still read its partials
 }
 
+#ifndef SG_FAMILY_TU  // engine.cu only (family.cu holds the templated kernels)
 // ---- R^2 of the re-integrated deaths (fit_window's finish) ------------------------
 //
 // r_squared_d (objectives.cpp:122-144) per fit, one thread each, with the
@@ -847,6 +851,8 @@ __global__ void r2_kernel(const double* __restrict__ states, const double* __res
     }
     r2[k] = ss_tot == 0.0 ? __longlong_as_double(0x7FF8000000000000LL) : dsub(1.0, ddiv(ss_res, ss_tot));
 }
+
+#endif  // SG_FAMILY_TU
 
 // ---- forecast-scenario ensemble ----------------------------------------------------
 // Sample k: 6 uniform01 draws of mt19937_64(mix_seed(seed, k)) mapped into the
@@ -874,6 +880,7 @@ __device__ __forceinline__ void x_of_sample(const double* lo, const double* hi, 
     repair_order(x);
 }
 
+#ifndef SG_FAMILY_TU  // engine.cu only (family.cu holds the templated kernels)
 // Evaluation order of an ensemble: every sample's parameters into SoA
 // planes and a key (day of t1, day of t2) — samples with equal keys ramp on
 // the same days, so sorting by it makes a warp's lanes ramp together (the
@@ -894,6 +901,8 @@ __global__ void __launch_bounds__(256) ens_sample_kernel(const double* __restric
     keys[k] = (day(x[2]) << 8) | day(x[3]);
     idx[k] = static_cast<uint32_t>(k);
 }
+
+#endif  // SG_FAMILY_TU
 
 template <int FAM, int MET, int SUB>
 __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWindow* __restrict__ win, DevWindow fwin,
@@ -975,6 +984,7 @@ constexpr int kBandP = 7;
 constexpr int kBandRanks = 2 * kBandP;  // lo and lo+1 per probability
 constexpr int kSelBinBits = 12;
 constexpr int kSelBins = 1 << kSelBinBits;  // per day; a CTA histogram fits in shared memory
+#ifndef SG_FAMILY_TU  // engine.cu only
 __device__ __constant__ double kBandProbs[kBandP] = {0.5, 0.25, 0.75, 0.05, 0.95, 0.025, 0.975};  // 352-358
 
 __host__ __device__ __forceinline__ uint64_t order_key(double x) {
@@ -1304,5 +1314,7 @@ __global__ void bands_kernel(const double* __restrict__ sorted, size_t n, double
 #pragma unroll
     for (int q = 0; q < 7; ++q) bands[q * n_days + d] = quantile_sorted_dev(col, k, ps[q]);
 }
+
+#endif  // SG_FAMILY_TU
 
 }  // namespace sirdgpu

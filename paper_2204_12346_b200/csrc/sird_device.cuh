@@ -39,7 +39,7 @@
 #endif
 #if SG_DAY_COUNTERS
 // Diagnostic build only: warp-days per class (0 constant, 1 switch, 2 ramp).
-__device__ unsigned long long g_day_class[3];
+static __device__ unsigned long long g_day_class[3];  // one copy per object (family.cu reads its own)
 #endif
 
 namespace sirdgpu {
