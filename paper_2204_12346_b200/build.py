@@ -29,11 +29,13 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++20", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
          f"-I{ROOT / 'include'}"]
 # translation units compiled in parallel: the templated kernels per
-# objective family and substep specialisation (family.cu four times), the
+# objective family and substep specialisation (family.cu six times), the
 # rest of the engine, the C++ API
+_FAMILY_UNITS = [(f, sub) for f in (0, 1) for sub in (24, -1, 0)]
 UNITS = [("engine", CSRC / "engine.cu", []), ("cub_sorts", CSRC / "cub_sorts.cu", []),
          ("host_api", CSRC / "host_api.cpp", [])] + [
-    (f"family{f}_s{sub}", CSRC / "family.cu", [f"-DSG_FAMILY={f}", f"-DSG_SUB={sub}"]) for f in (0, 1) for sub in (24, 0)]
+    (f"family{f}_s{'m1' if sub < 0 else sub}", CSRC / "family.cu", [f"-DSG_FAMILY={f}", f"-DSG_SUB={sub}", f"-DSG_UNIT={k}"])
+    for k, (f, sub) in enumerate(_FAMILY_UNITS)]
 
 
 def needs_build() -> bool:

@@ -130,7 +130,10 @@ double compartment_scale(const double* obs, int n) {
 
 // Kernel specialisation of a window: 24 = the reference default substep count
 // with the t_k table in shared memory; 0 = generic runtime substeps.
-int kernel_sub(int n_days, int substeps) { return uses_fast_grid(n_days, substeps) ? 24 : 0; }
+// -1 = any other substep count whose t_k table fits shared memory.
+int kernel_sub(int n_days, int substeps) {
+    return uses_fast_grid(n_days, substeps) ? 24 : (uses_time_table(n_days, substeps) ? -1 : 0);
+}
 
 bool valid_spec(int family, int metric) {
     return (family == SG_FAMILY_D_ONLY || family == SG_FAMILY_IRD_JOINT) && metric >= SG_METRIC_MXSE &&
@@ -140,12 +143,13 @@ bool valid_spec(int family, int metric) {
 // ---- template dispatch over (family, metric, substeps == 24) ------------------
 template <template <int, int, int> class K, class... Args>
 void dispatch(int family, int metric, int substeps, Args&&... args) {
-    const bool s24 = substeps == 24;  // callers pass 0 when the window is too long for the table
-#define SG_CASE(F, M)                                              \
-    if (family == F && metric == M) {                              \
-        if (s24) K<F, M, 24>::run(std::forward<Args>(args)...);    \
-        else K<F, M, 0>::run(std::forward<Args>(args)...);         \
-        return;                                                    \
+    // substeps: the kernel_sub() of the window(s): 24, -1 (table, runtime count) or 0
+#define SG_CASE(F, M)                                                           \
+    if (family == F && metric == M) {                                           \
+        if (substeps == 24) K<F, M, 24>::run(std::forward<Args>(args)...);      \
+        else if (substeps == -1) K<F, M, -1>::run(std::forward<Args>(args)...); \
+        else K<F, M, 0>::run(std::forward<Args>(args)...);                      \
+        return;                                                                 \
     }
     SG_CASE(0, 0) SG_CASE(0, 1) SG_CASE(0, 2) SG_CASE(0, 3)
     SG_CASE(1, 0) SG_CASE(1, 1) SG_CASE(1, 2) SG_CASE(1, 3)
@@ -160,6 +164,10 @@ int launch_integrate(sg_ctx* ctx, const DevWindow& w, const double* d_params, co
     if (uses_fast_grid(w.n_days, w.substeps)) {
         SG_CUDA(ctx, prepare_smem(integrate_kernel<24>, smem));
         integrate_kernel<24><<<grid, kEvalThreads, smem, ctx->stream>>>(w, d_params, d_init, init_stride, hold, n,
+                                                                        d_states, d_fin);
+    } else if (uses_time_table(w.n_days, w.substeps)) {
+        SG_CUDA(ctx, prepare_smem(integrate_kernel<-1>, smem));
+        integrate_kernel<-1><<<grid, kEvalThreads, smem, ctx->stream>>>(w, d_params, d_init, init_stride, hold, n,
                                                                         d_states, d_fin);
     } else {
         SG_CUDA(ctx, prepare_smem(integrate_kernel<0>, smem));
@@ -752,10 +760,10 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
         t.win = g.d_win + s.window;
         t.times = w.times;
         t.obs = reinterpret_cast<const double*>(w.obs);
-        t.times_bytes = static_cast<uint32_t>(
-            ((static_cast<size_t>(w.substeps) + tgrid_entries(w.n_days, w.substeps)) * sizeof(double) + 15) &
-            ~size_t(15));
-        t.obs_bytes = static_cast<uint32_t>((sizeof(ObsDay) * static_cast<size_t>(w.n_days) + 15) & ~size_t(15));
+        const WindowLayout L = window_layout(w.n_days, w.substeps, w.metric);
+        t.times_bytes = static_cast<uint16_t>(L.times_bytes);
+        t.obs_bytes = static_cast<uint16_t>(L.obs_bytes);
+        t.substeps = static_cast<uint32_t>(uses_time_table(w.n_days, w.substeps) ? w.substeps : 0);
     }
     SG_CUDA(ctx, cudaMemcpyAsync(g.d_task, tasks.data(), sizeof(CtaTask) * tasks.size(), cudaMemcpyHostToDevice, st));
     SG_CUDA(ctx, cudaStreamSynchronize(st));  // host vectors go out of scope
@@ -1329,16 +1337,18 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
 // ---- diagnostics -------------------------------------------------------------------
 
 #if SG_DAY_COUNTERS
-extern "C" int sg_day_classes_f0_s24(unsigned long long* out3);
-extern "C" int sg_day_classes_f1_s24(unsigned long long* out3);
-extern "C" int sg_day_classes_f0_s0(unsigned long long* out3);
-extern "C" int sg_day_classes_f1_s0(unsigned long long* out3);
+extern "C" int sg_day_classes_u0(unsigned long long* out3);
+extern "C" int sg_day_classes_u1(unsigned long long* out3);
+extern "C" int sg_day_classes_u2(unsigned long long* out3);
+extern "C" int sg_day_classes_u3(unsigned long long* out3);
+extern "C" int sg_day_classes_u4(unsigned long long* out3);
+extern "C" int sg_day_classes_u5(unsigned long long* out3);
 #endif
 
 extern "C" int sg_debug_day_classes(unsigned long long* out3) {
 #if SG_DAY_COUNTERS
-    int (*parts[4])(unsigned long long*) = {sg_day_classes_f0_s24, sg_day_classes_f1_s24, sg_day_classes_f0_s0,
-                                            sg_day_classes_f1_s0};
+    int (*parts[6])(unsigned long long*) = {sg_day_classes_u0, sg_day_classes_u1, sg_day_classes_u2,
+                                            sg_day_classes_u3, sg_day_classes_u4, sg_day_classes_u5};
     for (int k = 0; k < 3; ++k) out3[k] = 0;
     for (auto f : parts) {
         unsigned long long a[3];

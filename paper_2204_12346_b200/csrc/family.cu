@@ -1,12 +1,12 @@
 // family.cu — the templated kernels and their launchers for ONE objective
 // family (SG_FAMILY = 0: D-only, 1: IRD-joint) and one substep
-// specialisation (SG_SUB = 24 or 0), compiled four times by build.py in
+// specialisation (SG_SUB = 24, -1 or 0), compiled six times by build.py in
 // parallel with engine.cu.  See launchers.cuh.
 #define SG_FAMILY_TU 1
 #include "launchers.cuh"
 
-#if !defined(SG_FAMILY) || !defined(SG_SUB)
-#error "compile with -DSG_FAMILY=0|1 -DSG_SUB=24|0"
+#if !defined(SG_FAMILY) || !defined(SG_SUB) || !defined(SG_UNIT)
+#error "compile with -DSG_FAMILY=0|1 -DSG_SUB=24|-1|0 -DSG_UNIT=<0..5>"
 #endif
 
 namespace sirdgpu {
@@ -17,7 +17,7 @@ SG_LAUNCH_FAMILY_SUB(, SG_FAMILY, SG_SUB)
 // diagnostic build: this object's warp-day class counters (sird_device.cuh)
 #define SG_CAT2(a, b) a##b
 #define SG_CAT(a, b) SG_CAT2(a, b)
-extern "C" int SG_CAT(SG_CAT(sg_day_classes_f, SG_FAMILY), SG_CAT(_s, SG_SUB))(unsigned long long* out3) {
+extern "C" int SG_CAT(sg_day_classes_u, SG_UNIT)(unsigned long long* out3) {
     cudaMemcpyFromSymbol(out3, g_day_class, sizeof(unsigned long long) * 3);
     unsigned long long zero[3] = {0, 0, 0};
     cudaMemcpyToSymbol(g_day_class, zero, sizeof zero);

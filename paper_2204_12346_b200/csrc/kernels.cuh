@@ -51,7 +51,7 @@ struct SmemWindow {
 };
 
 __host__ __device__ inline int tgrid_entries(int n_days, int substeps) {
-    return uses_fast_grid(n_days, substeps) ? (n_days - 1) * substeps : 0;
+    return uses_time_table(n_days, substeps) ? (n_days - 1) * substeps : 0;
 }
 
 // Shared-memory image of a window (dynamic segment, every section 16-byte
@@ -534,9 +534,11 @@ struct CtaTask {
     const DevWindow* win;    // window descriptor (device)
     const double* times;     // its substep-time table (device)
     const double* obs;       // obs | robs | flags, 16-byte padded sections (device)
-    uint32_t times_bytes;    // 16-byte multiples
-    uint32_t obs_bytes;
+    uint16_t times_bytes;    // 16-byte multiples (<= 38.5 KB: the table is at most kMaxTgrid entries)
+    uint16_t obs_bytes;
+    uint32_t substeps;       // the window's substep count when it has a t_k table, else 0
 };
+static_assert(sizeof(CtaTask) == 64, "one 64-byte record per CTA");
 
 // ---- bulk asynchronous global -> shared copies (TMA, non-tensor) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -572,7 +574,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // Asynchronous staging of the CTA's window (specialised kernels, static
 // shared arrays): thread 0 arms the barrier and issues the bulk copies; the
 // caller overlaps them with the particle moves and waits with mbar_wait.
-template <int MET>
+template <int MET, int SUB>
 __device__ __forceinline__ SmemWindow stage_window_async(const CtaTask& t, DevWindow* sdesc, uint64_t* bar,
                                                          unsigned char* smem) {
     // WindowLayout: times | obs | robs | flags, the section sizes in the task
@@ -598,7 +600,8 @@ __device__ __forceinline__ SmemWindow stage_window_async(const CtaTask& t, DevWi
         }
     }
     __syncthreads();  // barrier initialised before anyone waits on it
-    return SmemWindow{sdesc, s_obs, s_robs, s_flag, TimeGrid{s_times + 24, s_times}};
+    // the t_k table follows subh[substeps]: a compile-time offset for SUB = 24
+    return SmemWindow{sdesc, s_obs, s_robs, s_flag, TimeGrid{s_times + (SUB > 0 ? SUB : t.substeps), s_times}};
 }
 
 // One Swarm::step (pso.cpp:77-101) for every swarm, iteration `it`, fused:
@@ -615,9 +618,9 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
     const uint32_t cta = blockIdx.x + cta_offset;
     const CtaTask task = tasks[cta];
     if (it >= task.max_iters) return;  // CTA-uniform
-    constexpr bool kAsync = SUB > 0 && SG_TMA_STAGE;
+    constexpr bool kAsync = SUB != 0 && SG_TMA_STAGE;
     SmemWindow win;
-    if constexpr (kAsync) win = stage_window_async<MET>(task, &sdesc, &bar, smem);
+    if constexpr (kAsync) win = stage_window_async<MET, SUB>(task, &sdesc, &bar, smem);
     else win = stage_window<MET, SUB>(task.win, &sdesc, smem);
     const int s = static_cast<int>(task.swarm);
     const DevSwarm& sw = swarms[s];
@@ -944,7 +947,7 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
         for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
         return;
     }
-    const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w, SUB > 0 ? sw.tg.tgrid : nullptr);
+    const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w, SUB != 0 ? sw.tg.tgrid : nullptr);
     double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
     ScoreSink<FAM, MET> score(w, sw.obs, sw.robs, sw.flag);  // starts from the day-0 contribution
     integrate_days<SUB>(p, w, sw.tg, S, I, R, D, score);

@@ -1,6 +1,6 @@
 // launchers.cuh — host-side launchers of the templated kernels, one struct
 // per kernel family with run() for every (objective family, metric,
-// substeps == 24) specialisation.  engine.cu dispatches to them; family.cu
+// substeps: 24 / -1 = any count with the t_k table / 0 = generic) specialisation.  engine.cu dispatches to them; family.cu
 // instantiates them, once per objective family, so the heavy kernel
 // templates compile in parallel translation units (build.py).
 #pragma once
@@ -119,6 +119,7 @@ void EnsembleLaunch<F, M, S>::run(const DevWindow* w, const DevWindow& fwin, con
     INST template struct EnsembleLaunch<F, M, S>;
 #define SG_LAUNCH_FAMILY_SUB(INST, F, S) \
     SG_LAUNCH_ONE(INST, F, 0, S) SG_LAUNCH_ONE(INST, F, 1, S) SG_LAUNCH_ONE(INST, F, 2, S) SG_LAUNCH_ONE(INST, F, 3, S)
-#define SG_LAUNCH_FAMILY(INST, F) SG_LAUNCH_FAMILY_SUB(INST, F, 24) SG_LAUNCH_FAMILY_SUB(INST, F, 0)
+#define SG_LAUNCH_FAMILY(INST, F) \
+    SG_LAUNCH_FAMILY_SUB(INST, F, 24) SG_LAUNCH_FAMILY_SUB(INST, F, -1) SG_LAUNCH_FAMILY_SUB(INST, F, 0)
 
 }  // namespace sirdgpu

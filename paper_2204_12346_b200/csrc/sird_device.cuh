@@ -257,13 +257,20 @@ struct TimeGrid {
 // kernel still fit in shared memory with the observations).
 constexpr int kMaxTgrid = 4800;
 
+// A window's t_k table fits in shared memory (any substep count).
+__host__ __device__ inline bool uses_time_table(int n_days, int substeps) {
+    return substeps >= 1 && static_cast<long long>(n_days - 1) * substeps <= kMaxTgrid;
+}
+
+// ... and the window takes the kernels specialised for the reference's 24 substeps.
 __host__ __device__ inline bool uses_fast_grid(int n_days, int substeps) {
-    return substeps == 24 && static_cast<long long>(n_days - 1) * substeps <= kMaxTgrid;
+    return substeps == 24 && uses_time_table(n_days, substeps);
 }
 
 // Integrate days 1..n_days-1 (model.cpp:92-106), calling sink.day(day, S, I, R, D)
 // after every day.  SUB > 0 fixes the substep count at compile time
-// (the reference default kDefaultSubsteps = 24, model.hpp:12); SUB == 0 reads
+// (the reference default kDefaultSubsteps = 24, model.hpp:12); SUB == -1
+// reads it from the window but has the t_k table; SUB == 0 reads
 // it from the window.
 template <int SUB, class Sink>
 __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindow& w, const TimeGrid& tg,
@@ -306,7 +313,7 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
         constexpr bool quiet = false;  // SG_DAY_SPLIT 2: quiet days never reach here
 #endif
         if (!quiet && __any_sync(mask, ramp_today)) {
-            if (SG_RAMP_MODE >= 1 && SUB > 0 && warp_fast && __all_sync(mask, lo <= 0 && hi >= nsub)) {
+            if (SG_RAMP_MODE >= 1 && SUB != 0 && warp_fast && __all_sync(mask, lo <= 0 && hi >= nsub)) {
                 // Every lane ramps through the whole day: no selects at all.
 #pragma unroll(SUB > 0 ? kRampUnroll : 4)
                 for (int sub = 0; sub < nsub; ++sub) {
@@ -314,7 +321,7 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
                     const double beta = dadd(p.b1, dmul(p.slope, dsub(t, p.t1)));
                     euler_substep(div_by_N(beta, rN, rN_lo), g, mu, h, S, I, R, D);
                 }
-            } else if (SG_RAMP_MODE >= 1 && SUB > 0 && warp_fast) {
+            } else if (SG_RAMP_MODE >= 1 && SUB != 0 && warp_fast) {
                 // Branch-free ramp day: every lane computes the ramp value
                 // (the warp would issue it anyway once any lane needs it) and
                 // selects; non-FP64 work per substep is two compares and
@@ -333,7 +340,7 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
                     double bp = sub < lo ? p.bp1 : p.bp2;
                     if (sub >= lo && sub < hi) {
                         double t;
-                        if constexpr (SUB > 0) t = tg.tgrid[kbase + sub];
+                        if constexpr (SUB != 0) t = tg.tgrid[kbase + sub];
                         else t = dadd(static_cast<double>(day - 1), tg.subh[sub]);
                         bp = ramp_bp(p, t, N, rN, rN_lo);
                     }
@@ -487,7 +494,7 @@ __device__ __forceinline__ double eval_particle(const double* x, const DevWindow
         if (ramp) *ramp = 0;
         return __longlong_as_double(0x7FF0000000000000LL);
     }
-    const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w, SUB > 0 ? tg.tgrid : nullptr);
+    const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w, SUB != 0 ? tg.tgrid : nullptr);
     if (ramp) *ramp = p.k2 - p.k1;
     double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
     ScoreSink<FAM, MET> sink(w, obs, robs, flag);  // starts from the day-0 contribution
