@@ -730,7 +730,6 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     SG_CUDA(ctx, b.alloc(&P.v, pblock_elems(g.n_total, 6)));
     SG_CUDA(ctx, b.alloc(&P.pb, pblock_elems(g.n_total, 6)));
     SG_CUDA(ctx, b.alloc(&P.pbc, g.n_total));
-    SG_CUDA(ctx, b.alloc(&P.cost, g.n_total));
     SG_CUDA(ctx, b.alloc(&P.mt, pblock_elems(g.n_total, kMtN)));
     SG_CUDA(ctx, b.alloc(&P.part_cost, g.n_ctas * kStepWarps));
     SG_CUDA(ctx, b.alloc(&P.part_idx, g.n_ctas * kStepWarps));
@@ -1050,9 +1049,9 @@ void sg_plan_destroy(sg_plan* plan) {
     delete plan;
 }
 
-// Device bytes per particle of a plan (x, v, pb: 18; pbc, cost: 2; 312
+// Device bytes per particle of a plan (x, v, pb: 18; pbc: 1; 312
 // engine words) — used to split oversized calls into sequential plans.
-static constexpr size_t kBytesPerParticle = (18 + 2 + kMtN) * sizeof(double);
+static constexpr size_t kBytesPerParticle = (18 + 1 + kMtN) * sizeof(double);
 
 void sg_trace_phase(const char* what) {
     static const bool on = std::getenv("SG_TRACE") != nullptr;

@@ -251,8 +251,7 @@ struct PsoPlanes {
     double* x;           // particle blocks of 6 fields (pblock_base(p, 6) + d*32)
     double* v;
     double* pb;
-    double* pbc;         // personal-best cost
-    double* cost;        // last evaluated cost
+    double* pbc;         // personal-best cost (the last evaluated costs never leave registers)
     uint64_t* mt;        // particle blocks of 312 engine words (pblock_base(p, 312) + w*32)
     size_t stride;       // total particles (plane length)
     double* part_cost;   // per warp of the step kernel
@@ -409,7 +408,6 @@ __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& s
 #pragma unroll
     for (int q = 0; q < NPT; ++q) {
         if (!active[q]) continue;
-        P.cost[p[q]] = c[q];
         double pbc = pbc_in[q];
         if (c[q] < pbc) {
             pbc = c[q];
@@ -601,7 +599,7 @@ __device__ __forceinline__ SmemWindow stage_window_async(const CtaTask& t, DevWi
     }
     __syncthreads();  // barrier initialised before anyone waits on it
     // the t_k table follows subh[substeps]: a compile-time offset for SUB = 24
-    return SmemWindow{sdesc, s_obs, s_robs, s_flag, TimeGrid{s_times + (SUB > 0 ? SUB : t.substeps), s_times}};
+    return SmemWindow{sdesc, s_obs, s_robs, s_flag, TimeGrid{s_times + (SUB > 0 ? static_cast<uint32_t>(SUB) : t.substeps), s_times}};
 }
 
 // One Swarm::step (pso.cpp:77-101) for every swarm, iteration `it`, fused:
@@ -816,7 +814,6 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 1) pso_swarm_kernel(const De
             P.pb[pblock_base(p, 6) + 32 * d] = pb[d];
         }
         P.pbc[p] = pbc;
-        P.cost[p] = c;
     }
     // per-thread count <= iterations * 840 < 2^32 / 32
     const unsigned long long wr = __reduce_add_sync(0xFFFFFFFFu, static_cast<unsigned int>(ramp_acc));
