@@ -1078,6 +1078,8 @@ int sg_fit_swarms(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg_
         SG_CUDA(ctx, cudaMemGetInfo(&free_b, &total_b));
         budget = std::max<size_t>(free_b / 10 * 7, size_t(1) << 28);
     }
+    static const char* budget_env = std::getenv("SG_PLAN_BUDGET_BYTES");  // diagnostic: force the split
+    if (budget_env) budget = std::min<size_t>(budget, std::strtoull(budget_env, nullptr, 10));
     size_t begin = 0;
     while (begin < n_swarms) {
         size_t end = begin, bytes = 0;

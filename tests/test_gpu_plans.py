@@ -142,3 +142,39 @@ def test_sharded_stability_study_matches_single_process(tmp_path):
     import json
     d = json.loads(line)
     assert d["ranks"] == 2 and d["units"] == 36 and d["identical_to_single_process"] is True
+
+
+def test_oversized_calls_split_into_sequential_plans_identically(tmp_path):
+    """sg_fit_swarms splits a call whose device state exceeds the memory
+    budget into sequential plans; forcing a tiny budget (SG_PLAN_BUDGET_BYTES)
+    must give the same results as one plan."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    script = tmp_path / "split.py"
+    script.write_text(f"""
+import sys, hashlib
+sys.path.insert(0, {str(root)!r})
+import numpy as np
+import paper_2204_12346_b200 as eng
+a = np.genfromtxt({str(root / 'tests' / 'golden' / 'poland_like.csv')!r}, delimiter=",", names=True)
+ctx = eng.Context(0)
+N = 38e6
+swarms, wins = [], []
+for k in range(12):
+    s = 20 * k
+    I, R, D = a["infectious"][s:s + 30], a["recovered_cum"][s:s + 30], a["deaths_cum"][s:s + 30]
+    w = eng.Window(ctx, I, R, D, [N - I[0] - R[0] - D[0], I[0], R[0], D[0]], N, "ird-mxse")
+    wins.append(w)
+    swarms.append(dict(window=w, lower=[0] * 6, upper=[2, 2, 22, 22, 1, 0.1], n_particles=1500, max_iters=8, seed=k))
+out = ctx.fit_swarms(swarms)
+h = hashlib.sha1(b"".join(o[3].tobytes() + o[1].tobytes() for o in out)).hexdigest()
+print(h, sum(o[0] for o in out))
+""")
+    plain = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, timeout=300)
+    env = dict(os.environ, SG_PLAN_BUDGET_BYTES=str(4 * 1500 * 331 * 8))  # ~4 swarms per plan
+    split = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, timeout=300, env=env)
+    assert plain.returncode == 0 and split.returncode == 0, plain.stderr[-800:] + split.stderr[-800:]
+    assert plain.stdout.split() == split.stdout.split() and plain.stdout.split()[1] == "0"
