@@ -44,3 +44,20 @@ def test_engine_line():
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["e2e"]["matches_device_run"] is True
     assert d["gpu_launches"] > 0
+
+
+def test_reference_arm_under_torchrun():
+    """N>1 launch of the reference arm (the driver's scaling run): rank 0
+    alone prints the line, the other rank exits 0 without work."""
+    from oracle import oracle_py
+    if not (oracle_py.REF_SO.exists() or oracle_py.PORT_SO.exists()):
+        pytest.skip("no CPU oracle built")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29537", str(ROOT / "bench.py"), "--impl", "reference", "--gpus", "2",
+           "--steps", "1", "--warmup", "0", "--ref-budget", "0.5"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
