@@ -14,11 +14,12 @@ from test_gpu_fuzz import _case  # noqa: E402
 
 def main():
     n_batches = int(sys.argv[1]) if len(sys.argv) > 1 else 50
+    seed_base = int(sys.argv[2]) if len(sys.argv) > 2 else 900000  # batch b uses default_rng(seed_base + b)
     ctx = eng.Context(0)
     port = oracle_py.load("port")
     bad = 0
     for batch in range(n_batches):
-        rng = np.random.default_rng(900000 + batch)
+        rng = np.random.default_rng(seed_base + batch)
         cases = [_case(rng) for _ in range(16)]
         wins, swarms = [], []
         for c in cases:
@@ -37,7 +38,7 @@ def main():
             if not ok:
                 bad += 1
                 print("MISMATCH batch", batch, "case", k, c["spec"], c["sub"], flush=True)
-    print(f"fuzz_long: {n_batches * 16} swarms, {bad} mismatches", flush=True)
+    print(f"fuzz_long: {n_batches * 16} swarms (seeds {seed_base}..{seed_base + n_batches - 1}), {bad} mismatches", flush=True)
     return 1 if bad else 0
 
 
