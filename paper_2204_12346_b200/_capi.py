@@ -8,14 +8,13 @@ immediately — there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import os
 import weakref
 from pathlib import Path
 
 import numpy as np
 
 from .errors import NoDeviceError, raise_for_status
-
-import os
 
 # SG_LIB overrides the library (tuning experiments only; the default is the in-tree build).
 LIB_PATH = Path(os.environ.get("SG_LIB", Path(__file__).resolve().parent / "libsirdgpu.so"))
