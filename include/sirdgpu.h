@@ -19,9 +19,11 @@
  *     one-to-one onto the reference's exception types (errors.hpp:8-50).
  *   - Host buffers are caller-owned and are fully consumed / filled before the
  *     call returns.  Device memory is owned by the context.
- *   - One context per device.  Calls on one context are externally serialized
- *     (the reference's BatchObjective is called from one thread,
- *     pso.cpp:81); different contexts may be driven from different threads.
+ *   - One context per device, shareable between host threads: every entry
+ *     point serialises on a per-context lock (the reference's objectives and
+ *     fit_window are reentrant), and sg_last_error() returns the calling
+ *     thread's last error on that context.  Different contexts (devices)
+ *     run concurrently.
  *   - Numerical blow-up is data, not an error: a particle whose trajectory
  *     leaves the finite range costs +inf (model.hpp:34-36,
  *     objectives.cpp:101-103), exactly as in the reference.
@@ -74,6 +76,9 @@ void sg_ctx_destroy(sg_ctx* ctx);
 const char* sg_last_error(const sg_ctx* ctx);
 /* Number of CUDA kernels this context has launched (telemetry for bench). */
 uint64_t sg_ctx_launch_count(const sg_ctx* ctx);
+/* Host->device and device->host bytes copied by this context's calls so far
+ * (telemetry for bench: the e2e transfer volume, counted at every copy). */
+void sg_ctx_copy_bytes(const sg_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
 /* Underlying cudaStream_t used by every call of this context. */
 void* sg_ctx_stream(const sg_ctx* ctx);
 
@@ -238,6 +243,18 @@ int sg_fit_all_windows_series(sg_ctx* ctx, const double* infectious, const doubl
                               const sg_fit_settings* settings, uint64_t base_seed, size_t max_windows,
                               size_t* n_windows, sg_fit_record* records, double* trajectories, double* mean_r2_d,
                               size_t* failed_count);
+
+/* fit_all_windows restricted to windows [first_window, first_window +
+ * max_windows) of the scheme — one rank's share of a sweep sharded over GPUs
+ * (SURVEY.md §8e): the same windows, seeds mix_seed(base_seed, w) and
+ * per-window failure records as the whole sweep (calibration.cpp:190-216),
+ * so the shards merged in window order equal sg_fit_all_windows_series.
+ * *n_windows receives the number of records written. */
+int sg_fit_window_range_series(sg_ctx* ctx, const double* infectious, const double* recovered_cum,
+                               const double* deaths_cum, size_t n_series, uint64_t tau, uint64_t delta,
+                               const sg_fit_settings* settings, uint64_t base_seed, uint64_t first_window,
+                               uint64_t max_windows, size_t* n_windows, sg_fit_record* records,
+                               double* trajectories);
 
 /* stability_study (calibration.cpp:378-436): repetitions fits of one window
  * (seeds mix_seed(base_seed, rep)) + forecast_extension(horizon).

@@ -81,6 +81,7 @@ SIGNATURES = {
     "sg_last_error": (ctypes.c_char_p, [ctypes.c_void_p]),
     "sg_ctx_launch_count": (ctypes.c_uint64, [ctypes.c_void_p]),
     "sg_ctx_stream": (ctypes.c_void_p, [ctypes.c_void_p]),
+    "sg_ctx_copy_bytes": (None, [ctypes.c_void_p, _u64p, _u64p]),
     "sg_window_create": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, ctypes.c_int, sg_state, ctypes.c_double,
                                         ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
     "sg_window_destroy": (None, [ctypes.c_void_p]),
@@ -112,6 +113,10 @@ SIGNATURES = {
                                                  ctypes.c_uint64, ctypes.POINTER(sg_fit_settings), ctypes.c_uint64,
                                                  ctypes.c_size_t, _szp, ctypes.POINTER(sg_fit_record), _dp, _dp,
                                                  _szp]),
+    "sg_fit_window_range_series": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, ctypes.c_size_t, ctypes.c_uint64,
+                                                  ctypes.c_uint64, ctypes.POINTER(sg_fit_settings), ctypes.c_uint64,
+                                                  ctypes.c_uint64, ctypes.c_uint64, _szp,
+                                                  ctypes.POINTER(sg_fit_record), _dp]),
     "sg_stability_study_series": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, ctypes.c_size_t, ctypes.c_uint64,
                                                  ctypes.c_uint64, ctypes.POINTER(sg_fit_settings), ctypes.c_uint64,
                                                  ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(sg_fit_record),
@@ -201,6 +206,13 @@ class Context:
     @property
     def launch_count(self) -> int:
         return int(lib().sg_ctx_launch_count(self._h))
+
+    @property
+    def copy_bytes(self) -> tuple[int, int]:
+        """(host->device, device->host) bytes this context has copied so far."""
+        a, b = ctypes.c_uint64(), ctypes.c_uint64()
+        lib().sg_ctx_copy_bytes(self._h, ctypes.byref(a), ctypes.byref(b))
+        return int(a.value), int(b.value)
 
     @property
     def stream(self) -> int:

@@ -13,14 +13,19 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
+#include <unordered_map>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 using namespace sirdgpu;
 
@@ -42,8 +47,15 @@ constexpr int kMaxLanes = SG_LANES;
 struct sg_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
-    std::string err;
-    uint64_t launches = 0;
+    // Every entry point that touches the context's stream, scratch buffers,
+    // lanes or plans holds this lock, so threads may share one context (the
+    // reference's objectives are reentrant); the C++ layer nests calls, hence
+    // recursive.  Error texts are kept per calling thread (last_errors()).
+    std::recursive_mutex mu;
+    std::atomic<uint64_t> launches{0};
+    // host <-> device bytes copied by the context's calls (telemetry: the
+    // e2e byte counts of bench.py)
+    std::atomic<uint64_t> h2d_bytes{0}, d2h_bytes{0};
     int sm_count = 0;
     // reusable scratch for sg_eval_costs (host-buffer path)
     double* d_pos = nullptr;
@@ -68,10 +80,38 @@ struct sg_window {
 
 namespace {
 
+// sg_last_error text per (calling thread, context): a failing call and the
+// caller's sg_last_error() see the same message even when other threads use
+// the context concurrently.
+std::unordered_map<const sg_ctx*, std::string>& last_errors() {
+    static thread_local std::unordered_map<const sg_ctx*, std::string> m;
+    return m;
+}
+
 int fail(sg_ctx* ctx, int code, const std::string& msg) {
-    if (ctx) ctx->err = msg;
+    if (ctx) last_errors()[ctx] = msg;
     return code;
 }
+
+using CtxLock = std::lock_guard<std::recursive_mutex>;
+
+// Every host <-> device copy of the engine goes through here (counted per
+// context, sg_ctx_copy_bytes).
+cudaError_t copy_async(sg_ctx* ctx, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
+    if (kind == cudaMemcpyHostToDevice) ctx->h2d_bytes += bytes;
+    else if (kind == cudaMemcpyDeviceToHost) ctx->d2h_bytes += bytes;
+    return cudaMemcpyAsync(dst, src, bytes, kind, st);
+}
+
+// NVTX range around an entry point (visible in nsys/ncu timelines; a no-op
+// without a tool attached).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+#define SG_ENTRY(ctx, name)       \
+    CtxLock sg_lock_((ctx)->mu);  \
+    NvtxRange sg_nvtx_(name)
 
 int cuda_fail(sg_ctx* ctx, cudaError_t e, const char* what) {
     const int code = e == cudaErrorMemoryAllocation ? SG_ERR_OUT_OF_MEMORY : SG_ERR_CUDA;
@@ -120,10 +160,9 @@ bool divisor_admits_two_op(double b) {
 
 // objectives.cpp:61-69 — scale of one compartment's residuals.
 double compartment_scale(const double* obs, int n) {
-    const double* lo = std::min_element(obs, obs + n);
-    const double* hi = std::max_element(obs, obs + n);
-    // std::minmax_element returns the first smallest and the last largest;
-    // only the values are used, and equal values are interchangeable.
+    // the same std::minmax_element as the reference: with NaN among the
+    // values the chosen elements depend on its comparison order
+    const auto [lo, hi] = std::minmax_element(obs, obs + n);
     const double range = *hi - *lo;
     return range > 0.0 ? 1.0 / range : 1.0 / std::max(1.0, std::fabs(*lo));
 }
@@ -242,6 +281,11 @@ int sg_ctx_create(int device, sg_ctx** out) {
 
 void sg_ctx_destroy(sg_ctx* ctx) {
     if (!ctx) return;
+    {
+        // wait for any call still inside the context before tearing it down
+        CtxLock wait_for_callers(ctx->mu);
+    }
+    last_errors().erase(ctx);
     cudaSetDevice(ctx->device);
     cudaFreeAsync(ctx->d_pos, ctx->stream);
     cudaFreeAsync(ctx->d_cost, ctx->stream);
@@ -255,17 +299,27 @@ void sg_ctx_destroy(sg_ctx* ctx) {
     delete ctx;
 }
 
-const char* sg_last_error(const sg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+const char* sg_last_error(const sg_ctx* ctx) {
+    if (!ctx) return "null context";
+    auto& m = last_errors();
+    auto it = m.find(ctx);
+    return it == m.end() ? "" : it->second.c_str();
+}
 
 }  // extern "C"
 
 void sg_set_last_error(sg_ctx* ctx, const std::string& message) {
-    if (ctx) ctx->err = message;
+    if (ctx) last_errors()[ctx] = message;
 }
 
 extern "C" {
 
-uint64_t sg_ctx_launch_count(const sg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+uint64_t sg_ctx_launch_count(const sg_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+void sg_ctx_copy_bytes(const sg_ctx* ctx, uint64_t* h2d, uint64_t* d2h) {
+    if (h2d) *h2d = ctx ? ctx->h2d_bytes.load() : 0;
+    if (d2h) *d2h = ctx ? ctx->d2h_bytes.load() : 0;
+}
 
 void* sg_ctx_stream(const sg_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
@@ -277,6 +331,7 @@ int sg_window_create(sg_ctx* ctx, const double* infectious, const double* recove
     if (!infectious || !recovered_cum || !deaths_cum)
         return fail(ctx, SG_ERR_INVALID_ARGUMENT, "window series must not be null");
     if (!valid_spec(family, metric)) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "unknown objective spec");
+    SG_ENTRY(ctx, "sg_window_create");
     // integrate_euler's guards (model.cpp:78-80)
     if (n_days < 1 || substeps < 1 || !(population > 0.0))
         return fail(ctx, SG_ERR_INVALID_ARGUMENT,
@@ -336,7 +391,10 @@ int sg_window_create(sg_ctx* ctx, const double* infectious, const double* recove
                 double e = o - pred[c];
                 if (family == SG_FAMILY_IRD_JOINT) e = e * d.scale[c];
                 const double e2 = e * e;
-                if (metric == SG_METRIC_MXSE) a = d.mxse_abs ? std::fabs(o - pred[c]) : ((0.0 < e2) ? e2 : 0.0);
+                // std::max(0.0, x) == (0.0 < x) ? x : 0.0 (objectives.cpp:22-26): a NaN residual
+                // leaves the accumulator at 0, in both forms
+                const double ad = std::fabs(o - pred[c]);
+                if (metric == SG_METRIC_MXSE) a = d.mxse_abs ? ((0.0 < ad) ? ad : 0.0) : ((0.0 < e2) ? e2 : 0.0);
                 else if (metric == SG_METRIC_MSE) a = 0.0 + e2;
                 else a = 0.0 + std::fabs(e);
             }
@@ -382,7 +440,7 @@ int sg_window_create(sg_ctx* ctx, const double* infectious, const double* recove
         std::memcpy(staging.data() + off_obs, obs.data(), obs_b);
         std::memcpy(staging.data() + off_robs, robs.data(), obs_b);
         std::memcpy(staging.data() + off_flag, flag.data(), flag.size());
-        e = cudaMemcpyAsync(block, staging.data(), total, cudaMemcpyHostToDevice, ctx->stream);
+        e = copy_async(ctx, block, staging.data(), total, cudaMemcpyHostToDevice, ctx->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     }
     if (e != cudaSuccess) {
@@ -400,6 +458,7 @@ int sg_window_create(sg_ctx* ctx, const double* infectious, const double* recove
 
 void sg_window_destroy(sg_window* w) {
     if (!w) return;
+    CtxLock lock(w->ctx->mu);
     if (w->d_block) cudaFreeAsync(w->d_block, w->ctx->stream);
     delete w;
 }
@@ -409,6 +468,7 @@ int sg_eval_costs_device(sg_window* w, const double* d_positions, size_t n, doub
     sg_ctx* ctx = w->ctx;
     if (n == 0) return SG_OK;
     if (!d_positions || !d_costs) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null device buffer");
+    SG_ENTRY(ctx, "sg_eval_costs_device");
     cudaStream_t st = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->stream;
     cudaError_t err = cudaSuccess;
     dispatch<EvalLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc, d_positions, n, d_costs,
@@ -425,6 +485,7 @@ int sg_eval_costs(sg_window* w, const double* positions, size_t n, size_t dim, d
     if (dim != 6) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "window objective expects 6-dim positions");
     if (n == 0) return SG_OK;
     if (!positions || !costs) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null host buffer");
+    SG_ENTRY(ctx, "sg_eval_costs");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     if (ctx->scratch_n < n) {
         cudaFreeAsync(ctx->d_pos, ctx->stream);
@@ -436,10 +497,10 @@ int sg_eval_costs(sg_window* w, const double* positions, size_t n, size_t dim, d
         SG_CUDA(ctx, dalloc(&ctx->d_cost, n, ctx->stream));
         ctx->scratch_n = n;
     }
-    SG_CUDA(ctx, cudaMemcpyAsync(ctx->d_pos, positions, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, ctx->d_pos, positions, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
     const int rc = sg_eval_costs_device(w, ctx->d_pos, n, ctx->d_cost, ctx->stream);
     if (rc) return rc;
-    SG_CUDA(ctx, cudaMemcpyAsync(costs, ctx->d_cost, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, costs, ctx->d_cost, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
     SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SG_OK;
 }
@@ -452,6 +513,7 @@ int sg_integrate_batch(sg_ctx* ctx, const double* params, size_t n, sg_state ini
                     "integrate_euler needs n_days >= 1, substeps >= 1 and a positive population");
     if (n == 0) return SG_OK;
     if (!params || !states || !finite) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null host buffer");
+    SG_ENTRY(ctx, "sg_integrate_batch");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     DevBufs b;
     b.st = ctx->stream;
@@ -462,14 +524,14 @@ int sg_integrate_batch(sg_ctx* ctx, const double* params, size_t n, sg_state ini
     SG_CUDA(ctx, b.alloc(&d_states, n * static_cast<size_t>(n_days) * 4));
     SG_CUDA(ctx, b.alloc(&d_fin, n));
     const double s0[4] = {init.S, init.I, init.R, init.D};
-    SG_CUDA(ctx, cudaMemcpyAsync(d_p, params, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
-    SG_CUDA(ctx, cudaMemcpyAsync(d_init, s0, sizeof s0, cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, d_p, params, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, d_init, s0, sizeof s0, cudaMemcpyHostToDevice, ctx->stream));
     const DevWindow w = integration_window(n_days, substeps, population);
     const int rc = launch_integrate(ctx, w, d_p, d_init, 0, 0, n, d_states, d_fin);
     if (rc) return rc;
-    SG_CUDA(ctx, cudaMemcpyAsync(states, d_states, sizeof(double) * n * n_days * 4, cudaMemcpyDeviceToHost,
+    SG_CUDA(ctx, copy_async(ctx, states, d_states, sizeof(double) * n * n_days * 4, cudaMemcpyDeviceToHost,
                                  ctx->stream));
-    SG_CUDA(ctx, cudaMemcpyAsync(finite, d_fin, n, cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, finite, d_fin, n, cudaMemcpyDeviceToHost, ctx->stream));
     SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SG_OK;
 }
@@ -482,6 +544,7 @@ int sg_integrate_states(sg_ctx* ctx, const double* params, const sg_state* inits
                     "integrate_euler needs n_days >= 1, substeps >= 1 and a positive population");
     if (n == 0) return SG_OK;
     if (!params || !inits || !states || !finite) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null host buffer");
+    SG_ENTRY(ctx, "sg_integrate_states");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     DevBufs b;
     b.st = ctx->stream;
@@ -491,14 +554,14 @@ int sg_integrate_states(sg_ctx* ctx, const double* params, const sg_state* inits
     SG_CUDA(ctx, b.alloc(&d_init, 4 * n));
     SG_CUDA(ctx, b.alloc(&d_states, n * static_cast<size_t>(n_days) * 4));
     SG_CUDA(ctx, b.alloc(&d_fin, n));
-    SG_CUDA(ctx, cudaMemcpyAsync(d_p, params, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
-    SG_CUDA(ctx, cudaMemcpyAsync(d_init, inits, sizeof(double) * 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, d_p, params, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, d_init, inits, sizeof(double) * 4 * n, cudaMemcpyHostToDevice, ctx->stream));
     const DevWindow w = integration_window(n_days, substeps, population);
     const int rc = launch_integrate(ctx, w, d_p, d_init, 4, 0, n, d_states, d_fin);
     if (rc) return rc;
-    SG_CUDA(ctx, cudaMemcpyAsync(states, d_states, sizeof(double) * n * n_days * 4, cudaMemcpyDeviceToHost,
+    SG_CUDA(ctx, copy_async(ctx, states, d_states, sizeof(double) * n * n_days * 4, cudaMemcpyDeviceToHost,
                                  ctx->stream));
-    SG_CUDA(ctx, cudaMemcpyAsync(finite, d_fin, n, cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, finite, d_fin, n, cudaMemcpyDeviceToHost, ctx->stream));
     SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SG_OK;
 }
@@ -513,6 +576,7 @@ int sg_integrate_states_r2(sg_ctx* ctx, const double* params, const sg_state* in
     if (n == 0) return SG_OK;
     if (!params || !inits || !observed_d || !states || !finite || !r2)
         return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null host buffer");
+    SG_ENTRY(ctx, "sg_integrate_states_r2");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     DevBufs b;
     b.st = ctx->stream;
@@ -525,18 +589,18 @@ int sg_integrate_states_r2(sg_ctx* ctx, const double* params, const sg_state* in
     SG_CUDA(ctx, b.alloc(&d_fin, n));
     SG_CUDA(ctx, b.alloc(&d_obs, nd));
     SG_CUDA(ctx, b.alloc(&d_r2, n));
-    SG_CUDA(ctx, cudaMemcpyAsync(d_p, params, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
-    SG_CUDA(ctx, cudaMemcpyAsync(d_init, inits, sizeof(double) * 4 * n, cudaMemcpyHostToDevice, ctx->stream));
-    SG_CUDA(ctx, cudaMemcpyAsync(d_obs, observed_d, sizeof(double) * nd, cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, d_p, params, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, d_init, inits, sizeof(double) * 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, d_obs, observed_d, sizeof(double) * nd, cudaMemcpyHostToDevice, ctx->stream));
     const DevWindow w = integration_window(n_days, substeps, population);
     const int rc = launch_integrate(ctx, w, d_p, d_init, 4, 0, n, d_states, d_fin);
     if (rc) return rc;
     r2_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, ctx->stream>>>(d_states, d_obs, n, n_days, d_r2);
     ctx->launches += 1;
     SG_CUDA(ctx, cudaGetLastError());
-    SG_CUDA(ctx, cudaMemcpyAsync(states, d_states, sizeof(double) * nd * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    SG_CUDA(ctx, cudaMemcpyAsync(finite, d_fin, n, cudaMemcpyDeviceToHost, ctx->stream));
-    SG_CUDA(ctx, cudaMemcpyAsync(r2, d_r2, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, states, d_states, sizeof(double) * nd * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, finite, d_fin, n, cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, r2, d_r2, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
     SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SG_OK;
 }
@@ -548,6 +612,7 @@ int sg_forecast_batch(sg_ctx* ctx, const double* params, const sg_state* junctio
         return fail(ctx, SG_ERR_INVALID_ARGUMENT, "forecast needs horizon >= 0, substeps >= 1, population > 0");
     if (n == 0) return SG_OK;
     if (!params || !junction || !states || !finite) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null host buffer");
+    SG_ENTRY(ctx, "sg_forecast_batch");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     const int n_days = horizon + 1;
     DevBufs b;
@@ -559,14 +624,14 @@ int sg_forecast_batch(sg_ctx* ctx, const double* params, const sg_state* junctio
     SG_CUDA(ctx, b.alloc(&d_states, n * static_cast<size_t>(n_days) * 4));
     SG_CUDA(ctx, b.alloc(&d_fin, n));
     static_assert(sizeof(sg_state) == 4 * sizeof(double), "sg_state layout");
-    SG_CUDA(ctx, cudaMemcpyAsync(d_p, params, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
-    SG_CUDA(ctx, cudaMemcpyAsync(d_init, junction, sizeof(double) * 4 * n, cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, d_p, params, sizeof(double) * 6 * n, cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, d_init, junction, sizeof(double) * 4 * n, cudaMemcpyHostToDevice, ctx->stream));
     const DevWindow w = integration_window(n_days, substeps, population);
     const int rc = launch_integrate(ctx, w, d_p, d_init, 4, 1, n, d_states, d_fin);
     if (rc) return rc;
-    SG_CUDA(ctx, cudaMemcpyAsync(states, d_states, sizeof(double) * n * n_days * 4, cudaMemcpyDeviceToHost,
+    SG_CUDA(ctx, copy_async(ctx, states, d_states, sizeof(double) * n * n_days * 4, cudaMemcpyDeviceToHost,
                                  ctx->stream));
-    SG_CUDA(ctx, cudaMemcpyAsync(finite, d_fin, n, cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, finite, d_fin, n, cudaMemcpyDeviceToHost, ctx->stream));
     SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SG_OK;
 }
@@ -742,9 +807,9 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     P.stride = g.n_total;
     P.hist_stride = g.iters;
     cudaStream_t st = ctx->stream;
-    SG_CUDA(ctx, cudaMemcpyAsync(g.d_sw, sw.data(), sizeof(DevSwarm) * sw.size(), cudaMemcpyHostToDevice, st));
-    SG_CUDA(ctx, cudaMemcpyAsync(g.d_cta, cta_swarm.data(), sizeof(uint32_t) * g.n_ctas, cudaMemcpyHostToDevice, st));
-    SG_CUDA(ctx, cudaMemcpyAsync(g.d_win, wtab.data(), sizeof(DevWindow) * wtab.size(), cudaMemcpyHostToDevice, st));
+    SG_CUDA(ctx, copy_async(ctx, g.d_sw, sw.data(), sizeof(DevSwarm) * sw.size(), cudaMemcpyHostToDevice, st));
+    SG_CUDA(ctx, copy_async(ctx, g.d_cta, cta_swarm.data(), sizeof(uint32_t) * g.n_ctas, cudaMemcpyHostToDevice, st));
+    SG_CUDA(ctx, copy_async(ctx, g.d_win, wtab.data(), sizeof(DevWindow) * wtab.size(), cudaMemcpyHostToDevice, st));
     std::vector<CtaTask> tasks(g.n_ctas);
     for (size_t c = 0; c < g.n_ctas; ++c) {
         const DevSwarm& s = sw[cta_swarm[c]];
@@ -760,11 +825,17 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
         t.times = w.times;
         t.obs = reinterpret_cast<const double*>(w.obs);
         const WindowLayout L = window_layout(w.n_days, w.substeps, w.metric);
-        t.times_bytes = static_cast<uint16_t>(L.times_bytes);
-        t.obs_bytes = static_cast<uint16_t>(L.obs_bytes);
-        t.substeps = static_cast<uint32_t>(uses_time_table(w.n_days, w.substeps) ? w.substeps : 0);
+        // field widths: the table is at most kMaxTgrid entries (+ subh), the
+        // observations at most the 200 KB window limit of sg_window_create
+        // (windows without a table stage cooperatively and ignore both sizes)
+        const bool table = uses_time_table(w.n_days, w.substeps);
+        if (table && (L.times_bytes > 0xFFFF || w.substeps > 0xFFFF || L.obs_bytes > 0xFFFFFFFFu))
+            return fail(ctx, SG_ERR_INVALID_ARGUMENT, "window too large for the step kernel's staging");
+        t.times_bytes = static_cast<uint16_t>(table ? L.times_bytes : 0);
+        t.obs_bytes = static_cast<uint32_t>(L.obs_bytes);
+        t.substeps = static_cast<uint16_t>(table ? w.substeps : 0);
     }
-    SG_CUDA(ctx, cudaMemcpyAsync(g.d_task, tasks.data(), sizeof(CtaTask) * tasks.size(), cudaMemcpyHostToDevice, st));
+    SG_CUDA(ctx, copy_async(ctx, g.d_task, tasks.data(), sizeof(CtaTask) * tasks.size(), cudaMemcpyHostToDevice, st));
     SG_CUDA(ctx, cudaStreamSynchronize(st));  // host vectors go out of scope
     return SG_OK;
 }
@@ -872,6 +943,7 @@ int sg_plan_create(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg
     if (!ctx || !out) return SG_ERR_INVALID_ARGUMENT;
     *out = nullptr;
     if (n_swarms > 0 && !swarms) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null swarm array");
+    SG_ENTRY(ctx, "sg_plan_create");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     sg_plan* plan = new (std::nothrow) sg_plan;
     if (!plan) return fail(ctx, SG_ERR_OUT_OF_MEMORY, "host allocation failed");
@@ -899,12 +971,12 @@ int sg_plan_create(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg
     for (size_t k = 0; k < n_swarms; ++k) {
         if (!swarm_config_valid(swarms[k], &why)) {
             plan->status[k] = SG_ERR_INVALID_ARGUMENT;
-            ctx->err = why;
+            fail(ctx, SG_ERR_INVALID_ARGUMENT, why);
             continue;
         }
         if (swarms[k].window->ctx != ctx) {
             plan->status[k] = SG_ERR_INVALID_ARGUMENT;
-            ctx->err = "swarm window belongs to another context";
+            fail(ctx, SG_ERR_INVALID_ARGUMENT, "swarm window belongs to another context");
             continue;
         }
         const DevWindow& w = swarms[k].window->host;
@@ -942,6 +1014,7 @@ int sg_plan_create(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg
 int sg_plan_run(sg_plan* plan) {
     if (!plan) return SG_ERR_INVALID_ARGUMENT;
     sg_ctx* ctx = plan->ctx;
+    SG_ENTRY(ctx, "sg_plan_run");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     for (SwarmGroup* g : plan->groups) {
         int rc = seed_group(ctx, *g);
@@ -955,6 +1028,7 @@ int sg_plan_run(sg_plan* plan) {
 int sg_plan_run_timed(sg_plan* plan, double* seed_ms, double* steps_ms) {
     if (!plan || !seed_ms || !steps_ms) return SG_ERR_INVALID_ARGUMENT;
     sg_ctx* ctx = plan->ctx;
+    SG_ENTRY(ctx, "sg_plan_run_timed");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     cudaEvent_t ev[3];
     for (cudaEvent_t& e : ev) SG_CUDA(ctx, cudaEventCreate(&e));
@@ -995,6 +1069,7 @@ uint64_t sg_plan_step_launches(const sg_plan* plan) {
 int sg_plan_results(sg_plan* plan, sg_swarm_result* results) {
     if (!plan || (!results && plan->n_desc)) return SG_ERR_INVALID_ARGUMENT;
     sg_ctx* ctx = plan->ctx;
+    SG_ENTRY(ctx, "sg_plan_results");
     if (!plan->ran) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "plan has not been run");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     for (size_t k = 0; k < plan->n_desc; ++k) {
@@ -1007,9 +1082,9 @@ int sg_plan_results(sg_plan* plan, sg_swarm_result* results) {
     for (SwarmGroup* g : plan->groups) {
         std::vector<DevSwarmState> state(g->idx.size());
         std::vector<double> hist(g->idx.size() * g->iters);
-        SG_CUDA(ctx, cudaMemcpyAsync(state.data(), g->d_state, sizeof(DevSwarmState) * state.size(),
+        SG_CUDA(ctx, copy_async(ctx, state.data(), g->d_state, sizeof(DevSwarmState) * state.size(),
                                      cudaMemcpyDeviceToHost, ctx->stream));
-        SG_CUDA(ctx, cudaMemcpyAsync(hist.data(), g->P.history, sizeof(double) * hist.size(), cudaMemcpyDeviceToHost,
+        SG_CUDA(ctx, copy_async(ctx, hist.data(), g->P.history, sizeof(double) * hist.size(), cudaMemcpyDeviceToHost,
                                      ctx->stream));
         SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
         for (size_t j = 0; j < g->idx.size(); ++j) {
@@ -1031,10 +1106,11 @@ uint64_t sg_plan_evals(const sg_plan* plan) { return plan ? plan->evals : 0; }
 uint64_t sg_plan_ramp_substeps(sg_plan* plan) {
     if (!plan || !plan->ran) return 0;
     sg_ctx* ctx = plan->ctx;
+    CtxLock lock(ctx->mu);
     uint64_t total = 0;
     for (SwarmGroup* g : plan->groups) {
         std::vector<DevSwarmState> state(g->idx.size());
-        if (cudaMemcpyAsync(state.data(), g->d_state, sizeof(DevSwarmState) * state.size(), cudaMemcpyDeviceToHost,
+        if (copy_async(ctx, state.data(), g->d_state, sizeof(DevSwarmState) * state.size(), cudaMemcpyDeviceToHost,
                             ctx->stream) != cudaSuccess ||
             cudaStreamSynchronize(ctx->stream) != cudaSuccess)
             return 0;
@@ -1045,6 +1121,7 @@ uint64_t sg_plan_ramp_substeps(sg_plan* plan) {
 
 void sg_plan_destroy(sg_plan* plan) {
     if (!plan) return;
+    CtxLock lock(plan->ctx->mu);
     cudaSetDevice(plan->ctx->device);
     delete plan;
 }
@@ -1066,6 +1143,7 @@ int sg_fit_swarms(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg_
     if (!ctx) return SG_ERR_INVALID_ARGUMENT;
     if (n_swarms == 0) return SG_OK;
     if (!swarms || !results) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null swarm arrays");
+    SG_ENTRY(ctx, "sg_fit_swarms");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     // Split oversized calls into sequential plans that fit in 70% of the
     // free memory; the (slow, driver-locking) memory query only runs when
@@ -1144,6 +1222,7 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
         if (!std::isfinite(lower[k]) || !std::isfinite(upper[k]) || lower[k] > upper[k])
             return fail(ctx, SG_ERR_INVALID_ARGUMENT, "pso: bound " + std::to_string(k) + " is invalid");
     if (n == 0) return SG_OK;
+    SG_ENTRY(ctx, "sg_forecast_ensemble");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     DevBufs b;
     b.st = ctx->stream;
@@ -1153,8 +1232,8 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
     if (costs) SG_CUDA(ctx, b.alloc(&d_cost, n));
     if (params_out) SG_CUDA(ctx, b.alloc(&d_par, 6 * n));
     SG_CUDA(ctx, b.alloc(&d_D, n * static_cast<size_t>(horizon + 1)));
-    SG_CUDA(ctx, cudaMemcpyAsync(d_lo, lower, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    SG_CUDA(ctx, cudaMemcpyAsync(d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, d_lo, lower, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     DevWindow fwin = integration_window(horizon + 1, w->host.substeps, w->host.N);
     uint32_t* perm = nullptr;
     double* planes = nullptr;
@@ -1166,10 +1245,10 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
                              &err);
     ctx->launches += 1;
     if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
-    if (costs) SG_CUDA(ctx, cudaMemcpyAsync(costs, d_cost, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (costs) SG_CUDA(ctx, copy_async(ctx, costs, d_cost, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     if (params_out)
-        SG_CUDA(ctx, cudaMemcpyAsync(params_out, d_par, 6 * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    SG_CUDA(ctx, cudaMemcpyAsync(deaths_out, d_D, n * (horizon + 1) * sizeof(double), cudaMemcpyDeviceToHost,
+        SG_CUDA(ctx, copy_async(ctx, params_out, d_par, 6 * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, deaths_out, d_D, n * (horizon + 1) * sizeof(double), cudaMemcpyDeviceToHost,
                                  ctx->stream));
     SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SG_OK;
@@ -1258,6 +1337,7 @@ int sg_forecast_ensemble_bands(sg_window* w, const double lower[6], const double
     if (!lower || !upper || !bands || !counts) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null buffer");
     if (const int rc = check_bands_args(ctx, lower, upper, n, horizon)) return rc;
     const int n_days = horizon + 1;
+    SG_ENTRY(ctx, "sg_forecast_ensemble_bands");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     DevBufs b;
     b.st = ctx->stream;
@@ -1268,15 +1348,15 @@ int sg_forecast_ensemble_bands(sg_window* w, const double lower[6], const double
     if (costs && n) SG_CUDA(ctx, b.alloc(&d_cost, n));
     SG_CUDA(ctx, b.alloc(&d_bands, 7 * static_cast<size_t>(n_days)));
     SG_CUDA(ctx, b.alloc(&d_counts, n_days));
-    SG_CUDA(ctx, cudaMemcpyAsync(d_lo, lower, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    SG_CUDA(ctx, cudaMemcpyAsync(d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, d_lo, lower, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     if (const int rc = enqueue_bands(ctx, w, b, ctx->stream, d_lo, d_hi, seed, n, horizon, d_cost, d_bands, d_counts))
         return rc;
     static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "count width");
-    SG_CUDA(ctx, cudaMemcpyAsync(bands, d_bands, 7 * n_days * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    SG_CUDA(ctx, cudaMemcpyAsync(counts, d_counts, n_days * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, bands, d_bands, 7 * n_days * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, counts, d_counts, n_days * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
     if (costs && n)
-        SG_CUDA(ctx, cudaMemcpyAsync(costs, d_cost, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        SG_CUDA(ctx, copy_async(ctx, costs, d_cost, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SG_OK;
 }
@@ -1293,6 +1373,7 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
             return fail(ctx, SG_ERR_INVALID_ARGUMENT, "windows must be non-null and share one context");
     if (const int rc = check_bands_args(ctx, lower, upper, n, horizon)) return rc;
     const int n_days = horizon + 1;
+    SG_ENTRY(ctx, "sg_forecast_ensemble_bands_batch");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     if (const int rc = ensure_lanes(ctx)) return rc;
     DevBufs b;
@@ -1303,8 +1384,8 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
     SG_CUDA(ctx, b.alloc(&d_hi, 6));
     SG_CUDA(ctx, b.alloc(&d_bands, 7 * static_cast<size_t>(n_days) * n_windows));
     SG_CUDA(ctx, b.alloc(&d_counts, static_cast<size_t>(n_days) * n_windows));
-    SG_CUDA(ctx, cudaMemcpyAsync(d_lo, lower, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    SG_CUDA(ctx, cudaMemcpyAsync(d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, d_lo, lower, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     // Windows alternate between two side streams, so one window's band
     // selection (small kernels) overlaps the next window's evaluation.
     constexpr int kBandStreams = 2;
@@ -1325,9 +1406,9 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
         SG_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join[l], 0));
     }
     if (rc) return rc;
-    SG_CUDA(ctx, cudaMemcpyAsync(bands, d_bands, 7 * n_days * n_windows * sizeof(double), cudaMemcpyDeviceToHost,
+    SG_CUDA(ctx, copy_async(ctx, bands, d_bands, 7 * n_days * n_windows * sizeof(double), cudaMemcpyDeviceToHost,
                                  ctx->stream));
-    SG_CUDA(ctx, cudaMemcpyAsync(counts, d_counts, n_days * n_windows * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+    SG_CUDA(ctx, copy_async(ctx, counts, d_counts, n_days * n_windows * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                  ctx->stream));
     SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SG_OK;
@@ -1387,6 +1468,7 @@ __global__ void __launch_bounds__(256) fp64_probe_kernel(double* out, int iters,
 
 extern "C" int sg_probe_fp64_rate(sg_ctx* ctx, double* ops_per_s) {
     if (!ctx || !ops_per_s) return SG_ERR_INVALID_ARGUMENT;
+    SG_ENTRY(ctx, "sg_probe_fp64_rate");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     DevBufs b;
     b.st = ctx->stream;

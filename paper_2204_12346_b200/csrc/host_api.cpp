@@ -777,6 +777,28 @@ int sg_fit_all_windows_series(sg_ctx* ctx, const double* I, const double* R, con
     });
 }
 
+int sg_fit_window_range_series(sg_ctx* ctx, const double* I, const double* R, const double* D, size_t n_series,
+                               uint64_t tau, uint64_t delta, const sg_fit_settings* s, uint64_t base_seed,
+                               uint64_t first_window, uint64_t max_windows, size_t* n_windows, sg_fit_record* records,
+                               double* trajectories) {
+    if (!ctx || !I || !R || !D || !s || !n_windows || (max_windows && !records)) return SG_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        const EpiSeries data = series_of(I, R, D, n_series);
+        const WindowScheme scheme{static_cast<std::size_t>(tau), static_cast<std::size_t>(delta)};
+        const std::vector<Window> all = make_windows(data.size(), scheme);  // calibration.cpp:193
+        const std::size_t begin = std::min<std::size_t>(first_window, all.size());
+        const std::size_t end = std::min<std::size_t>(begin + max_windows, all.size());
+        std::vector<Job> jobs;
+        for (std::size_t w = begin; w < end; ++w) jobs.push_back(Job{all[w], mix_seed(base_seed, all[w].index)});
+        const std::vector<JobOutcome> out = fit_jobs(data, jobs, settings_of(*s));
+        for (std::size_t k = 0; k < out.size(); ++k) {
+            record_of(out[k].fit, out[k].status, records + k);
+            if (trajectories) trajectory_out(out[k].fit, trajectories + k * (tau + 1) * 4);
+        }
+        *n_windows = out.size();
+    });
+}
+
 int sg_stability_study_series(sg_ctx* ctx, const double* I, const double* R, const double* D, size_t n_series,
                               uint64_t start, uint64_t length, const sg_fit_settings* s, uint64_t repetitions,
                               uint64_t horizon, uint64_t base_seed, sg_fit_record* records, double* day_bands,

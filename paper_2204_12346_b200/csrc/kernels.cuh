@@ -37,6 +37,9 @@ namespace sirdgpu {
 constexpr int kEvalThreads = 128;
 constexpr int kStepThreads = SG_STEP_THREADS;
 constexpr int kNP = 1;  // particles per thread in the flat step kernel (2, interleaved, measured slower)
+// pso_step_kernel evaluates slot 0 only: raising kNP needs an evaluation loop
+// over the slots first, or idle slots would enter finish_step with cost 0.
+static_assert(kNP == 1, "pso_step_kernel evaluates one particle per thread");
 constexpr int kStepWarps = kStepThreads / 32;
 
 // Shared-memory staging of one window: the descriptor in static shared memory,
@@ -533,8 +536,8 @@ struct CtaTask {
     const double* times;     // its substep-time table (device)
     const double* obs;       // obs | robs | flags, 16-byte padded sections (device)
     uint16_t times_bytes;    // 16-byte multiples (<= 38.5 KB: the table is at most kMaxTgrid entries)
-    uint16_t obs_bytes;
-    uint32_t substeps;       // the window's substep count when it has a t_k table, else 0
+    uint16_t substeps;       // the window's substep count when it has a t_k table (<= kMaxTgrid), else 0
+    uint32_t obs_bytes;      // 24 B per day: beyond 16 bits from 2,731 days on (still inside the 200 KB window)
 };
 static_assert(sizeof(CtaTask) == 64, "one 64-byte record per CTA");
 

@@ -37,7 +37,7 @@ def test_engine_line():
     d = _line(["--steps", "3", "--warmup", "3", "--iters", "5", "--no-cpu"], 600)
     assert BASE_KEYS <= set(d)
     assert {"e2e", "roofline", "clocks", "gpu_launches"} <= set(d)
-    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["scaling"] == "weak"
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["scaling"] == "strong"
     r = d["roofline"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r)
     assert 0.0 < r["frac"] < 1.0
@@ -61,3 +61,36 @@ def test_reference_arm_under_torchrun():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+@pytest.mark.gpu
+def test_engine_line_carries_parity_and_one_thread_baseline():
+    """The cpu_baseline leg's whole-window reference fits are compared bit for
+    bit with the device plan; short iterations keep the
+    CPU leg to seconds."""
+    d = _line(["--steps", "3", "--warmup", "3", "--iters", "20", "--cpu-budget", "2", "--cpu1-budget", "0.5"], 900)
+    assert d["parity"]["bit_exact"] is True and len(d["parity"]["windows"]) >= 1
+    assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["value_1thread"] > 0
+    assert d["roofline"]["frac"] == pytest.approx(d["roofline"]["achieved"] / d["roofline"]["peak"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("split", ["windows", "restarts"])
+def test_engine_arm_under_torchrun(split):
+    """The ours arm's N>1 path: two ranks share cuda:0
+    over gloo (functional only — value is the shared GPU's throughput); rank 0
+    prints one line with n_gpus == 2, the other rank prints nothing."""
+    import os
+    env = dict(os.environ, SG_BENCH_BACKEND="gloo")
+    port = 29541 if split == "windows" else 29543
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), "--gpus", "2", "--steps", "3",
+           "--warmup", "3", "--iters", "10", "--split", split, "--cpu-budget", "1", "--cpu1-budget", "0.3"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["split"] == split
+    assert d["scaling"] == ("strong" if split == "windows" else "weak")
+    assert d["cpu_baseline"]["value"] > 0 and d["parity"]["bit_exact"] is True

@@ -63,3 +63,31 @@ def test_cpp_api_matches_python_api(demo):
     win = eng.Window(sf.context(), I, R, D, [N - I[0] - R[0] - D[0], I[0], R[0], D[0]], N, "ird-mape")
     costs = win.eval_costs(np.array([[0.3, 0.2, 5.0, 20.0, 0.1, 0.01], [1.5, 0.05, 30.0, 2.0, 0.5, 0.002]]))
     assert (got["objective.cost0"], got["objective.cost1"]) == (costs[0], costs[1])
+
+
+@pytest.fixture(scope="module")
+def threads_demo(tmp_path_factory):
+    if not LIB.exists():
+        pytest.skip("libsirdgpu.so not built")
+    if shutil.which("g++") is None:
+        pytest.skip("no g++")
+    exe = tmp_path_factory.mktemp("cpp") / "threads_demo"
+    subprocess.run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-pthread", f"-I{ROOT / 'include'}",
+                    str(ROOT / "tests" / "cpp" / "threads_demo.cpp"), "-o", str(exe), f"-L{LIB.parent}", "-lsirdgpu",
+                    f"-Wl,-rpath,{LIB.parent}"], check=True)
+    return exe
+
+
+def test_cpp_threads_demo_compiles(threads_demo):
+    assert threads_demo.exists()
+
+
+@pytest.mark.gpu
+def test_shared_context_is_reentrant(threads_demo):
+    """Four threads share objectives of one context (scratch regrowth
+    included) while a fifth runs fit_window: every result equals the
+    single-threaded one bit for bit (host_api.cpp:92)."""
+    from conftest import GOLDEN
+    out = subprocess.run([str(threads_demo), str(GOLDEN / "poland_like.csv")], capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0 and out.stdout.startswith("threads ok"), out.stdout + out.stderr

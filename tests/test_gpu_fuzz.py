@@ -124,3 +124,55 @@ def test_mxse_largest_residual_shortcut_edges(ctx, port, poland, edge):
     for spec in ("ird-mxse", "d-mxse", "ird-mse"):
         w = eng.Window(ctx, I, R, D, init, N, spec)
         assert_bitwise(w.eval_costs(pos), port.eval_costs(spec, I, R, D, init, N, pos), f"{edge} {spec}")
+
+
+@pytest.mark.parametrize("edge", ["I0", "R0", "D0", "I0_mid"])
+def test_nan_first_observation(ctx, port, reference, poland, edge):
+    """A NaN first observation (init supplied separately, as
+    make_window_objective allows): the reference seeds MXSE with
+    std::max(0.0, NaN) = 0 and picks the IRD scale with std::minmax_element
+    over a NaN-led series (engine.cu:339).  Checked against the
+    reference itself, all specs."""
+    import paper_2204_12346_b200 as eng
+    a = 120
+    I, R, D = (poland[k][a:a + 36].copy() for k in ("I", "R", "D"))
+    N = poland["N"]
+    init = [N - I[0] - R[0] - D[0], I[0], R[0], D[0]]
+    {"I0": I, "R0": R, "D0": D, "I0_mid": I}[edge][0] = np.nan
+    if edge == "I0_mid":
+        D[17] = np.nan
+    rng = np.random.default_rng(4)
+    pos = rng.uniform([0, 0, 0, 0, 0, 0], [2, 2, 28, 28, 1, 0.1], (300, 6))
+    for spec in SPECS:
+        w = eng.Window(ctx, I, R, D, init, N, spec)
+        assert_bitwise(w.eval_costs(pos), reference.eval_costs(spec, I, R, D, init, N, pos), f"{edge} {spec}")
+
+
+def test_long_window_one_substep_flat_plan(ctx, port):
+    """substeps = 1 and a ~3,000-day window keep the substep-time table
+    (SUB = -1 kernels, bulk-copied staging) and 72 KB of observations: the
+    CTA task's byte counts no longer fit 16 bits (engine.cu:764).
+    A flat plan (more swarms than one wave of clusters) must follow optimize()."""
+    import paper_2204_12346_b200 as eng
+    n_days = 3001
+    N = 5e6
+    st, fin = port.integrate([0.12, 0.08, 700.0, 1900.0, 0.1, 0.003], [N - 50, 50, 0, 0], N, n_days, 1)
+    assert fin
+    I, R, D = st[:, 1].copy(), st[:, 2].copy(), st[:, 3].copy()
+    rng = np.random.default_rng(5)
+    D *= rng.uniform(0.98, 1.02, n_days)
+    init = list(st[0])
+    hi = [0.3, 0.3, float(n_days - 1), float(n_days - 1), 0.3, 0.01]
+    for spec in ("ird-mxse", "d-mape"):
+        w = eng.Window(ctx, I, R, D, init, N, spec, substeps=1)
+        swarms = [dict(window=w, lower=[0.0] * 6, upper=hi, n_particles=1100, max_iters=3, seed=31)]
+        swarms += [dict(window=w, lower=[0.0] * 6, upper=hi, n_particles=1, max_iters=1, seed=j) for j in range(300)]
+        got = ctx.fit_swarms(swarms)
+        for k in (0, 1, 299):
+            s = swarms[k]
+            rc, best, cost, hist = port.fit_swarm(spec, I, R, D, init, N, s["lower"], s["upper"], s["n_particles"],
+                                                  s["max_iters"], seed=s["seed"], substeps=1)
+            assert got[k][0] == rc
+            assert_bitwise(got[k][3], hist, f"{spec} swarm {k} history")
+            if rc == 0:
+                assert_bitwise(got[k][1], best, f"{spec} swarm {k} best")
