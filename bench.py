@@ -244,7 +244,7 @@ def _window_inputs(I, R, D, w):
     return I[sl], R[sl], D[sl], [POPULATION - I[a] - R[a] - D[a], I[a], R[a], D[a]]
 
 
-def cpu_reference_sample(I, R, D, budget_s=12.0, threads=None, windows=None, base=BASE_SEED):
+def cpu_reference_sample(I, R, D, budget_s=12.0, threads=None, windows=None, base=BASE_SEED, max_iters=ITERS):
     """The reference C++ (oracle/_ref) or, absent, the C restatement, on the
     host cores: whole window swarms of the sweep (PARTICLES particles, up to
     ITERS iterations, the workload's seeds mix_seed(base, w)), windows in
@@ -266,7 +266,7 @@ def cpu_reference_sample(I, R, D, budget_s=12.0, threads=None, windows=None, bas
 
     order = stratified(windows if windows is not None else range(n_windows(len(I))))
     t2, _ = run(order[0], 2, threads)
-    iters = int(max(2, min(ITERS, budget_s / max(t2 / 2, 1e-6))))
+    iters = int(max(min(2, max_iters), min(max_iters, budget_s / max(t2 / 2, 1e-6))))
     spent, evals, sampled = 0.0, 0, []
     for w in order:
         dt, out = run(w, iters, threads)
@@ -280,7 +280,7 @@ def cpu_reference_sample(I, R, D, budget_s=12.0, threads=None, windows=None, bas
                                           "evals": evals, "seconds": spent}, results
 
 
-def cpu_reference_one_thread(I, R, D, budget_s=3.0, w=69, base=BASE_SEED):
+def cpu_reference_one_thread(I, R, D, budget_s=3.0, w=69, base=BASE_SEED, max_iters=ITERS):
     """The same reference path on ONE host thread (SURVEY.md
     §8d: the reference is sometimes faster single-threaded, since
     parallel_for spawns threads per call): one window, a bounded number of
@@ -292,7 +292,7 @@ def cpu_reference_one_thread(I, R, D, budget_s=3.0, w=69, base=BASE_SEED):
     ora.fit_swarm(SPEC, Iw, Rw, Dw, init, POPULATION, [0.0] * 6, STAGE2_HI, PARTICLES, 2, seed=mix_seed(base, w),
                   n_threads=1)
     per_iter = (time.perf_counter() - t) / 2
-    iters = int(max(2, min(ITERS, budget_s / max(per_iter, 1e-6))))
+    iters = int(max(min(2, max_iters), min(max_iters, budget_s / max(per_iter, 1e-6))))
     t = time.perf_counter()
     ora.fit_swarm(SPEC, Iw, Rw, Dw, init, POPULATION, [0.0] * 6, STAGE2_HI, PARTICLES, iters, seed=mix_seed(base, w),
                   n_threads=1)
@@ -496,8 +496,9 @@ def bench_ours(args):
     cpu, parity = None, None
     if rank == 0 and not args.no_cpu:
         v, kind, cores, sample, cpu_res = cpu_reference_sample(I, R, D, budget_s=args.cpu_budget, windows=mine,
-                                                               base=base)
-        v1, sample1 = cpu_reference_one_thread(I, R, D, budget_s=args.cpu1_budget, w=mine[len(mine) // 2], base=base)
+                                                               base=base, max_iters=iters)
+        v1, sample1 = cpu_reference_one_thread(I, R, D, budget_s=args.cpu1_budget, w=mine[len(mine) // 2], base=base,
+                                               max_iters=iters)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                "sample": f"windows {sample['windows']} of the sweep, {PARTICLES} particles x {sample['iterations']} "
                          f"iterations each ({sample['evals']} evals, {sample['seconds']:.1f} s)",

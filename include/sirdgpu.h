@@ -182,6 +182,51 @@ uint64_t sg_plan_step_launches(const sg_plan* plan);  /* fused step launches per
 uint64_t sg_plan_ramp_substeps(sg_plan* plan);
 void sg_plan_destroy(sg_plan* plan);
 
+/* --- the general swarm: Swarm / optimize for any objective -----------------
+ * Swarm (pso.hpp:56-86, pso.cpp:47-127) of any dimension with its state in
+ * device memory: positions, velocities and personal bests row-major n x dim,
+ * one mt19937_64(mix_seed(seed, i)) per particle.  A step is: put the costs
+ * of the current positions (sg_gswarm_set_costs from a host objective, or
+ * sg_gswarm_eval_window for a window objective, evaluated on the device),
+ * then sg_gswarm_step = personal bests, global best, move (+ repair when
+ * repair_time_order).  An arbitrary host repair hook is applied by the caller
+ * between steps through get/set_positions.  Bit-identical to the reference's
+ * Swarm for the same seeds.  (The fused many-swarm plans above are the fast
+ * path for window objectives.) */
+typedef struct sg_gswarm sg_gswarm;
+int sg_gswarm_create(sg_ctx* ctx, int dim, const double* lower, const double* upper, uint64_t n_particles,
+                     double inertia, double cognitive, double social, uint64_t seed, int repair_time_order,
+                     sg_gswarm** out);
+void sg_gswarm_destroy(sg_gswarm* swarm);
+const double* sg_gswarm_positions_device(const sg_gswarm* swarm);  /* n x dim, row-major */
+double* sg_gswarm_costs_device(sg_gswarm* swarm);                  /* n                    */
+int sg_gswarm_get_positions(sg_gswarm* swarm, double* positions);  /* n x dim host copy    */
+int sg_gswarm_set_positions(sg_gswarm* swarm, const double* positions);
+/* Initial positions after a host repair hook: also resets the personal-best
+ * positions to them (Swarm::Swarm repairs before pbest = x, pso.cpp:70-74). */
+int sg_gswarm_set_initial_positions(sg_gswarm* swarm, const double* positions);
+int sg_gswarm_set_costs(sg_gswarm* swarm, const double* costs);
+int sg_gswarm_eval_window(sg_gswarm* swarm, sg_window* window);   /* dim 6: costs on the device */
+/* pso.cpp:83-98 (everything of Swarm::step after the objective); *best_cost
+ * (optional) receives best_cost_ after the step. */
+int sg_gswarm_step(sg_gswarm* swarm, double* best_cost);
+int sg_gswarm_best(sg_gswarm* swarm, double* best_position, double* best_cost);
+
+/* --- scoring of given trajectories ---------------------------------------
+ * objective_value (objectives.cpp:95-120) of n trajectories (states: n x
+ * n_days x 4; finite: n flags or NULL) against one observed window (three
+ * series of n_days), on the device. */
+int sg_objective_values(sg_ctx* ctx, int family, int metric, const double* infectious, const double* recovered_cum,
+                        const double* deaths_cum, size_t n_days, const double* states, const uint8_t* finite, size_t n,
+                        double* costs);
+/* metric_value (objectives.cpp:72-81) of n series pairs (observed,
+ * predicted: n x n_days each). */
+int sg_metric_values(sg_ctx* ctx, int metric, const double* observed, const double* predicted, size_t n_days,
+                     size_t n, double* out);
+/* sird_rhs (model.cpp:66-74) for n (state, beta, gamma, mu) at one population. */
+int sg_sird_rhs_batch(sg_ctx* ctx, const sg_state* states, const double* beta, const double* gamma, const double* mu,
+                      double population, size_t n, sg_state* out);
+
 /* --- forecast ---------------------------------------------------------------
  * forecast_extension (calibration.cpp:298-322), batched: for each k, holds
  * beta = beta2 and integrates horizon+1 days from junction[k] (the fitted

@@ -8,6 +8,10 @@ arm import this module, as the checker.  The product package never does.
     load("hybrid")     -> oracle/_ref/libsirdhybrid.so: the reference's own
                           Swarm driving the GPU objective through the C-ABI
                           (the drop-in under test)
+
+build("refcallers") also builds the reference's own callers (acceptance
+harness, pybind module) against the unmodified reference and against
+ref_binding/ into oracle/_ref/.
 """
 from __future__ import annotations
 
@@ -49,8 +53,11 @@ def build(kind: str = "all") -> None:
         targets.append("ref")
     if kind in ("all", "hybrid") and REFERENCE_SRC.exists() and ENGINE_SO.exists():
         targets.append("hybrid")
+    if kind in ("all", "refcallers") and REFERENCE_SRC.exists() and ENGINE_SO.exists():
+        targets.append("refcallers")
     if targets:
-        subprocess.run(["make", "-s", "-C", str(ORACLE_DIR), *targets], check=True)
+        subprocess.run(["make", "-s", "-j", str(min(16, os.cpu_count() or 1)), "-C", str(ORACLE_DIR), *targets],
+                       check=True)
 
 
 _FIT_SWARM_ARGS = [ctypes.c_int, ctypes.c_int, _dp, _dp, _dp, ctypes.c_int, _dp, ctypes.c_double, ctypes.c_int,

@@ -7,27 +7,15 @@
 // is produced by the kernels in kernels.cuh.
 #include "sirdgpu.h"
 
-#include "engine_internal.h"
+#include "engine_core.cuh"
 #include "launchers.cuh"
 
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <mutex>
 #include <new>
-#include <string>
-#include <unordered_map>
-#include <vector>
-
-#include <nvtx3/nvToolsExt.h>
-
-using namespace sirdgpu;
 
 // The launchers of the templated kernels are instantiated in family.cu (one
 // object per objective family, compiled in parallel by build.py).
@@ -36,101 +24,7 @@ SG_LAUNCH_FAMILY(extern, 0)
 SG_LAUNCH_FAMILY(extern, 1)
 }  // namespace sirdgpu
 
-// Independent swarm partitions run as separate launch sequences on their own
-// streams so one partition's per-iteration tail overlaps the next
-// partition's iteration (swarms never synchronise with each other).
-#ifndef SG_LANES
-#define SG_LANES 4
-#endif
-constexpr int kMaxLanes = SG_LANES;
-
-struct sg_ctx {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    // Every entry point that touches the context's stream, scratch buffers,
-    // lanes or plans holds this lock, so threads may share one context (the
-    // reference's objectives are reentrant); the C++ layer nests calls, hence
-    // recursive.  Error texts are kept per calling thread (last_errors()).
-    std::recursive_mutex mu;
-    std::atomic<uint64_t> launches{0};
-    // host <-> device bytes copied by the context's calls (telemetry: the
-    // e2e byte counts of bench.py)
-    std::atomic<uint64_t> h2d_bytes{0}, d2h_bytes{0};
-    int sm_count = 0;
-    // reusable scratch for sg_eval_costs (host-buffer path)
-    double* d_pos = nullptr;
-    double* d_cost = nullptr;
-    size_t scratch_n = 0;
-    // side streams for concurrent swarm partitions (see step_group)
-    cudaStream_t side[kMaxLanes] = {};
-    cudaEvent_t fork = nullptr;
-    cudaEvent_t join[kMaxLanes] = {};
-};
-
-struct sg_window {
-    sg_ctx* ctx = nullptr;
-    DevWindow host{};          // device pointers inside
-    DevWindow* d_desc = nullptr;
-    ObsDay* d_obs = nullptr;
-    ObsDay* d_robs = nullptr;
-    unsigned char* d_flag = nullptr;
-    unsigned char* d_block = nullptr;  // the one allocation holding desc/obs/robs/flags
-    size_t smem = 0;
-};
-
 namespace {
-
-// sg_last_error text per (calling thread, context): a failing call and the
-// caller's sg_last_error() see the same message even when other threads use
-// the context concurrently.
-std::unordered_map<const sg_ctx*, std::string>& last_errors() {
-    static thread_local std::unordered_map<const sg_ctx*, std::string> m;
-    return m;
-}
-
-int fail(sg_ctx* ctx, int code, const std::string& msg) {
-    if (ctx) last_errors()[ctx] = msg;
-    return code;
-}
-
-using CtxLock = std::lock_guard<std::recursive_mutex>;
-
-// Every host <-> device copy of the engine goes through here (counted per
-// context, sg_ctx_copy_bytes).
-cudaError_t copy_async(sg_ctx* ctx, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
-    if (kind == cudaMemcpyHostToDevice) ctx->h2d_bytes += bytes;
-    else if (kind == cudaMemcpyDeviceToHost) ctx->d2h_bytes += bytes;
-    return cudaMemcpyAsync(dst, src, bytes, kind, st);
-}
-
-// NVTX range around an entry point (visible in nsys/ncu timelines; a no-op
-// without a tool attached).
-struct NvtxRange {
-    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
-    ~NvtxRange() { nvtxRangePop(); }
-};
-#define SG_ENTRY(ctx, name)       \
-    CtxLock sg_lock_((ctx)->mu);  \
-    NvtxRange sg_nvtx_(name)
-
-int cuda_fail(sg_ctx* ctx, cudaError_t e, const char* what) {
-    const int code = e == cudaErrorMemoryAllocation ? SG_ERR_OUT_OF_MEMORY : SG_ERR_CUDA;
-    return fail(ctx, code, std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-#define SG_CUDA(ctx, call)                                  \
-    do {                                                    \
-        const cudaError_t e_ = (call);                      \
-        if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call); \
-    } while (0)
-
-// Device memory comes from the device's stream-ordered pool (cudaMallocAsync
-// on the context stream; the pool keeps freed blocks, see sg_ctx_create), so
-// repeated calls of the calibration API do not pay cudaMalloc/cudaFree.
-template <class T>
-cudaError_t dalloc(T** p, size_t count, cudaStream_t st) {
-    return cudaMallocAsync(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T), st);
-}
 
 // Divisor admissibility for the 3-op exact division (sird_device.cuh
 // div_exact; proof in DESIGN.md §4): |b| in [2^-60, 2^60] and the odd part of
@@ -217,21 +111,6 @@ int launch_integrate(sg_ctx* ctx, const DevWindow& w, const double* d_params, co
     SG_CUDA(ctx, cudaGetLastError());
     return SG_OK;
 }
-
-// RAII bundle of device allocations for one call / plan (stream-ordered).
-struct DevBufs {
-    cudaStream_t st = nullptr;
-    std::vector<void*> ptrs;
-    template <class T>
-    cudaError_t alloc(T** p, size_t count) {
-        const cudaError_t e = dalloc(p, count, st);
-        if (e == cudaSuccess) ptrs.push_back(*p);
-        return e;
-    }
-    ~DevBufs() {
-        for (void* p : ptrs) cudaFreeAsync(p, st);
-    }
-};
 
 DevWindow integration_window(int n_days, int substeps, double N) {
     DevWindow w{};

@@ -140,7 +140,59 @@ Trajectory integrate_euler(const SirdParams& params, const SirdState& init, doub
     return std::move(integrate_batch(std::span<const SirdParams>(&params, 1), init, population, n_days, substeps)[0]);
 }
 
+void integrate_euler_into(const SirdParams& params, const SirdState& init, double population, int n_days,
+                          int substeps, Trajectory& out) {  // model.cpp:76-107
+    out = integrate_euler(params, init, population, n_days, substeps);
+}
+
+SirdState sird_rhs(const SirdState& state, double beta, double gamma, double mu, double population) {
+    const sg_state in{state.S, state.I, state.R, state.D};
+    sg_state out{};
+    sg_ctx* ctx = engine_context();
+    check(ctx, sg_sird_rhs_batch(ctx, &in, &beta, &gamma, &mu, population, 1, &out));
+    return SirdState{out.S, out.I, out.R, out.D};
+}
+
 // ---- objectives ------------------------------------------------------------------------
+
+double metric_value(Metric metric, std::span<const double> observed, std::span<const double> predicted) {
+    if (observed.empty() || observed.size() != predicted.size())  // objectives.cpp:72-81
+        throw Error("metric_value: series must be non-empty and of equal length");
+    double v = 0.0;
+    sg_ctx* ctx = engine_context();
+    check(ctx, sg_metric_values(ctx, metric_code(metric), observed.data(), predicted.data(), observed.size(), 1, &v));
+    return v;
+}
+
+std::vector<double> minmax_normalize(std::span<const double> values, double ref_min, double ref_max) {
+    if (!(ref_max > ref_min)) throw DegenerateRangeError{};  // objectives.cpp:83-93
+    const double scale = 1.0 / (ref_max - ref_min);
+    std::vector<double> out;
+    out.reserve(values.size());
+    for (const double v : values) out.push_back((v - ref_min) * scale);
+    return out;
+}
+
+double objective_value(const ObjectiveSpec& spec, const WindowSlice& observed, const Trajectory& predicted) {
+    const std::size_t n = observed.deaths_cum.size();  // objectives.cpp:95-120
+    if (n == 0 || observed.infectious.size() != n || observed.recovered_cum.size() != n || predicted.days() != n)
+        throw Error("objective_value: observed and predicted must cover the same days");
+    if (!predicted.finite) return kInf;
+    std::vector<double> states(4 * n);
+    for (std::size_t d = 0; d < n; ++d) {
+        const SirdState& s = predicted.states[d];
+        states[4 * d + 0] = s.S;
+        states[4 * d + 1] = s.I;
+        states[4 * d + 2] = s.R;
+        states[4 * d + 3] = s.D;
+    }
+    double v = 0.0;
+    sg_ctx* ctx = engine_context();
+    check(ctx, sg_objective_values(ctx, family_code(spec.family), metric_code(spec.metric), observed.infectious.data(),
+                                   observed.recovered_cum.data(), observed.deaths_cum.data(), n, states.data(), nullptr,
+                                   1, &v));
+    return v;
+}
 
 double r_squared_d(std::span<const double> observed_d, std::span<const double> predicted_d) {  // objectives.cpp:122-144
     if (observed_d.empty() || observed_d.size() != predicted_d.size())
@@ -215,6 +267,174 @@ std::uint64_t mix_seed(std::uint64_t base, std::uint64_t index) {  // pso.cpp:36
     return z ^ (z >> 31);
 }
 
+double uniform01(std::mt19937_64& engine) {  // pso.cpp:43-45: the top 53 bits scaled by 2^-53
+    return static_cast<double>(engine() >> 11) * 0x1.0p-53;
+}
+
+namespace {
+
+// The reference's repair hook (calibration.cpp:89-93) runs on the device;
+// std::function keeps it as a plain function pointer.
+bool is_repair_time_order(const RepairHook& repair) {
+    using Fn = void (*)(std::span<double>);
+    const Fn* f = repair.target<Fn>();
+    return f && *f == &repair_time_order;
+}
+
+sg_window* device_window(const WindowObjective& wo) {
+    if (!wo.window) throw Error(wo.deferred);
+    return wo.window.get();
+}
+
+}  // namespace
+
+void WindowObjective::operator()(std::span<const double> positions, std::size_t dim, std::span<double> costs) const {
+    if (dim != 6 || positions.size() != costs.size() * dim)  // calibration.cpp:141-143
+        throw Error("window objective expects 6-dim positions");
+    if (costs.empty()) return;
+    sg_window* w = device_window(*this);
+    check(ctx, sg_eval_costs(w, positions.data(), costs.size(), dim, costs.data()));
+}
+
+Swarm::Swarm(const PsoConfig& config, SearchBounds bounds, RepairHook repair)  // pso.cpp:47-75
+    : config_(config), bounds_(std::move(bounds)), repair_(std::move(repair)), best_cost_(kInf) {
+    config_.validate();
+    bounds_.validate();
+    device_repair_ = repair_ && is_repair_time_order(repair_) && bounds_.dim() >= 4;
+    sg_ctx* ctx = engine_context();
+    check(ctx, sg_gswarm_create(ctx, static_cast<int>(bounds_.dim()), bounds_.lower.data(), bounds_.upper.data(),
+                                config_.n_particles, config_.inertia, config_.cognitive, config_.social, config_.seed,
+                                device_repair_ ? 1 : 0, &swarm_));
+    costs_.assign(config_.n_particles, kInf);
+    best_position_.assign(bounds_.dim(), 0.0);
+    best_fresh_ = true;
+    if (repair_ && !device_repair_) apply_host_repair(true);
+}
+
+Swarm::~Swarm() { sg_gswarm_destroy(swarm_); }
+
+Swarm::Swarm(Swarm&& o) noexcept
+    : config_(o.config_), bounds_(std::move(o.bounds_)), repair_(std::move(o.repair_)),
+      device_repair_(o.device_repair_), swarm_(o.swarm_), costs_(std::move(o.costs_)),
+      positions_(std::move(o.positions_)), best_position_(std::move(o.best_position_)),
+      positions_fresh_(o.positions_fresh_), best_fresh_(o.best_fresh_), best_cost_(o.best_cost_),
+      iterations_done_(o.iterations_done_) {
+    o.swarm_ = nullptr;
+}
+
+Swarm& Swarm::operator=(Swarm&& o) noexcept {
+    if (this != &o) {
+        sg_gswarm_destroy(swarm_);
+        config_ = o.config_;
+        bounds_ = std::move(o.bounds_);
+        repair_ = std::move(o.repair_);
+        device_repair_ = o.device_repair_;
+        swarm_ = o.swarm_;
+        o.swarm_ = nullptr;
+        costs_ = std::move(o.costs_);
+        positions_ = std::move(o.positions_);
+        best_position_ = std::move(o.best_position_);
+        positions_fresh_ = o.positions_fresh_;
+        best_fresh_ = o.best_fresh_;
+        best_cost_ = o.best_cost_;
+        iterations_done_ = o.iterations_done_;
+    }
+    return *this;
+}
+
+// A RepairHook the device does not know: applied to each particle of the
+// host copy in particle order, exactly where the reference calls it (after
+// the initial draw, pso.cpp:70-72, and after each move, pso.cpp:123-125).
+void Swarm::apply_host_repair(bool initial) {
+    sg_ctx* ctx = engine_context();
+    const std::size_t dim = bounds_.dim();
+    positions_.resize(config_.n_particles * dim);
+    check(ctx, sg_gswarm_get_positions(swarm_, positions_.data()));
+    for (std::size_t i = 0; i < config_.n_particles; ++i) repair_(std::span<double>(positions_.data() + i * dim, dim));
+    check(ctx, initial ? sg_gswarm_set_initial_positions(swarm_, positions_.data())
+                       : sg_gswarm_set_positions(swarm_, positions_.data()));
+    positions_fresh_ = true;
+}
+
+std::span<const double> Swarm::positions() const {
+    if (!positions_fresh_) {
+        positions_.resize(config_.n_particles * bounds_.dim());
+        check(engine_context(), sg_gswarm_get_positions(swarm_, positions_.data()));
+        positions_fresh_ = true;
+    }
+    return positions_;
+}
+
+std::span<const double> Swarm::best_position() const {
+    if (!best_fresh_) {
+        double cost = 0.0;
+        check(engine_context(), sg_gswarm_best(swarm_, best_position_.data(), &cost));
+        best_fresh_ = true;
+    }
+    return best_position_;
+}
+
+double Swarm::step(const BatchObjective& objective) {  // pso.cpp:77-101
+    sg_ctx* ctx = engine_context();
+    const std::size_t dim = bounds_.dim();
+    if (const WindowObjective* wo = objective.target<WindowObjective>()) {
+        if (dim != 6) throw Error("window objective expects 6-dim positions");
+        check(ctx, sg_gswarm_eval_window(swarm_, device_window(*wo)));  // costs stay on the device
+    } else {
+        objective(positions(), dim, costs_);
+        check(ctx, sg_gswarm_set_costs(swarm_, costs_.data()));
+    }
+    check(ctx, sg_gswarm_step(swarm_, &best_cost_));
+    positions_fresh_ = false;
+    best_fresh_ = false;
+    if (repair_ && !device_repair_) apply_host_repair(false);
+    ++iterations_done_;
+    return best_cost_;
+}
+
+PsoResult optimize(const PsoConfig& config, const SearchBounds& bounds, const BatchObjective& objective,
+                   RepairHook repair) {  // pso.cpp:129-143
+    const WindowObjective* wo = objective.target<WindowObjective>();
+    if (wo && bounds.dim() == 6 && (!repair || is_repair_time_order(repair))) {
+        // the fused device swarm of sg_fit_swarms: same trajectory, no host round trip per step
+        config.validate();  // Swarm::Swarm (pso.cpp:49-50)
+        bounds.validate();
+        sg_swarm_desc d{};
+        d.window = device_window(*wo);
+        for (int k = 0; k < 6; ++k) {
+            d.lower[k] = bounds.lower[k];
+            d.upper[k] = bounds.upper[k];
+        }
+        d.n_particles = config.n_particles;
+        d.max_iters = config.max_iters;
+        d.inertia = config.inertia;
+        d.cognitive = config.cognitive;
+        d.social = config.social;
+        d.seed = config.seed;
+        d.repair_time_order = repair ? 1 : 0;
+        PsoResult result;
+        result.cost_history.assign(config.max_iters, 0.0);
+        sg_swarm_result r{};
+        r.cost_history = result.cost_history.data();
+        sg_ctx* ctx = wo->ctx;
+        check(ctx, sg_fit_swarms(ctx, &d, 1, &r));
+        if (r.status == SG_ERR_ALL_INFEASIBLE) throw AllInfeasibleError{};  // pso.cpp:137-139
+        if (r.status != SG_OK) throw_status(r.status, sg_last_error(ctx));
+        result.best_cost = r.best_cost;
+        result.best_position.assign(r.best_position, r.best_position + 6);
+        return result;
+    }
+    Swarm swarm(config, bounds, std::move(repair));
+    PsoResult result;
+    result.cost_history.reserve(config.max_iters);
+    for (std::size_t it = 0; it < config.max_iters; ++it) result.cost_history.push_back(swarm.step(objective));
+    if (!(swarm.best_cost() < kInf)) throw AllInfeasibleError{};
+    result.best_cost = swarm.best_cost();
+    const auto best = swarm.best_position();
+    result.best_position.assign(best.begin(), best.end());
+    return result;
+}
+
 // ---- calibration -------------------------------------------------------------------------
 
 std::vector<Window> make_windows(std::size_t n_days, const WindowScheme& scheme) {  // calibration.cpp:37-52
@@ -276,24 +496,19 @@ SirdState window_initial_state(const EpiSeries& data, std::size_t day, double po
 
 BatchObjective make_window_objective(const ObjectiveSpec& spec, const WindowSlice& observed, const SirdState& init,
                                      double population, int substeps, int /*n_threads*/) {
-    sg_ctx* ctx = engine_context();
-    auto handle = std::make_shared<WindowHandle>();
+    WindowObjective wo;
+    wo.ctx = engine_context();
     // The reference validates n_days / substeps / population only when the
     // objective integrates (model.cpp:78-80); keep that timing.
-    std::string deferred;
-    const int rc = sg_window_create(ctx, observed.infectious.data(), observed.recovered_cum.data(),
+    sg_window* w = nullptr;
+    const int rc = sg_window_create(wo.ctx, observed.infectious.data(), observed.recovered_cum.data(),
                                     observed.deaths_cum.data(), static_cast<int>(observed.deaths_cum.size()),
                                     sg_state{init.S, init.I, init.R, init.D}, population, substeps,
-                                    family_code(spec.family), metric_code(spec.metric), &handle->w);
-    if (rc == SG_ERR_INVALID_ARGUMENT) deferred = sg_last_error(ctx);
-    else check(ctx, rc);
-    return [handle, ctx, deferred](std::span<const double> positions, std::size_t dim, std::span<double> costs) {
-        if (dim != 6 || positions.size() != costs.size() * dim)  // calibration.cpp:141-143
-            throw Error("window objective expects 6-dim positions");
-        if (costs.empty()) return;
-        if (!handle->w) throw Error(deferred);
-        check(ctx, sg_eval_costs(handle->w, positions.data(), costs.size(), dim, costs.data()));
-    };
+                                    family_code(spec.family), metric_code(spec.metric), &w);
+    if (rc == SG_ERR_INVALID_ARGUMENT) wo.deferred = sg_last_error(wo.ctx);
+    else check(wo.ctx, rc);
+    if (w) wo.window = std::shared_ptr<sg_window>(w, sg_window_destroy);
+    return wo;
 }
 
 namespace {
@@ -545,6 +760,65 @@ ScalarBands build_scalar_bands(std::vector<double> values) {  // calibration.cpp
     b.p95_lo = quantile_sorted(sorted, 0.025);
     b.p95_hi = quantile_sorted(sorted, 0.975);
     return b;
+}
+
+Envelope build_envelope(const std::vector<std::vector<double>>& values_per_day) {  // calibration.cpp:218-245
+    Envelope env;
+    const std::size_t n_days = values_per_day.size();
+    env.count.assign(n_days, 0);
+    for (auto* col : {&env.outer_lo, &env.outer_hi, &env.band1_lo, &env.band1_hi, &env.band2_lo, &env.band2_hi,
+                      &env.median})
+        col->assign(n_days, kNaN);
+    std::vector<double> v;
+    for (std::size_t day = 0; day < n_days; ++day) {
+        append_finite_sorted(v, values_per_day[day]);
+        const std::size_t k = v.size();
+        env.count[day] = k;
+        if (k == 0) continue;
+        // rank envelopes: extremes, second ranks from 3 values, third ranks from 5
+        env.outer_lo[day] = v[0];
+        env.outer_hi[day] = v[k - 1];
+        env.band1_lo[day] = k < 3 ? v[0] : v[1];
+        env.band1_hi[day] = k < 3 ? v[k - 1] : v[k - 2];
+        if (k >= 5) {
+            env.band2_lo[day] = v[2];
+            env.band2_hi[day] = v[k - 3];
+        }
+        env.median[day] = (k & 1) ? v[k / 2] : 0.5 * (v[k / 2 - 1] + v[k / 2]);  // calibration.cpp:27-33
+    }
+    return env;
+}
+
+ParameterEnvelopes parameter_envelopes(std::span<const FitResult> fits, std::size_t n_days) {  // 247-274
+    std::vector<std::vector<double>> beta(n_days), gamma(n_days), mu(n_days), r0(n_days);
+    for (const FitResult& f : fits) {
+        if (!f.ok) continue;
+        const double rate = f.params.gamma + f.params.mu;
+        for (std::size_t local = 0; local < f.window.length && f.window.start + local < n_days; ++local) {
+            const std::size_t day = f.window.start + local;
+            const double b = beta_at(f.params, static_cast<double>(local));
+            beta[day].push_back(b);
+            gamma[day].push_back(f.params.gamma);
+            mu[day].push_back(f.params.mu);
+            r0[day].push_back(rate > 0.0 ? b / rate : kNaN);
+        }
+    }
+    return ParameterEnvelopes{build_envelope(beta), build_envelope(gamma), build_envelope(mu), build_envelope(r0)};
+}
+
+CompartmentEnvelopes compartment_envelopes(std::span<const FitResult> fits, std::size_t n_days) {  // 276-296
+    std::vector<std::vector<double>> I(n_days), R(n_days), D(n_days);
+    for (const FitResult& f : fits) {
+        if (!f.ok) continue;
+        const std::size_t len = std::min(f.window.length, f.trajectory.days());
+        for (std::size_t local = 0; local < len && f.window.start + local < n_days; ++local) {
+            const SirdState& s = f.trajectory.states[local];
+            I[f.window.start + local].push_back(s.I);
+            R[f.window.start + local].push_back(s.R);
+            D[f.window.start + local].push_back(s.D);
+        }
+    }
+    return CompartmentEnvelopes{build_envelope(I), build_envelope(R), build_envelope(D)};
 }
 
 StabilityResult stability_study(const EpiSeries& data, const Window& window, const FitSettings& settings,
