@@ -121,6 +121,25 @@ SIGNATURES = {
                                                  ctypes.c_uint64, ctypes.POINTER(sg_fit_settings), ctypes.c_uint64,
                                                  ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(sg_fit_record),
                                                  _dp, _u64p, _dp, _u64p, _u64p]),
+    "sg_gswarm_create": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _dp, _dp, ctypes.c_uint64, ctypes.c_double,
+                                        ctypes.c_double, ctypes.c_double, ctypes.c_uint64, ctypes.c_int,
+                                        ctypes.POINTER(ctypes.c_void_p)]),
+    "sg_gswarm_destroy": (None, [ctypes.c_void_p]),
+    "sg_gswarm_positions_device": (ctypes.c_void_p, [ctypes.c_void_p]),
+    "sg_gswarm_costs_device": (ctypes.c_void_p, [ctypes.c_void_p]),
+    "sg_gswarm_get_positions": (ctypes.c_int, [ctypes.c_void_p, _dp]),
+    "sg_gswarm_set_positions": (ctypes.c_int, [ctypes.c_void_p, _dp]),
+    "sg_gswarm_set_initial_positions": (ctypes.c_int, [ctypes.c_void_p, _dp]),
+    "sg_gswarm_set_costs": (ctypes.c_int, [ctypes.c_void_p, _dp]),
+    "sg_gswarm_eval_window": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "sg_gswarm_step": (ctypes.c_int, [ctypes.c_void_p, _dp]),
+    "sg_gswarm_best": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp]),
+    "sg_objective_values": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _dp, _dp, _dp,
+                                           ctypes.c_size_t, _dp, _u8p, ctypes.c_size_t, _dp]),
+    "sg_metric_values": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _dp, _dp, ctypes.c_size_t, ctypes.c_size_t,
+                                        _dp]),
+    "sg_sird_rhs_batch": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(sg_state), _dp, _dp, _dp, ctypes.c_double,
+                                         ctypes.c_size_t, ctypes.POINTER(sg_state)]),
     "sg_forecast_batch": (ctypes.c_int, [ctypes.c_void_p, _dp, ctypes.POINTER(sg_state), ctypes.c_size_t,
                                          ctypes.c_double, ctypes.c_int, ctypes.c_int, _dp, _u8p]),
     "sg_forecast_ensemble": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, ctypes.c_uint64, ctypes.c_size_t,

@@ -19,7 +19,7 @@ HEADER = ROOT / "include" / "sirdgpu.h"
 
 def declared_symbols():
     text = HEADER.read_text()
-    decl = r"^(?:int|void|uint64_t|const char\s*\*|void\s*\*)\s*\*?\s*(sg_[a-z0-9_]+)\s*\("
+    decl = r"^(?:int|void|uint64_t|const char\s*\*|void\s*\*|const double\s*\*|double\s*\*)\s*\*?\s*(sg_[a-z0-9_]+)\s*\("
     return sorted(set(re.findall(decl, text, re.M)))
 
 
