@@ -454,6 +454,7 @@ __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& s
         unsigned int t = 0;
         if (lane == 0) t = atomicAdd(&P.group_arrived[sw.group_begin + g], 1u);
         t = __shfl_sync(0xFFFFFFFFu, t, 0);
+        SG_CHECK(t < g_n);  // the counter was reset by the previous iteration's last warp, each warp arrives once
         if (t != g_n - 1) return;
         __threadfence();
         double gc = __longlong_as_double(0x7FF0000000000000LL);
@@ -475,6 +476,7 @@ __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& s
                 gi = oi;
             }
         }
+        SG_CHECK(gi < sw.n);  // every group holds at least one active particle
         if (lane == 0) {
             P.gpart_cost[sw.group_begin + g] = gc;
             P.gpart_idx[sw.group_begin + g] = gi;
@@ -490,6 +492,7 @@ __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& s
     unsigned int ticket = 0;
     if (lane == 0) ticket = atomicAdd(&st.arrived, 1u);
     ticket = __shfl_sync(0xFFFFFFFFu, ticket, 0);
+    SG_CHECK(ticket < fold_n);
     if (ticket != fold_n - 1) return;
     __threadfence();
     double bc = __longlong_as_double(0x7FF0000000000000LL);
@@ -511,6 +514,8 @@ __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& s
             bi = oi;
         }
     }
+    SG_CHECK(bi < sw.n);
+    SG_CHECK(it < P.hist_stride);
     if (lane == 0) {
         if (bc < st.best_cost) {  // strict: an equal later cost never replaces (pso.cpp:91)
             st.best_cost = bc;
@@ -584,6 +589,11 @@ __device__ __forceinline__ SmemWindow stage_window_async(const CtaTask& t, DevWi
     ObsDay* s_robs = reinterpret_cast<ObsDay*>(smem + t.times_bytes + t.obs_bytes);
     unsigned char* s_flag = smem + t.times_bytes + 2 * t.obs_bytes;
     if (threadIdx.x == 0) {
+#if SG_CHECKED
+        uint32_t dyn = 0;
+        asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+        SG_CHECK(t.times_bytes + (MET == kMetMAPE ? 2u : 1u) * t.obs_bytes <= dyn);
+#endif
         const uint32_t b = smem_u32(bar);
         mbar_init(b, 1);
         // obs_bytes = round16(24 n) is the obs and the robs section size
@@ -619,6 +629,7 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
     const uint32_t cta = blockIdx.x + cta_offset;
     const CtaTask task = tasks[cta];
     if (it >= task.max_iters) return;  // CTA-uniform
+    SG_CHECK(task.n_valid >= 1 && task.n_valid <= kStepThreads * kNP && task.p0 + task.n_valid <= P.stride);
     constexpr bool kAsync = SUB != 0 && SG_TMA_STAGE;
     SmemWindow win;
     if constexpr (kAsync) win = stage_window_async<MET, SUB>(task, &sdesc, &bar, smem);
@@ -798,8 +809,10 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 1) pso_swarm_kernel(const De
             const SwarmPartial* best = nullptr;
             for (unsigned r = 0; r < n_ranks; ++r) {
                 const SwarmPartial* q = cluster.map_shared_rank(&part[it & 1], r);
+                SG_CHECK(q->idx == ~0ULL || q->idx < n);  // a partial of THIS iteration (double buffer)
                 if (!best || better(q->cost, q->idx, best->cost, best->idx)) best = q;
             }
+            SG_CHECK(best != nullptr && best->idx < n);
             const double bc = best->cost;
             if (bc < gbest_cost) {  // strict: an equal later cost never replaces
                 gbest_cost = bc;

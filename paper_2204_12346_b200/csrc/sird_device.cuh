@@ -13,6 +13,21 @@
 
 #include <cstdint>
 
+// SG_CHECKED=1 (a diagnostic build, tools/checked_build.py): device-side
+// asserts of the invariants the lock-free folds, the cluster kernel and the
+// bulk staging rely on.  compute-sanitizer is not available on the GPU pool,
+// so these asserts, run under the GPU test suite, stand in for it.
+#ifndef SG_CHECKED
+#define SG_CHECKED 0
+#endif
+#if SG_CHECKED
+#undef NDEBUG
+#include <cassert>
+#define SG_CHECK(cond) assert(cond)
+#else
+#define SG_CHECK(cond) ((void)0)
+#endif
+
 #ifndef SG_RAMP_MODE
 #define SG_RAMP_MODE 1
 #endif
@@ -555,6 +570,7 @@ __device__ __forceinline__ double to_uniform01(uint64_t x) {
 template <int NDRAW>
 __device__ __forceinline__ void mt_draw(uint64_t* __restrict__ mt, int i0, double* out) {
     static_assert(NDRAW >= 1 && NDRAW < kMtM, "batch must not reach its own far words");
+    SG_CHECK(i0 >= 0 && i0 < kMtN);
     uint64_t* const row = mt + 32 * i0;            // word i0 + j at row[32*j] ...
     uint64_t* const row_w = row - 32 * kMtN;       // ... or, past word 311, at row_w[32*j]
     const int wrap = kMtN - i0;                    // first j that wraps
