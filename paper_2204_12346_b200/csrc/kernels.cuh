@@ -476,7 +476,7 @@ __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& s
                 gi = oi;
             }
         }
-        SG_CHECK(gi < sw.n);  // every group holds at least one active particle
+        SG_CHECK(lane != 0 || gi < sw.n);  // lane 0 holds the fold; every group has an active particle
         if (lane == 0) {
             P.gpart_cost[sw.group_begin + g] = gc;
             P.gpart_idx[sw.group_begin + g] = gi;
@@ -514,7 +514,7 @@ __device__ __forceinline__ void finish_step(const DevSwarm& sw, DevSwarmState& s
             bi = oi;
         }
     }
-    SG_CHECK(bi < sw.n);
+    SG_CHECK(lane != 0 || bi < sw.n);  // lane 0 holds the fold (shfl_down)
     SG_CHECK(it < P.hist_stride);
     if (lane == 0) {
         if (bc < st.best_cost) {  // strict: an equal later cost never replaces (pso.cpp:91)
