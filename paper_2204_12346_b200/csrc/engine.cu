@@ -635,8 +635,10 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     // Partition swarms into up to kMaxLanes lanes of about equal CTA count
     // (swarm boundaries only).  Small plans stay on one lane.
     {
-        const int want = g.n_ctas >= 4 * static_cast<size_t>(ctx->sm_count) ? kMaxLanes
-                         : g.n_ctas >= 2 * static_cast<size_t>(ctx->sm_count) ? std::min(2, kMaxLanes) : 1;
+        int want = g.n_ctas >= 4 * static_cast<size_t>(ctx->sm_count) ? std::min(4, kMaxLanes)
+                   : g.n_ctas >= 2 * static_cast<size_t>(ctx->sm_count) ? std::min(2, kMaxLanes) : 1;
+        static const char* lanes_env = std::getenv("SG_PLAN_LANES");  // diagnostic override
+        if (lanes_env) want = std::max(1, std::min(kMaxLanes, std::atoi(lanes_env)));
         const size_t target = (g.n_ctas + want - 1) / want;
         SwarmGroup::Lane cur{0, 0, 0, 0};
         for (const DevSwarm& s : sw) {

@@ -25,7 +25,7 @@ using namespace sirdgpu;
 // streams so one partition's per-iteration tail overlaps the next
 // partition's iteration (swarms never synchronise with each other).
 #ifndef SG_LANES
-#define SG_LANES 4
+#define SG_LANES 32
 #endif
 constexpr int kMaxLanes = SG_LANES;
 
