@@ -632,11 +632,18 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     }
     g.n_total = offset;
     g.n_ctas = cta_swarm.size();
-    // Partition swarms into up to kMaxLanes lanes of about equal CTA count
-    // (swarm boundaries only).  Small plans stay on one lane.
+    // Partition swarms into up to kPlanLanes lanes of about equal CTA count
+    // (swarm boundaries only).  Lanes let one lane's per-iteration tail
+    // overlap the others' iterations; that matters most when the plan is
+    // about one wave (measured, rank 0's share of the sweep on 8 GPUs, 18
+    // swarms / 576 CTAs: 74.3 ms with 2 lanes, 62.3 ms with 8; the full
+    // sweep is the same with 4, 8 or 16, profiles/r02d_lanes.jsonl).  Plans
+    // under one CTA per SM stay on one lane (host enqueue would dominate).
     {
-        int want = g.n_ctas >= 4 * static_cast<size_t>(ctx->sm_count) ? std::min(4, kMaxLanes)
-                   : g.n_ctas >= 2 * static_cast<size_t>(ctx->sm_count) ? std::min(2, kMaxLanes) : 1;
+        constexpr int kPlanLanes = 8;
+        int want = g.n_ctas >= static_cast<size_t>(ctx->sm_count)
+                       ? static_cast<int>(std::min<size_t>(std::min(kPlanLanes, kMaxLanes), sw.size()))
+                       : 1;
         static const char* lanes_env = std::getenv("SG_PLAN_LANES");  // diagnostic override
         if (lanes_env) want = std::max(1, std::min(kMaxLanes, std::atoi(lanes_env)));
         const size_t target = (g.n_ctas + want - 1) / want;
