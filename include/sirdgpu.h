@@ -328,14 +328,22 @@ int sg_probe_fp64_rate(sg_ctx* ctx, double* ops_per_s);
  * ensemble of 10^6 sets per window never leaves HBM.  bands: 7 x (horizon+1)
  * doubles, rows median, p50_lo, p50_hi, p90_lo, p90_hi, p95_lo, p95_hi;
  * counts: finite samples per day (horizon+1); costs: n window costs or NULL.
- * n must fit in an int (one device radix sort per forecast day). */
+ * n must fit in an int. */
 int sg_forecast_ensemble_bands(sg_window* window, const double lower[6], const double upper[6], uint64_t seed,
                                size_t n, int horizon, double* bands, uint64_t* counts, double* costs);
 
+/* build_quantile_bands (calibration.cpp:337-361) of n_days columns of n
+ * values each (values: day-major, n_days x n, host), on the device by the
+ * same order-statistic selection as the ensemble bands (non-finite values
+ * dropped, calibration.cpp:17-25).  bands: 7 x n_days (median, p50_lo,
+ * p50_hi, p90_lo, p90_hi, p95_lo, p95_hi); counts: n_days. */
+int sg_quantile_bands(sg_ctx* ctx, const double* values, size_t n, int n_days, double* bands, uint64_t* counts);
+
 /* The same for many windows in one call (C5: every window of the sweep):
  * window k uses seeds[k]; bands: n_windows x 7 x (horizon + 1), counts:
- * n_windows x (horizon + 1).  Windows are pipelined on two streams, so one
- * window's band selection overlaps the next window's evaluation. */
+ * n_windows x (horizon + 1).  Windows are pipelined on two streams (the
+ * band selection at a higher priority), so one window's band selection
+ * overlaps the next window's evaluation. */
 int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows, const double lower[6],
                                      const double upper[6], const uint64_t* seeds, size_t n, int horizon,
                                      double* bands, uint64_t* counts);

@@ -146,6 +146,7 @@ SIGNATURES = {
                                             ctypes.c_int, _dp, _dp, _dp]),
     "sg_forecast_ensemble_bands": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, ctypes.c_uint64, ctypes.c_size_t,
                                                   ctypes.c_int, _dp, _u64p, _dp]),
+    "sg_quantile_bands": (ctypes.c_int, [ctypes.c_void_p, _dp, ctypes.c_size_t, ctypes.c_int, _dp, _u64p]),
     "sg_forecast_ensemble_bands_batch": (ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.c_size_t, _dp, _dp,
                                                         _u64p, ctypes.c_size_t, ctypes.c_int, _dp, _u64p]),
 }
@@ -275,6 +276,18 @@ class Context:
         return states, fin.astype(bool)
 
     # -- swarms -------------------------------------------------------------------
+    def quantile_bands(self, values):
+        """build_quantile_bands on the device: values n_days x n (day-major) ->
+        (bands 7 x n_days, counts n_days)."""
+        v = _f64(values)
+        if v.ndim != 2:
+            raise ValueError("values must be 2-D (days x values)")
+        n_days, n = v.shape
+        bands = np.zeros((7, n_days))
+        counts = np.zeros(n_days, dtype=np.uint64)
+        self.check(lib().sg_quantile_bands(self._h, _d(v), n, n_days, _d(bands), counts.ctypes.data_as(_u64p)))
+        return bands, counts
+
     def forecast_ensemble_bands_batch(self, windows, lower, upper, seeds, n: int, horizon: int):
         """sg_forecast_ensemble_bands for many windows in one pipelined call:
         -> (bands n_windows x 7 x (horizon+1), counts n_windows x (horizon+1))."""

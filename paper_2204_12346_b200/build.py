@@ -20,7 +20,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-SOURCES = [CSRC / "engine.cu", CSRC / "gswarm.cu", CSRC / "family.cu", CSRC / "cub_sorts.cu", CSRC / "host_api.cpp"]
+SOURCES = [CSRC / "engine.cu", CSRC / "gswarm.cu", CSRC / "family.cu", CSRC / "host_api.cpp"]
 HEADERS = [CSRC / "sird_device.cuh", CSRC / "kernels.cuh", CSRC / "launchers.cuh", CSRC / "engine_internal.h",
            CSRC / "engine_core.cuh",
            ROOT / "include" / "sirdgpu.h", ROOT / "include" / "sirdfit_b200.hpp"]
@@ -34,7 +34,6 @@ FLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++20", "-Xcompiler", "-fPIC",
 # rest of the engine, the C++ API
 _FAMILY_UNITS = [(f, sub) for f in (0, 1) for sub in (24, -1, 0)]
 UNITS = [("engine", CSRC / "engine.cu", []), ("gswarm", CSRC / "gswarm.cu", []),
-         ("cub_sorts", CSRC / "cub_sorts.cu", []),
          ("host_api", CSRC / "host_api.cpp", [])] + [
     (f"family{f}_s{'m1' if sub < 0 else sub}", CSRC / "family.cu", [f"-DSG_FAMILY={f}", f"-DSG_SUB={sub}", f"-DSG_UNIT={k}"])
     for k, (f, sub) in enumerate(_FAMILY_UNITS)]

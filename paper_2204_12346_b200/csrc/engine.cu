@@ -174,6 +174,8 @@ void sg_ctx_destroy(sg_ctx* ctx) {
         if (ctx->join[l]) cudaEventDestroy(ctx->join[l]);
     }
     if (ctx->fork) cudaEventDestroy(ctx->fork);
+    if (ctx->band_eval) cudaStreamDestroy(ctx->band_eval);
+    if (ctx->band_sel) cudaStreamDestroy(ctx->band_sel);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -1071,33 +1073,19 @@ int sg_fit_swarms(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg_
     return SG_OK;
 }
 
-// Ramp-coherent evaluation order of an ensemble (ens_sample_kernel + a
-// 16-bit radix sort of the (day t1, day t2) keys): returns perm and planes.
-static cudaError_t ensemble_order(sg_ctx* ctx, DevBufs& b, const double* d_lo, const double* d_hi, uint64_t seed,
-                                  size_t n, uint32_t** perm, double** planes, cudaStream_t st = nullptr) {
-    if (!st) st = ctx->stream;
-    uint32_t *keys, *keys_sorted, *idx, *idx_sorted;
-    cudaError_t e;
-    if ((e = b.alloc(planes, 6 * n)) != cudaSuccess) return e;
-    if ((e = b.alloc(&keys, n)) != cudaSuccess) return e;
-    if ((e = b.alloc(&keys_sorted, n)) != cudaSuccess) return e;
-    if ((e = b.alloc(&idx, n)) != cudaSuccess) return e;
-    if ((e = b.alloc(&idx_sorted, n)) != cudaSuccess) return e;
-    ens_sample_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(d_lo, d_hi, seed, n, *planes,
-                                                                                     keys, idx);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    size_t temp_bytes = 0;
-    if ((e = sg_sort_pairs_u32(nullptr, temp_bytes, keys, keys_sorted, idx, idx_sorted,
-                                             static_cast<int>(n), 0, 16, st)) != cudaSuccess)
-        return e;
-    unsigned char* temp;
-    if ((e = b.alloc(&temp, std::max<size_t>(temp_bytes, 16))) != cudaSuccess) return e;
-    if ((e = sg_sort_pairs_u32(temp, temp_bytes, keys, keys_sorted, idx, idx_sorted,
-                                             static_cast<int>(n), 0, 16, st)) != cudaSuccess)
-        return e;
-    ctx->launches += 2;
-    *perm = idx_sorted;
-    return cudaSuccess;
+// Ramp-coherent evaluation order of an ensemble: ens_sample_kernel draws
+// every sample into SoA planes with its (day t1, day t2) key and counts the
+// keys; a scan and a scatter complete the counting sort into perm.
+static int ensemble_order(sg_ctx* ctx, const double* d_lo, const double* d_hi, uint64_t seed, size_t n,
+                          double* planes, uint32_t* keys, unsigned int* key_count, uint32_t* perm, cudaStream_t st) {
+    SG_CUDA(ctx, cudaMemsetAsync(key_count, 0, sizeof(unsigned int) * 65536, st));
+    const unsigned grid = static_cast<unsigned>((n + 255) / 256);
+    ens_sample_kernel<<<grid, 256, 0, st>>>(d_lo, d_hi, seed, n, planes, keys, key_count);
+    ens_scan_kernel<<<1, 1024, 0, st>>>(key_count);
+    ens_scatter_kernel<<<grid, 256, 0, st>>>(keys, n, key_count, perm);
+    ctx->launches += 3;
+    SG_CUDA(ctx, cudaGetLastError());
+    return SG_OK;
 }
 
 int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper[6], uint64_t seed, size_t n,
@@ -1125,85 +1113,91 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
     DevWindow fwin = integration_window(horizon + 1, w->host.substeps, w->host.N);
     uint32_t* perm = nullptr;
     double* planes = nullptr;
-    if (n <= static_cast<size_t>(INT32_MAX)) SG_CUDA(ctx, ensemble_order(ctx, b, d_lo, d_hi, seed, n, &perm, &planes));
+    if (n <= static_cast<size_t>(INT32_MAX)) {
+        uint32_t* keys;
+        unsigned int* key_count;
+        SG_CUDA(ctx, b.alloc(&planes, 6 * n));
+        SG_CUDA(ctx, b.alloc(&keys, n));
+        SG_CUDA(ctx, b.alloc(&perm, n));
+        SG_CUDA(ctx, b.alloc(&key_count, 65536));
+        if (const int rc = ensemble_order(ctx, d_lo, d_hi, seed, n, planes, keys, key_count, perm, ctx->stream))
+            return rc;
+    }
     cudaError_t err = cudaSuccess;
     dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc,
                              fwin, d_lo, d_hi, seed, n, horizon, d_cost, d_par, d_D,
-                             static_cast<size_t>(horizon + 1), size_t(1), perm, planes, 0, w->smem, ctx->stream,
-                             &err);
+                             static_cast<size_t>(horizon + 1), size_t(1), perm, planes, 0, static_cast<SelDay*>(nullptr),
+                             w->smem, ctx->stream, &err);
     ctx->launches += 1;
     if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
     if (costs) SG_CUDA(ctx, copy_async(ctx, costs, d_cost, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     if (params_out)
         SG_CUDA(ctx, copy_async(ctx, params_out, d_par, 6 * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     SG_CUDA(ctx, copy_async(ctx, deaths_out, d_D, n * (horizon + 1) * sizeof(double), cudaMemcpyDeviceToHost,
-                                 ctx->stream));
+                            ctx->stream));
     SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SG_OK;
 }
 
-// The whole C5 pipeline of one window on stream `st` (buffers from `b`,
-// whose allocations and frees are ordered on `st`): ensemble order,
-// evaluation, band selection; bands (7 x n_days) and counts land in device
-// memory.
-static int enqueue_bands(sg_ctx* ctx, sg_window* w, DevBufs& b, cudaStream_t st, const double* d_lo,
-                         const double* d_hi, uint64_t seed, size_t n, int horizon, double* d_cost, double* d_bands,
-                         unsigned long long* d_counts) {
+// Device buffers of one window in flight in the C5 pipeline.
+struct BandSlot {
+    double *planes = nullptr, *D = nullptr, *cand = nullptr, *scratch = nullptr;
+    uint32_t *keys = nullptr, *perm = nullptr;
+    unsigned int *key_count = nullptr, *hist = nullptr;
+    SelDay* days = nullptr;
+};
+
+static int alloc_band_slot(sg_ctx* ctx, DevBufs& b, BandSlot& s, size_t n, int n_days) {
+    const size_t nd = n * static_cast<size_t>(n_days);
+    SG_CUDA(ctx, b.alloc(&s.planes, 6 * n));
+    SG_CUDA(ctx, b.alloc(&s.keys, n));
+    SG_CUDA(ctx, b.alloc(&s.perm, n));
+    SG_CUDA(ctx, b.alloc(&s.key_count, 65536));
+    SG_CUDA(ctx, b.alloc(&s.D, nd));
+    SG_CUDA(ctx, b.alloc(&s.cand, nd));
+    SG_CUDA(ctx, b.alloc(&s.scratch, 2 * nd));  // only bins too full for one CTA's shared memory touch it
+    SG_CUDA(ctx, b.alloc(&s.days, n_days));
+    SG_CUDA(ctx, b.alloc(&s.hist, static_cast<size_t>(n_days) * kSelBins));
+    return SG_OK;
+}
+
+// C5, first half (FP64-bound): ensemble order, evaluation of the window and
+// forecast into the slot's day-major deaths plane, with each day's key range
+// and finite count reduced in the kernel's epilogue.
+static int enqueue_band_eval(sg_ctx* ctx, sg_window* w, BandSlot& s, cudaStream_t st, const double* d_lo,
+                             const double* d_hi, uint64_t seed, size_t n, int horizon, double* d_cost) {
     const int n_days = horizon + 1;
-    if (n == 0) {
-        bands_kernel<<<n_days, 32, 0, st>>>(nullptr, 0, d_bands, d_counts, n_days);  // k = 0: NaN bands
-        ctx->launches += 1;
-        SG_CUDA(ctx, cudaGetLastError());
-        return SG_OK;
-    }
-    double *d_D, *d_sorted;
-    SG_CUDA(ctx, b.alloc(&d_D, n * n_days));
-    SG_CUDA(ctx, b.alloc(&d_sorted, n * n_days));
+    if (const int rc = ensemble_order(ctx, d_lo, d_hi, seed, n, s.planes, s.keys, s.key_count, s.perm, st)) return rc;
+    sel_init_kernel<<<static_cast<unsigned>((n_days + 127) / 128), 128, 0, st>>>(s.days, n_days);
+    ctx->launches += 1;
     const DevWindow fwin = integration_window(n_days, w->host.substeps, w->host.N);
-    uint32_t* perm = nullptr;
-    double* planes = nullptr;
-    SG_CUDA(ctx, ensemble_order(ctx, b, d_lo, d_hi, seed, n, &perm, &planes, st));
     cudaError_t err = cudaSuccess;
     // day-major columns in evaluation order: the bands only need each day's multiset
     dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc,
-                             fwin, d_lo, d_hi, seed, n, horizon, d_cost, static_cast<double*>(nullptr), d_D, size_t(1),
-                             n, perm, planes, 1, w->smem, st, &err);
+                             fwin, d_lo, d_hi, seed, n, horizon, d_cost, static_cast<double*>(nullptr), s.D, size_t(1),
+                             n, s.perm, s.planes, 1, s.days, w->smem, st, &err);
     ctx->launches += 1;
     if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
-    // per forecast day: k and the order statistics quantile_sorted reads
-    // (calibration.cpp:17-25, 324-361), by bin selection (kernels.cuh)
-    SelDay* d_days;
-    unsigned int* d_hist;
-    int *d_beg, *d_end;
-    SG_CUDA(ctx, b.alloc(&d_days, n_days));
-    SG_CUDA(ctx, b.alloc(&d_hist, static_cast<size_t>(n_days) * kSelBins));
-    SG_CUDA(ctx, b.alloc(&d_beg, static_cast<size_t>(n_days) * kBandRanks));
-    SG_CUDA(ctx, b.alloc(&d_end, static_cast<size_t>(n_days) * kBandRanks));
-    SG_CUDA(ctx, cudaMemsetAsync(d_hist, 0, sizeof(unsigned int) * n_days * kSelBins, st));
-    const unsigned small = static_cast<unsigned>((n_days + 127) / 128);
-    sel_init_kernel<<<small, 128, 0, st>>>(d_days, n_days);
+    return SG_OK;
+}
+
+// C5, second half (memory-bound): per forecast day the bins of the wanted
+// ranks (calibration.cpp:17-25, 324-361) — histogram, locate, gather — then
+// one CTA per day sorts them in shared memory and writes the bands.
+static int enqueue_band_select(sg_ctx* ctx, BandSlot& s, cudaStream_t st, size_t n, int n_days, double* d_bands,
+                               unsigned long long* d_counts) {
+    SG_CUDA(ctx, cudaMemsetAsync(s.hist, 0, sizeof(unsigned int) * n_days * kSelBins, st));
     const unsigned chunks = static_cast<unsigned>(std::min<size_t>(64, (n + 4095) / 4096));
     const dim3 grid(chunks, static_cast<unsigned>(n_days));
-    sel_range_kernel<<<grid, 256, 0, st>>>(d_D, n, d_days);
     const dim3 hgrid(static_cast<unsigned>(std::min<size_t>(16, (n + 16383) / 16384)), static_cast<unsigned>(n_days));
-    sel_hist_kernel<<<hgrid, 1024, 0, st>>>(d_D, n, d_days, d_hist);
-    sel_locate_kernel<<<static_cast<unsigned>(n_days), 1024, 0, st>>>(d_hist, d_days);
-    sel_gather_kernel<<<grid, 256, 0, st>>>(d_D, n, d_days, d_sorted);
-    const int n_seg = n_days * kBandRanks;
-    sel_segments_kernel<<<static_cast<unsigned>((n_seg + 127) / 128), 128, 0, st>>>(d_days, n, n_days, d_beg, d_end);
-    ctx->launches += 6;
-    SG_CUDA(ctx, cudaGetLastError());
-    size_t temp_bytes = 0;
-    const int n_items = static_cast<int>(n * n_days);
-    SG_CUDA(ctx, sg_segmented_sort_f64(nullptr, temp_bytes, d_sorted, d_D, n_items, n_seg, d_beg, d_end,
-                                                     st));
-    unsigned char* d_temp;
-    SG_CUDA(ctx, b.alloc(&d_temp, std::max<size_t>(temp_bytes, 16)));
-    SG_CUDA(ctx, sg_segmented_sort_f64(d_temp, temp_bytes, d_sorted, d_D, n_items, n_seg, d_beg, d_end,
-                                                     st));
-    ctx->launches += 1;
-    sel_bands_kernel<<<small, 128, 0, st>>>(d_days, d_D, n, d_bands, d_counts, n_days);
-    ctx->launches += 1;
+    sel_hist_kernel<<<hgrid, 1024, 0, st>>>(s.D, n, s.days, s.hist);
+    sel_locate_kernel<<<static_cast<unsigned>(n_days), 1024, 0, st>>>(s.hist, s.days);
+    sel_gather_kernel<<<grid, 256, 0, st>>>(s.D, n, s.days, s.cand);
+    const size_t smem = kSelCap * sizeof(unsigned long long) + kSelBins * sizeof(unsigned int);
+    SG_CUDA(ctx, prepare_smem(sel_finish_kernel, smem));
+    sel_finish_kernel<<<static_cast<unsigned>(n_days), kSelFinishThreads, smem, st>>>(s.days, s.cand, s.scratch, n,
+                                                                                     d_bands, d_counts, n_days);
+    ctx->launches += 4;
     SG_CUDA(ctx, cudaGetLastError());
     return SG_OK;
 }
@@ -1213,8 +1207,8 @@ static int check_bands_args(sg_ctx* ctx, const double* lower, const double* uppe
     for (int k = 0; k < 6; ++k)
         if (!std::isfinite(lower[k]) || !std::isfinite(upper[k]) || lower[k] > upper[k])
             return fail(ctx, SG_ERR_INVALID_ARGUMENT, "pso: bound " + std::to_string(k) + " is invalid");
-    if (n * static_cast<size_t>(horizon + 1) > static_cast<size_t>(INT32_MAX))
-        return fail(ctx, SG_ERR_INVALID_ARGUMENT, "ensemble too large for one device selection (n x days > 2^31)");
+    if (n > static_cast<size_t>(INT32_MAX))
+        return fail(ctx, SG_ERR_INVALID_ARGUMENT, "ensemble too large for one device selection (n > 2^31)");
     return SG_OK;
 }
 
@@ -1238,14 +1232,72 @@ int sg_forecast_ensemble_bands(sg_window* w, const double lower[6], const double
     SG_CUDA(ctx, b.alloc(&d_counts, n_days));
     SG_CUDA(ctx, copy_async(ctx, d_lo, lower, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     SG_CUDA(ctx, copy_async(ctx, d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    if (const int rc = enqueue_bands(ctx, w, b, ctx->stream, d_lo, d_hi, seed, n, horizon, d_cost, d_bands, d_counts))
-        return rc;
+    if (n == 0) {
+        bands_kernel<<<n_days, 32, 0, ctx->stream>>>(nullptr, 0, d_bands, d_counts, n_days);  // k = 0: NaN bands
+        ctx->launches += 1;
+        SG_CUDA(ctx, cudaGetLastError());
+    } else {
+        BandSlot s;
+        if (const int rc = alloc_band_slot(ctx, b, s, n, n_days)) return rc;
+        if (const int rc = enqueue_band_eval(ctx, w, s, ctx->stream, d_lo, d_hi, seed, n, horizon, d_cost)) return rc;
+        if (const int rc = enqueue_band_select(ctx, s, ctx->stream, n, n_days, d_bands, d_counts)) return rc;
+    }
     static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "count width");
     SG_CUDA(ctx, copy_async(ctx, bands, d_bands, 7 * n_days * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     SG_CUDA(ctx, copy_async(ctx, counts, d_counts, n_days * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
     if (costs && n)
         SG_CUDA(ctx, copy_async(ctx, costs, d_cost, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SG_OK;
+}
+
+int sg_quantile_bands(sg_ctx* ctx, const double* values, size_t n, int n_days, double* bands, uint64_t* counts) {
+    if (!ctx) return SG_ERR_INVALID_ARGUMENT;
+    if (n_days < 1 || (n && !values) || !bands || !counts) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "null buffer");
+    if (n > static_cast<size_t>(INT32_MAX)) return fail(ctx, SG_ERR_INVALID_ARGUMENT, "too many values per day (> 2^31)");
+    SG_ENTRY(ctx, "sg_quantile_bands");
+    SG_CUDA(ctx, cudaSetDevice(ctx->device));
+    DevBufs b;
+    b.st = ctx->stream;
+    double* d_bands;
+    unsigned long long* d_counts;
+    SG_CUDA(ctx, b.alloc(&d_bands, 7 * static_cast<size_t>(n_days)));
+    SG_CUDA(ctx, b.alloc(&d_counts, n_days));
+    if (n == 0) {
+        bands_kernel<<<n_days, 32, 0, ctx->stream>>>(nullptr, 0, d_bands, d_counts, n_days);
+        ctx->launches += 1;
+    } else {
+        BandSlot s;
+        const size_t nd = n * static_cast<size_t>(n_days);
+        SG_CUDA(ctx, b.alloc(&s.D, nd));
+        SG_CUDA(ctx, b.alloc(&s.cand, nd));
+        SG_CUDA(ctx, b.alloc(&s.scratch, 2 * nd));
+        SG_CUDA(ctx, b.alloc(&s.days, n_days));
+        SG_CUDA(ctx, b.alloc(&s.hist, static_cast<size_t>(n_days) * kSelBins));
+        SG_CUDA(ctx, copy_async(ctx, s.D, values, sizeof(double) * nd, cudaMemcpyHostToDevice, ctx->stream));
+        sel_init_kernel<<<static_cast<unsigned>((n_days + 127) / 128), 128, 0, ctx->stream>>>(s.days, n_days);
+        const dim3 grid(static_cast<unsigned>(std::min<size_t>(64, (n + 4095) / 4096)), static_cast<unsigned>(n_days));
+        sel_range_kernel<<<grid, 256, 0, ctx->stream>>>(s.D, n, s.days);
+        ctx->launches += 2;
+        if (const int rc = enqueue_band_select(ctx, s, ctx->stream, n, n_days, d_bands, d_counts)) return rc;
+    }
+    SG_CUDA(ctx, cudaGetLastError());
+    SG_CUDA(ctx, copy_async(ctx, bands, d_bands, 7 * n_days * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, copy_async(ctx, counts, d_counts, n_days * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SG_OK;
+}
+
+// Many windows (C5): a two-slot pipeline on two streams.  The evaluation
+// stream (low priority) runs window k's FP64-bound ensemble while the
+// selection stream (high priority, so its memory-bound CTAs take SM slots
+// as soon as ensemble CTAs retire) reduces window k-1 to bands.
+static int ensure_band_streams(sg_ctx* ctx) {
+    if (ctx->band_eval) return SG_OK;
+    int least = 0, greatest = 0;
+    SG_CUDA(ctx, cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    SG_CUDA(ctx, cudaStreamCreateWithPriority(&ctx->band_eval, cudaStreamNonBlocking, least));
+    SG_CUDA(ctx, cudaStreamCreateWithPriority(&ctx->band_sel, cudaStreamNonBlocking, greatest));
     return SG_OK;
 }
 
@@ -1260,10 +1312,20 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
         if (!windows[k] || windows[k]->ctx != ctx)
             return fail(ctx, SG_ERR_INVALID_ARGUMENT, "windows must be non-null and share one context");
     if (const int rc = check_bands_args(ctx, lower, upper, n, horizon)) return rc;
+    if (n == 0) {  // NaN bands for every window, like the single-window call
+        for (size_t k = 0; k < n_windows; ++k) {
+            const int rc = sg_forecast_ensemble_bands(windows[k], lower, upper, seeds[k], 0, horizon,
+                                                      bands + 7 * static_cast<size_t>(horizon + 1) * k,
+                                                      counts + static_cast<size_t>(horizon + 1) * k, nullptr);
+            if (rc) return rc;
+        }
+        return SG_OK;
+    }
     const int n_days = horizon + 1;
     SG_ENTRY(ctx, "sg_forecast_ensemble_bands_batch");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     if (const int rc = ensure_lanes(ctx)) return rc;
+    if (const int rc = ensure_band_streams(ctx)) return rc;
     DevBufs b;
     b.st = ctx->stream;
     double *d_lo, *d_hi, *d_bands;
@@ -1272,32 +1334,50 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
     SG_CUDA(ctx, b.alloc(&d_hi, 6));
     SG_CUDA(ctx, b.alloc(&d_bands, 7 * static_cast<size_t>(n_days) * n_windows));
     SG_CUDA(ctx, b.alloc(&d_counts, static_cast<size_t>(n_days) * n_windows));
+    constexpr int kSlots = 2;
+    BandSlot slot[kSlots];
+    for (BandSlot& s : slot)
+        if (const int rc = alloc_band_slot(ctx, b, s, n, n_days)) return rc;
     SG_CUDA(ctx, copy_async(ctx, d_lo, lower, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     SG_CUDA(ctx, copy_async(ctx, d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    // Windows alternate between two side streams, so one window's band
-    // selection (small kernels) overlaps the next window's evaluation.
-    constexpr int kBandStreams = 2;
-    SG_CUDA(ctx, cudaEventRecord(ctx->fork, ctx->stream));
-    for (int l = 0; l < kBandStreams; ++l) SG_CUDA(ctx, cudaStreamWaitEvent(ctx->side[l], ctx->fork, 0));
+    cudaEvent_t evaluated[kSlots], selected[kSlots];
+    for (int k = 0; k < kSlots; ++k) {
+        SG_CUDA(ctx, cudaEventCreateWithFlags(&evaluated[k], cudaEventDisableTiming));
+        SG_CUDA(ctx, cudaEventCreateWithFlags(&selected[k], cudaEventDisableTiming));
+    }
+    cudaStream_t E = ctx->band_eval, S = ctx->band_sel;
+    SG_CUDA(ctx, cudaEventRecord(ctx->fork, ctx->stream));  // buffers allocated, bounds uploaded
+    SG_CUDA(ctx, cudaStreamWaitEvent(E, ctx->fork, 0));
+    SG_CUDA(ctx, cudaStreamWaitEvent(S, ctx->fork, 0));
     int rc = SG_OK;
     for (size_t k = 0; k < n_windows && !rc; ++k) {
-        cudaStream_t st = ctx->side[k % kBandStreams];
-        DevBufs wb;  // per-window scratch, freed in stream order on st
-        wb.st = st;
-        rc = enqueue_bands(ctx, windows[k], wb, st, d_lo, d_hi, seeds[k], n, horizon, nullptr,
-                           d_bands + 7 * static_cast<size_t>(n_days) * k, d_counts + static_cast<size_t>(n_days) * k);
+        const int j = static_cast<int>(k % kSlots);
+        // the slot's previous window must be reduced before its buffers are rewritten
+        if (k >= kSlots && (rc = cudaStreamWaitEvent(E, selected[j], 0)) != cudaSuccess) break;
+        rc = enqueue_band_eval(ctx, windows[k], slot[j], E, d_lo, d_hi, seeds[k], n, horizon, nullptr);
+        if (rc) break;
+        if (cudaEventRecord(evaluated[j], E) != cudaSuccess || cudaStreamWaitEvent(S, evaluated[j], 0) != cudaSuccess) {
+            rc = SG_ERR_CUDA;
+            break;
+        }
+        rc = enqueue_band_select(ctx, slot[j], S, n, n_days, d_bands + 7 * static_cast<size_t>(n_days) * k,
+                                 d_counts + static_cast<size_t>(n_days) * k);
+        if (!rc && cudaEventRecord(selected[j], S) != cudaSuccess) rc = SG_ERR_CUDA;
     }
-    // join the side streams even after a failure: the shared buffers are
-    // released in ctx->stream order
-    for (int l = 0; l < kBandStreams; ++l) {
-        SG_CUDA(ctx, cudaEventRecord(ctx->join[l], ctx->side[l]));
-        SG_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join[l], 0));
+    // join both streams even after a failure: the buffers are released in ctx->stream order
+    SG_CUDA(ctx, cudaEventRecord(ctx->join[0], E));
+    SG_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join[0], 0));
+    SG_CUDA(ctx, cudaEventRecord(ctx->join[1], S));
+    SG_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join[1], 0));
+    for (int k = 0; k < kSlots; ++k) {
+        cudaEventDestroy(evaluated[k]);
+        cudaEventDestroy(selected[k]);
     }
-    if (rc) return rc;
+    if (rc) return rc == SG_ERR_CUDA ? cuda_fail(ctx, cudaGetLastError(), "band pipeline") : rc;
     SG_CUDA(ctx, copy_async(ctx, bands, d_bands, 7 * n_days * n_windows * sizeof(double), cudaMemcpyDeviceToHost,
-                                 ctx->stream));
+                            ctx->stream));
     SG_CUDA(ctx, copy_async(ctx, counts, d_counts, n_days * n_windows * sizeof(uint64_t), cudaMemcpyDeviceToHost,
-                                 ctx->stream));
+                            ctx->stream));
     SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return SG_OK;
 }

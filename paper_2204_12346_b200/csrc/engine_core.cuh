@@ -50,6 +50,9 @@ struct sg_ctx {
     cudaStream_t side[kMaxLanes] = {};
     cudaEvent_t fork = nullptr;
     cudaEvent_t join[kMaxLanes] = {};
+    // the C5 band pipeline: ensemble evaluation (low priority) and band
+    // selection (high priority) streams
+    cudaStream_t band_eval = nullptr, band_sel = nullptr;
 };
 
 struct sg_window {

@@ -896,112 +896,22 @@ __device__ __forceinline__ void x_of_sample(const double* lo, const double* hi, 
     repair_order(x);
 }
 
-#ifndef SG_FAMILY_TU  // engine.cu only (family.cu holds the templated kernels)
-// Evaluation order of an ensemble: every sample's parameters into SoA
-// planes and a key (day of t1, day of t2) — samples with equal keys ramp on
-// the same days, so sorting by it makes a warp's lanes ramp together (the
-// warp pays a ramp substep if any lane ramps).  The order never changes a
-// result: every sample is evaluated by the same code into its own slot.
-__global__ void __launch_bounds__(256) ens_sample_kernel(const double* __restrict__ lo, const double* __restrict__ hi,
-                                                         uint64_t seed, size_t n, double* __restrict__ planes,
-                                                         uint32_t* __restrict__ keys, uint32_t* __restrict__ idx) {
-    const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    double x[6];
-    x_of_sample(lo, hi, seed, k, x);
-#pragma unroll
-    for (int d = 0; d < 6; ++d) planes[d * n + k] = x[d];
-    auto day = [](double t) -> uint32_t {  // NaN and negatives -> 0, capped at 255
-        return t > 0.0 ? static_cast<uint32_t>(fmin(floor(t), 255.0)) : 0u;
-    };
-    keys[k] = (day(x[2]) << 8) | day(x[3]);
-    idx[k] = static_cast<uint32_t>(k);
-}
-
-#endif  // SG_FAMILY_TU
-
-template <int FAM, int MET, int SUB>
-__global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWindow* __restrict__ win, DevWindow fwin,
-                                                                const double* __restrict__ lo,
-                                                                const double* __restrict__ hi, uint64_t seed,
-                                                                size_t n, int horizon, double* __restrict__ costs,
-                                                                double* __restrict__ params_out,
-                                                                double* __restrict__ deaths_out, size_t sstride,
-                                                                size_t dstride, const uint32_t* __restrict__ perm,
-                                                                const double* __restrict__ planes, int out_by_slot) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ DevWindow sdesc;
-    const SmemWindow sw = stage_window<MET, SUB>(win, &sdesc, smem);
-    // Thread slot -> sample k: identity, or the ramp-coherent order of
-    // ens_sample_kernel + sort (perm), with the sample's parameters read from
-    // its planes.  Costs and parameters always land at k; the deaths row at k,
-    // or at the slot when the caller only needs the per-day multiset (bands).
-    const size_t slot = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (slot >= n) return;
-    const size_t k = perm ? perm[slot] : slot;
-    double x[6];
-    if (planes) {
-#pragma unroll
-        for (int d = 0; d < 6; ++d) x[d] = planes[d * n + k];
-    } else {
-        x_of_sample(lo, hi, seed, k, x);
-    }
-    if (params_out) {
-#pragma unroll
-        for (int d = 0; d < 6; ++d) params_out[6 * k + d] = x[d];
-    }
-    const DevWindow& w = *sw.w;
-    const double nan = __longlong_as_double(0x7FF8000000000000LL);
-    // deaths of sample k, forecast day d at deaths_out[k*sstride + d*dstride]
-    // (sample-major rows, or day-major columns for the on-device bands)
-    double* drow = deaths_out + (out_by_slot ? slot : k) * sstride;
-    if (!w.init_finite) {
-        if (costs) costs[k] = __longlong_as_double(0x7FF0000000000000LL);
-        for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
-        return;
-    }
-    const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w, SUB != 0 ? sw.tg.tgrid : nullptr);
-    double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
-    ScoreSink<FAM, MET> score(w, sw.obs, sw.robs, sw.flag);  // starts from the day-0 contribution
-    integrate_days<SUB>(p, w, sw.tg, S, I, R, D, score);
-    const bool fin_w = all_finite(S, I, R, D);
-    // forecast_extension re-checks the junction through integrate_euler's
-    // isfinite(init.total()) (model.cpp:83).
-    const bool fin_j = fin_w && isfinite(dadd(dadd(dadd(S, I), R), D));
-    if (costs) costs[k] = score.finish(fin_w);
-    if (!fin_j) {  // forecast_extension throws NonFiniteError (calibration.cpp:301-303, 318-320)
-        for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
-        return;
-    }
-    // Forecast: fwin carries n_days = horizon + 1 and the same N, h, substeps.
-    const Particle held = make_particle(x[1], x[1], 0.0, 0.0, x[4], x[5], fwin);
-    drow[0] = D;
-    ForecastDSink fs{drow, dstride};
-    // held parameters never enter the ramp, so no time table is read
-    integrate_days<SUB>(held, fwin, TimeGrid{nullptr, sw.tg.subh}, S, I, R, D, fs);
-    if (!all_finite(S, I, R, D)) {  // calibration.cpp:318-320
-        for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
-    }
-}
-
-// ---- quantile bands by selection (C5) ------------------------------------------
+// ---- quantile bands by selection (C5): shared declarations ---------------------
 //
 // build_quantile_bands (calibration.cpp:337-361) needs, per forecast day, the
 // count k of finite values and the order statistics at ranks lo and lo+1 of
 // h = (k-1)*p for 7 probabilities — at most 14 ranks out of 10^6.  Instead of
 // sorting every day column, the values are mapped to order-preserving 64-bit
 // keys, bucketed into 2^12 bins over each day's key range (monotone, so rank
-// intervals of bins are exact), only the bins holding a wanted rank are
-// gathered and sorted (segmented sort), and the ranks are read from there.
-// The order statistics are values of the data, so the bands are the full
-// sort's to the bit (ties between -0 and +0 keep the radix order, as CUB's
-// sort of the whole column does).
+// intervals of bins are exact), and only the bins holding a wanted rank are
+// gathered and sorted — in one CTA's shared memory, with a finer histogram
+// level for a bin too full to sort there.  The order statistics are values of
+// the data, so the bands are the full sort's to the bit (ties between -0 and
+// +0 follow the key order, as a radix sort of the column does).
 constexpr int kBandP = 7;
 constexpr int kBandRanks = 2 * kBandP;  // lo and lo+1 per probability
 constexpr int kSelBinBits = 12;
 constexpr int kSelBins = 1 << kSelBinBits;  // per day; a CTA histogram fits in shared memory
-#ifndef SG_FAMILY_TU  // engine.cu only
-__device__ __constant__ double kBandProbs[kBandP] = {0.5, 0.25, 0.75, 0.05, 0.95, 0.025, 0.975};  // 352-358
 
 __host__ __device__ __forceinline__ uint64_t order_key(double x) {
 #ifdef __CUDA_ARCH__
@@ -1011,6 +921,11 @@ __host__ __device__ __forceinline__ uint64_t order_key(double x) {
     std::memcpy(&b, &x, sizeof b);
 #endif
     return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+
+__device__ __forceinline__ double key_value(uint64_t k) {
+    const uint64_t b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFULL) : ~k;
+    return __longlong_as_double(static_cast<long long>(b));
 }
 
 struct SelDay {                   // per forecast day, device memory
@@ -1023,6 +938,74 @@ struct SelDay {                   // per forecast day, device memory
     uint32_t seg_fill[kBandRanks];
 };
 
+#ifndef SG_FAMILY_TU  // engine.cu only (family.cu holds the templated kernels)
+// Evaluation order of an ensemble: every sample's parameters into SoA
+// planes and a key (day of t1, day of t2) — samples with equal keys ramp on
+// the same days, so grouping them makes a warp's lanes ramp together (the
+// warp pays a ramp substep if any lane ramps).  The order never changes a
+// result: every sample is evaluated by the same code into its own slot, and
+// the bands only need each day's multiset.  Fused: the key histogram of the
+// counting sort (ens_scan_kernel, ens_scatter_kernel).
+__global__ void __launch_bounds__(256) ens_sample_kernel(const double* __restrict__ lo, const double* __restrict__ hi,
+                                                         uint64_t seed, size_t n, double* __restrict__ planes,
+                                                         uint32_t* __restrict__ keys,
+                                                         unsigned int* __restrict__ key_count) {
+    const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double x[6];
+    x_of_sample(lo, hi, seed, k, x);
+#pragma unroll
+    for (int d = 0; d < 6; ++d) planes[d * n + k] = x[d];
+    auto day = [](double t) -> uint32_t {  // NaN and negatives -> 0, capped at 255
+        return t > 0.0 ? static_cast<uint32_t>(fmin(floor(t), 255.0)) : 0u;
+    };
+    const uint32_t key = (day(x[2]) << 8) | day(x[3]);
+    keys[k] = key;
+    atomicAdd(&key_count[key], 1u);
+}
+
+// Exclusive scan of the 2^16 key counts into bucket cursors (one CTA).
+__global__ void __launch_bounds__(1024) ens_scan_kernel(unsigned int* __restrict__ key_count) {
+    constexpr int kPer = 65536 / 1024;
+    __shared__ unsigned int warp_sum[32];
+    unsigned int mine = 0;
+    for (int j = 0; j < kPer; ++j) mine += key_count[threadIdx.x * kPer + j];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned int incl = mine;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const unsigned int o = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    if (lane == 31) warp_sum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned int w = warp_sum[lane];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned int o = __shfl_up_sync(0xFFFFFFFFu, w, off);
+            if (lane >= off) w += o;
+        }
+        warp_sum[lane] = w - warp_sum[lane];
+    }
+    __syncthreads();
+    unsigned int run = warp_sum[warp] + (incl - mine);
+    for (int j = 0; j < kPer; ++j) {
+        const unsigned int c = key_count[threadIdx.x * kPer + j];
+        key_count[threadIdx.x * kPer + j] = run;
+        run += c;
+    }
+}
+
+// Counting-sort scatter: sample k takes the next slot of its key's bucket.
+__global__ void __launch_bounds__(256) ens_scatter_kernel(const uint32_t* __restrict__ keys, size_t n,
+                                                          unsigned int* __restrict__ cursor,
+                                                          uint32_t* __restrict__ perm) {
+    const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    perm[atomicAdd(&cursor[keys[k]], 1u)] = static_cast<uint32_t>(k);
+}
+
 __global__ void sel_init_kernel(SelDay* __restrict__ days, int n_days) {
     const int d = blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= n_days) return;
@@ -1031,8 +1014,127 @@ __global__ void sel_init_kernel(SelDay* __restrict__ days, int n_days) {
     days[d].count = 0;
     days[d].n_seg = 0;
 }
+#endif  // SG_FAMILY_TU
 
-// k and the key range of every day (grid: chunks x days).
+template <int FAM, int MET, int SUB>
+__global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWindow* __restrict__ win, DevWindow fwin,
+                                                                const double* __restrict__ lo,
+                                                                const double* __restrict__ hi, uint64_t seed,
+                                                                size_t n, int horizon, double* __restrict__ costs,
+                                                                double* __restrict__ params_out,
+                                                                double* __restrict__ deaths_out, size_t sstride,
+                                                                size_t dstride, const uint32_t* __restrict__ perm,
+                                                                const double* __restrict__ planes, int out_by_slot,
+                                                                SelDay* __restrict__ days) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ DevWindow sdesc;
+    const SmemWindow sw = stage_window<MET, SUB>(win, &sdesc, smem);
+    // Thread slot -> sample k: identity, or the ramp-coherent order of
+    // ens_sample_kernel + counting sort (perm), with the sample's parameters
+    // read from its planes.  Costs and parameters always land at k; the
+    // deaths row at k, or at the slot when the caller only needs the per-day
+    // multiset (bands).
+    const size_t slot = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool live = slot < n;
+    const size_t k = live ? (perm ? perm[slot] : slot) : 0;
+    // deaths of sample k, forecast day d at deaths_out[k*sstride + d*dstride]
+    // (sample-major rows, or day-major columns for the on-device bands)
+    double* drow = deaths_out + (out_by_slot ? slot : k) * sstride;
+    if (live) {
+        [&] {
+            double x[6];
+            if (planes) {
+#pragma unroll
+                for (int d = 0; d < 6; ++d) x[d] = planes[d * n + k];
+            } else {
+                x_of_sample(lo, hi, seed, k, x);
+            }
+            if (params_out) {
+#pragma unroll
+                for (int d = 0; d < 6; ++d) params_out[6 * k + d] = x[d];
+            }
+            const DevWindow& w = *sw.w;
+            const double nan = __longlong_as_double(0x7FF8000000000000LL);
+            if (!w.init_finite) {
+                if (costs) costs[k] = __longlong_as_double(0x7FF0000000000000LL);
+                for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
+                return;
+            }
+            const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w, SUB != 0 ? sw.tg.tgrid : nullptr);
+            double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
+            ScoreSink<FAM, MET> score(w, sw.obs, sw.robs, sw.flag);  // starts from the day-0 contribution
+            integrate_days<SUB>(p, w, sw.tg, S, I, R, D, score);
+            const bool fin_w = all_finite(S, I, R, D);
+            // forecast_extension re-checks the junction through integrate_euler's
+            // isfinite(init.total()) (model.cpp:83).
+            const bool fin_j = fin_w && isfinite(dadd(dadd(dadd(S, I), R), D));
+            if (costs) costs[k] = score.finish(fin_w);
+            if (!fin_j) {  // forecast_extension throws NonFiniteError (calibration.cpp:301-303, 318-320)
+                for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
+                return;
+            }
+            // Forecast: fwin carries n_days = horizon + 1 and the same N, h, substeps.
+            const Particle held = make_particle(x[1], x[1], 0.0, 0.0, x[4], x[5], fwin);
+            drow[0] = D;
+            ForecastDSink fs{drow, dstride};
+            // held parameters never enter the ramp, so no time table is read
+            integrate_days<SUB>(held, fwin, TimeGrid{nullptr, sw.tg.subh}, S, I, R, D, fs);
+            if (!all_finite(S, I, R, D)) {  // calibration.cpp:318-320
+                for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
+            }
+        }();
+    }
+    if (!days) return;
+    // Band selection, fused: the key range and the count of each day's
+    // finite values (the first pass of the selection, without re-reading
+    // the deaths plane from HBM): a warp reduction, one atomic per warp and day.
+    for (int d = 0; d <= horizon; ++d) {
+        const double v = live ? drow[d * dstride] : __longlong_as_double(0x7FF8000000000000LL);
+        const bool fin = isfinite(v);
+        unsigned long long kl = fin ? order_key(v) : ~0ULL, kh = fin ? order_key(v) : 0ULL;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const unsigned long long ol = __shfl_xor_sync(0xFFFFFFFFu, kl, off);
+            const unsigned long long oh = __shfl_xor_sync(0xFFFFFFFFu, kh, off);
+            kl = ol < kl ? ol : kl;
+            kh = oh > kh ? oh : kh;
+        }
+        const unsigned cnt = __popc(__ballot_sync(0xFFFFFFFFu, fin));
+        if ((threadIdx.x & 31) == 0 && cnt) {
+            atomicMin(&days[d].kmin, kl);
+            atomicMax(&days[d].kmax, kh);
+            atomicAdd(&days[d].count, static_cast<unsigned long long>(cnt));
+        }
+    }
+}
+
+#ifndef SG_FAMILY_TU  // engine.cu only
+__device__ __constant__ double kBandProbs[kBandP] = {0.5, 0.25, 0.75, 0.05, 0.95, 0.025, 0.975};  // 352-358
+
+__device__ __forceinline__ int sel_shift(unsigned long long range) {
+    const int bits = range ? 64 - __clzll(static_cast<long long>(range)) : 0;
+    return bits > kSelBinBits ? bits - kSelBinBits : 0;
+}
+
+// The ranks quantile_sorted reads for k finite values (calibration.cpp:324-335).
+__device__ __forceinline__ int band_ranks(uint64_t k, uint64_t* ranks) {
+    int m = 0;
+    for (int q = 0; q < kBandP; ++q) {
+        const double hq = dmul(static_cast<double>(k - 1), kBandProbs[q]);
+        const uint64_t lo = static_cast<uint64_t>(hq);
+        if (lo + 1 >= k) {
+            ranks[m++] = k - 1;
+        } else {
+            ranks[m++] = lo;
+            ranks[m++] = lo + 1;
+        }
+    }
+    return m;
+}
+
+// k and the key range of every day of a given plane (grid: chunks x days) —
+// the ensemble kernel's fused epilogue as a kernel of its own, for bands of
+// values that come from elsewhere (sg_quantile_bands).
 __global__ void sel_range_kernel(const double* __restrict__ col, size_t n, SelDay* __restrict__ days) {
     const int d = blockIdx.y;
     const double* c = col + static_cast<size_t>(d) * n;
@@ -1046,7 +1148,6 @@ __global__ void sel_range_kernel(const double* __restrict__ col, size_t n, SelDa
         hi = k > hi ? k : hi;
         ++cnt;
     }
-    // 64-bit warp reductions by shuffles
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         const unsigned long long olo = __shfl_xor_sync(0xFFFFFFFFu, lo, off);
@@ -1060,11 +1161,6 @@ __global__ void sel_range_kernel(const double* __restrict__ col, size_t n, SelDa
         atomicMax(&days[d].kmax, hi);
         atomicAdd(&days[d].count, cnt);
     }
-}
-
-__device__ __forceinline__ int sel_shift(unsigned long long range) {
-    const int bits = range ? 64 - __clzll(static_cast<long long>(range)) : 0;
-    return bits > kSelBinBits ? bits - kSelBinBits : 0;
 }
 
 // Histogram of every day's finite values over its bins: per CTA in shared
@@ -1123,21 +1219,7 @@ __global__ void __launch_bounds__(1024) sel_locate_kernel(const unsigned int* __
         if (lane >= off) incl += o;
     }
     if (lane == 31) warp_sum[warp] = incl;
-    if (threadIdx.x == 0) {
-        // the ranks quantile_sorted reads (calibration.cpp:324-335)
-        int m = 0;
-        for (int q = 0; q < kBandP; ++q) {
-            const double hq = dmul(static_cast<double>(k - 1), kBandProbs[q]);
-            const uint64_t lo = static_cast<uint64_t>(hq);
-            if (lo + 1 >= k) {
-                ranks[m++] = k - 1;
-            } else {
-                ranks[m++] = lo;
-                ranks[m++] = lo + 1;
-            }
-        }
-        n_ranks = m;
-    }
+    if (threadIdx.x == 0) n_ranks = band_ranks(k, ranks);
     __syncthreads();
     if (warp == 0) {
         uint32_t w = warp_sum[lane];
@@ -1191,16 +1273,9 @@ __global__ void __launch_bounds__(1024) sel_locate_kernel(const unsigned int* __
     }
 }
 
-// Segment j of day d occupies cand[d*n + seg_rank0[j] - seg_rank0[0] + ...]:
-// the day's segments are packed in bin order at the start of its slice.
-__device__ __forceinline__ uint64_t sel_seg_offset(const SelDay& sd, int j) {
-    uint64_t off = 0;
-    for (int t = 0; t < j; ++t) off += sd.seg_count[t];
-    return off;
-}
-
 // Copy the values of the wanted bins into their segments (a shared-memory
-// bin -> segment table, warp-aggregated slot reservation).
+// bin -> segment table, warp-aggregated slot reservation).  Segment j of day
+// d occupies cand[d*n + sum of the earlier segments' counts ...].
 __global__ void __launch_bounds__(256) sel_gather_kernel(const double* __restrict__ col, size_t n,
                                                          SelDay* __restrict__ days, double* __restrict__ cand) {
     __shared__ unsigned char seg_of[kSelBins];
@@ -1245,55 +1320,155 @@ __global__ void __launch_bounds__(256) sel_gather_kernel(const double* __restric
     }
 }
 
-// Segment boundaries for the segmented sort: day d, slot j < kBandRanks.
-__global__ void sel_segments_kernel(const SelDay* __restrict__ days, size_t n, int n_days,
-                                    int* __restrict__ begin, int* __restrict__ end) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n_days * kBandRanks) return;
-    const int d = t / kBandRanks, j = t % kBandRanks;
-    const SelDay& sd = days[d];
-    const int base = d * static_cast<int>(n);  // n_days * n <= INT_MAX (host check)
-    if (sd.count == 0 || j >= sd.n_seg) {
-        begin[t] = end[t] = base;
-        return;
+// ---- finishing a day in one CTA: sort the wanted bins, read the ranks ----------
+constexpr int kSelCap = 8192;          // keys sorted at once in shared memory (64 KB)
+constexpr int kSelFinishThreads = 512;
+
+// Ascending bitonic sort of m (a power of two) keys in shared memory.
+__device__ __forceinline__ void smem_bitonic_sort(unsigned long long* a, int m) {
+    for (int size = 2; size <= m; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < m; i += blockDim.x) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const unsigned long long x = a[i], y = a[j];
+                    if ((x > y) == ((i & size) == 0)) {
+                        a[i] = y;
+                        a[j] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
     }
-    const int off = static_cast<int>(sel_seg_offset(sd, j));
-    begin[t] = base + off;
-    end[t] = base + off + static_cast<int>(sd.seg_count[j]);
 }
 
-// Order statistic of rank r of day d from its sorted segments.
-__device__ __forceinline__ double sel_rank(const SelDay& sd, const double* sorted_day, uint64_t r) {
-    uint64_t off = 0;
-    for (int j = 0; j < sd.n_seg; ++j) {
-        if (r >= sd.seg_rank0[j] && r < sd.seg_rank0[j] + sd.seg_count[j]) return sorted_day[off + (r - sd.seg_rank0[j])];
-        off += sd.seg_count[j];
-    }
-    return __longlong_as_double(0x7FF8000000000000LL);  // unreachable: every wanted rank has a segment
+// Keys of `count` values (<= kSelCap) sorted into shared memory `keys`.
+__device__ __forceinline__ void sort_values(const double* src, uint32_t count, unsigned long long* keys) {
+    int m = 1;
+    while (m < static_cast<int>(count)) m <<= 1;
+    for (int i = threadIdx.x; i < m; i += blockDim.x)
+        keys[i] = i < static_cast<int>(count) ? order_key(src[i]) : ~0ULL;  // padding sorts last
+    __syncthreads();
+    smem_bitonic_sort(keys, m);
 }
 
-// quantile_sorted (calibration.cpp:324-335) on the selected order statistics.
-__global__ void sel_bands_kernel(const SelDay* __restrict__ days, const double* __restrict__ sorted, size_t n,
-                                 double* __restrict__ bands, unsigned long long* __restrict__ counts, int n_days) {
-    const int d = blockIdx.x * blockDim.x + threadIdx.x;
-    if (d >= n_days) return;
+// The order statistic of local rank `target` among the `count` values of one
+// bin (keys in [base, base + 2^shift)) that do not fit in shared memory:
+// finer histogram levels of 2^12 sub-bins, each keeping only the sub-bin
+// that holds the rank (gathered into the scratch pair), until the rest fits
+// or the sub-bin is a single key.  CTA-uniform; result in *out (thread 0).
+__device__ void select_large(const double* src, uint32_t count, unsigned long long base, int shift, uint32_t target,
+                             double* scratch_a, double* scratch_b, unsigned long long* keys, unsigned int* hist,
+                             double* out) {
+    __shared__ uint32_t s_bin, s_before, s_fill;
+    double* dst = scratch_a;
+    while (true) {
+        if (count <= static_cast<uint32_t>(kSelCap)) {
+            sort_values(src, count, keys);
+            if (threadIdx.x == 0) *out = key_value(keys[target]);
+            __syncthreads();
+            return;
+        }
+        if (shift == 0) {  // every value of the bin is this key
+            if (threadIdx.x == 0) *out = key_value(base);
+            __syncthreads();
+            return;
+        }
+        const int sub = shift > kSelBinBits ? shift - kSelBinBits : 0;
+        for (int b = threadIdx.x; b < kSelBins; b += blockDim.x) hist[b] = 0;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < count; i += blockDim.x)
+            atomicAdd(&hist[static_cast<uint32_t>((order_key(src[i]) - base) >> sub)], 1u);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t acc = 0, b = 0;
+            while (acc + hist[b] <= target) acc += hist[b++];
+            s_bin = b;
+            s_before = acc;
+            s_fill = 0;
+        }
+        __syncthreads();
+        const uint32_t bin = s_bin;
+        for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) {
+            const double x = src[i];
+            if (static_cast<uint32_t>((order_key(x) - base) >> sub) == bin) dst[atomicAdd(&s_fill, 1u)] = x;
+        }
+        __syncthreads();
+        count = hist[bin];
+        target -= s_before;
+        base += static_cast<unsigned long long>(bin) << sub;
+        shift = sub;
+        src = dst;
+        dst = dst == scratch_a ? scratch_b : scratch_a;
+        __syncthreads();
+    }
+}
+
+// One CTA per day: the wanted order statistics from the day's gathered
+// segments (each sorted in shared memory once), then quantile_sorted
+// (calibration.cpp:324-335) with the reference's operation order.
+// scratch: 2 x n doubles per day (only touched by bins too full to sort).
+__global__ void __launch_bounds__(kSelFinishThreads) sel_finish_kernel(const SelDay* __restrict__ days,
+                                                                        const double* __restrict__ cand,
+                                                                        double* __restrict__ scratch, size_t n,
+                                                                        double* __restrict__ bands,
+                                                                        unsigned long long* __restrict__ counts,
+                                                                        int n_days) {
+    extern __shared__ __align__(16) unsigned long long keys[];  // kSelCap keys, then kSelBins counters
+    unsigned int* hist = reinterpret_cast<unsigned int*>(keys + kSelCap);
+    __shared__ uint64_t ranks[kBandRanks];
+    __shared__ double vals[kBandRanks];
+    __shared__ int n_ranks;
+    const int d = blockIdx.x;
     const SelDay& sd = days[d];
     const uint64_t k = sd.count;
-    counts[d] = k;
-    const double* s = sorted + static_cast<size_t>(d) * n;
-    for (int q = 0; q < kBandP; ++q) {
-        double v;
-        if (k == 0) {
-            v = __longlong_as_double(0x7FF8000000000000LL);
+    if (threadIdx.x == 0) {
+        counts[d] = k;
+        n_ranks = k ? band_ranks(k, ranks) : 0;
+    }
+    __syncthreads();
+    if (k == 0) {
+        if (threadIdx.x < kBandP) bands[threadIdx.x * n_days + d] = __longlong_as_double(0x7FF8000000000000LL);
+        return;
+    }
+    const double* day_cand = cand + static_cast<size_t>(d) * n;
+    double* sa = scratch + static_cast<size_t>(d) * 2 * n;
+    uint64_t off = 0;
+    for (int j = 0; j < sd.n_seg; ++j) {
+        const uint32_t cnt = sd.seg_count[j];
+        const uint64_t r0 = sd.seg_rank0[j];
+        const unsigned long long base = sd.kmin + (static_cast<unsigned long long>(sd.seg_bin[j]) << sd.shift);
+        if (cnt <= static_cast<uint32_t>(kSelCap) && sd.shift > 0) {
+            sort_values(day_cand + off, cnt, keys);
+            for (int r = threadIdx.x; r < n_ranks; r += blockDim.x)
+                if (ranks[r] >= r0 && ranks[r] < r0 + cnt) vals[r] = key_value(keys[ranks[r] - r0]);
+            __syncthreads();
         } else {
-            const double h = dmul(static_cast<double>(k - 1), kBandProbs[q]);
-            const uint64_t lo = static_cast<uint64_t>(h);
-            if (lo + 1 >= k) {
-                v = sel_rank(sd, s, k - 1);
-            } else {
-                const double a = sel_rank(sd, s, lo), b = sel_rank(sd, s, lo + 1);
-                v = dadd(a, dmul(dsub(h, static_cast<double>(lo)), dsub(b, a)));
+            for (int r = 0; r < n_ranks; ++r) {  // CTA-uniform
+                if (!(ranks[r] >= r0 && ranks[r] < r0 + cnt)) continue;
+                select_large(day_cand + off, cnt, base, sd.shift, static_cast<uint32_t>(ranks[r] - r0), sa, sa + n,
+                             keys, hist, &vals[r]);
             }
+        }
+        off += cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    auto rank_value = [&](uint64_t r) {
+        for (int t = 0; t < n_ranks; ++t)
+            if (ranks[t] == r) return vals[t];
+        return __longlong_as_double(0x7FF8000000000000LL);  // unreachable: every wanted rank was resolved
+    };
+    for (int q = 0; q < kBandP; ++q) {
+        const double h = dmul(static_cast<double>(k - 1), kBandProbs[q]);
+        const uint64_t lo = static_cast<uint64_t>(h);
+        double v;
+        if (lo + 1 >= k) {
+            v = rank_value(k - 1);
+        } else {
+            const double a = rank_value(lo), b = rank_value(lo + 1);
+            v = dadd(a, dmul(dsub(h, static_cast<double>(lo)), dsub(b, a)));
         }
         bands[q * n_days + d] = v;
     }

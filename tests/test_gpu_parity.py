@@ -314,3 +314,48 @@ def test_ensemble_bands_batch_equals_per_window_calls(ctx, poland):
         b1, c1, _ = w.forecast_ensemble_bands(lo, hi, seeds[k], 50_000, 21)
         assert counts[k].tolist() == c1.tolist()
         assert_bitwise(bands[k].ravel(), b1.ravel(), f"window {k}")
+
+
+@pytest.mark.parametrize("case", ["cluster_outliers", "two_clusters", "spiky_key_range", "nan_mix", "constant",
+                                  "tiny_counts"])
+def test_quantile_bands_selection_paths(ctx, reference, case):
+    """sg_quantile_bands (build_quantile_bands, calibration.cpp:337-361) on
+    synthetic columns that drive every path of the selection: a bin too full
+    for one CTA's shared memory (a dense cluster plus far outliers, so the
+    bins are wide and one holds > 8,192 values: the finer histogram levels),
+    two clusters, a key range collapsing to single keys, NaN/inf mixed in,
+    constant columns and columns with 0-3 finite values.  Against the
+    reference's own build_quantile_bands (oracle/_ref), bit for bit."""
+    import ctypes
+    rng = np.random.default_rng(31)
+    n, n_days = 60_000, 5
+    cols = np.empty((n_days, n))
+    for d in range(n_days):
+        if case == "cluster_outliers":
+            c = 1000.0 + rng.random(n) * 1e-3 * (d + 1)
+            c[rng.choice(n, 40, replace=False)] = 10.0 ** rng.uniform(6, 12, 40)
+        elif case == "two_clusters":
+            c = np.where(rng.random(n) < 0.3, 5.0 + rng.random(n) * 1e-6, 7e5 + rng.random(n))
+        elif case == "spiky_key_range":
+            c = 2.0 + np.floor(rng.random(n) * 37) * np.finfo(float).eps * 2  # 37 distinct neighbouring doubles
+        elif case == "nan_mix":
+            c = rng.normal(1e4, 50.0, n)
+            c[rng.random(n) < 0.2] = np.nan
+            c[rng.random(n) < 0.01] = np.inf
+            c[rng.random(n) < 0.01] = -np.inf
+        elif case == "constant":
+            c = np.full(n, 3.25)
+        else:
+            c = np.full(n, np.nan)
+            c[:d % 4] = rng.random(d % 4)
+        cols[d] = c
+    bands, counts = ctx.quantile_bands(cols)
+    want = np.zeros((7, n_days))
+    want_counts = np.zeros(n_days, dtype=np.uint64)
+    samples = np.ascontiguousarray(cols.T)  # the shim takes sample-major values
+    dp = ctypes.POINTER(ctypes.c_double)
+    rc = reference.lib.ref_quantile_bands(samples.ctypes.data_as(dp), n, n_days, want.ctypes.data_as(dp),
+                                          want_counts.ctypes.data_as(ctypes.POINTER(ctypes.c_size_t)))
+    assert rc == 0
+    assert counts.tolist() == want_counts.tolist()
+    assert_bitwise(bands.ravel(), want.ravel(), case)
