@@ -1141,11 +1141,22 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
 
 // Device buffers of one window in flight in the C5 pipeline.
 struct BandSlot {
-    double *planes = nullptr, *D = nullptr, *cand = nullptr, *scratch = nullptr;
+    double *planes = nullptr, *D = nullptr, *cand = nullptr, *scratch = nullptr, *vals = nullptr;
     uint32_t *keys = nullptr, *perm = nullptr;
     unsigned int *key_count = nullptr, *hist = nullptr;
     SelDay* days = nullptr;
 };
+
+// The key range of the band selection comes from the ensemble kernel's
+// epilogue (default) or, with SG_FUSED_RANGE=0 (diagnostic A/B), from a
+// separate pass over the deaths plane on the selection stream.
+static bool fused_range() {
+    static const bool on = [] {
+        const char* e = std::getenv("SG_FUSED_RANGE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 static int alloc_band_slot(sg_ctx* ctx, DevBufs& b, BandSlot& s, size_t n, int n_days) {
     const size_t nd = n * static_cast<size_t>(n_days);
@@ -1158,6 +1169,7 @@ static int alloc_band_slot(sg_ctx* ctx, DevBufs& b, BandSlot& s, size_t n, int n
     SG_CUDA(ctx, b.alloc(&s.scratch, 2 * nd));  // only bins too full for one CTA's shared memory touch it
     SG_CUDA(ctx, b.alloc(&s.days, n_days));
     SG_CUDA(ctx, b.alloc(&s.hist, static_cast<size_t>(n_days) * kSelBins));
+    SG_CUDA(ctx, b.alloc(&s.vals, static_cast<size_t>(n_days) * kBandRanks));
     return SG_OK;
 }
 
@@ -1175,7 +1187,7 @@ static int enqueue_band_eval(sg_ctx* ctx, sg_window* w, BandSlot& s, cudaStream_
     // day-major columns in evaluation order: the bands only need each day's multiset
     dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc,
                              fwin, d_lo, d_hi, seed, n, horizon, d_cost, static_cast<double*>(nullptr), s.D, size_t(1),
-                             n, s.perm, s.planes, 1, s.days, w->smem, st, &err);
+                             n, s.perm, s.planes, 1, fused_range() ? s.days : nullptr, w->smem, st, &err);
     ctx->launches += 1;
     if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
     return SG_OK;
@@ -1183,21 +1195,26 @@ static int enqueue_band_eval(sg_ctx* ctx, sg_window* w, BandSlot& s, cudaStream_
 
 // C5, second half (memory-bound): per forecast day the bins of the wanted
 // ranks (calibration.cpp:17-25, 324-361) — histogram, locate, gather — then
-// one CTA per day sorts them in shared memory and writes the bands.
+// one CTA per (bin, day) resolves the bin's wanted ranks in shared memory,
+// and quantile_sorted turns them into the bands.
 static int enqueue_band_select(sg_ctx* ctx, BandSlot& s, cudaStream_t st, size_t n, int n_days, double* d_bands,
-                               unsigned long long* d_counts) {
+                               unsigned long long* d_counts, bool standalone = false) {
     SG_CUDA(ctx, cudaMemsetAsync(s.hist, 0, sizeof(unsigned int) * n_days * kSelBins, st));
     const unsigned chunks = static_cast<unsigned>(std::min<size_t>(64, (n + 4095) / 4096));
     const dim3 grid(chunks, static_cast<unsigned>(n_days));
+    if (!fused_range() && !standalone) {
+        sel_range_kernel<<<grid, 256, 0, st>>>(s.D, n, s.days);
+        ctx->launches += 1;
+    }
     const dim3 hgrid(static_cast<unsigned>(std::min<size_t>(16, (n + 16383) / 16384)), static_cast<unsigned>(n_days));
     sel_hist_kernel<<<hgrid, 1024, 0, st>>>(s.D, n, s.days, s.hist);
     sel_locate_kernel<<<static_cast<unsigned>(n_days), 1024, 0, st>>>(s.hist, s.days);
     sel_gather_kernel<<<grid, 256, 0, st>>>(s.D, n, s.days, s.cand);
-    const size_t smem = kSelCap * sizeof(unsigned long long) + kSelBins * sizeof(unsigned int);
-    SG_CUDA(ctx, prepare_smem(sel_finish_kernel, smem));
-    sel_finish_kernel<<<static_cast<unsigned>(n_days), kSelFinishThreads, smem, st>>>(s.days, s.cand, s.scratch, n,
-                                                                                     d_bands, d_counts, n_days);
-    ctx->launches += 4;
+    sel_finish_kernel<<<dim3(kBandRanks, static_cast<unsigned>(n_days)), kSelFinishThreads, 0, st>>>(
+        s.days, s.cand, s.scratch, n, s.vals);
+    sel_bands_kernel<<<static_cast<unsigned>((n_days + 127) / 128), 128, 0, st>>>(s.days, s.vals, d_bands, d_counts,
+                                                                                 n_days);
+    ctx->launches += 5;
     SG_CUDA(ctx, cudaGetLastError());
     return SG_OK;
 }
@@ -1274,12 +1291,13 @@ int sg_quantile_bands(sg_ctx* ctx, const double* values, size_t n, int n_days, d
         SG_CUDA(ctx, b.alloc(&s.scratch, 2 * nd));
         SG_CUDA(ctx, b.alloc(&s.days, n_days));
         SG_CUDA(ctx, b.alloc(&s.hist, static_cast<size_t>(n_days) * kSelBins));
+        SG_CUDA(ctx, b.alloc(&s.vals, static_cast<size_t>(n_days) * kBandRanks));
         SG_CUDA(ctx, copy_async(ctx, s.D, values, sizeof(double) * nd, cudaMemcpyHostToDevice, ctx->stream));
         sel_init_kernel<<<static_cast<unsigned>((n_days + 127) / 128), 128, 0, ctx->stream>>>(s.days, n_days);
         const dim3 grid(static_cast<unsigned>(std::min<size_t>(64, (n + 4095) / 4096)), static_cast<unsigned>(n_days));
         sel_range_kernel<<<grid, 256, 0, ctx->stream>>>(s.D, n, s.days);
         ctx->launches += 2;
-        if (const int rc = enqueue_band_select(ctx, s, ctx->stream, n, n_days, d_bands, d_counts)) return rc;
+        if (const int rc = enqueue_band_select(ctx, s, ctx->stream, n, n_days, d_bands, d_counts, true)) return rc;
     }
     SG_CUDA(ctx, cudaGetLastError());
     SG_CUDA(ctx, copy_async(ctx, bands, d_bands, 7 * n_days * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));

@@ -1320,58 +1320,63 @@ __global__ void __launch_bounds__(256) sel_gather_kernel(const double* __restric
     }
 }
 
-// ---- finishing a day in one CTA: sort the wanted bins, read the ranks ----------
-constexpr int kSelCap = 8192;          // keys sorted at once in shared memory (64 KB)
-constexpr int kSelFinishThreads = 512;
+// ---- the wanted ranks of each gathered bin, one CTA per (day, bin) -----------------
+constexpr int kSelDirect = 512;        // values ranked directly (all pairs) in shared memory
+constexpr int kSelFinishThreads = 256;
 
-// Ascending bitonic sort of m (a power of two) keys in shared memory.
-__device__ __forceinline__ void smem_bitonic_sort(unsigned long long* a, int m) {
-    for (int size = 2; size <= m; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int i = threadIdx.x; i < m; i += blockDim.x) {
-                const int j = i ^ stride;
-                if (j > i) {
-                    const unsigned long long x = a[i], y = a[j];
-                    if ((x > y) == ((i & size) == 0)) {
-                        a[i] = y;
-                        a[j] = x;
-                    }
-                }
-            }
-            __syncthreads();
+// Rank selection among `count` (<= kSelDirect) keys in shared memory: the
+// key of local rank r is the key with #(keys < key) <= r < #(keys <= key).
+// Ties are equal keys, hence equal values.  Writes *out for every wanted
+// local rank found (CTA-uniform call).
+__device__ __forceinline__ void rank_select(const unsigned long long* keys, uint32_t count, const uint32_t* want,
+                                            int n_want, double* const* out) {
+    for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) {
+        const unsigned long long x = keys[i];
+        uint32_t lt = 0, le = 0;
+        for (uint32_t j = 0; j < count; ++j) {
+            const unsigned long long y = keys[j];  // broadcast read
+            lt += y < x;
+            le += y <= x;
         }
+        for (int t = 0; t < n_want; ++t)
+            if (want[t] >= lt && want[t] < le) *out[t] = key_value(x);
     }
 }
 
-// Keys of `count` values (<= kSelCap) sorted into shared memory `keys`.
-__device__ __forceinline__ void sort_values(const double* src, uint32_t count, unsigned long long* keys) {
-    int m = 1;
-    while (m < static_cast<int>(count)) m <<= 1;
-    for (int i = threadIdx.x; i < m; i += blockDim.x)
-        keys[i] = i < static_cast<int>(count) ? order_key(src[i]) : ~0ULL;  // padding sorts last
+// The values of local ranks want[0..n_want) among the `count` values of one
+// bin (keys in [base, base + 2^shift)) at src: finer histogram levels of
+// 2^12 sub-bins, each keeping the sub-bin that holds the (first) wanted
+// rank — into shared memory once it fits, else into the scratch pair —
+// until the rest is small enough to rank directly or is a single key.
+// Called per group of wanted ranks that share every level's sub-bin; a rank
+// leaving the group's sub-bin is resolved by its own call.  CTA-uniform.
+__device__ void select_in_bin(const double* src, uint32_t count, unsigned long long base, int shift,
+                              const uint32_t* want_in, int n_want_in, double* const* out_in, double* scratch_a,
+                              double* scratch_b, unsigned long long* keys, unsigned int* hist) {
+    __shared__ uint32_t s_bin, s_before, s_fill, s_want[kBandRanks];
+    __shared__ double* s_out[kBandRanks];
+    __shared__ int s_n;
+    if (threadIdx.x == 0) {
+        s_n = n_want_in;
+        for (int t = 0; t < n_want_in; ++t) {
+            s_want[t] = want_in[t];
+            s_out[t] = out_in[t];
+        }
+    }
     __syncthreads();
-    smem_bitonic_sort(keys, m);
-}
-
-// The order statistic of local rank `target` among the `count` values of one
-// bin (keys in [base, base + 2^shift)) that do not fit in shared memory:
-// finer histogram levels of 2^12 sub-bins, each keeping only the sub-bin
-// that holds the rank (gathered into the scratch pair), until the rest fits
-// or the sub-bin is a single key.  CTA-uniform; result in *out (thread 0).
-__device__ void select_large(const double* src, uint32_t count, unsigned long long base, int shift, uint32_t target,
-                             double* scratch_a, double* scratch_b, unsigned long long* keys, unsigned int* hist,
-                             double* out) {
-    __shared__ uint32_t s_bin, s_before, s_fill;
     double* dst = scratch_a;
+    bool in_smem = false;  // src values already staged as keys in shared memory
     while (true) {
-        if (count <= static_cast<uint32_t>(kSelCap)) {
-            sort_values(src, count, keys);
-            if (threadIdx.x == 0) *out = key_value(keys[target]);
+        if (count <= static_cast<uint32_t>(kSelDirect)) {
+            if (!in_smem)
+                for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) keys[i] = order_key(src[i]);
+            __syncthreads();
+            rank_select(keys, count, s_want, s_n, s_out);
             __syncthreads();
             return;
         }
         if (shift == 0) {  // every value of the bin is this key
-            if (threadIdx.x == 0) *out = key_value(base);
+            if (threadIdx.x < static_cast<unsigned>(s_n)) *s_out[threadIdx.x] = key_value(base);
             __syncthreads();
             return;
         }
@@ -1382,95 +1387,133 @@ __device__ void select_large(const double* src, uint32_t count, unsigned long lo
             atomicAdd(&hist[static_cast<uint32_t>((order_key(src[i]) - base) >> sub)], 1u);
         __syncthreads();
         if (threadIdx.x == 0) {
+            // the sub-bin of the first wanted rank; wanted ranks outside it
+            // are resolved by their own (recursive) call below
             uint32_t acc = 0, b = 0;
-            while (acc + hist[b] <= target) acc += hist[b++];
+            while (acc + hist[b] <= s_want[0]) acc += hist[b++];
             s_bin = b;
             s_before = acc;
             s_fill = 0;
         }
         __syncthreads();
-        const uint32_t bin = s_bin;
-        for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) {
-            const double x = src[i];
-            if (static_cast<uint32_t>((order_key(x) - base) >> sub) == bin) dst[atomicAdd(&s_fill, 1u)] = x;
+        const uint32_t bin = s_bin, before = s_before, c_bin = hist[bin];
+        // ranks of this group outside the chosen sub-bin: split off (rare: lo
+        // and lo+1 straddling a sub-bin boundary)
+        if (threadIdx.x == 0) {
+            int m = 0;
+            for (int t = 0; t < s_n; ++t) {
+                if (s_want[t] >= before && s_want[t] < before + c_bin) {
+                    s_want[m] = s_want[t] - before;
+                    s_out[m] = s_out[t];
+                    ++m;
+                }
+            }
+            s_n = m;
         }
         __syncthreads();
-        count = hist[bin];
-        target -= s_before;
+        const bool to_smem = c_bin <= static_cast<uint32_t>(kSelDirect);
+        for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) {
+            const double x = src[i];
+            const unsigned long long key = order_key(x);
+            if (static_cast<uint32_t>((key - base) >> sub) == bin) {
+                const uint32_t slot = atomicAdd(&s_fill, 1u);
+                if (to_smem) keys[slot] = key;
+                else dst[slot] = x;
+            }
+        }
+        __syncthreads();
+        count = c_bin;
         base += static_cast<unsigned long long>(bin) << sub;
         shift = sub;
+        in_smem = to_smem;
         src = dst;
         dst = dst == scratch_a ? scratch_b : scratch_a;
-        __syncthreads();
     }
 }
 
-// One CTA per day: the wanted order statistics from the day's gathered
-// segments (each sorted in shared memory once), then quantile_sorted
-// (calibration.cpp:324-335) with the reference's operation order.
-// scratch: 2 x n doubles per day (only touched by bins too full to sort).
+// One CTA per (gathered bin, day): the bin's wanted ranks.  vals: 14 per day,
+// indexed like band_ranks().  scratch: 2 x n doubles per day (only touched by
+// bins that need more than one finer level outside shared memory).
 __global__ void __launch_bounds__(kSelFinishThreads) sel_finish_kernel(const SelDay* __restrict__ days,
                                                                         const double* __restrict__ cand,
                                                                         double* __restrict__ scratch, size_t n,
-                                                                        double* __restrict__ bands,
-                                                                        unsigned long long* __restrict__ counts,
-                                                                        int n_days) {
-    extern __shared__ __align__(16) unsigned long long keys[];  // kSelCap keys, then kSelBins counters
-    unsigned int* hist = reinterpret_cast<unsigned int*>(keys + kSelCap);
+                                                                        double* __restrict__ vals) {
+    __shared__ unsigned long long keys[kSelDirect];
+    __shared__ unsigned int hist[kSelBins];
     __shared__ uint64_t ranks[kBandRanks];
-    __shared__ double vals[kBandRanks];
-    __shared__ int n_ranks;
-    const int d = blockIdx.x;
+    __shared__ uint32_t want[kBandRanks];
+    __shared__ double* outp[kBandRanks];
+    __shared__ int n_ranks, n_want;
+    const int d = blockIdx.y;
+    const int j = blockIdx.x;
     const SelDay& sd = days[d];
-    const uint64_t k = sd.count;
+    if (sd.count == 0 || j >= sd.n_seg) return;
+    const uint32_t cnt = sd.seg_count[j];
+    const uint64_t r0 = sd.seg_rank0[j];
     if (threadIdx.x == 0) {
-        counts[d] = k;
-        n_ranks = k ? band_ranks(k, ranks) : 0;
-    }
-    __syncthreads();
-    if (k == 0) {
-        if (threadIdx.x < kBandP) bands[threadIdx.x * n_days + d] = __longlong_as_double(0x7FF8000000000000LL);
-        return;
-    }
-    const double* day_cand = cand + static_cast<size_t>(d) * n;
-    double* sa = scratch + static_cast<size_t>(d) * 2 * n;
-    uint64_t off = 0;
-    for (int j = 0; j < sd.n_seg; ++j) {
-        const uint32_t cnt = sd.seg_count[j];
-        const uint64_t r0 = sd.seg_rank0[j];
-        const unsigned long long base = sd.kmin + (static_cast<unsigned long long>(sd.seg_bin[j]) << sd.shift);
-        if (cnt <= static_cast<uint32_t>(kSelCap) && sd.shift > 0) {
-            sort_values(day_cand + off, cnt, keys);
-            for (int r = threadIdx.x; r < n_ranks; r += blockDim.x)
-                if (ranks[r] >= r0 && ranks[r] < r0 + cnt) vals[r] = key_value(keys[ranks[r] - r0]);
-            __syncthreads();
-        } else {
-            for (int r = 0; r < n_ranks; ++r) {  // CTA-uniform
-                if (!(ranks[r] >= r0 && ranks[r] < r0 + cnt)) continue;
-                select_large(day_cand + off, cnt, base, sd.shift, static_cast<uint32_t>(ranks[r] - r0), sa, sa + n,
-                             keys, hist, &vals[r]);
+        n_ranks = band_ranks(sd.count, ranks);
+        int m = 0;
+        for (int r = 0; r < n_ranks; ++r) {
+            if (ranks[r] < r0 || ranks[r] >= r0 + cnt) continue;
+            bool dup = false;  // lo of one probability may equal lo+1 of another
+            for (int t = 0; t < m; ++t) dup = dup || want[t] == static_cast<uint32_t>(ranks[r] - r0);
+            if (dup) continue;
+            // ascending insertion: the group's first rank picks the sub-bin
+            int at = m++;
+            while (at > 0 && want[at - 1] > static_cast<uint32_t>(ranks[r] - r0)) {
+                want[at] = want[at - 1];
+                outp[at] = outp[at - 1];
+                --at;
             }
+            want[at] = static_cast<uint32_t>(ranks[r] - r0);
+            outp[at] = vals + static_cast<size_t>(d) * kBandRanks + r;
         }
-        off += cnt;
+        n_want = m;
     }
     __syncthreads();
-    if (threadIdx.x != 0) return;
-    auto rank_value = [&](uint64_t r) {
+    uint64_t off = 0;
+    for (int t = 0; t < j; ++t) off += sd.seg_count[t];
+    const double* src = cand + static_cast<size_t>(d) * n + off;
+    double* sa = scratch + static_cast<size_t>(d) * 2 * n;
+    const unsigned long long base = sd.kmin + (static_cast<unsigned long long>(sd.seg_bin[j]) << sd.shift);
+    // each wanted rank is resolved by the group that starts at it (ranks
+    // split off inside select_in_bin are picked up by their own pass here)
+    for (int t = 0; t < n_want; ++t) {
+        const uint32_t w1 = want[t];
+        double* o1 = outp[t];
+        select_in_bin(src, cnt, base, sd.shift, &w1, 1, &o1, sa, sa + n, keys, hist);
+    }
+}
+
+// quantile_sorted (calibration.cpp:324-335) of every day from its resolved
+// order statistics, with the reference's operation order.
+__global__ void sel_bands_kernel(const SelDay* __restrict__ days, const double* __restrict__ vals,
+                                 double* __restrict__ bands, unsigned long long* __restrict__ counts, int n_days) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= n_days) return;
+    const uint64_t k = days[d].count;
+    counts[d] = k;
+    uint64_t ranks[kBandRanks];
+    const int n_ranks = k ? band_ranks(k, ranks) : 0;
+    const double* v = vals + static_cast<size_t>(d) * kBandRanks;
+    auto at = [&](uint64_t r) {
         for (int t = 0; t < n_ranks; ++t)
-            if (ranks[t] == r) return vals[t];
-        return __longlong_as_double(0x7FF8000000000000LL);  // unreachable: every wanted rank was resolved
+            if (ranks[t] == r) return v[t];
+        return __longlong_as_double(0x7FF8000000000000LL);  // unreachable
     };
     for (int q = 0; q < kBandP; ++q) {
-        const double h = dmul(static_cast<double>(k - 1), kBandProbs[q]);
-        const uint64_t lo = static_cast<uint64_t>(h);
-        double v;
-        if (lo + 1 >= k) {
-            v = rank_value(k - 1);
-        } else {
-            const double a = rank_value(lo), b = rank_value(lo + 1);
-            v = dadd(a, dmul(dsub(h, static_cast<double>(lo)), dsub(b, a)));
+        double x = __longlong_as_double(0x7FF8000000000000LL);
+        if (k) {
+            const double h = dmul(static_cast<double>(k - 1), kBandProbs[q]);
+            const uint64_t lo = static_cast<uint64_t>(h);
+            if (lo + 1 >= k) {
+                x = at(k - 1);
+            } else {
+                const double a = at(lo), b = at(lo + 1);
+                x = dadd(a, dmul(dsub(h, static_cast<double>(lo)), dsub(b, a)));
+            }
         }
-        bands[q * n_days + d] = v;
+        bands[q * n_days + d] = x;
     }
 }
 
