@@ -964,36 +964,41 @@ __global__ void __launch_bounds__(256) ens_sample_kernel(const double* __restric
     atomicAdd(&key_count[key], 1u);
 }
 
-// Exclusive scan of the 2^16 key counts into bucket cursors (one CTA).
+// Exclusive scan of the 2^16 key counts into bucket cursors (one CTA of 32
+// warps; warp w owns entries [2048 w, 2048 (w + 1)), read 32 at a time).
 __global__ void __launch_bounds__(1024) ens_scan_kernel(unsigned int* __restrict__ key_count) {
-    constexpr int kPer = 65536 / 1024;
-    __shared__ unsigned int warp_sum[32];
-    unsigned int mine = 0;
-    for (int j = 0; j < kPer; ++j) mine += key_count[threadIdx.x * kPer + j];
+    constexpr int kChunk = 65536 / 32;
+    __shared__ unsigned int warp_base[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned int incl = mine;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const unsigned int o = __shfl_up_sync(0xFFFFFFFFu, incl, off);
-        if (lane >= off) incl += o;
-    }
-    if (lane == 31) warp_sum[warp] = incl;
+    unsigned int* const c = key_count + warp * kChunk;
+    unsigned int total = 0;
+#pragma unroll 8
+    for (int i = lane; i < kChunk; i += 32) total += c[i];
+    total = __reduce_add_sync(0xFFFFFFFFu, total);
+    if (lane == 0) warp_base[warp] = total;
     __syncthreads();
     if (warp == 0) {
-        unsigned int w = warp_sum[lane];
+        const unsigned int v = warp_base[lane];
+        unsigned int incl = v;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
-            const unsigned int o = __shfl_up_sync(0xFFFFFFFFu, w, off);
-            if (lane >= off) w += o;
+            const unsigned int o = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+            if (lane >= off) incl += o;
         }
-        warp_sum[lane] = w - warp_sum[lane];
+        warp_base[lane] = incl - v;
     }
     __syncthreads();
-    unsigned int run = warp_sum[warp] + (incl - mine);
-    for (int j = 0; j < kPer; ++j) {
-        const unsigned int c = key_count[threadIdx.x * kPer + j];
-        key_count[threadIdx.x * kPer + j] = run;
-        run += c;
+    unsigned int carry = warp_base[warp];
+    for (int i = 0; i < kChunk; i += 32) {
+        const unsigned int v = c[i + lane];
+        unsigned int incl = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned int o = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+            if (lane >= off) incl += o;
+        }
+        c[i + lane] = carry + incl - v;
+        carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
     }
 }
 
@@ -1087,7 +1092,11 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
     if (!days) return;
     // Band selection, fused: the key range and the count of each day's
     // finite values (the first pass of the selection, without re-reading
-    // the deaths plane from HBM): a warp reduction, one atomic per warp and day.
+    // the deaths plane from HBM): warp reductions, then one atomic per CTA,
+    // day and quantity.
+    __shared__ unsigned long long s_lo[kEvalThreads / 32], s_hi[kEvalThreads / 32];
+    __shared__ unsigned int s_cnt[kEvalThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int d = 0; d <= horizon; ++d) {
         const double v = live ? drow[d * dstride] : __longlong_as_double(0x7FF8000000000000LL);
         const bool fin = isfinite(v);
@@ -1100,11 +1109,27 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
             kh = oh > kh ? oh : kh;
         }
         const unsigned cnt = __popc(__ballot_sync(0xFFFFFFFFu, fin));
-        if ((threadIdx.x & 31) == 0 && cnt) {
-            atomicMin(&days[d].kmin, kl);
-            atomicMax(&days[d].kmax, kh);
-            atomicAdd(&days[d].count, static_cast<unsigned long long>(cnt));
+        if (lane == 0) {
+            s_lo[wid] = kl;
+            s_hi[wid] = kh;
+            s_cnt[wid] = cnt;
         }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long lo = s_lo[0], hi = s_hi[0];
+            unsigned int c = s_cnt[0];
+            for (int w = 1; w < kEvalThreads / 32; ++w) {
+                lo = s_lo[w] < lo ? s_lo[w] : lo;
+                hi = s_hi[w] > hi ? s_hi[w] : hi;
+                c += s_cnt[w];
+            }
+            if (c) {
+                atomicMin(&days[d].kmin, lo);
+                atomicMax(&days[d].kmax, hi);
+                atomicAdd(&days[d].count, static_cast<unsigned long long>(c));
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -1316,6 +1341,7 @@ __global__ void __launch_bounds__(256) sel_gather_kernel(const double* __restric
         uint32_t base = 0;
         if (static_cast<int>(lane) == leader) base = atomicAdd(&sd.seg_fill[seg], static_cast<unsigned>(__popc(peers)));
         base = __shfl_sync(peers, base, leader);
+        SG_CHECK(base + __popc(peers & ((1u << lane) - 1u)) < sd.seg_count[seg]);
         out[seg_off[seg] + base + __popc(peers & ((1u << lane) - 1u))] = x;
     }
 }
@@ -1383,8 +1409,10 @@ __device__ void select_in_bin(const double* src, uint32_t count, unsigned long l
         const int sub = shift > kSelBinBits ? shift - kSelBinBits : 0;
         for (int b = threadIdx.x; b < kSelBins; b += blockDim.x) hist[b] = 0;
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < count; i += blockDim.x)
+        for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) {
+            SG_CHECK(((order_key(src[i]) - base) >> sub) < static_cast<unsigned long long>(kSelBins));
             atomicAdd(&hist[static_cast<uint32_t>((order_key(src[i]) - base) >> sub)], 1u);
+        }
         __syncthreads();
         if (threadIdx.x == 0) {
             // the sub-bin of the first wanted rank; wanted ranks outside it
@@ -1417,6 +1445,7 @@ __device__ void select_in_bin(const double* src, uint32_t count, unsigned long l
             const unsigned long long key = order_key(x);
             if (static_cast<uint32_t>((key - base) >> sub) == bin) {
                 const uint32_t slot = atomicAdd(&s_fill, 1u);
+                SG_CHECK(slot < c_bin);
                 if (to_smem) keys[slot] = key;
                 else dst[slot] = x;
             }
@@ -1473,15 +1502,18 @@ __global__ void __launch_bounds__(kSelFinishThreads) sel_finish_kernel(const Sel
     __syncthreads();
     uint64_t off = 0;
     for (int t = 0; t < j; ++t) off += sd.seg_count[t];
+    SG_CHECK(off + cnt <= n && n_want >= 1);
     const double* src = cand + static_cast<size_t>(d) * n + off;
-    double* sa = scratch + static_cast<size_t>(d) * 2 * n;
+    // the scratch pair of this bin: 2 x cnt doubles of the day's 2 x n (the
+    // CTAs of one day's bins run concurrently)
+    double* sa = scratch + static_cast<size_t>(d) * 2 * n + 2 * off;
     const unsigned long long base = sd.kmin + (static_cast<unsigned long long>(sd.seg_bin[j]) << sd.shift);
     // each wanted rank is resolved by the group that starts at it (ranks
     // split off inside select_in_bin are picked up by their own pass here)
     for (int t = 0; t < n_want; ++t) {
         const uint32_t w1 = want[t];
         double* o1 = outp[t];
-        select_in_bin(src, cnt, base, sd.shift, &w1, 1, &o1, sa, sa + n, keys, hist);
+        select_in_bin(src, cnt, base, sd.shift, &w1, 1, &o1, sa, sa + cnt, keys, hist);
     }
 }
 
