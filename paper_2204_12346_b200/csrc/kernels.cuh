@@ -1092,41 +1092,53 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
     if (!days) return;
     // Band selection, fused: the key range and the count of each day's
     // finite values (the first pass of the selection, without re-reading
-    // the deaths plane from HBM): warp reductions, then one atomic per CTA,
-    // day and quantity.
-    __shared__ unsigned long long s_lo[kEvalThreads / 32], s_hi[kEvalThreads / 32];
-    __shared__ unsigned int s_cnt[kEvalThreads / 32];
+    // the deaths plane from HBM).  Days in chunks of 8: the chunk's values
+    // are loaded back together (one L2 latency, not 8), reduced per warp by
+    // shuffles, then across the CTA's warps: one atomic per CTA, day and
+    // quantity.
+    constexpr int kChunk = 8;
+    constexpr int kWarps = kEvalThreads / 32;
+    __shared__ unsigned long long s_lo[kChunk][kWarps], s_hi[kChunk][kWarps];
+    __shared__ unsigned int s_cnt[kChunk][kWarps];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int d = 0; d <= horizon; ++d) {
-        const double v = live ? drow[d * dstride] : __longlong_as_double(0x7FF8000000000000LL);
-        const bool fin = isfinite(v);
-        unsigned long long kl = fin ? order_key(v) : ~0ULL, kh = fin ? order_key(v) : 0ULL;
+    for (int d0 = 0; d0 <= horizon; d0 += kChunk) {
+        double v[kChunk];
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const unsigned long long ol = __shfl_xor_sync(0xFFFFFFFFu, kl, off);
-            const unsigned long long oh = __shfl_xor_sync(0xFFFFFFFFu, kh, off);
-            kl = ol < kl ? ol : kl;
-            kh = oh > kh ? oh : kh;
-        }
-        const unsigned cnt = __popc(__ballot_sync(0xFFFFFFFFu, fin));
-        if (lane == 0) {
-            s_lo[wid] = kl;
-            s_hi[wid] = kh;
-            s_cnt[wid] = cnt;
+        for (int c = 0; c < kChunk; ++c)
+            v[c] = live && d0 + c <= horizon ? drow[(d0 + c) * dstride] : __longlong_as_double(0x7FF8000000000000LL);
+#pragma unroll
+        for (int c = 0; c < kChunk; ++c) {
+            const bool fin = isfinite(v[c]);
+            unsigned long long kl = fin ? order_key(v[c]) : ~0ULL, kh = fin ? order_key(v[c]) : 0ULL;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const unsigned long long ol = __shfl_xor_sync(0xFFFFFFFFu, kl, off);
+                const unsigned long long oh = __shfl_xor_sync(0xFFFFFFFFu, kh, off);
+                kl = ol < kl ? ol : kl;
+                kh = oh > kh ? oh : kh;
+            }
+            const unsigned cnt = __popc(__ballot_sync(0xFFFFFFFFu, fin));
+            if (lane == 0) {
+                s_lo[c][wid] = kl;
+                s_hi[c][wid] = kh;
+                s_cnt[c][wid] = cnt;
+            }
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned long long lo = s_lo[0], hi = s_hi[0];
-            unsigned int c = s_cnt[0];
-            for (int w = 1; w < kEvalThreads / 32; ++w) {
-                lo = s_lo[w] < lo ? s_lo[w] : lo;
-                hi = s_hi[w] > hi ? s_hi[w] : hi;
-                c += s_cnt[w];
+        if (threadIdx.x < kChunk && d0 + static_cast<int>(threadIdx.x) <= horizon) {
+            const int c = threadIdx.x;
+            unsigned long long lo = s_lo[c][0], hi = s_hi[c][0];
+            unsigned int n_fin = s_cnt[c][0];
+#pragma unroll
+            for (int w = 1; w < kWarps; ++w) {
+                lo = s_lo[c][w] < lo ? s_lo[c][w] : lo;
+                hi = s_hi[c][w] > hi ? s_hi[c][w] : hi;
+                n_fin += s_cnt[c][w];
             }
-            if (c) {
-                atomicMin(&days[d].kmin, lo);
-                atomicMax(&days[d].kmax, hi);
-                atomicAdd(&days[d].count, static_cast<unsigned long long>(c));
+            if (n_fin) {
+                atomicMin(&days[d0 + c].kmin, lo);
+                atomicMax(&days[d0 + c].kmax, hi);
+                atomicAdd(&days[d0 + c].count, static_cast<unsigned long long>(n_fin));
             }
         }
         __syncthreads();
@@ -1350,6 +1362,34 @@ __global__ void __launch_bounds__(256) sel_gather_kernel(const double* __restric
 constexpr int kSelDirect = 512;        // values ranked directly (all pairs) in shared memory
 constexpr int kSelFinishThreads = 256;
 
+// Exclusive prefix sum of one value per thread over the CTA (<= 1024 threads).
+__device__ __forceinline__ uint32_t block_exclusive_sum(uint32_t v) {
+    __shared__ uint32_t warp_sums[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n_warps = (blockDim.x + 31) >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    if (lane == 31) warp_sums[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = lane < n_warps ? warp_sums[lane] : 0;
+        uint32_t wi = w;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, wi, off);
+            if (lane >= off) wi += o;
+        }
+        if (lane < n_warps) warp_sums[lane] = wi - w;
+    }
+    __syncthreads();
+    const uint32_t r = warp_sums[warp] + incl - v;
+    __syncthreads();  // warp_sums reusable by the next call
+    return r;
+}
+
 // Rank selection among `count` (<= kSelDirect) keys in shared memory: the
 // key of local rank r is the key with #(keys < key) <= r < #(keys <= key).
 // Ties are equal keys, hence equal values.  Writes *out for every wanted
@@ -1414,14 +1454,22 @@ __device__ void select_in_bin(const double* src, uint32_t count, unsigned long l
             atomicAdd(&hist[static_cast<uint32_t>((order_key(src[i]) - base) >> sub)], 1u);
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            // the sub-bin of the first wanted rank; wanted ranks outside it
-            // are resolved by their own (recursive) call below
-            uint32_t acc = 0, b = 0;
-            while (acc + hist[b] <= s_want[0]) acc += hist[b++];
-            s_bin = b;
-            s_before = acc;
-            s_fill = 0;
+        // the sub-bin of the first wanted rank: a block scan of the bins
+        // (each thread owns kSelBins / blockDim consecutive bins)
+        {
+            const int per = kSelBins / static_cast<int>(blockDim.x);
+            uint32_t mine = 0;
+            for (int b = 0; b < per; ++b) mine += hist[threadIdx.x * per + b];
+            const uint32_t before_me = block_exclusive_sum(mine);
+            const uint32_t want0 = s_want[0];
+            if (want0 >= before_me && want0 < before_me + mine) {
+                uint32_t acc = before_me;
+                int b = threadIdx.x * per;
+                while (acc + hist[b] <= want0) acc += hist[b++];
+                s_bin = static_cast<uint32_t>(b);
+                s_before = acc;
+            }
+            if (threadIdx.x == 0) s_fill = 0;
         }
         __syncthreads();
         const uint32_t bin = s_bin, before = s_before, c_bin = hist[bin];
