@@ -164,6 +164,8 @@ def lib() -> ctypes.CDLL:
                 "(the engine has no CPU fallback)")
         handle = ctypes.CDLL(str(LIB_PATH))
         for name, (res, args) in SIGNATURES.items():
+            if "SG_LIB" in os.environ and not hasattr(handle, name):
+                continue  # A/B against an older build (diagnostics only)
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args

@@ -1173,15 +1173,23 @@ static int alloc_band_slot(sg_ctx* ctx, DevBufs& b, BandSlot& s, size_t n, int n
     return SG_OK;
 }
 
-// C5, first half (FP64-bound): ensemble order, evaluation of the window and
-// forecast into the slot's day-major deaths plane, with each day's key range
-// and finite count reduced in the kernel's epilogue.
-static int enqueue_band_eval(sg_ctx* ctx, sg_window* w, BandSlot& s, cudaStream_t st, const double* d_lo,
-                             const double* d_hi, uint64_t seed, size_t n, int horizon, double* d_cost) {
-    const int n_days = horizon + 1;
+// C5, stage 1 (integer work): the samples and their ramp-coherent order;
+// the slot's day records reset for the selection.
+static int enqueue_band_order(sg_ctx* ctx, BandSlot& s, cudaStream_t st, const double* d_lo, const double* d_hi,
+                              uint64_t seed, size_t n, int n_days) {
     if (const int rc = ensemble_order(ctx, d_lo, d_hi, seed, n, s.planes, s.keys, s.key_count, s.perm, st)) return rc;
     sel_init_kernel<<<static_cast<unsigned>((n_days + 127) / 128), 128, 0, st>>>(s.days, n_days);
     ctx->launches += 1;
+    SG_CUDA(ctx, cudaGetLastError());
+    return SG_OK;
+}
+
+// C5, stage 2 (FP64-bound): evaluation of the window and forecast into the
+// slot's day-major deaths plane (with each day's key range and finite count
+// reduced in the kernel's epilogue when SG_FUSED_RANGE is on).
+static int enqueue_band_eval(sg_ctx* ctx, sg_window* w, BandSlot& s, cudaStream_t st, const double* d_lo,
+                             const double* d_hi, uint64_t seed, size_t n, int horizon, double* d_cost) {
+    const int n_days = horizon + 1;
     const DevWindow fwin = integration_window(n_days, w->host.substeps, w->host.N);
     cudaError_t err = cudaSuccess;
     // day-major columns in evaluation order: the bands only need each day's multiset
@@ -1193,7 +1201,7 @@ static int enqueue_band_eval(sg_ctx* ctx, sg_window* w, BandSlot& s, cudaStream_
     return SG_OK;
 }
 
-// C5, second half (memory-bound): per forecast day the bins of the wanted
+// C5, stage 3 (memory-bound): per forecast day the bins of the wanted
 // ranks (calibration.cpp:17-25, 324-361) — histogram, locate, gather — then
 // one CTA per (bin, day) resolves the bin's wanted ranks in shared memory,
 // and quantile_sorted turns them into the bands.
@@ -1256,6 +1264,7 @@ int sg_forecast_ensemble_bands(sg_window* w, const double lower[6], const double
     } else {
         BandSlot s;
         if (const int rc = alloc_band_slot(ctx, b, s, n, n_days)) return rc;
+        if (const int rc = enqueue_band_order(ctx, s, ctx->stream, d_lo, d_hi, seed, n, n_days)) return rc;
         if (const int rc = enqueue_band_eval(ctx, w, s, ctx->stream, d_lo, d_hi, seed, n, horizon, d_cost)) return rc;
         if (const int rc = enqueue_band_select(ctx, s, ctx->stream, n, n_days, d_bands, d_counts)) return rc;
     }
@@ -1314,8 +1323,14 @@ static int ensure_band_streams(sg_ctx* ctx) {
     if (ctx->band_eval) return SG_OK;
     int least = 0, greatest = 0;
     SG_CUDA(ctx, cudaDeviceGetStreamPriorityRange(&least, &greatest));
-    SG_CUDA(ctx, cudaStreamCreateWithPriority(&ctx->band_eval, cudaStreamNonBlocking, least));
-    SG_CUDA(ctx, cudaStreamCreateWithPriority(&ctx->band_sel, cudaStreamNonBlocking, greatest));
+    // SG_BAND_PRIO (diagnostic A/B): priority of the selection stream
+    // relative to the evaluation stream: high (default), equal or low
+    static const char* prio = std::getenv("SG_BAND_PRIO");
+    const std::string p = prio ? prio : "high";
+    const int eval_prio = p == "low" ? greatest : least;
+    const int sel_prio = p == "high" ? greatest : least;
+    SG_CUDA(ctx, cudaStreamCreateWithPriority(&ctx->band_eval, cudaStreamNonBlocking, eval_prio));
+    SG_CUDA(ctx, cudaStreamCreateWithPriority(&ctx->band_sel, cudaStreamNonBlocking, sel_prio));
     return SG_OK;
 }
 
@@ -1358,29 +1373,43 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
         if (const int rc = alloc_band_slot(ctx, b, s, n, n_days)) return rc;
     SG_CUDA(ctx, copy_async(ctx, d_lo, lower, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     SG_CUDA(ctx, copy_async(ctx, d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    cudaEvent_t evaluated[kSlots], selected[kSlots];
+    cudaEvent_t ordered[kSlots], evaluated[kSlots], selected[kSlots];
     for (int k = 0; k < kSlots; ++k) {
+        SG_CUDA(ctx, cudaEventCreateWithFlags(&ordered[k], cudaEventDisableTiming));
         SG_CUDA(ctx, cudaEventCreateWithFlags(&evaluated[k], cudaEventDisableTiming));
         SG_CUDA(ctx, cudaEventCreateWithFlags(&selected[k], cudaEventDisableTiming));
     }
+    // Three stages per window over two slots: order (S) -> evaluate (E) ->
+    // select (S).  S runs window k+1's order while E evaluates window k, then
+    // window k's selection; E evaluates back to back.
     cudaStream_t E = ctx->band_eval, S = ctx->band_sel;
     SG_CUDA(ctx, cudaEventRecord(ctx->fork, ctx->stream));  // buffers allocated, bounds uploaded
     SG_CUDA(ctx, cudaStreamWaitEvent(E, ctx->fork, 0));
     SG_CUDA(ctx, cudaStreamWaitEvent(S, ctx->fork, 0));
-    int rc = SG_OK;
+    auto step = [&](cudaError_t e) { return e == cudaSuccess ? SG_OK : cuda_fail(ctx, e, "band pipeline"); };
+    int rc = enqueue_band_order(ctx, slot[0], S, d_lo, d_hi, seeds[0], n, n_days);
+    if (!rc) rc = step(cudaEventRecord(ordered[0], S));
     for (size_t k = 0; k < n_windows && !rc; ++k) {
         const int j = static_cast<int>(k % kSlots);
-        // the slot's previous window must be reduced before its buffers are rewritten
-        if (k >= kSlots && (rc = cudaStreamWaitEvent(E, selected[j], 0)) != cudaSuccess) break;
-        rc = enqueue_band_eval(ctx, windows[k], slot[j], E, d_lo, d_hi, seeds[k], n, horizon, nullptr);
-        if (rc) break;
-        if (cudaEventRecord(evaluated[j], E) != cudaSuccess || cudaStreamWaitEvent(S, evaluated[j], 0) != cudaSuccess) {
-            rc = SG_ERR_CUDA;
-            break;
+        // E: window k once ordered, into a deaths plane its slot's previous
+        // window has been reduced from
+        rc = step(cudaStreamWaitEvent(E, ordered[j], 0));
+        if (!rc && k >= kSlots) rc = step(cudaStreamWaitEvent(E, selected[j], 0));
+        if (!rc) rc = enqueue_band_eval(ctx, windows[k], slot[j], E, d_lo, d_hi, seeds[k], n, horizon, nullptr);
+        if (!rc) rc = step(cudaEventRecord(evaluated[j], E));
+        // S: the next window's order (its slot's planes were read by window
+        // k-1's evaluation), then window k's selection
+        if (!rc && k + 1 < n_windows) {
+            const int j1 = static_cast<int>((k + 1) % kSlots);
+            if (k >= 1) rc = step(cudaStreamWaitEvent(S, evaluated[j1], 0));
+            if (!rc) rc = enqueue_band_order(ctx, slot[j1], S, d_lo, d_hi, seeds[k + 1], n, n_days);
+            if (!rc) rc = step(cudaEventRecord(ordered[j1], S));
         }
-        rc = enqueue_band_select(ctx, slot[j], S, n, n_days, d_bands + 7 * static_cast<size_t>(n_days) * k,
-                                 d_counts + static_cast<size_t>(n_days) * k);
-        if (!rc && cudaEventRecord(selected[j], S) != cudaSuccess) rc = SG_ERR_CUDA;
+        if (!rc) rc = step(cudaStreamWaitEvent(S, evaluated[j], 0));
+        if (!rc)
+            rc = enqueue_band_select(ctx, slot[j], S, n, n_days, d_bands + 7 * static_cast<size_t>(n_days) * k,
+                                     d_counts + static_cast<size_t>(n_days) * k);
+        if (!rc) rc = step(cudaEventRecord(selected[j], S));
     }
     // join both streams even after a failure: the buffers are released in ctx->stream order
     SG_CUDA(ctx, cudaEventRecord(ctx->join[0], E));
@@ -1388,10 +1417,11 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
     SG_CUDA(ctx, cudaEventRecord(ctx->join[1], S));
     SG_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join[1], 0));
     for (int k = 0; k < kSlots; ++k) {
+        cudaEventDestroy(ordered[k]);
         cudaEventDestroy(evaluated[k]);
         cudaEventDestroy(selected[k]);
     }
-    if (rc) return rc == SG_ERR_CUDA ? cuda_fail(ctx, cudaGetLastError(), "band pipeline") : rc;
+    if (rc) return rc;
     SG_CUDA(ctx, copy_async(ctx, bands, d_bands, 7 * n_days * n_windows * sizeof(double), cudaMemcpyDeviceToHost,
                             ctx->stream));
     SG_CUDA(ctx, copy_async(ctx, counts, d_counts, n_days * n_windows * sizeof(uint64_t), cudaMemcpyDeviceToHost,
