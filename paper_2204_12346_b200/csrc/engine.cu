@@ -1147,13 +1147,16 @@ struct BandSlot {
     SelDay* days = nullptr;
 };
 
-// The key range of the band selection comes from the ensemble kernel's
-// epilogue (default) or, with SG_FUSED_RANGE=0 (diagnostic A/B), from a
-// separate pass over the deaths plane on the selection stream.
+// The key range of the band selection comes from a separate pass over the
+// deaths plane on the selection stream (default), or from the ensemble
+// kernel's epilogue with SG_FUSED_RANGE=1 (diagnostic A/B).  Measured, 139
+// windows: 187.9 ms separate vs 194.1 ms fused — the epilogue adds ~63 us
+// to every FP64-bound evaluation (profiles/r02h_c5_*), the separate pass
+// overlaps it on the other stream.
 static bool fused_range() {
     static const bool on = [] {
         const char* e = std::getenv("SG_FUSED_RANGE");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     return on;
 }
@@ -1324,7 +1327,8 @@ static int ensure_band_streams(sg_ctx* ctx) {
     int least = 0, greatest = 0;
     SG_CUDA(ctx, cudaDeviceGetStreamPriorityRange(&least, &greatest));
     // SG_BAND_PRIO (diagnostic A/B): priority of the selection stream
-    // relative to the evaluation stream: high (default), equal or low
+    // relative to the evaluation stream: high (default; 187.9 ms for the
+    // 139-window C5 vs 217.3 equal or low), equal or low
     static const char* prio = std::getenv("SG_BAND_PRIO");
     const std::string p = prio ? prio : "high";
     const int eval_prio = p == "low" ? greatest : least;
