@@ -176,10 +176,6 @@ void sg_ctx_destroy(sg_ctx* ctx) {
     if (ctx->fork) cudaEventDestroy(ctx->fork);
     if (ctx->band_eval) cudaStreamDestroy(ctx->band_eval);
     if (ctx->band_sel) cudaStreamDestroy(ctx->band_sel);
-    for (int l = 0; l < kMaxLanes; ++l) {
-        if (ctx->draw_side[l]) cudaStreamDestroy(ctx->draw_side[l]);
-        if (ctx->draw_join[l]) cudaEventDestroy(ctx->draw_join[l]);
-    }
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -579,13 +575,7 @@ struct SwarmGroup {
     // calibration call, timing loops with one warm-up) never pay it.
     int runs = 0;
     cudaGraphExec_t steps_exec = nullptr;
-    // draw-ahead (SG_DRAW_AHEAD=1): per lane, drawn[parity] after the draw
-    // kernel of an iteration, stepped[parity] after its step kernel
-    bool draw_ahead = false;
-    std::vector<cudaEvent_t> drawn, stepped;
     ~SwarmGroup() {
-        for (cudaEvent_t ev : drawn) cudaEventDestroy(ev);
-        for (cudaEvent_t ev : stepped) cudaEventDestroy(ev);
         if (steps_exec) cudaGraphExecDestroy(steps_exec);
     }
 };
@@ -605,29 +595,6 @@ struct sg_plan {
 };
 
 namespace {
-
-// SG_DRAW_AHEAD=1 (experiment): the MT19937-64 draws of iteration it+1 run
-// in their own kernel beside iteration it, on a low-priority stream per lane.
-bool draw_ahead_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("SG_DRAW_AHEAD");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
-int ensure_draw_streams(sg_ctx* ctx) {
-    if (ctx->draw_side[0]) return SG_OK;
-    int least = 0, greatest = 0;
-    SG_CUDA(ctx, cudaDeviceGetStreamPriorityRange(&least, &greatest));
-    static const char* prio = std::getenv("SG_DRAW_PRIO");  // low (default) or equal
-    const int p = prio && std::string(prio) == "equal" ? 0 : least;
-    for (int l = 0; l < kMaxLanes; ++l) {
-        SG_CUDA(ctx, cudaStreamCreateWithPriority(&ctx->draw_side[l], cudaStreamNonBlocking, p));
-        SG_CUDA(ctx, cudaEventCreateWithFlags(&ctx->draw_join[l], cudaEventDisableTiming));
-    }
-    return SG_OK;
-}
 
 int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     std::vector<const sg_window*> wins;
@@ -729,17 +696,6 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
     SG_CUDA(ctx, b.alloc(&P.history, sw.size() * g.iters));
     P.stride = g.n_total;
     P.hist_stride = g.iters;
-    P.draws = nullptr;
-    P.draw_elems = 0;
-    if (draw_ahead_enabled() && !g.persistent && g.iters > 1) {
-        g.draw_ahead = true;
-        P.draw_elems = pblock_elems(g.n_total, 12);
-        SG_CUDA(ctx, b.alloc(&P.draws, 2 * P.draw_elems));
-        g.drawn.resize(2 * g.lanes.size());
-        g.stepped.resize(2 * g.lanes.size());
-        for (cudaEvent_t& ev : g.drawn) SG_CUDA(ctx, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        for (cudaEvent_t& ev : g.stepped) SG_CUDA(ctx, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    }
     cudaStream_t st = ctx->stream;
     SG_CUDA(ctx, copy_async(ctx, g.d_sw, sw.data(), sizeof(DevSwarm) * sw.size(), cudaMemcpyHostToDevice, st));
     SG_CUDA(ctx, copy_async(ctx, g.d_cta, cta_swarm.data(), sizeof(uint32_t) * g.n_ctas, cudaMemcpyHostToDevice, st));
@@ -849,48 +805,14 @@ int enqueue_steps(sg_ctx* ctx, SwarmGroup& g) {
         SG_CUDA(ctx, cudaEventRecord(ctx->fork, ctx->stream));
         for (size_t l = 0; l < n_lanes; ++l) SG_CUDA(ctx, cudaStreamWaitEvent(ctx->side[l], ctx->fork, 0));
     }
-    if (g.draw_ahead) {
-        if (const int rc = ensure_lanes(ctx)) return rc;
-        if (const int rc = ensure_draw_streams(ctx)) return rc;
-        SG_CUDA(ctx, cudaEventRecord(ctx->fork, ctx->stream));  // after the seeding
-        for (size_t l = 0; l < n_lanes; ++l) SG_CUDA(ctx, cudaStreamWaitEvent(ctx->draw_side[l], ctx->fork, 0));
-    }
-    auto draw = [&](size_t l, uint64_t it) -> cudaError_t {  // draws of iteration it, lane l
-        const SwarmGroup::Lane& ln = g.lanes[l];
-        cudaStream_t ds = ctx->draw_side[l];
-        cudaError_t e = cudaSuccess;
-        // the plane of parity it was read by iteration it-2's step kernel
-        if (it >= 3) e = cudaStreamWaitEvent(ds, g.stepped[2 * l + (it & 1)], 0);
-        if (e == cudaSuccess) {
-            pso_draw_kernel<<<ln.n_ctas, kStepThreads, 0, ds>>>(g.d_task, g.P, it, ln.cta_begin);
-            ctx->launches += 1;
-            e = cudaGetLastError();
-        }
-        if (e == cudaSuccess) e = cudaEventRecord(g.drawn[2 * l + (it & 1)], ds);
-        return e;
-    };
     cudaError_t err = cudaSuccess;
-    if (g.draw_ahead)
-        for (size_t l = 0; l < n_lanes && err == cudaSuccess; ++l) err = draw(l, 1);
     for (uint64_t it = 0; it < g.iters && err == cudaSuccess; ++it) {
         for (size_t l = 0; l < n_lanes && err == cudaSuccess; ++l) {
             const SwarmGroup::Lane& ln = g.lanes[l];
             cudaStream_t st = n_lanes > 1 ? ctx->side[l] : ctx->stream;
-            if (g.draw_ahead && it >= 1) err = cudaStreamWaitEvent(st, g.drawn[2 * l + (it & 1)], 0);
-            if (err != cudaSuccess) break;
             dispatch<StepLaunch>(g.family, g.metric, g.substeps, ln.n_ctas, ln.cta_begin, g.d_task, g.d_sw, g.P,
                                  g.d_state, it, g.smem, st, &err);
             ctx->launches += 1;
-            if (g.draw_ahead && err == cudaSuccess) {
-                err = cudaEventRecord(g.stepped[2 * l + (it & 1)], st);
-                if (err == cudaSuccess && it + 2 < g.iters) err = draw(l, it + 2);
-            }
-        }
-    }
-    if (g.draw_ahead) {  // join the draw streams (capture and buffer order)
-        for (size_t l = 0; l < n_lanes; ++l) {
-            SG_CUDA(ctx, cudaEventRecord(ctx->draw_join[l], ctx->draw_side[l]));
-            SG_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->draw_join[l], 0));
         }
     }
     if (n_lanes > 1) {  // join the lanes even after a failed launch (capture and buffer order need it)

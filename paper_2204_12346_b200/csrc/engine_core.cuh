@@ -53,9 +53,6 @@ struct sg_ctx {
     // the C5 band pipeline: ensemble evaluation (low priority) and band
     // selection (high priority) streams
     cudaStream_t band_eval = nullptr, band_sel = nullptr;
-    // draw-ahead streams, one per launch lane (low priority)
-    cudaStream_t draw_side[kMaxLanes] = {};
-    cudaEvent_t draw_join[kMaxLanes] = {};
 };
 
 struct sg_window {

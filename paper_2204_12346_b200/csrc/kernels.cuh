@@ -264,12 +264,6 @@ struct PsoPlanes {
     unsigned int* group_arrived;  // per fold group: warps arrived this iteration
     double* history;     // per swarm, max_iters_max entries
     uint64_t hist_stride;
-    // draw-ahead (SG_DRAW_AHEAD): the 12 uniforms of iteration it's move,
-    // drawn by pso_draw_kernel while iteration it-1 runs, in particle blocks
-    // of 12 fields, two planes by iteration parity; null: the step kernel
-    // draws them itself
-    double* draws;
-    size_t draw_elems;
 };
 
 __device__ __forceinline__ void repair_order(double* x) {  // calibration.cpp:89-93
@@ -361,13 +355,7 @@ __device__ __forceinline__ void move_particle(const DevSwarm& sw, double best_co
     }
     const double2 wc1 = *reinterpret_cast<const double2*>(&sw.w);
     double u[12];
-    if (P.draws) {
-        const double* dp = P.draws + (it & 1) * P.draw_elems + pblock_base(p, 12);
-#pragma unroll
-        for (int j = 0; j < 12; ++j) u[j] = dp[32 * j];
-    } else {
-        mt_draw<12>(P.mt + pblock_base(p, kMtN), move_draw_word(it), u);
-    }
+    mt_draw<12>(P.mt + pblock_base(p, kMtN), move_draw_word(it), u);
     double* const vb = P.v + pblock_base(p, 6);
     const double* const pbb = P.pb + pblock_base(p, 6);
     double* const xb = P.x + pblock_base(p, 6);
@@ -557,24 +545,6 @@ struct CtaTask {
     uint32_t obs_bytes;      // 24 B per day: beyond 16 bits from 2,731 days on (still inside the 200 KB window)
 };
 static_assert(sizeof(CtaTask) == 64, "one 64-byte record per CTA");
-
-#ifndef SG_FAMILY_TU  // engine.cu only
-// Draw-ahead: the 12 draws of iteration it's move for every particle of a
-// lane's CTA tasks (pso.cpp:114-115; the same lazy twist as the step
-// kernel), into the parity plane the step kernel of iteration it reads.
-// Nothing here depends on the global best, so it runs beside iteration it-1.
-__global__ void __launch_bounds__(kStepThreads) pso_draw_kernel(const CtaTask* __restrict__ tasks, PsoPlanes P,
-                                                                uint64_t it, uint32_t cta_offset) {
-    const CtaTask t = tasks[blockIdx.x + cta_offset];
-    if (it >= t.max_iters || threadIdx.x >= t.n_valid) return;
-    const size_t p = t.p0 + threadIdx.x;
-    double u[12];
-    mt_draw<12>(P.mt + pblock_base(p, kMtN), move_draw_word(it), u);
-    double* dp = P.draws + (it & 1) * P.draw_elems + pblock_base(p, 12);
-#pragma unroll
-    for (int j = 0; j < 12; ++j) dp[32 * j] = u[j];
-}
-#endif  // SG_FAMILY_TU
 
 // ---- bulk asynchronous global -> shared copies (TMA, non-tensor) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
