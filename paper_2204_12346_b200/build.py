@@ -32,10 +32,10 @@ FLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++20", "-Xcompiler", "-fPIC",
 # translation units compiled in parallel: the templated kernels per
 # objective family and substep specialisation (family.cu six times), the
 # rest of the engine, the C++ API
-_FAMILY_UNITS = [(f, sub) for f in (0, 1) for sub in (24, -1, 0)]
+_FAMILY_UNITS = [(f, sub) for f in (0, 1) for sub in (24, -24, -1, 0)]
 UNITS = [("engine", CSRC / "engine.cu", []), ("gswarm", CSRC / "gswarm.cu", []),
          ("host_api", CSRC / "host_api.cpp", [])] + [
-    (f"family{f}_s{'m1' if sub < 0 else sub}", CSRC / "family.cu", [f"-DSG_FAMILY={f}", f"-DSG_SUB={sub}", f"-DSG_UNIT={k}"])
+    (f"family{f}_s{str(sub).replace('-', 'm')}", CSRC / "family.cu", [f"-DSG_FAMILY={f}", f"-DSG_SUB={sub}", f"-DSG_UNIT={k}"])
     for k, (f, sub) in enumerate(_FAMILY_UNITS)]
 
 

@@ -65,7 +65,8 @@ double compartment_scale(const double* obs, int n) {
 // with the t_k table in shared memory; 0 = generic runtime substeps.
 // -1 = any other substep count whose t_k table fits shared memory.
 int kernel_sub(int n_days, int substeps) {
-    return uses_fast_grid(n_days, substeps) ? 24 : (uses_time_table(n_days, substeps) ? -1 : 0);
+    if (substeps == 24) return uses_fast_grid(n_days, substeps) ? 24 : kSub24NoTable;
+    return uses_time_table(n_days, substeps) ? -1 : 0;
 }
 
 bool valid_spec(int family, int metric) {
@@ -80,6 +81,7 @@ void dispatch(int family, int metric, int substeps, Args&&... args) {
 #define SG_CASE(F, M)                                                           \
     if (family == F && metric == M) {                                           \
         if (substeps == 24) K<F, M, 24>::run(std::forward<Args>(args)...);      \
+        else if (substeps == -24) K<F, M, -24>::run(std::forward<Args>(args)...); \
         else if (substeps == -1) K<F, M, -1>::run(std::forward<Args>(args)...); \
         else K<F, M, 0>::run(std::forward<Args>(args)...);                      \
         return;                                                                 \
@@ -1445,12 +1447,15 @@ extern "C" int sg_day_classes_u2(unsigned long long* out3);
 extern "C" int sg_day_classes_u3(unsigned long long* out3);
 extern "C" int sg_day_classes_u4(unsigned long long* out3);
 extern "C" int sg_day_classes_u5(unsigned long long* out3);
+extern "C" int sg_day_classes_u6(unsigned long long* out3);
+extern "C" int sg_day_classes_u7(unsigned long long* out3);
 #endif
 
 extern "C" int sg_debug_day_classes(unsigned long long* out3) {
 #if SG_DAY_COUNTERS
-    int (*parts[6])(unsigned long long*) = {sg_day_classes_u0, sg_day_classes_u1, sg_day_classes_u2,
-                                            sg_day_classes_u3, sg_day_classes_u4, sg_day_classes_u5};
+    int (*parts[8])(unsigned long long*) = {sg_day_classes_u0, sg_day_classes_u1, sg_day_classes_u2,
+                                            sg_day_classes_u3, sg_day_classes_u4, sg_day_classes_u5,
+                                            sg_day_classes_u6, sg_day_classes_u7};
     for (int k = 0; k < 3; ++k) out3[k] = 0;
     for (auto f : parts) {
         unsigned long long a[3];

@@ -6,7 +6,7 @@
 #include "launchers.cuh"
 
 #if !defined(SG_FAMILY) || !defined(SG_SUB) || !defined(SG_UNIT)
-#error "compile with -DSG_FAMILY=0|1 -DSG_SUB=24|-1|0 -DSG_UNIT=<0..5>"
+#error "compile with -DSG_FAMILY=0|1 -DSG_SUB=24|-24|-1|0 -DSG_UNIT=<0..7>"
 #endif
 
 namespace sirdgpu {

@@ -612,7 +612,9 @@ __device__ __forceinline__ SmemWindow stage_window_async(const CtaTask& t, DevWi
     }
     __syncthreads();  // barrier initialised before anyone waits on it
     // the t_k table follows subh[substeps]: a compile-time offset for SUB = 24
-    return SmemWindow{sdesc, s_obs, s_robs, s_flag, TimeGrid{s_times + (SUB > 0 ? static_cast<uint32_t>(SUB) : t.substeps), s_times}};
+    // (no table for SUB = kSub24NoTable: ramp times are computed from subh)
+    const double* tgrid = SubKind<SUB>::kTable ? s_times + (SUB > 0 ? static_cast<uint32_t>(SUB) : t.substeps) : nullptr;
+    return SmemWindow{sdesc, s_obs, s_robs, s_flag, TimeGrid{tgrid, s_times}};
 }
 
 // One Swarm::step (pso.cpp:77-101) for every swarm, iteration `it`, fused:
@@ -1065,7 +1067,8 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
                 for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
                 return;
             }
-            const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w, SUB != 0 ? sw.tg.tgrid : nullptr);
+            const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w,
+                                             SubKind<SUB>::kTable ? sw.tg.tgrid : nullptr);
             double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
             ScoreSink<FAM, MET> score(w, sw.obs, sw.robs, sw.flag);  // starts from the day-0 contribution
             integrate_days<SUB>(p, w, sw.tg, S, I, R, D, score);

@@ -120,6 +120,7 @@ void EnsembleLaunch<F, M, S>::run(const DevWindow* w, const DevWindow& fwin, con
 #define SG_LAUNCH_FAMILY_SUB(INST, F, S) \
     SG_LAUNCH_ONE(INST, F, 0, S) SG_LAUNCH_ONE(INST, F, 1, S) SG_LAUNCH_ONE(INST, F, 2, S) SG_LAUNCH_ONE(INST, F, 3, S)
 #define SG_LAUNCH_FAMILY(INST, F) \
-    SG_LAUNCH_FAMILY_SUB(INST, F, 24) SG_LAUNCH_FAMILY_SUB(INST, F, -1) SG_LAUNCH_FAMILY_SUB(INST, F, 0)
+    SG_LAUNCH_FAMILY_SUB(INST, F, 24) SG_LAUNCH_FAMILY_SUB(INST, F, -24) SG_LAUNCH_FAMILY_SUB(INST, F, -1) \
+    SG_LAUNCH_FAMILY_SUB(INST, F, 0)
 
 }  // namespace sirdgpu

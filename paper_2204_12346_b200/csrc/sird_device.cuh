@@ -282,15 +282,30 @@ __host__ __device__ inline bool uses_fast_grid(int n_days, int substeps) {
     return substeps == 24 && uses_time_table(n_days, substeps);
 }
 
+// Kernel specialisations by substep handling (the SUB template parameter):
+//   SUB > 0   the substep count fixed at compile time (24, the reference
+//             default kDefaultSubsteps, model.hpp:12) with the t_k table in
+//             shared memory;
+//   -24       24 substeps at compile time for windows whose table does not
+//             fit shared memory (over 201 days): ramp times are computed as
+//             RN(RN(day-1) + subh[sub]) (model.cpp:94), like the generic path;
+//   -1        a runtime count with the table;
+//   0         a runtime count without it (generic).
+constexpr int kSub24NoTable = -24;
+template <int SUB>
+struct SubKind {
+    static constexpr int kCount = SUB > 0 ? SUB : (SUB == kSub24NoTable ? 24 : 0);  // 0: runtime
+    static constexpr bool kTable = SUB > 0 || SUB == -1;  // reads the t_k table
+    static constexpr bool kFast = SUB != 0;               // branch-free ramp days, bulk-copy staging
+};
+
 // Integrate days 1..n_days-1 (model.cpp:92-106), calling sink.day(day, S, I, R, D)
-// after every day.  SUB > 0 fixes the substep count at compile time
-// (the reference default kDefaultSubsteps = 24, model.hpp:12); SUB == -1
-// reads it from the window but has the t_k table; SUB == 0 reads
-// it from the window.
+// after every day, with the substep handling of SubKind<SUB>.
 template <int SUB, class Sink>
 __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindow& w, const TimeGrid& tg,
                                                double& S, double& I, double& R, double& D, Sink& sink) {
-    const int nsub = SUB > 0 ? SUB : w.substeps;
+    using K = SubKind<SUB>;
+    const int nsub = K::kCount > 0 ? K::kCount : w.substeps;
     const double h = w.h;
     const double g = p.g, mu = p.mu;
     const double N = w.N, rN = w.rN, rN_lo = w.rN_lo;
@@ -327,47 +342,48 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
 #else
         constexpr bool quiet = false;  // SG_DAY_SPLIT 2: quiet days never reach here
 #endif
+        // t_k of substep `sub` today (model.cpp:94): the table, or computed
+        const double dayf = static_cast<double>(day - 1);
+        auto t_at = [&](int sub) -> double {
+            if constexpr (K::kTable) return tg.tgrid[kbase + sub];
+            else return dadd(dayf, tg.subh[sub]);
+        };
         if (!quiet && __any_sync(mask, ramp_today)) {
-            if (SG_RAMP_MODE >= 1 && SUB != 0 && warp_fast && __all_sync(mask, lo <= 0 && hi >= nsub)) {
+            if (SG_RAMP_MODE >= 1 && K::kFast && warp_fast && __all_sync(mask, lo <= 0 && hi >= nsub)) {
                 // Every lane ramps through the whole day: no selects at all.
-#pragma unroll(SUB > 0 ? kRampUnroll : 4)
+#pragma unroll(K::kCount > 0 ? kRampUnroll : 4)
                 for (int sub = 0; sub < nsub; ++sub) {
-                    const double t = tg.tgrid[kbase + sub];
+                    const double t = t_at(sub);
                     const double beta = dadd(p.b1, dmul(p.slope, dsub(t, p.t1)));
                     euler_substep(div_by_N(beta, rN, rN_lo), g, mu, h, S, I, R, D);
                 }
-            } else if (SG_RAMP_MODE >= 1 && SUB != 0 && warp_fast) {
+            } else if (SG_RAMP_MODE >= 1 && K::kFast && warp_fast) {
                 // Branch-free ramp day: every lane computes the ramp value
                 // (the warp would issue it anyway once any lane needs it) and
                 // selects; non-FP64 work per substep is two compares and
                 // selects plus the t_k load.
-#pragma unroll(SUB > 0 ? kRampUnroll : 4)
+#pragma unroll(K::kCount > 0 ? kRampUnroll : 4)
                 for (int sub = 0; sub < nsub; ++sub) {
-                    const double t = tg.tgrid[kbase + sub];
+                    const double t = t_at(sub);
                     const double beta = dadd(p.b1, dmul(p.slope, dsub(t, p.t1)));
                     const double q = div_by_N(beta, rN, rN_lo);
                     const double bp = sub < lo ? p.bp1 : (sub < hi ? q : p.bp2);
                     euler_substep(bp, g, mu, h, S, I, R, D);
                 }
             } else {
-#pragma unroll(SUB > 0 ? kSlowUnroll : 4)  // rare path (a lane outside the 2-op division range)
+#pragma unroll(K::kCount > 0 ? kSlowUnroll : 4)  // rare path (a lane outside the 2-op division range)
                 for (int sub = 0; sub < nsub; ++sub) {
                     double bp = sub < lo ? p.bp1 : p.bp2;
-                    if (sub >= lo && sub < hi) {
-                        double t;
-                        if constexpr (SUB != 0) t = tg.tgrid[kbase + sub];
-                        else t = dadd(static_cast<double>(day - 1), tg.subh[sub]);
-                        bp = ramp_bp(p, t, N, rN, rN_lo);
-                    }
+                    if (sub >= lo && sub < hi) bp = ramp_bp(p, t_at(sub), N, rN, rN_lo);
                     euler_substep(bp, g, mu, h, S, I, R, D);
                 }
             }
         } else if (!quiet && __any_sync(mask, switch_today)) {
-#pragma unroll(SUB > 0 ? kRampUnroll : 4)
+#pragma unroll(K::kCount > 0 ? kRampUnroll : 4)
             for (int sub = 0; sub < nsub; ++sub) euler_substep(sub < lo ? p.bp1 : p.bp2, g, mu, h, S, I, R, D);
         } else {
             const double bp = lo >= nsub ? p.bp1 : p.bp2;
-#pragma unroll(SUB > 0 ? kConstUnroll : 4)
+#pragma unroll(K::kCount > 0 ? kConstUnroll : 4)
             for (int sub = 0; sub < nsub; ++sub) euler_substep(bp, g, mu, h, S, I, R, D);
         }
     };
@@ -390,7 +406,7 @@ __device__ __forceinline__ void integrate_days(const Particle& p, const DevWindo
         const int end = seg == 0 ? (d_first < n_days ? d_first : n_days) : n_days;
         const double bpq = seg == 0 ? p.bp1 : p.bp2;
         for (; day < end; ++day) {
-#pragma unroll(SUB > 0 ? kQuietUnroll : 4)
+#pragma unroll(K::kCount > 0 ? kQuietUnroll : 4)
             for (int sub = 0; sub < nsub; ++sub) euler_substep(bpq, g, mu, h, S, I, R, D);
             sink.day(day, S, I, R, D);
         }
@@ -509,7 +525,7 @@ __device__ __forceinline__ double eval_particle(const double* x, const DevWindow
         if (ramp) *ramp = 0;
         return __longlong_as_double(0x7FF0000000000000LL);
     }
-    const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w, SUB != 0 ? tg.tgrid : nullptr);
+    const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w, SubKind<SUB>::kTable ? tg.tgrid : nullptr);
     if (ramp) *ramp = p.k2 - p.k1;
     double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
     ScoreSink<FAM, MET> sink(w, obs, robs, flag);  // starts from the day-0 contribution
