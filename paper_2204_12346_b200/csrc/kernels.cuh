@@ -540,7 +540,7 @@ struct CtaTask {
     const DevWindow* win;    // window descriptor (device)
     const double* times;     // its substep-time table (device)
     const double* obs;       // obs | robs | flags, 16-byte padded sections (device)
-    uint16_t times_bytes;    // 16-byte multiples (<= 38.5 KB: the table is at most kMaxTgrid entries)
+    uint16_t times_x16;      // staged subh + t_k table bytes / 16 (the table is at most kMaxTgrid entries)
     uint16_t substeps;       // the window's substep count when it has a t_k table (<= kMaxTgrid), else 0
     uint32_t obs_bytes;      // 24 B per day: beyond 16 bits from 2,731 days on (still inside the 200 KB window)
 };
@@ -585,24 +585,25 @@ __device__ __forceinline__ SmemWindow stage_window_async(const CtaTask& t, DevWi
                                                          unsigned char* smem) {
     // WindowLayout: times | obs | robs | flags, the section sizes in the task
     double* s_times = reinterpret_cast<double*>(smem);
-    ObsDay* s_obs = reinterpret_cast<ObsDay*>(smem + t.times_bytes);
-    ObsDay* s_robs = reinterpret_cast<ObsDay*>(smem + t.times_bytes + t.obs_bytes);
-    unsigned char* s_flag = smem + t.times_bytes + 2 * t.obs_bytes;
+    const uint32_t times_bytes = 16u * t.times_x16;
+    ObsDay* s_obs = reinterpret_cast<ObsDay*>(smem + times_bytes);
+    ObsDay* s_robs = reinterpret_cast<ObsDay*>(smem + times_bytes + t.obs_bytes);
+    unsigned char* s_flag = smem + times_bytes + 2 * t.obs_bytes;
     if (threadIdx.x == 0) {
 #if SG_CHECKED
         uint32_t dyn = 0;
         asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
-        SG_CHECK(t.times_bytes + (MET == kMetMAPE ? 2u : 1u) * t.obs_bytes <= dyn);
+        SG_CHECK(times_bytes + (MET == kMetMAPE ? 2u : 1u) * t.obs_bytes <= dyn);
 #endif
         const uint32_t b = smem_u32(bar);
         mbar_init(b, 1);
         // obs_bytes = round16(24 n) is the obs and the robs section size
         const uint32_t flag_bytes = MET == kMetMAPE ? (3u * (t.obs_bytes / 24u) + 15u) & ~15u : 0u;
         const uint32_t n_days_bytes = t.obs_bytes;
-        mbar_expect_tx(b, static_cast<uint32_t>(sizeof(DevWindow)) + t.times_bytes + n_days_bytes +
+        mbar_expect_tx(b, static_cast<uint32_t>(sizeof(DevWindow)) + times_bytes + n_days_bytes +
                               (MET == kMetMAPE ? n_days_bytes + flag_bytes : 0u));
         bulk_g2s(smem_u32(sdesc), t.win, sizeof(DevWindow), b);
-        bulk_g2s(smem_u32(s_times), t.times, t.times_bytes, b);
+        bulk_g2s(smem_u32(s_times), t.times, times_bytes, b);
         bulk_g2s(smem_u32(s_obs), t.obs, n_days_bytes, b);
         if (MET == kMetMAPE) {
             const unsigned char* o = reinterpret_cast<const unsigned char*>(t.obs);

@@ -176,3 +176,32 @@ def test_long_window_one_substep_flat_plan(ctx, port):
             assert_bitwise(got[k][3], hist, f"{spec} swarm {k} history")
             if rc == 0:
                 assert_bitwise(got[k][1], best, f"{spec} swarm {k} best")
+
+
+@pytest.mark.parametrize("n_days", [230, 301, 560])
+def test_long_windows_all_kernel_paths(ctx, port, n_days):
+    """Windows past the 5-CTA shared-memory table (202-534 days stage a
+    larger t_k table at lower occupancy) and past the table altogether (560
+    days: the compile-time-24 kernels that compute t_k, SUB = -24), through
+    the flat plan (with ballast swarms), the cluster kernel and boundary 1."""
+    import paper_2204_12346_b200 as eng
+    N = 2e7
+    st, fin = port.integrate([0.21, 0.12, 90.0, 400.0, 0.1, 0.004], [N - 300, 300, 0, 0], N, n_days)
+    assert fin
+    I, R, D = st[:, 1].copy(), st[:, 2].copy(), st[:, 3].copy()
+    D *= np.random.default_rng(n_days).uniform(0.99, 1.01, n_days)
+    init = list(st[0])
+    hi = [0.5, 0.5, float(n_days - 8), float(n_days - 8), 0.5, 0.02]
+    for spec in ("ird-mxse", "d-mape"):
+        w = eng.Window(ctx, I, R, D, init, N, spec)
+        pos = np.random.default_rng(2).uniform(0, 1, (257, 6)) * np.array(hi)
+        assert_bitwise(w.eval_costs(pos), port.eval_costs(spec, I, R, D, init, N, pos), f"{n_days} {spec} costs")
+        main = dict(window=w, lower=[0.0] * 6, upper=hi, n_particles=700, max_iters=4, seed=17)
+        flat = ctx.fit_swarms([main] + [dict(main, n_particles=1, max_iters=1, seed=j) for j in range(300)])[0]
+        single = ctx.fit_swarms([main])[0]
+        rc, best, cost, hist = port.fit_swarm(spec, I, R, D, init, N, main["lower"], main["upper"], 700, 4, seed=17)
+        for name, got in (("flat", flat), ("cluster", single)):
+            assert got[0] == rc
+            assert_bitwise(got[3], hist, f"{n_days} {spec} {name} history")
+            if rc == 0:
+                assert_bitwise(got[1], best, f"{n_days} {spec} {name} best")

@@ -1,4 +1,5 @@
-"""Throughput vs window length (tau): 40 windows x 4096 particles x 100 iterations, ird-mxse, stage2 box."""
+"""Throughput vs window length (tau): 40 swarms x 4096 particles x 100 iterations, ird-mxse, stage2 box
+(the series' windows of that length, repeated with other seeds when there are fewer than 40)."""
 import sys
 from pathlib import Path
 
@@ -13,10 +14,10 @@ def main():
     ctx = eng.Context(0)
     peak = eng.probe_fp64_rate(ctx)
     for tau in [int(x) for x in sys.argv[1:]] or [20, 35, 60, 85, 86, 100, 150, 200]:
-        n_win = min(40, (450 - tau - 1) // bench.DELTA)
+        n_win = max(1, min(40, 1 + (450 - tau - 1) // bench.DELTA))
         wins = [window(ctx, w, tau) for w in range(n_win)]
-        swarms = [dict(window=wins[w], lower=[0] * 6, upper=stage2(tau), n_particles=4096, max_iters=100,
-                       seed=bench.mix_seed(5, w)) for w in range(n_win)]
+        swarms = [dict(window=wins[k % n_win], lower=[0] * 6, upper=stage2(tau), n_particles=4096, max_iters=100,
+                       seed=bench.mix_seed(5, k)) for k in range(40)]
         plan = eng.Plan(ctx, swarms)
         plan.run_timed()
         s, k = plan.run_timed()
