@@ -721,9 +721,11 @@ int build_group(sg_ctx* ctx, const sg_swarm_desc* descs, SwarmGroup& g) {
         // observations at most the 200 KB window limit of sg_window_create
         // (windows without a table stage cooperatively and ignore both sizes)
         const bool table = uses_time_table(w.n_days, w.substeps);
-        if (table && (L.times_bytes / 16 > 0xFFFF || w.substeps > 0xFFFF || L.obs_bytes > 0xFFFFFFFFu))
+        if (L.times_bytes / 16 > 0xFFFF || (table && w.substeps > 0xFFFF) || L.obs_bytes > 0xFFFFFFFFu)
             return fail(ctx, SG_ERR_INVALID_ARGUMENT, "window too large for the step kernel's staging");
-        t.times_x16 = static_cast<uint16_t>(table ? L.times_bytes / 16 : 0);
+        // subh (+ the table when it is staged): the kSub24NoTable kernels
+        // stage subh too, to compute their ramp times from it
+        t.times_x16 = static_cast<uint16_t>(L.times_bytes / 16);
         t.obs_bytes = static_cast<uint32_t>(L.obs_bytes);
         t.substeps = static_cast<uint16_t>(table ? w.substeps : 0);
     }

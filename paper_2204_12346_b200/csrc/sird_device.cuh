@@ -267,13 +267,13 @@ struct TimeGrid {
     const double* subh;   // substeps entries: RN(sub*h)
 };
 
-// Largest t_k table kept in shared memory (entries, 100 KB): windows up to
-// 534 days at 24 substeps stage it.  Up to 201 days five step CTAs still fit
-// per SM; longer tables cost occupancy, and that is still faster than
-// computing the times (measured 0.86-0.90 of P for 202-331 days with the
-// table against ~0.80 without it, profiles/r02l_long_windows.txt).  Longer
-// windows take the kSub24NoTable / generic kernels.
-constexpr int kMaxTgrid = 12800;
+// Largest t_k table kept in shared memory (entries, 47 KB): windows up to
+// 251 days at 24 substeps stage it (four step CTAs per SM still fit from 202
+// days on, five below).  Longer windows compute their ramp times from subh
+// (kSub24NoTable), which beats a larger table at lower occupancy: measured
+// 0.89-0.90 of P with the table up to 251 days against 0.88 computed, 0.86
+// against 0.88 at 301 days (profiles/r02l_long_windows.txt).
+constexpr int kMaxTgrid = 6000;
 
 // A window's t_k table fits in shared memory (any substep count).
 __host__ __device__ inline bool uses_time_table(int n_days, int substeps) {
