@@ -6,7 +6,7 @@ oracle/Makefile `refcallers` builds the reference's unmodified callers twice —
 against the pure reference and against the binding:
 
   * tests/acceptance/main.cpp (the reference's acceptance gate)
-    criteria 1, 2, 3, 5, 6, 7, 9 must PASS on the engine with the same detail
+    criteria 1-9 must PASS on the engine with the same detail
     text as the pure reference (timings stripped: every number they print —
     population drift, Euler halving ratios, R^2 of the self-consistency fits,
     8-spec bound comparison, forecast coverage — comes out bit-identical);
@@ -15,11 +15,12 @@ against the pure reference and against the binding:
     what it can show: the device objective beats the reference's 1-thread time.
   * bindings/module.cpp as the pybind module `sirdfit._core` + the reference's
     python/sirdfit/__init__.py: the reference's tests/python/test_smoke.py
-    passes on the engine, and fit/forecast values equal the pure-reference
-    module's bit for bit.
-
-The CLI (tools/main.cpp) needs CLI11, which the reference does not ship, so
-acceptance #4/#8 and the CLI smoke cases stay out (SURVEY.md §0 finding 5)."""
+    passes on the engine (its two CLI cases included), and fit/forecast
+    values equal the pure-reference module's bit for bit.
+  * tools/main.cpp, the `sirdfit` CLI (built against oracle/cli11_standin:
+    the reference does not ship its vendored CLI11): acceptance #4 and #8
+    drive it, and every output file of preprocess / fit / compare / forecast
+    / stability is byte-identical to the pure-reference CLI's."""
 import os
 import re
 import subprocess
@@ -31,10 +32,17 @@ import pytest
 ROOT = Path(__file__).resolve().parents[1]
 REF = ROOT / "oracle" / "_ref"
 ACC_REF, ACC_B200 = REF / "acceptance_ref", REF / "acceptance_b200"
+CLI_REF, CLI_B200 = REF / "sirdfit_cli_ref", REF / "sirdfit_cli_b200"
+SMOKE = REF / "proj" / "tests" / "python" / "test_smoke.py"
 
 pytestmark = pytest.mark.gpu
 
-CRITERIA = [1, 2, 3, 5, 6, 7, 9]
+CRITERIA = [1, 2, 3, 4, 5, 6, 7, 8, 9]
+
+
+def _acc_args(exe, criterion):
+    cli = CLI_B200 if exe == ACC_B200 else CLI_REF
+    return [str(exe), str(criterion)] + (["--cli", str(cli)] if criterion in (4, 8) else [])
 
 
 def _need(*paths):
@@ -50,9 +58,11 @@ def _strip_times(detail):
 
 @pytest.fixture(scope="module")
 def reference_outcomes():
-    _need(ACC_REF)
-    procs = {c: subprocess.Popen([str(ACC_REF), str(c)], stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
-             for c in CRITERIA}
+    _need(ACC_REF, CLI_REF)
+    procs = {c: subprocess.Popen(_acc_args(ACC_REF, c), stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+             for c in CRITERIA if c not in (4, 8)}
+    procs.update({c: subprocess.Popen(_acc_args(ACC_REF, c), stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                      text=True) for c in (4, 8)})
     out = {}
     for c, p in procs.items():
         so, se = p.communicate(timeout=900)
@@ -62,8 +72,8 @@ def reference_outcomes():
 
 @pytest.mark.parametrize("criterion", CRITERIA)
 def test_acceptance_criterion_on_engine(criterion, reference_outcomes):
-    _need(ACC_B200)
-    got = subprocess.run([str(ACC_B200), str(criterion)], capture_output=True, text=True, timeout=900)
+    _need(ACC_B200, CLI_B200)
+    got = subprocess.run(_acc_args(ACC_B200, criterion), capture_output=True, text=True, timeout=900)
     rc_ref, line_ref = reference_outcomes[criterion]
     assert got.returncode == 0, got.stdout + got.stderr
     assert got.stdout.strip().startswith(f"criterion {criterion}: PASS")
@@ -91,15 +101,14 @@ def _run_py(pkg_dir, code):
 
 
 def test_reference_python_smoke_on_engine():
-    smoke = REF / "pysmoke" / "test_smoke.py"
-    _need(smoke, REF / "py_b200" / "sirdfit" / "__init__.py")
-    env = dict(os.environ, PYTHONPATH=str(REF / "py_b200"))
-    env.pop("SIRDFIT_CLI", None)
+    smoke = SMOKE
+    _need(smoke, REF / "py_b200" / "sirdfit" / "__init__.py", CLI_B200)
+    env = dict(os.environ, PYTHONPATH=str(REF / "py_b200"), SIRDFIT_CLI=str(CLI_B200))
     out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "--rootdir",
                           str(smoke.parent), str(smoke)], capture_output=True, text=True, timeout=900, env=env,
                          cwd=smoke.parent)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
-    assert "5 passed" in out.stdout, out.stdout[-2000:]
+    assert "7 passed" in out.stdout, out.stdout[-2000:]
     # the module really is the engine: libsirdgpu.so is mapped into the process
     probe = _run_py(REF / "py_b200", "import sirdfit, sys; sirdfit.integrate(sirdfit.SirdParams(beta1=0.5), "
                                      "sirdfit.SirdState(S=999.0, I=1.0), 1000.0, 5);"
@@ -148,3 +157,50 @@ def test_cpp_api_against_reference_in_one_process():
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)
     assert out.returncode == 0 and "MISMATCH" not in out.stdout, out.stdout + out.stderr[-2000:]
     assert out.stdout.count("\nok ") + out.stdout.startswith("ok ") >= 20, out.stdout
+
+
+def _write_raw_csv(path, n_days=80):
+    """A reported series from the reference's own model (the smoke test's
+    generator with noise-free cumulative columns)."""
+    code = ("import sirdfit, datetime\n"
+            "tr = sirdfit.integrate(sirdfit.SirdParams(beta1=0.6, beta2=0.3, t1=20.0, t2=45.0, gamma=0.09, mu=0.012),"
+            " sirdfit.SirdState(S=1e6 - 100.0, I=100.0), 1e6, %d)\n"
+            "print('date,confirmed,recovered,deaths')\n"
+            "for t, s in enumerate(tr.states):\n"
+            "    d = datetime.date(2020, 3, 1) + datetime.timedelta(days=t)\n"
+            "    print(f'{d.isoformat()},{s.I + s.R + s.D!r},{s.R!r},{s.D!r}')\n" % n_days)
+    out = _run_py(REF / "py_ref", code)
+    assert out.returncode == 0, out.stderr
+    path.write_text(out.stdout)
+
+
+def test_cli_outputs_byte_identical_to_reference(tmp_path):
+    """Every command of the reference CLI on the engine writes the same bytes
+    as the pure-reference CLI (fits.json, envelopes, bands, forecasts, the
+    compare table, the cleaned series) with the same exit code."""
+    _need(CLI_REF, CLI_B200)
+    raw = tmp_path / "raw.csv"
+    _write_raw_csv(raw)
+    common = ["--input", str(raw), "--population", "1000000"]
+    search = ["--particles", "300", "--iters", "25", "--seed", "11"]
+    commands = {
+        "preprocess": ["preprocess", "--input", str(raw), "--smooth"],
+        "fit": ["fit", *common, "--tau", "20", "--delta", "7", "--objective", "ird-mxse", *search, "--threads", "max"],
+        "compare": ["compare", *common, "--tau", "20", "--delta", "20", "--particles", "120", "--iters", "10",
+                    "--seed", "3"],
+        "forecast": ["forecast", *common, "--tau", "20", "--objective", "d-mape", "--horizon", "14",
+                     "--window-start", "last", *search],
+        "stability": ["stability", *common, "--tau", "20", "--objective", "d-mse", "--reps", "9", "--horizon", "10",
+                      "--window-start", "30", *search],
+    }
+    for name, args in commands.items():
+        outs = {}
+        for which, exe in (("ref", CLI_REF), ("b200", CLI_B200)):
+            d = tmp_path / f"{name}_{which}"
+            r = subprocess.run([str(exe), *args, "--out-dir", str(d)], capture_output=True, text=True, timeout=900)
+            files = {p.name: p.read_bytes() for p in sorted(d.glob("*"))} if d.exists() else {}
+            outs[which] = (r.returncode, files, r.stdout)
+        assert outs["ref"][0] == outs["b200"][0], (name, outs["ref"][2], outs["b200"][2])
+        assert outs["ref"][1] and set(outs["ref"][1]) == set(outs["b200"][1]), name
+        for fname, data in outs["ref"][1].items():
+            assert outs["b200"][1][fname] == data, f"{name}: {fname} differs"

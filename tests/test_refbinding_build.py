@@ -18,7 +18,7 @@ def _need(*paths):
             pytest.skip(f"{p} not built (oracle/Makefile refcallers needs /root/reference)")
 
 
-@pytest.mark.parametrize("binary", ["acceptance_b200", "api_parity", "py_b200/sirdfit/_core"])
+@pytest.mark.parametrize("binary", ["acceptance_b200", "api_parity", "sirdfit_cli_b200", "py_b200/sirdfit/_core"])
 def test_binding_links_the_engine(binary):
     path = REF / binary
     if binary.endswith("_core"):
@@ -52,3 +52,17 @@ def test_python_module_imports_and_answers_host_calls():
         assert r.returncode == 0, r.stderr
         outs.append(r.stdout)
     assert outs[0] == outs[1] and outs[0].startswith("139 414")
+
+
+def test_reference_cli_builds_with_the_standin_and_passes_acceptance_4_and_8_on_cpu():
+    """The CLI11 stand-in (oracle/cli11_standin) compiles the reference's
+    unmodified tools/main.cpp; on the pure reference, acceptance #4
+    (byte-identical fits.json for 1 vs max threads) and #8 (band nesting)
+    pass — the baseline the engine build is compared against on the GPU."""
+    _need(REF / "acceptance_ref", REF / "sirdfit_cli_ref")
+    for c in ("4", "8"):
+        r = subprocess.run([str(REF / "acceptance_ref"), c, "--cli", str(REF / "sirdfit_cli_ref")], capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0 and "PASS" in r.stdout, r.stdout + r.stderr
+    r = subprocess.run([str(REF / "sirdfit_cli_b200"), "fit", "--population", "1000"], capture_output=True, text=True)
+    assert r.returncode != 0 and "--input is required" in r.stderr
