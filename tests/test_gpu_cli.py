@@ -127,3 +127,58 @@ def test_failed_windows_exit_1(raw_csv, tmp_path):
                      "--particles", "30", "--iters", "5", "--out-dir", str(tmp_path / "f")]) == 1
     doc = json.loads((tmp_path / "f" / "fits.json").read_text())
     assert doc["failed_count"] == doc["n_windows"] and doc["mean_r2_d"] is None
+
+
+def test_python_cli_byte_identical_to_reference_cli(tmp_path):
+    """`python -m paper_2204_12346_b200.cli` against the reference's own
+    `sirdfit` CLI (oracle/_ref/sirdfit_cli_ref: tools/main.cpp over the pure
+    reference, built with the CLI11 stand-in): every output file of every
+    command is byte-identical (JSON layout and number formatting included)
+    and the exit codes agree."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    ROOT = Path(__file__).resolve().parents[1]
+    ref_cli = ROOT / "oracle" / "_ref" / "sirdfit_cli_ref"
+    if not ref_cli.exists():
+        pytest.skip("reference CLI not built (oracle/Makefile refcallers)")
+    raw = tmp_path / "raw.csv"
+    lines = ["date,confirmed,recovered,deaths"]
+    import datetime
+    from oracle import oracle_py
+    port = oracle_py.load("port")
+    st, _ = port.integrate([0.6, 0.3, 20.0, 45.0, 0.09, 0.012], [1e6 - 100, 100, 0, 0], 1e6, 80)
+    st = st.tolist()
+    for t, (S_, I_, R_, D_) in enumerate(st):
+        d = datetime.date(2020, 3, 1) + datetime.timedelta(days=t)
+        lines.append(f"{d.isoformat()},{I_ + R_ + D_!r},{R_!r},{D_!r}")
+    raw.write_text("\n".join(lines) + "\n")
+    common = ["--input", str(raw), "--population", "1000000"]
+    search = ["--particles", "300", "--iters", "25", "--seed", "11"]
+    commands = {
+        "preprocess": ["preprocess", "--input", str(raw), "--smooth"],
+        "fit": ["fit", *common, "--tau", "20", "--delta", "7", "--objective", "ird-mxse", *search, "--threads", "max"],
+        "compare": ["compare", *common, "--tau", "20", "--delta", "20", "--particles", "120", "--iters", "10",
+                    "--seed", "3"],
+        "forecast": ["forecast", *common, "--tau", "20", "--objective", "d-mape", "--horizon", "14",
+                     "--window-start", "last", *search],
+        "stability": ["stability", *common, "--tau", "20", "--objective", "d-mse", "--reps", "9", "--horizon", "10",
+                      "--window-start", "30", *search],
+    }
+    mismatches = []
+    for name, args in commands.items():
+        d_ref, d_eng = tmp_path / f"{name}_ref", tmp_path / f"{name}_eng"
+        r = subprocess.run([str(ref_cli), *args, "--out-dir", str(d_ref)], capture_output=True, text=True,
+                           timeout=600)
+        e = subprocess.run([sys.executable, "-m", "paper_2204_12346_b200.cli", *args, "--out-dir", str(d_eng)],
+                           capture_output=True, text=True, timeout=600, cwd=ROOT)
+        assert r.returncode == e.returncode, (name, r.stderr, e.stderr)
+        ref_files = {p.name: p.read_bytes() for p in sorted(d_ref.glob("*"))}
+        eng_files = {p.name: p.read_bytes() for p in sorted(d_eng.glob("*"))}
+        assert ref_files and set(ref_files) == set(eng_files), (name, sorted(ref_files), sorted(eng_files))
+        for fname, data in ref_files.items():
+            if eng_files[fname] != data:
+                a, b = data.decode().splitlines(), eng_files[fname].decode().splitlines()
+                diff = [(i, x, y) for i, (x, y) in enumerate(zip(a, b)) if x != y][:3]
+                mismatches.append((name, fname, len(a), len(b), diff))
+    assert not mismatches, mismatches
