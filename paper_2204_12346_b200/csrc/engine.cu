@@ -176,7 +176,9 @@ void sg_ctx_destroy(sg_ctx* ctx) {
         if (ctx->join[l]) cudaEventDestroy(ctx->join[l]);
     }
     if (ctx->fork) cudaEventDestroy(ctx->fork);
-    if (ctx->band_eval) cudaStreamDestroy(ctx->band_eval);
+    if (ctx->band_stats) cudaFree(ctx->band_stats);
+    for (cudaStream_t e : ctx->band_eval)
+        if (e) cudaStreamDestroy(e);
     if (ctx->band_sel) cudaStreamDestroy(ctx->band_sel);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -202,6 +204,20 @@ uint64_t sg_ctx_launch_count(const sg_ctx* ctx) { return ctx ? ctx->launches.loa
 void sg_ctx_copy_bytes(const sg_ctx* ctx, uint64_t* h2d, uint64_t* d2h) {
     if (h2d) *h2d = ctx ? ctx->h2d_bytes.load() : 0;
     if (d2h) *d2h = ctx ? ctx->d2h_bytes.load() : 0;
+}
+
+int sg_ctx_band_stats(sg_ctx* ctx, uint64_t* fused_days, uint64_t* pass_days) {
+    if (!ctx) return SG_ERR_INVALID_ARGUMENT;
+    SG_ENTRY(ctx, "sg_ctx_band_stats");
+    unsigned long long v[2] = {0, 0};
+    if (ctx->band_stats) {
+        SG_CUDA(ctx, cudaSetDevice(ctx->device));
+        SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        SG_CUDA(ctx, cudaMemcpy(v, ctx->band_stats, sizeof v, cudaMemcpyDeviceToHost));
+    }
+    if (fused_days) *fused_days = v[0];
+    if (pass_days) *pass_days = v[1];
+    return SG_OK;
 }
 
 void* sg_ctx_stream(const sg_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
@@ -1077,16 +1093,23 @@ int sg_fit_swarms(sg_ctx* ctx, const sg_swarm_desc* swarms, size_t n_swarms, sg_
     return SG_OK;
 }
 
+// Days of t1/t2 per ordering-key step: 1 while the box's switch times stay
+// below day 64, coarser beyond (the key has 64 steps per switch time).
+static int order_step(const double upper[6]) {
+    const double t = std::max(upper[2], upper[3]);
+    return t < 63.0 ? 1 : static_cast<int>(std::min(4096.0, std::ceil((t + 1.0) / 64.0)));
+}
+
 // Ramp-coherent evaluation order of an ensemble: ens_sample_kernel draws
 // every sample into SoA planes with its (day t1, day t2) key and counts the
 // keys; a scan and a scatter complete the counting sort into perm.
-static int ensemble_order(sg_ctx* ctx, const double* d_lo, const double* d_hi, uint64_t seed, size_t n,
+// key_count: 2 x kOrderKeys, the counts zero on entry (and again on exit).
+static int ensemble_order(sg_ctx* ctx, const double* d_lo, const double* d_hi, uint64_t seed, size_t n, int q,
                           double* planes, uint32_t* keys, unsigned int* key_count, uint32_t* perm, cudaStream_t st) {
-    SG_CUDA(ctx, cudaMemsetAsync(key_count, 0, sizeof(unsigned int) * 65536, st));
-    const unsigned grid = static_cast<unsigned>((n + 255) / 256);
-    ens_sample_kernel<<<grid, 256, 0, st>>>(d_lo, d_hi, seed, n, planes, keys, key_count);
-    ens_scan_kernel<<<1, 1024, 0, st>>>(key_count);
-    ens_scatter_kernel<<<grid, 256, 0, st>>>(keys, n, key_count, perm);
+    const unsigned grid = static_cast<unsigned>((n + kSampleThreads - 1) / kSampleThreads);
+    ens_sample_kernel<<<grid, kSampleThreads, 0, st>>>(d_lo, d_hi, seed, n, q, planes, keys, key_count);
+    ens_scan_kernel<<<1, kBgThreads, 0, st>>>(key_count);
+    ens_scatter_kernel<<<grid, kSampleThreads, 0, st>>>(keys, n, key_count + kOrderKeys, perm);
     ctx->launches += 3;
     SG_CUDA(ctx, cudaGetLastError());
     return SG_OK;
@@ -1123,15 +1146,17 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
         SG_CUDA(ctx, b.alloc(&planes, 6 * n));
         SG_CUDA(ctx, b.alloc(&keys, n));
         SG_CUDA(ctx, b.alloc(&perm, n));
-        SG_CUDA(ctx, b.alloc(&key_count, 65536));
-        if (const int rc = ensemble_order(ctx, d_lo, d_hi, seed, n, planes, keys, key_count, perm, ctx->stream))
+        SG_CUDA(ctx, b.alloc(&key_count, 2 * kOrderKeys));
+        SG_CUDA(ctx, cudaMemsetAsync(key_count, 0, sizeof(unsigned int) * kOrderKeys, ctx->stream));
+        if (const int rc = ensemble_order(ctx, d_lo, d_hi, seed, n, order_step(upper), planes, keys, key_count, perm,
+                                          ctx->stream))
             return rc;
     }
     cudaError_t err = cudaSuccess;
     dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc,
                              fwin, d_lo, d_hi, seed, n, horizon, d_cost, d_par, d_D,
                              static_cast<size_t>(horizon + 1), size_t(1), perm, planes, 0, static_cast<SelDay*>(nullptr),
-                             w->smem, ctx->stream, &err);
+                             static_cast<unsigned int*>(nullptr), w->smem, ctx->stream, &err);
     ctx->launches += 1;
     if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
     if (costs) SG_CUDA(ctx, copy_async(ctx, costs, d_cost, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1157,10 +1182,23 @@ struct BandSlot {
 // windows: 187.9 ms separate vs 194.1 ms fused — the epilogue adds ~63 us
 // to every FP64-bound evaluation (profiles/r02h_c5_*), the separate pass
 // overlaps it on the other stream.
-static bool fused_range() {
+// The ensemble kernel reduces each day's key range and finite count as the
+// forecast runs (lane d of a warp holds day d, so horizon < 32);
+// SG_FUSED_RANGE=0 runs sel_range_kernel over the plane instead (A/B).
+static bool fused_range(int horizon) {
     static const bool on = [] {
         const char* e = std::getenv("SG_FUSED_RANGE");
-        return e && e[0] == '1';
+        return !(e && e[0] == '0');
+    }();
+    return on && horizon < 32;
+}
+
+// The ensemble kernel's fused histogram over predicted bins (SelDay);
+// SG_FUSED_HIST=0 sends every day through the histogram pass (A/B).
+static bool fused_hist() {
+    static const bool on = [] {
+        const char* e = std::getenv("SG_FUSED_HIST");
+        return !(e && e[0] == '0');
     }();
     return on;
 }
@@ -1170,22 +1208,28 @@ static int alloc_band_slot(sg_ctx* ctx, DevBufs& b, BandSlot& s, size_t n, int n
     SG_CUDA(ctx, b.alloc(&s.planes, 6 * n));
     SG_CUDA(ctx, b.alloc(&s.keys, n));
     SG_CUDA(ctx, b.alloc(&s.perm, n));
-    SG_CUDA(ctx, b.alloc(&s.key_count, 65536));
+    SG_CUDA(ctx, b.alloc(&s.key_count, 2 * kOrderKeys));
     SG_CUDA(ctx, b.alloc(&s.D, nd));
     SG_CUDA(ctx, b.alloc(&s.cand, nd));
     SG_CUDA(ctx, b.alloc(&s.scratch, 2 * nd));  // only bins too full for one CTA's shared memory touch it
     SG_CUDA(ctx, b.alloc(&s.days, n_days));
     SG_CUDA(ctx, b.alloc(&s.hist, static_cast<size_t>(n_days) * kSelBins));
     SG_CUDA(ctx, b.alloc(&s.vals, static_cast<size_t>(n_days) * kBandRanks));
+    // zero once: ens_scan_kernel and sel_locate_kernel leave them zero
+    SG_CUDA(ctx, cudaMemsetAsync(s.key_count, 0, sizeof(unsigned int) * kOrderKeys, b.st));
+    SG_CUDA(ctx, cudaMemsetAsync(s.hist, 0, sizeof(unsigned int) * n_days * kSelBins, b.st));
+    SG_CUDA(ctx, cudaMemsetAsync(s.days, 0, sizeof(SelDay) * n_days, b.st));  // no prediction for the first window
     return SG_OK;
 }
 
 // C5, stage 1 (integer work): the samples and their ramp-coherent order;
 // the slot's day records reset for the selection.
 static int enqueue_band_order(sg_ctx* ctx, BandSlot& s, cudaStream_t st, const double* d_lo, const double* d_hi,
-                              uint64_t seed, size_t n, int n_days) {
-    if (const int rc = ensemble_order(ctx, d_lo, d_hi, seed, n, s.planes, s.keys, s.key_count, s.perm, st)) return rc;
-    sel_init_kernel<<<static_cast<unsigned>((n_days + 127) / 128), 128, 0, st>>>(s.days, n_days);
+                              uint64_t seed, size_t n, int q, int n_days) {
+    if (const int rc = ensemble_order(ctx, d_lo, d_hi, seed, n, q, s.planes, s.keys, s.key_count, s.perm, st))
+        return rc;
+    sel_init_kernel<<<static_cast<unsigned>((n_days + kBgThreads - 1) / kBgThreads), kBgThreads, 0, st>>>(
+        s.days, n_days, fused_range(n_days - 1) && fused_hist() ? 1 : 0);
     ctx->launches += 1;
     SG_CUDA(ctx, cudaGetLastError());
     return SG_OK;
@@ -1202,7 +1246,7 @@ static int enqueue_band_eval(sg_ctx* ctx, sg_window* w, BandSlot& s, cudaStream_
     // day-major columns in evaluation order: the bands only need each day's multiset
     dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc,
                              fwin, d_lo, d_hi, seed, n, horizon, d_cost, static_cast<double*>(nullptr), s.D, size_t(1),
-                             n, s.perm, s.planes, 1, fused_range() ? s.days : nullptr, w->smem, st, &err);
+                             n, s.perm, s.planes, 1, fused_range(horizon) ? s.days : nullptr, s.hist, w->smem, st, &err);
     ctx->launches += 1;
     if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
     return SG_OK;
@@ -1214,22 +1258,27 @@ static int enqueue_band_eval(sg_ctx* ctx, sg_window* w, BandSlot& s, cudaStream_
 // and quantile_sorted turns them into the bands.
 static int enqueue_band_select(sg_ctx* ctx, BandSlot& s, cudaStream_t st, size_t n, int n_days, double* d_bands,
                                unsigned long long* d_counts, bool standalone = false) {
-    SG_CUDA(ctx, cudaMemsetAsync(s.hist, 0, sizeof(unsigned int) * n_days * kSelBins, st));
+    if (!ctx->band_stats) {
+        SG_CUDA(ctx, cudaMalloc(&ctx->band_stats, 2 * sizeof(unsigned long long)));
+        SG_CUDA(ctx, cudaMemset(ctx->band_stats, 0, 2 * sizeof(unsigned long long)));
+    }
     const unsigned chunks = static_cast<unsigned>(std::min<size_t>(64, (n + 4095) / 4096));
     const dim3 grid(chunks, static_cast<unsigned>(n_days));
-    if (!fused_range() && !standalone) {
-        sel_range_kernel<<<grid, 256, 0, st>>>(s.D, n, s.days);
+    if (!fused_range(n_days - 1) && !standalone) {  // standalone: the caller ran it
+        sel_range_kernel<<<grid, kSampleThreads, 0, st>>>(s.D, n, s.days);
         ctx->launches += 1;
     }
     const dim3 hgrid(static_cast<unsigned>(std::min<size_t>(16, (n + 16383) / 16384)), static_cast<unsigned>(n_days));
-    sel_hist_kernel<<<hgrid, 1024, 0, st>>>(s.D, n, s.days, s.hist);
-    sel_locate_kernel<<<static_cast<unsigned>(n_days), 1024, 0, st>>>(s.hist, s.days);
-    sel_gather_kernel<<<grid, 256, 0, st>>>(s.D, n, s.days, s.cand);
-    sel_finish_kernel<<<dim3(kBandRanks, static_cast<unsigned>(n_days)), kSelFinishThreads, 0, st>>>(
-        s.days, s.cand, s.scratch, n, s.vals);
-    sel_bands_kernel<<<static_cast<unsigned>((n_days + 127) / 128), 128, 0, st>>>(s.days, s.vals, d_bands, d_counts,
-                                                                                 n_days);
-    ctx->launches += 5;
+    // the fused histogram, else (per day) the histogram pass over the plane
+    sel_locate_kernel<<<static_cast<unsigned>(n_days), kBgThreads, 0, st>>>(s.hist, s.days, 0, ctx->band_stats);
+    sel_hist_kernel<<<hgrid, kHistThreads, 0, st>>>(s.D, n, s.days, s.hist);
+    sel_locate_kernel<<<static_cast<unsigned>(n_days), kBgThreads, 0, st>>>(s.hist, s.days, 1, nullptr);
+    sel_gather_kernel<<<grid, kSampleThreads, 0, st>>>(s.D, n, s.days, s.cand);
+    sel_finish_kernel<<<static_cast<unsigned>(kBandRanks * n_days), kSampleThreads, 0, st>>>(
+        n_days, s.days, s.cand, s.scratch, n, s.vals);
+    sel_bands_kernel<<<static_cast<unsigned>((n_days + kBgThreads - 1) / kBgThreads), kBgThreads, 0, st>>>(
+        s.days, s.vals, d_bands, d_counts, n_days);
+    ctx->launches += 6;
     SG_CUDA(ctx, cudaGetLastError());
     return SG_OK;
 }
@@ -1271,7 +1320,8 @@ int sg_forecast_ensemble_bands(sg_window* w, const double lower[6], const double
     } else {
         BandSlot s;
         if (const int rc = alloc_band_slot(ctx, b, s, n, n_days)) return rc;
-        if (const int rc = enqueue_band_order(ctx, s, ctx->stream, d_lo, d_hi, seed, n, n_days)) return rc;
+        if (const int rc = enqueue_band_order(ctx, s, ctx->stream, d_lo, d_hi, seed, n, order_step(upper), n_days))
+            return rc;
         if (const int rc = enqueue_band_eval(ctx, w, s, ctx->stream, d_lo, d_hi, seed, n, horizon, d_cost)) return rc;
         if (const int rc = enqueue_band_select(ctx, s, ctx->stream, n, n_days, d_bands, d_counts)) return rc;
     }
@@ -1308,10 +1358,11 @@ int sg_quantile_bands(sg_ctx* ctx, const double* values, size_t n, int n_days, d
         SG_CUDA(ctx, b.alloc(&s.days, n_days));
         SG_CUDA(ctx, b.alloc(&s.hist, static_cast<size_t>(n_days) * kSelBins));
         SG_CUDA(ctx, b.alloc(&s.vals, static_cast<size_t>(n_days) * kBandRanks));
+        SG_CUDA(ctx, cudaMemsetAsync(s.hist, 0, sizeof(unsigned int) * n_days * kSelBins, ctx->stream));
         SG_CUDA(ctx, copy_async(ctx, s.D, values, sizeof(double) * nd, cudaMemcpyHostToDevice, ctx->stream));
-        sel_init_kernel<<<static_cast<unsigned>((n_days + 127) / 128), 128, 0, ctx->stream>>>(s.days, n_days);
+        sel_init_kernel<<<static_cast<unsigned>((n_days + 127) / 128), 128, 0, ctx->stream>>>(s.days, n_days, 0);
         const dim3 grid(static_cast<unsigned>(std::min<size_t>(64, (n + 4095) / 4096)), static_cast<unsigned>(n_days));
-        sel_range_kernel<<<grid, 256, 0, ctx->stream>>>(s.D, n, s.days);
+        sel_range_kernel<<<grid, kSampleThreads, 0, ctx->stream>>>(s.D, n, s.days);
         ctx->launches += 2;
         if (const int rc = enqueue_band_select(ctx, s, ctx->stream, n, n_days, d_bands, d_counts, true)) return rc;
     }
@@ -1327,7 +1378,7 @@ int sg_quantile_bands(sg_ctx* ctx, const double* values, size_t n, int n_days, d
 // selection stream (high priority, so its memory-bound CTAs take SM slots
 // as soon as ensemble CTAs retire) reduces window k-1 to bands.
 static int ensure_band_streams(sg_ctx* ctx) {
-    if (ctx->band_eval) return SG_OK;
+    if (ctx->band_eval[0]) return SG_OK;
     int least = 0, greatest = 0;
     SG_CUDA(ctx, cudaDeviceGetStreamPriorityRange(&least, &greatest));
     // SG_BAND_PRIO (diagnostic A/B): priority of the selection stream
@@ -1337,7 +1388,7 @@ static int ensure_band_streams(sg_ctx* ctx) {
     const std::string p = prio ? prio : "high";
     const int eval_prio = p == "low" ? greatest : least;
     const int sel_prio = p == "high" ? greatest : least;
-    SG_CUDA(ctx, cudaStreamCreateWithPriority(&ctx->band_eval, cudaStreamNonBlocking, eval_prio));
+    for (cudaStream_t& e : ctx->band_eval) SG_CUDA(ctx, cudaStreamCreateWithPriority(&e, cudaStreamNonBlocking, eval_prio));
     SG_CUDA(ctx, cudaStreamCreateWithPriority(&ctx->band_sel, cudaStreamNonBlocking, sel_prio));
     return SG_OK;
 }
@@ -1363,6 +1414,7 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
         return SG_OK;
     }
     const int n_days = horizon + 1;
+    const int q = order_step(upper);
     SG_ENTRY(ctx, "sg_forecast_ensemble_bands_batch");
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     if (const int rc = ensure_lanes(ctx)) return rc;
@@ -1375,7 +1427,7 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
     SG_CUDA(ctx, b.alloc(&d_hi, 6));
     SG_CUDA(ctx, b.alloc(&d_bands, 7 * static_cast<size_t>(n_days) * n_windows));
     SG_CUDA(ctx, b.alloc(&d_counts, static_cast<size_t>(n_days) * n_windows));
-    constexpr int kSlots = 2;
+    constexpr int kSlots = sg_ctx::kBandSlots;
     BandSlot slot[kSlots];
     for (BandSlot& s : slot)
         if (const int rc = alloc_band_slot(ctx, b, s, n, n_days)) return rc;
@@ -1387,18 +1439,21 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
         SG_CUDA(ctx, cudaEventCreateWithFlags(&evaluated[k], cudaEventDisableTiming));
         SG_CUDA(ctx, cudaEventCreateWithFlags(&selected[k], cudaEventDisableTiming));
     }
-    // Three stages per window over two slots: order (S) -> evaluate (E) ->
-    // select (S).  S runs window k+1's order while E evaluates window k, then
-    // window k's selection; E evaluates back to back.
-    cudaStream_t E = ctx->band_eval, S = ctx->band_sel;
+    // Three stages per window over kSlots slots: order (S) -> evaluate (E)
+    // -> select (S).  S runs window k+1's order while E evaluates window k,
+    // then window k's selection.  Each slot evaluates on its own stream:
+    // nothing orders window k+1's evaluation after window k's, so its CTAs
+    // fill the SMs window k's last wave leaves idle.
+    cudaStream_t S = ctx->band_sel;
     SG_CUDA(ctx, cudaEventRecord(ctx->fork, ctx->stream));  // buffers allocated, bounds uploaded
-    SG_CUDA(ctx, cudaStreamWaitEvent(E, ctx->fork, 0));
+    for (cudaStream_t e : ctx->band_eval) SG_CUDA(ctx, cudaStreamWaitEvent(e, ctx->fork, 0));
     SG_CUDA(ctx, cudaStreamWaitEvent(S, ctx->fork, 0));
     auto step = [&](cudaError_t e) { return e == cudaSuccess ? SG_OK : cuda_fail(ctx, e, "band pipeline"); };
-    int rc = enqueue_band_order(ctx, slot[0], S, d_lo, d_hi, seeds[0], n, n_days);
+    int rc = enqueue_band_order(ctx, slot[0], S, d_lo, d_hi, seeds[0], n, q, n_days);
     if (!rc) rc = step(cudaEventRecord(ordered[0], S));
     for (size_t k = 0; k < n_windows && !rc; ++k) {
         const int j = static_cast<int>(k % kSlots);
+        cudaStream_t E = ctx->band_eval[j];
         // E: window k once ordered, into a deaths plane its slot's previous
         // window has been reduced from
         rc = step(cudaStreamWaitEvent(E, ordered[j], 0));
@@ -1406,11 +1461,11 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
         if (!rc) rc = enqueue_band_eval(ctx, windows[k], slot[j], E, d_lo, d_hi, seeds[k], n, horizon, nullptr);
         if (!rc) rc = step(cudaEventRecord(evaluated[j], E));
         // S: the next window's order (its slot's planes were read by window
-        // k-1's evaluation), then window k's selection
+        // k+1-kSlots's evaluation), then window k's selection
         if (!rc && k + 1 < n_windows) {
             const int j1 = static_cast<int>((k + 1) % kSlots);
-            if (k >= 1) rc = step(cudaStreamWaitEvent(S, evaluated[j1], 0));
-            if (!rc) rc = enqueue_band_order(ctx, slot[j1], S, d_lo, d_hi, seeds[k + 1], n, n_days);
+            if (k + 1 >= kSlots) rc = step(cudaStreamWaitEvent(S, evaluated[j1], 0));
+            if (!rc) rc = enqueue_band_order(ctx, slot[j1], S, d_lo, d_hi, seeds[k + 1], n, q, n_days);
             if (!rc) rc = step(cudaEventRecord(ordered[j1], S));
         }
         if (!rc) rc = step(cudaStreamWaitEvent(S, evaluated[j], 0));
@@ -1419,11 +1474,13 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
                                      d_counts + static_cast<size_t>(n_days) * k);
         if (!rc) rc = step(cudaEventRecord(selected[j], S));
     }
-    // join both streams even after a failure: the buffers are released in ctx->stream order
-    SG_CUDA(ctx, cudaEventRecord(ctx->join[0], E));
-    SG_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join[0], 0));
-    SG_CUDA(ctx, cudaEventRecord(ctx->join[1], S));
-    SG_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join[1], 0));
+    // join the streams even after a failure: the buffers are released in ctx->stream order
+    for (int e = 0; e < kSlots; ++e) {
+        SG_CUDA(ctx, cudaEventRecord(ctx->join[e], ctx->band_eval[e]));
+        SG_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join[e], 0));
+    }
+    SG_CUDA(ctx, cudaEventRecord(ctx->join[kSlots], S));
+    SG_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join[kSlots], 0));
     for (int k = 0; k < kSlots; ++k) {
         cudaEventDestroy(ordered[k]);
         cudaEventDestroy(evaluated[k]);

@@ -50,9 +50,12 @@ struct sg_ctx {
     cudaStream_t side[kMaxLanes] = {};
     cudaEvent_t fork = nullptr;
     cudaEvent_t join[kMaxLanes] = {};
-    // the C5 band pipeline: ensemble evaluation (low priority) and band
-    // selection (high priority) streams
-    cudaStream_t band_eval = nullptr, band_sel = nullptr;
+    // the C5 band pipeline: ensemble evaluation and band selection streams
+    static constexpr int kBandSlots = 2;  // windows in flight (one evaluation stream each; 3 measured no faster)
+    cudaStream_t band_eval[kBandSlots] = {}, band_sel = nullptr;
+    // band-selection telemetry (device): days resolved from the ensemble's
+    // fused histogram, days that took the histogram pass
+    unsigned long long* band_stats = nullptr;
 };
 
 struct sg_window {

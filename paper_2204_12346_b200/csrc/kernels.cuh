@@ -932,97 +932,199 @@ __device__ __forceinline__ double key_value(uint64_t k) {
 }
 
 struct SelDay {                   // per forecast day, device memory
-    unsigned long long kmin, kmax, count;  // finite values: key range and k
-    int shift;                    // bin = (key - kmin) >> shift
+    unsigned long long kmin, kmax, count;  // finite values: key range (a superset when fused) and k
+    unsigned long long base;      // bin origin of the selection: bin = (key - base) >> shift
+    int shift;
     int n_seg;                    // distinct bins holding wanted ranks
+    // The ensemble kernel's fused histogram (band path): bins predicted from
+    // the key range the slot's previous window had, widened by half its width
+    // on both sides (sel_init_kernel); values outside counted apart.  A day
+    // whose wanted ranks fall outside the predicted bins takes the histogram
+    // pass over its exact range instead (full = 1).
+    unsigned long long pbase;
+    int pshift;                   // -1: no prediction
+    int full;
+    unsigned long long under, over;
     uint32_t seg_bin[kBandRanks];
     uint64_t seg_rank0[kBandRanks];   // rank of the bin's first value
     uint32_t seg_count[kBandRanks];
     uint32_t seg_fill[kBandRanks];
 };
 
-#ifndef SG_FAMILY_TU  // engine.cu only (family.cu holds the templated kernels)
-// Evaluation order of an ensemble: every sample's parameters into SoA
-// planes and a key (day of t1, day of t2) — samples with equal keys ramp on
-// the same days, so grouping them makes a warp's lanes ramp together (the
-// warp pays a ramp substep if any lane ramps).  The order never changes a
-// result: every sample is evaluated by the same code into its own slot, and
-// the bands only need each day's multiset.  Fused: the key histogram of the
-// counting sort (ens_scan_kernel, ens_scatter_kernel).
-__global__ void __launch_bounds__(256) ens_sample_kernel(const double* __restrict__ lo, const double* __restrict__ hi,
-                                                         uint64_t seed, size_t n, double* __restrict__ planes,
-                                                         uint32_t* __restrict__ keys,
-                                                         unsigned int* __restrict__ key_count) {
-    const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    double x[6];
-    x_of_sample(lo, hi, seed, k, x);
-#pragma unroll
-    for (int d = 0; d < 6; ++d) planes[d * n + k] = x[d];
-    auto day = [](double t) -> uint32_t {  // NaN and negatives -> 0, capped at 255
-        return t > 0.0 ? static_cast<uint32_t>(fmin(floor(t), 255.0)) : 0u;
-    };
-    const uint32_t key = (day(x[2]) << 8) | day(x[3]);
-    keys[k] = key;
-    atomicAdd(&key_count[key], 1u);
+__host__ __device__ __forceinline__ int sel_shift(unsigned long long range) {
+#ifdef __CUDA_ARCH__
+    const int bits = range ? 64 - __clzll(static_cast<long long>(range)) : 0;
+#else
+    const int bits = range ? 64 - __builtin_clzll(range) : 0;
+#endif
+    return bits > kSelBinBits ? bits - kSelBinBits : 0;
 }
 
-// Exclusive scan of the 2^16 key counts into bucket cursors (one CTA of 32
-// warps; warp w owns entries [2048 w, 2048 (w + 1)), read 32 at a time).
-__global__ void __launch_bounds__(1024) ens_scan_kernel(unsigned int* __restrict__ key_count) {
-    constexpr int kChunk = 65536 / 32;
-    __shared__ unsigned int warp_base[32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned int* const c = key_count + warp * kChunk;
-    unsigned int total = 0;
-#pragma unroll 8
-    for (int i = lane; i < kChunk; i += 32) total += c[i];
-    total = __reduce_add_sync(0xFFFFFFFFu, total);
-    if (lane == 0) warp_base[warp] = total;
-    __syncthreads();
-    if (warp == 0) {
-        const unsigned int v = warp_base[lane];
-        unsigned int incl = v;
+#ifndef SG_FAMILY_TU  // engine.cu only (family.cu holds the templated kernels)
+// Thread counts of the selection stream's kernels (ordering and band
+// selection).  They run beside the FP64-bound ensemble kernel of the next
+// window and take CTA slots from it as they go (the hardware dispatches a
+// lower-priority grid's CTAs only once the higher one has none left to
+// place, so they cannot be confined to the registers the ensemble's 5 CTAs
+// leave free — measured): each is sized for its shortest
+// standalone time, which is the ensemble time it costs.
+constexpr int kBgThreads = 128;       // small kernels (init, scan, locate, bands)
+constexpr int kSampleThreads = 256;   // ens_sample / ens_scatter / sel_range / sel_gather / sel_finish
+constexpr int kHistThreads = 1024;    // sel_hist (a CTA histogram in shared memory)
+
+// Evaluation order of an ensemble: every sample's parameters into SoA
+// planes and a key (day of t1, day of t2, each in steps of `q` days and
+// capped at 63) — samples with equal keys ramp on the same days, so
+// grouping them makes a warp's lanes ramp together (the warp pays a ramp
+// substep if any lane ramps).  The order never changes a result: every
+// sample is evaluated by the same code into its own slot, and the bands
+// only need each day's multiset.  Fused: the key histogram of the counting
+// sort (ens_scan_kernel, ens_scatter_kernel).
+constexpr int kOrderKeys = 4096;
+__global__ void __launch_bounds__(kSampleThreads) ens_sample_kernel(const double* __restrict__ lo, const double* __restrict__ hi,
+                                               uint64_t seed, size_t n, int q, double* __restrict__ planes,
+                                               uint32_t* __restrict__ keys, unsigned int* __restrict__ key_count) {
+    auto day = [q](double t) -> uint32_t {  // NaN and negatives -> 0, capped at 63 steps
+        return t > 0.0 ? static_cast<uint32_t>(fmin(floor(t), 4096.0)) / q : 0u;
+    };
+    for (size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        double x[6];
+        x_of_sample(lo, hi, seed, k, x);
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const unsigned int o = __shfl_up_sync(0xFFFFFFFFu, incl, off);
-            if (lane >= off) incl += o;
-        }
-        warp_base[lane] = incl - v;
+        for (int d = 0; d < 6; ++d) planes[d * n + k] = x[d];
+        const uint32_t key = (min(day(x[2]), 63u) << 6) | min(day(x[3]), 63u);
+        keys[k] = key;
+        atomicAdd(&key_count[key], 1u);
     }
-    __syncthreads();
-    unsigned int carry = warp_base[warp];
-    for (int i = 0; i < kChunk; i += 32) {
-        const unsigned int v = c[i + lane];
-        unsigned int incl = v;
+}
+
+// Exclusive scan of the kOrderKeys key counts into bucket cursors
+// (key_count[kOrderKeys + key]); the counts are zeroed for the next window.
+// One CTA: thread t owns 32 consecutive keys.
+__global__ void __launch_bounds__(kBgThreads) ens_scan_kernel(unsigned int* __restrict__ key_count) {
+    constexpr int kPer = kOrderKeys / kBgThreads;
+    __shared__ unsigned int warp_base[kBgThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint4* const c = reinterpret_cast<uint4*>(key_count) + threadIdx.x * (kPer / 4);
+    unsigned int total = 0;
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const unsigned int o = __shfl_up_sync(0xFFFFFFFFu, incl, off);
-            if (lane >= off) incl += o;
-        }
-        c[i + lane] = carry + incl - v;
-        carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    for (int i = 0; i < kPer / 4; ++i) {
+        const uint4 u = c[i];
+        total += u.x + u.y + u.z + u.w;
+    }
+    unsigned int incl = total;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const unsigned int o = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+        if (lane >= off) incl += o;
+    }
+    if (lane == 31) warp_base[warp] = incl;
+    __syncthreads();
+    unsigned int carry = incl - total;
+    for (int w = 0; w < warp; ++w) carry += warp_base[w];
+    uint4* const cur = reinterpret_cast<uint4*>(key_count + kOrderKeys) + threadIdx.x * (kPer / 4);
+#pragma unroll 4
+    for (int i = 0; i < kPer / 4; ++i) {
+        const uint4 v = c[i];
+        c[i] = make_uint4(0u, 0u, 0u, 0u);
+        uint4 u;
+        u.x = carry;
+        u.y = u.x + v.x;
+        u.z = u.y + v.y;
+        u.w = u.z + v.z;
+        carry = u.w + v.w;
+        cur[i] = u;
     }
 }
 
 // Counting-sort scatter: sample k takes the next slot of its key's bucket.
-__global__ void __launch_bounds__(256) ens_scatter_kernel(const uint32_t* __restrict__ keys, size_t n,
-                                                          unsigned int* __restrict__ cursor,
-                                                          uint32_t* __restrict__ perm) {
-    const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    perm[atomicAdd(&cursor[keys[k]], 1u)] = static_cast<uint32_t>(k);
+__global__ void __launch_bounds__(kSampleThreads) ens_scatter_kernel(const uint32_t* __restrict__ keys, size_t n,
+                                                unsigned int* __restrict__ cursor, uint32_t* __restrict__ perm) {
+    for (size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+         k += static_cast<size_t>(gridDim.x) * blockDim.x)
+        perm[atomicAdd(&cursor[keys[k]], 1u)] = static_cast<uint32_t>(k);
 }
 
-__global__ void sel_init_kernel(SelDay* __restrict__ days, int n_days) {
+// Reset a slot's day records for its next window; with `predict`, each
+// day's fused-histogram bins come from the key range the slot's previous
+// window had (two windows back in the pipeline), widened by half its width
+// on each side.
+__global__ void __launch_bounds__(kBgThreads) sel_init_kernel(SelDay* __restrict__ days, int n_days, int predict) {
     const int d = blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= n_days) return;
-    days[d].kmin = ~0ULL;
-    days[d].kmax = 0;
-    days[d].count = 0;
-    days[d].n_seg = 0;
+    SelDay& sd = days[d];
+    sd.pshift = -1;
+    if (predict && sd.count > 0 && sd.kmax >= sd.kmin) {
+        const unsigned long long half = (sd.kmax - sd.kmin) / 2;
+        const unsigned long long lo = sd.kmin > half ? sd.kmin - half : 0ULL;
+        const unsigned long long hi = ~0ULL - sd.kmax > half ? sd.kmax + half : ~0ULL;
+        sd.pbase = lo;
+        sd.pshift = sel_shift(hi - lo);
+    }
+    sd.kmin = ~0ULL;
+    sd.kmax = 0;
+    sd.count = 0;
+    sd.n_seg = 0;
+    sd.full = 0;
+    sd.under = 0;
+    sd.over = 0;
 }
 #endif  // SG_FAMILY_TU
+
+// Scores nothing: the band path needs no cost per sample.
+struct NullSink {
+    __device__ __forceinline__ void day(int, double, double, double, double) {}
+};
+
+// The band path's forecast sink: writes the deaths row (when `on`) and
+// does the selection's first two passes as the days arrive, without
+// re-reading the plane:
+//   * each day's key range, reduced over the warp — the top 32 bits of the
+//     order key by REDUX, so the range is a superset of the exact one by
+//     < 2^32 key units, which only widens the bins of a histogram pass
+//     (lane d keeps day d's warp range; horizon < 32);
+//   * each day's histogram over the bins predicted for it (SelDay::pbase,
+//     pshift), values outside the predicted bins counted apart.
+// Every lane of the warp must run the loop: the reductions name the full warp.
+struct BandDSink {
+    double* out;
+    size_t dstride;
+    bool on;          // this lane's row is written and counted
+    uint32_t lo, hi;  // lane d: day d's warp range (hi32 of the keys)
+    const unsigned long long* pbase;  // shared memory, per day
+    const int* pshift;                // shared memory, per day (-1: no prediction)
+    unsigned int* hist;               // n_days x kSelBins
+    SelDay* days;
+    // One value into (+1) or out of (-1, a row that blows up later) the
+    // day's predicted histogram.
+    __device__ __forceinline__ void count(int d, unsigned long long key, int delta) {
+        const int sh = pshift[d];
+        if (sh < 0) return;
+        const unsigned long long base = pbase[d];
+        if (key < base) {
+            atomicAdd(&days[d].under, static_cast<unsigned long long>(static_cast<long long>(delta)));
+        } else if (((key - base) >> sh) >= static_cast<unsigned long long>(kSelBins)) {
+            atomicAdd(&days[d].over, static_cast<unsigned long long>(static_cast<long long>(delta)));
+        } else {
+            atomicAdd(&hist[d * kSelBins + static_cast<int>((key - base) >> sh)], static_cast<unsigned>(delta));
+        }
+    }
+    __device__ __forceinline__ void put(int d, double D) {
+        if (on) out[d * dstride] = D;
+        const bool fin = on && isfinite(D);
+        const unsigned long long key = order_key(D);
+        if (fin) count(d, key, 1);
+        const uint32_t k32 = static_cast<uint32_t>(key >> 32);
+        const uint32_t mn = __reduce_min_sync(0xFFFFFFFFu, fin ? k32 : 0xFFFFFFFFu);
+        const uint32_t mx = __reduce_max_sync(0xFFFFFFFFu, fin ? k32 : 0u);
+        if ((threadIdx.x & 31) == static_cast<unsigned>(d)) {
+            lo = mn;
+            hi = mx;
+        }
+    }
+    __device__ __forceinline__ void day(int d, double, double, double, double D) { put(d, D); }
+};
 
 template <int FAM, int MET, int SUB>
 __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWindow* __restrict__ win, DevWindow fwin,
@@ -1033,10 +1135,17 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
                                                                 double* __restrict__ deaths_out, size_t sstride,
                                                                 size_t dstride, const uint32_t* __restrict__ perm,
                                                                 const double* __restrict__ planes, int out_by_slot,
-                                                                SelDay* __restrict__ days) {
+                                                                SelDay* __restrict__ days,
+                                                                unsigned int* __restrict__ hist) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ DevWindow sdesc;
-    const SmemWindow sw = stage_window<MET, SUB>(win, &sdesc, smem);
+    __shared__ unsigned long long s_pbase[32];
+    __shared__ int s_pshift[32];
+    if (days && static_cast<int>(threadIdx.x) <= horizon) {  // the band path (horizon < 32)
+        s_pbase[threadIdx.x] = days[threadIdx.x].pbase;
+        s_pshift[threadIdx.x] = days[threadIdx.x].pshift;
+    }
+    const SmemWindow sw = stage_window<MET, SUB>(win, &sdesc, smem);  // ends with a barrier
     // Thread slot -> sample k: identity, or the ramp-coherent order of
     // ens_sample_kernel + counting sort (perm), with the sample's parameters
     // read from its planes.  Costs and parameters always land at k; the
@@ -1048,114 +1157,96 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
     // deaths of sample k, forecast day d at deaths_out[k*sstride + d*dstride]
     // (sample-major rows, or day-major columns for the on-device bands)
     double* drow = deaths_out + (out_by_slot ? slot : k) * sstride;
+    const DevWindow& w = *sw.w;
+    const double nan = __longlong_as_double(0x7FF8000000000000LL);
+    if (!w.init_finite) {  // the whole launch (one window): no finite row, count 0
+        if (live) {
+            if (costs) costs[k] = __longlong_as_double(0x7FF0000000000000LL);
+            for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
+        }
+        return;
+    }
+    double x[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     if (live) {
-        [&] {
-            double x[6];
-            if (planes) {
+        if (planes) {
 #pragma unroll
-                for (int d = 0; d < 6; ++d) x[d] = planes[d * n + k];
-            } else {
-                x_of_sample(lo, hi, seed, k, x);
-            }
-            if (params_out) {
-#pragma unroll
-                for (int d = 0; d < 6; ++d) params_out[6 * k + d] = x[d];
-            }
-            const DevWindow& w = *sw.w;
-            const double nan = __longlong_as_double(0x7FF8000000000000LL);
-            if (!w.init_finite) {
-                if (costs) costs[k] = __longlong_as_double(0x7FF0000000000000LL);
-                for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
-                return;
-            }
-            const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w,
-                                             SubKind<SUB>::kTable ? sw.tg.tgrid : nullptr);
-            double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
-            ScoreSink<FAM, MET> score(w, sw.obs, sw.robs, sw.flag);  // starts from the day-0 contribution
-            integrate_days<SUB>(p, w, sw.tg, S, I, R, D, score);
-            const bool fin_w = all_finite(S, I, R, D);
-            // forecast_extension re-checks the junction through integrate_euler's
-            // isfinite(init.total()) (model.cpp:83).
-            const bool fin_j = fin_w && isfinite(dadd(dadd(dadd(S, I), R), D));
-            if (costs) costs[k] = score.finish(fin_w);
-            if (!fin_j) {  // forecast_extension throws NonFiniteError (calibration.cpp:301-303, 318-320)
-                for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
-                return;
-            }
-            // Forecast: fwin carries n_days = horizon + 1 and the same N, h, substeps.
-            const Particle held = make_particle(x[1], x[1], 0.0, 0.0, x[4], x[5], fwin);
-            drow[0] = D;
-            ForecastDSink fs{drow, dstride};
-            // held parameters never enter the ramp, so no time table is read
-            integrate_days<SUB>(held, fwin, TimeGrid{nullptr, sw.tg.subh}, S, I, R, D, fs);
-            if (!all_finite(S, I, R, D)) {  // calibration.cpp:318-320
-                for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
-            }
-        }();
-    }
-    if (!days) return;
-    // Band selection, fused: the key range and the count of each day's
-    // finite values (the first pass of the selection, without re-reading
-    // the deaths plane from HBM).  Days in chunks of 8: the chunk's values
-    // are loaded back together (one L2 latency, not 8), reduced per warp by
-    // shuffles, then across the CTA's warps: one atomic per CTA, day and
-    // quantity.
-    constexpr int kChunk = 8;
-    constexpr int kWarps = kEvalThreads / 32;
-    __shared__ unsigned long long s_lo[kChunk][kWarps], s_hi[kChunk][kWarps];
-    __shared__ unsigned int s_cnt[kChunk][kWarps];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int d0 = 0; d0 <= horizon; d0 += kChunk) {
-        double v[kChunk];
-#pragma unroll
-        for (int c = 0; c < kChunk; ++c)
-            v[c] = live && d0 + c <= horizon ? drow[(d0 + c) * dstride] : __longlong_as_double(0x7FF8000000000000LL);
-#pragma unroll
-        for (int c = 0; c < kChunk; ++c) {
-            const bool fin = isfinite(v[c]);
-            unsigned long long kl = fin ? order_key(v[c]) : ~0ULL, kh = fin ? order_key(v[c]) : 0ULL;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                const unsigned long long ol = __shfl_xor_sync(0xFFFFFFFFu, kl, off);
-                const unsigned long long oh = __shfl_xor_sync(0xFFFFFFFFu, kh, off);
-                kl = ol < kl ? ol : kl;
-                kh = oh > kh ? oh : kh;
-            }
-            const unsigned cnt = __popc(__ballot_sync(0xFFFFFFFFu, fin));
-            if (lane == 0) {
-                s_lo[c][wid] = kl;
-                s_hi[c][wid] = kh;
-                s_cnt[c][wid] = cnt;
-            }
+            for (int d = 0; d < 6; ++d) x[d] = planes[d * n + k];
+        } else {
+            x_of_sample(lo, hi, seed, k, x);
         }
-        __syncthreads();
-        if (threadIdx.x < kChunk && d0 + static_cast<int>(threadIdx.x) <= horizon) {
-            const int c = threadIdx.x;
-            unsigned long long lo = s_lo[c][0], hi = s_hi[c][0];
-            unsigned int n_fin = s_cnt[c][0];
+        if (params_out) {
 #pragma unroll
-            for (int w = 1; w < kWarps; ++w) {
-                lo = s_lo[c][w] < lo ? s_lo[c][w] : lo;
-                hi = s_hi[c][w] > hi ? s_hi[c][w] : hi;
-                n_fin += s_cnt[c][w];
-            }
-            if (n_fin) {
-                atomicMin(&days[d0 + c].kmin, lo);
-                atomicMax(&days[d0 + c].kmax, hi);
-                atomicAdd(&days[d0 + c].count, static_cast<unsigned long long>(n_fin));
-            }
+            for (int d = 0; d < 6; ++d) params_out[6 * k + d] = x[d];
         }
-        __syncthreads();
     }
+    // The window (from its initial state to the junction), scored only when
+    // the caller wants costs.  Lanes past n run it on zero parameters and
+    // discard the result, so a band warp stays whole for its reductions.
+    const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w,
+                                     SubKind<SUB>::kTable ? sw.tg.tgrid : nullptr);
+    double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
+    bool fin_w;
+    if (costs) {
+        ScoreSink<FAM, MET> score(w, sw.obs, sw.robs, sw.flag);  // starts from the day-0 contribution
+        integrate_days<SUB>(p, w, sw.tg, S, I, R, D, score);
+        fin_w = all_finite(S, I, R, D);
+        if (live) costs[k] = score.finish(fin_w);
+    } else {
+        NullSink none;
+        integrate_days<SUB>(p, w, sw.tg, S, I, R, D, none);
+        fin_w = all_finite(S, I, R, D);
+    }
+    // forecast_extension re-checks the junction through integrate_euler's
+    // isfinite(init.total()) (model.cpp:83); it throws NonFiniteError for a
+    // non-finite junction or forecast (calibration.cpp:301-303, 318-320).
+    const bool fin_j = fin_w && isfinite(dadd(dadd(dadd(S, I), R), D));
+    // Forecast: fwin carries n_days = horizon + 1 and the same N, h,
+    // substeps; held parameters never enter the ramp, so no time table is read.
+    const Particle held = make_particle(x[1], x[1], 0.0, 0.0, x[4], x[5], fwin);
+    const TimeGrid ftg{nullptr, sw.tg.subh};
+    if (!days) {
+        if (!live) return;
+        if (!fin_j) {
+            for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
+            return;
+        }
+        drow[0] = D;
+        ForecastDSink fs{drow, dstride};
+        integrate_days<SUB>(held, fwin, ftg, S, I, R, D, fs);
+        if (!all_finite(S, I, R, D)) {  // calibration.cpp:318-320
+            for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
+        }
+        return;
+    }
+    // Band path with the selection's first pass fused (horizon < 32): every
+    // lane runs the forecast, the warp reduces each day's key range as the
+    // day arrives, and the finite rows are counted at the end (a row is all
+    // finite or all NaN: non-finiteness is absorbing, model.cpp:101-104).
+    BandDSink bs{drow, dstride, live && fin_j, 0xFFFFFFFFu, 0u, s_pbase, s_pshift, hist, days};
+    bs.put(0, D);
+    integrate_days<SUB>(held, fwin, ftg, S, I, R, D, bs);
+    const bool row_ok = bs.on && all_finite(S, I, R, D);
+    if (bs.on && !row_ok) {  // blew up after some finite days: take them back out of the histograms
+        for (int d = 0; d <= horizon; ++d) {
+            const double v = drow[d * dstride];
+            if (isfinite(v)) bs.count(d, order_key(v), -1);
+        }
+    }
+    if (live && !row_ok) {  // a non-finite junction or forecast: the whole row NaN
+        for (int d = 0; d <= horizon; ++d) drow[d * dstride] = nan;
+    }
+    const unsigned n_ok = __popc(__ballot_sync(0xFFFFFFFFu, row_ok));
+    const int lane = threadIdx.x & 31;
+    if (lane <= horizon && bs.lo <= bs.hi) {
+        atomicMin(&days[lane].kmin, static_cast<unsigned long long>(bs.lo) << 32);
+        atomicMax(&days[lane].kmax, (static_cast<unsigned long long>(bs.hi) << 32) | 0xFFFFFFFFull);
+    }
+    if (lane <= horizon && n_ok) atomicAdd(&days[lane].count, static_cast<unsigned long long>(n_ok));
 }
 
 #ifndef SG_FAMILY_TU  // engine.cu only
 __device__ __constant__ double kBandProbs[kBandP] = {0.5, 0.25, 0.75, 0.05, 0.95, 0.025, 0.975};  // 352-358
 
-__device__ __forceinline__ int sel_shift(unsigned long long range) {
-    const int bits = range ? 64 - __clzll(static_cast<long long>(range)) : 0;
-    return bits > kSelBinBits ? bits - kSelBinBits : 0;
-}
 
 // The ranks quantile_sorted reads for k finite values (calibration.cpp:324-335).
 __device__ __forceinline__ int band_ranks(uint64_t k, uint64_t* ranks) {
@@ -1176,7 +1267,7 @@ __device__ __forceinline__ int band_ranks(uint64_t k, uint64_t* ranks) {
 // k and the key range of every day of a given plane (grid: chunks x days) —
 // the ensemble kernel's fused epilogue as a kernel of its own, for bands of
 // values that come from elsewhere (sg_quantile_bands).
-__global__ void sel_range_kernel(const double* __restrict__ col, size_t n, SelDay* __restrict__ days) {
+__global__ void __launch_bounds__(kSampleThreads) sel_range_kernel(const double* __restrict__ col, size_t n, SelDay* __restrict__ days) {
     const int d = blockIdx.y;
     const double* c = col + static_cast<size_t>(d) * n;
     unsigned long long lo = ~0ULL, hi = 0, cnt = 0;
@@ -1204,25 +1295,33 @@ __global__ void sel_range_kernel(const double* __restrict__ col, size_t n, SelDa
     }
 }
 
-// Histogram of every day's finite values over its bins: per CTA in shared
-// memory, then one global add per non-empty bin.
-__global__ void __launch_bounds__(1024) sel_hist_kernel(const double* __restrict__ col, size_t n,
-                                                        const SelDay* __restrict__ days,
-                                                        unsigned int* __restrict__ hist) {
+// Histogram pass over the plane for the days that need it (no prediction,
+// or a wanted rank outside the predicted bins: SelDay::full), over the
+// day's key range: per CTA in shared memory, then one global add per
+// non-empty bin.
+__global__ void __launch_bounds__(kHistThreads) sel_hist_kernel(const double* __restrict__ col, size_t n,
+                                             const SelDay* __restrict__ days, unsigned int* __restrict__ hist) {
     __shared__ unsigned int sh[kSelBins];
     const int d = blockIdx.y;
     const SelDay& sd = days[d];
-    if (sd.count == 0) return;
+    if (sd.count == 0 || !sd.full) return;
     for (int b = threadIdx.x; b < kSelBins; b += blockDim.x) sh[b] = 0;
     __syncthreads();
-    const int shift = sel_shift(sd.kmax - sd.kmin);
-    const unsigned long long kmin = sd.kmin;
+    const int shift = sd.shift;
+    const unsigned long long base = sd.base;
     const double* c = col + static_cast<size_t>(d) * n;
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const double x = c[i];
-        if (!isfinite(x)) continue;
-        atomicAdd(&sh[static_cast<unsigned>((order_key(x) - kmin) >> shift)], 1u);
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    constexpr int kBatch = 8;  // loads in flight per thread
+    for (size_t i0 = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i0 < n; i0 += kBatch * stride) {
+        double xs[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            const size_t i = i0 + u * stride;
+            xs[u] = i < n ? c[i] : __longlong_as_double(0x7FF8000000000000LL);
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u)
+            if (isfinite(xs[u])) atomicAdd(&sh[static_cast<unsigned>((order_key(xs[u]) - base) >> shift)], 1u);
     }
     __syncthreads();
     unsigned int* h = hist + static_cast<size_t>(d) * kSelBins;
@@ -1230,28 +1329,34 @@ __global__ void __launch_bounds__(1024) sel_hist_kernel(const double* __restrict
         if (sh[b]) atomicAdd(&h[b], sh[b]);
 }
 
-// One CTA (1024 threads) per day: exclusive scan of the bins, then the bins
-// holding the wanted ranks (deduplicated, ascending) and their rank offsets.
-__global__ void __launch_bounds__(1024) sel_locate_kernel(const unsigned int* __restrict__ hist,
-                                                          SelDay* __restrict__ days) {
+// One CTA per day: the bins holding the wanted ranks (deduplicated,
+// ascending) and their rank offsets, from the day's histogram, which is
+// left zero for the slot's next window.
+//   pass 0: the fused histogram over the predicted bins, when every wanted
+//           rank falls inside them (the counts outside come first: `under`);
+//           else the day is marked for the histogram pass (full = 1) over
+//           its key range;
+//   pass 1: the days marked full, from the pass's histogram.
+__global__ void __launch_bounds__(kBgThreads) sel_locate_kernel(unsigned int* __restrict__ hist, SelDay* __restrict__ days,
+                                               int pass, unsigned long long* __restrict__ stats) {
+    constexpr int kPer = kSelBins / kBgThreads;
+    constexpr int kWarps = kBgThreads / 32;
     const int d = blockIdx.x;
     SelDay& sd = days[d];
     const unsigned long long k = sd.count;
-    if (threadIdx.x == 0) {
-        sd.shift = sel_shift(sd.kmax - sd.kmin);
-        sd.n_seg = 0;
+    if (k == 0 || (pass == 1 && !sd.full)) {
+        if (threadIdx.x == 0 && k == 0) sd.n_seg = 0;
+        return;
     }
-    if (k == 0) return;
-    const unsigned int* h = hist + static_cast<size_t>(d) * kSelBins;
-    constexpr int kPer = kSelBins / 1024;
-    uint32_t mine = 0;
-    for (int j = 0; j < kPer; ++j) mine += h[threadIdx.x * kPer + j];
-    __shared__ uint32_t warp_sum[32];
+    unsigned int* h = hist + static_cast<size_t>(d) * kSelBins;
+    __shared__ uint32_t warp_sum[kWarps];
     __shared__ uint64_t ranks[kBandRanks];
-    __shared__ int n_ranks;
+    __shared__ int n_ranks, s_ok;
     __shared__ uint32_t bins[kBandRanks];
     __shared__ uint64_t bin_rank0[kBandRanks];
     __shared__ uint32_t bin_count[kBandRanks];
+    uint32_t mine = 0;
+    for (int j = 0; j < kPer; ++j) mine += h[threadIdx.x * kPer + j];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t incl = mine;
 #pragma unroll
@@ -1260,38 +1365,59 @@ __global__ void __launch_bounds__(1024) sel_locate_kernel(const unsigned int* __
         if (lane >= off) incl += o;
     }
     if (lane == 31) warp_sum[warp] = incl;
+    const unsigned long long under = pass == 0 ? sd.under : 0ULL;
     if (threadIdx.x == 0) n_ranks = band_ranks(k, ranks);
     __syncthreads();
-    if (warp == 0) {
-        uint32_t w = warp_sum[lane];
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, w, off);
-            if (lane >= off) w += o;
+    uint64_t base = under + (incl - mine);  // values before this thread's bins
+    uint64_t in_bins = 0;
+    for (int w = 0; w < kWarps; ++w) {
+        if (w < warp) base += warp_sum[w];
+        in_bins += warp_sum[w];
+    }
+    if (threadIdx.x == 0) {
+        bool ok = true;
+        if (pass == 0) {
+            // the prediction holds when it counted every finite value and
+            // every wanted rank lies inside its bins
+            ok = sd.pshift >= 0 && under + in_bins + sd.over == k;
+            for (int r = 0; r < n_ranks && ok; ++r) ok = ranks[r] >= under && ranks[r] < under + in_bins;
         }
-        warp_sum[lane] = w - warp_sum[lane];  // exclusive over warps
+        s_ok = ok;
+        if (pass == 0 && stats) atomicAdd(&stats[ok ? 0 : 1], 1ULL);
+        if (!ok) {  // the histogram pass over the day's key range
+            sd.full = 1;
+            sd.base = sd.kmin;
+            sd.shift = sel_shift(sd.kmax - sd.kmin);
+            sd.n_seg = 0;
+        } else if (pass == 0) {
+            sd.base = sd.pbase;
+            sd.shift = sd.pshift;
+        }
     }
     __syncthreads();
-    uint64_t base = warp_sum[warp] + (incl - mine);  // values before this thread's bins
-    // the thread whose bins cover a wanted rank finds the exact bin
-    for (int r = 0; r < n_ranks; ++r) {
-        const uint64_t want = ranks[r];
-        if (want >= base && want < base + mine) {
-            uint64_t acc = base;
-            for (int j = 0; j < kPer; ++j) {
-                const uint32_t c = h[threadIdx.x * kPer + j];
-                if (want < acc + c) {
-                    bins[r] = threadIdx.x * kPer + j;
-                    bin_rank0[r] = acc;
-                    bin_count[r] = c;
-                    break;
+    if (s_ok) {
+        // the thread whose bins cover a wanted rank finds the exact bin
+        for (int r = 0; r < n_ranks; ++r) {
+            const uint64_t want = ranks[r];
+            if (want >= base && want < base + mine) {
+                uint64_t acc = base;
+                for (int j = 0; j < kPer; ++j) {
+                    const uint32_t c = h[threadIdx.x * kPer + j];
+                    if (want < acc + c) {
+                        bins[r] = threadIdx.x * kPer + j;
+                        bin_rank0[r] = acc;
+                        bin_count[r] = c;
+                        break;
+                    }
+                    acc += c;
                 }
-                acc += c;
             }
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    // the day's histogram is consumed: leave it zero for the pass / the next window
+    for (int j = 0; j < kPer; ++j) h[threadIdx.x * kPer + j] = 0;
+    if (threadIdx.x == 0 && s_ok) {
         // distinct bins in ascending order (ranks were produced unordered)
         int ns = 0;
         for (int r = 0; r < n_ranks; ++r) {
@@ -1317,7 +1443,7 @@ __global__ void __launch_bounds__(1024) sel_locate_kernel(const unsigned int* __
 // Copy the values of the wanted bins into their segments (a shared-memory
 // bin -> segment table, warp-aggregated slot reservation).  Segment j of day
 // d occupies cand[d*n + sum of the earlier segments' counts ...].
-__global__ void __launch_bounds__(256) sel_gather_kernel(const double* __restrict__ col, size_t n,
+__global__ void __launch_bounds__(kSampleThreads) sel_gather_kernel(const double* __restrict__ col, size_t n,
                                                          SelDay* __restrict__ days, double* __restrict__ cand) {
     __shared__ unsigned char seg_of[kSelBins];
     __shared__ uint64_t seg_off[kBandRanks];
@@ -1335,36 +1461,48 @@ __global__ void __launch_bounds__(256) sel_gather_kernel(const double* __restric
         }
     }
     __syncthreads();
-    const unsigned long long kmin = sd.kmin;
+    const unsigned long long kmin = sd.base;
     const int shift = sd.shift;
     const double* c = col + static_cast<size_t>(d) * n;
     double* out = cand + static_cast<size_t>(d) * n;
     const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
     const size_t end = (n + stride - 1) / stride * stride;  // whole warps iterate together
     const unsigned lane = threadIdx.x & 31;
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < end; i += stride) {
-        const double x = i < n ? c[i] : __longlong_as_double(0x7FF8000000000000LL);
-        int seg = -1;
-        if (isfinite(x)) {
-            const unsigned char j = seg_of[static_cast<uint32_t>((order_key(x) - kmin) >> shift)];
-            if (j != 0xFF) seg = j;
+    constexpr int kBatch = 8;  // loads in flight per thread (one CTA per SM: latency needs ILP)
+    for (size_t i0 = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i0 < end; i0 += kBatch * stride) {
+        double xs[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            const size_t i = i0 + u * stride;
+            xs[u] = i < n ? c[i] : __longlong_as_double(0x7FF8000000000000LL);
         }
-        const unsigned want = __ballot_sync(0xFFFFFFFFu, seg >= 0);
-        if (want == 0) continue;
-        const unsigned peers = __match_any_sync(0xFFFFFFFFu, seg);
-        if (seg < 0) continue;
-        const int leader = __ffs(peers) - 1;
-        uint32_t base = 0;
-        if (static_cast<int>(lane) == leader) base = atomicAdd(&sd.seg_fill[seg], static_cast<unsigned>(__popc(peers)));
-        base = __shfl_sync(peers, base, leader);
-        SG_CHECK(base + __popc(peers & ((1u << lane) - 1u)) < sd.seg_count[seg]);
-        out[seg_off[seg] + base + __popc(peers & ((1u << lane) - 1u))] = x;
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            const double x = xs[u];
+            int seg = -1;
+            const unsigned long long key = order_key(x);
+            // finite and inside the bins (predicted bins need not cover every value)
+            if (isfinite(x) && key >= kmin && ((key - kmin) >> shift) < static_cast<unsigned long long>(kSelBins)) {
+                const unsigned char j = seg_of[static_cast<uint32_t>((key - kmin) >> shift)];
+                if (j != 0xFF) seg = j;
+            }
+            const unsigned want = __ballot_sync(0xFFFFFFFFu, seg >= 0);
+            if (want == 0) continue;
+            const unsigned peers = __match_any_sync(0xFFFFFFFFu, seg);
+            if (seg < 0) continue;
+            const int leader = __ffs(peers) - 1;
+            uint32_t base = 0;
+            if (static_cast<int>(lane) == leader)
+                base = atomicAdd(&sd.seg_fill[seg], static_cast<unsigned>(__popc(peers)));
+            base = __shfl_sync(peers, base, leader);
+            SG_CHECK(base + __popc(peers & ((1u << lane) - 1u)) < sd.seg_count[seg]);
+            out[seg_off[seg] + base + __popc(peers & ((1u << lane) - 1u))] = x;
+        }
     }
 }
 
 // ---- the wanted ranks of each gathered bin, one CTA per (day, bin) -----------------
 constexpr int kSelDirect = 512;        // values ranked directly (all pairs) in shared memory
-constexpr int kSelFinishThreads = 256;
 
 // Exclusive prefix sum of one value per thread over the CTA (<= 1024 threads).
 __device__ __forceinline__ uint32_t block_exclusive_sum(uint32_t v) {
@@ -1512,23 +1650,12 @@ __device__ void select_in_bin(const double* src, uint32_t count, unsigned long l
     }
 }
 
-// One CTA per (gathered bin, day): the bin's wanted ranks.  vals: 14 per day,
-// indexed like band_ranks().  scratch: 2 x n doubles per day (only touched by
-// bins that need more than one finer level outside shared memory).
-__global__ void __launch_bounds__(kSelFinishThreads) sel_finish_kernel(const SelDay* __restrict__ days,
-                                                                        const double* __restrict__ cand,
-                                                                        double* __restrict__ scratch, size_t n,
-                                                                        double* __restrict__ vals) {
-    __shared__ unsigned long long keys[kSelDirect];
-    __shared__ unsigned int hist[kSelBins];
-    __shared__ uint64_t ranks[kBandRanks];
-    __shared__ uint32_t want[kBandRanks];
-    __shared__ double* outp[kBandRanks];
-    __shared__ int n_ranks, n_want;
-    const int d = blockIdx.y;
-    const int j = blockIdx.x;
-    const SelDay& sd = days[d];
-    if (sd.count == 0 || j >= sd.n_seg) return;
+// Segment j (a gathered bin) of day d: its wanted ranks, resolved in shared
+// memory (CTA-uniform).
+__device__ void finish_segment(const SelDay& sd, int d, int j, const double* __restrict__ cand,
+                               double* __restrict__ scratch, size_t n, double* __restrict__ vals,
+                               unsigned long long* keys, unsigned int* hist, uint64_t* ranks, uint32_t* want,
+                               double** outp, int& n_ranks, int& n_want) {
     const uint32_t cnt = sd.seg_count[j];
     const uint64_t r0 = sd.seg_rank0[j];
     if (threadIdx.x == 0) {
@@ -1559,7 +1686,7 @@ __global__ void __launch_bounds__(kSelFinishThreads) sel_finish_kernel(const Sel
     // the scratch pair of this bin: 2 x cnt doubles of the day's 2 x n (the
     // CTAs of one day's bins run concurrently)
     double* sa = scratch + static_cast<size_t>(d) * 2 * n + 2 * off;
-    const unsigned long long base = sd.kmin + (static_cast<unsigned long long>(sd.seg_bin[j]) << sd.shift);
+    const unsigned long long base = sd.base + (static_cast<unsigned long long>(sd.seg_bin[j]) << sd.shift);
     // each wanted rank is resolved by the group that starts at it (ranks
     // split off inside select_in_bin are picked up by their own pass here)
     for (int t = 0; t < n_want; ++t) {
@@ -1569,9 +1696,32 @@ __global__ void __launch_bounds__(kSelFinishThreads) sel_finish_kernel(const Sel
     }
 }
 
+// One CTA per (gathered bin, day): the bin's wanted ranks.  vals: 14 per day,
+// indexed like band_ranks().  scratch: 2 x n doubles per day (only touched by
+// bins that need more than one finer level outside shared memory).
+__global__ void __launch_bounds__(kSampleThreads) sel_finish_kernel(int n_days, const SelDay* __restrict__ days,
+                                                                        const double* __restrict__ cand,
+                                                                        double* __restrict__ scratch, size_t n,
+                                                                        double* __restrict__ vals) {
+    __shared__ unsigned long long keys[kSelDirect];
+    __shared__ unsigned int hist[kSelBins];
+    __shared__ uint64_t ranks[kBandRanks];
+    __shared__ uint32_t want[kBandRanks];
+    __shared__ double* outp[kBandRanks];
+    __shared__ int n_ranks, n_want;
+    for (int pair = blockIdx.x; pair < kBandRanks * n_days; pair += gridDim.x) {
+        const int d = pair / kBandRanks;
+        const int j = pair - d * kBandRanks;
+        const SelDay& sd = days[d];
+        if (sd.count == 0 || j >= sd.n_seg) continue;  // CTA-uniform
+        finish_segment(sd, d, j, cand, scratch, n, vals, keys, hist, ranks, want, outp, n_ranks, n_want);
+        __syncthreads();  // the shared arrays are reused by the next pair
+    }
+}
+
 // quantile_sorted (calibration.cpp:324-335) of every day from its resolved
 // order statistics, with the reference's operation order.
-__global__ void sel_bands_kernel(const SelDay* __restrict__ days, const double* __restrict__ vals,
+__global__ void __launch_bounds__(kBgThreads) sel_bands_kernel(const SelDay* __restrict__ days, const double* __restrict__ vals,
                                  double* __restrict__ bands, unsigned long long* __restrict__ counts, int n_days) {
     const int d = blockIdx.x * blockDim.x + threadIdx.x;
     if (d >= n_days) return;

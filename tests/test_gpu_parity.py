@@ -316,6 +316,30 @@ def test_ensemble_bands_batch_equals_per_window_calls(ctx, poland):
         assert_bitwise(bands[k].ravel(), b1.ravel(), f"window {k}")
 
 
+def test_ensemble_bands_batch_prediction_hits_and_misses(ctx, poland):
+    """The pipelined call predicts each window's histogram bins from the
+    window two back (the same slot); windows whose deaths scale jumps
+    (populations 1e3x apart) miss and take the histogram pass, repeated
+    windows hit.  Both paths give each window its single-window bands."""
+    import paper_2204_12346_b200 as eng
+    N = poland["N"]
+    wins = []
+    for a, scale in ((0, 1.0), (3, 1.0), (6, 1e3), (9, 1e3), (12, 1.0), (12, 1.0), (12, 1.0), (15, 1e-3)):
+        I, R, D = (poland[c][a:a + 36] * scale for c in "IRD")
+        Ns = N * scale
+        wins.append(eng.Window(ctx, I, R, D, [Ns - I[0] - R[0] - D[0], I[0], R[0], D[0]], Ns, "ird-mxse"))
+    lo, hi = [0.0] * 6, [2.0, 2.0, 28.0, 28.0, 1.0, 0.1]
+    seeds = [21, 22, 23, 24, 25, 26, 27, 28]
+    f0, p0 = ctx.band_stats
+    bands, counts = ctx.forecast_ensemble_bands_batch(wins, lo, hi, seeds, 40_000, 21)
+    f1, p1 = ctx.band_stats
+    assert f1 - f0 > 0 and p1 - p0 > 0, (f1 - f0, p1 - p0)
+    for k, w in enumerate(wins):
+        b1, c1, _ = w.forecast_ensemble_bands(lo, hi, seeds[k], 40_000, 21)
+        assert counts[k].tolist() == c1.tolist()
+        assert_bitwise(bands[k].ravel(), b1.ravel(), f"window {k}")
+
+
 @pytest.mark.parametrize("case", ["cluster_outliers", "two_clusters", "spiky_key_range", "nan_mix", "constant",
                                   "tiny_counts"])
 def test_quantile_bands_selection_paths(ctx, reference, case):
