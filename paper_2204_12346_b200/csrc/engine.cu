@@ -1102,7 +1102,8 @@ static int order_step(const double upper[6]) {
 
 // Ramp-coherent evaluation order of an ensemble: ens_sample_kernel draws
 // every sample into SoA planes with its (day t1, day t2) key and counts the
-// keys; a scan and a scatter complete the counting sort into perm.
+// keys (ranking each sample within its key); a scan and an atomic-free
+// scatter complete the counting sort into perm.
 // key_count: 2 x kOrderKeys, the counts zero on entry (and again on exit).
 static int ensemble_order(sg_ctx* ctx, const double* d_lo, const double* d_hi, uint64_t seed, size_t n, int q,
                           double* planes, uint32_t* keys, unsigned int* key_count, uint32_t* perm, cudaStream_t st) {
@@ -1144,7 +1145,7 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
         uint32_t* keys;
         unsigned int* key_count;
         SG_CUDA(ctx, b.alloc(&planes, 6 * n));
-        SG_CUDA(ctx, b.alloc(&keys, n));
+        SG_CUDA(ctx, b.alloc(&keys, 2 * n));
         SG_CUDA(ctx, b.alloc(&perm, n));
         SG_CUDA(ctx, b.alloc(&key_count, 2 * kOrderKeys));
         SG_CUDA(ctx, cudaMemsetAsync(key_count, 0, sizeof(unsigned int) * kOrderKeys, ctx->stream));
@@ -1174,6 +1175,7 @@ struct BandSlot {
     uint32_t *keys = nullptr, *perm = nullptr;
     unsigned int *key_count = nullptr, *hist = nullptr;
     SelDay* days = nullptr;
+    bool unordered = false;  // SG_BAND_ORDER=0 (diagnostic)
 };
 
 // The key range of the band selection comes from a separate pass over the
@@ -1206,7 +1208,7 @@ static bool fused_hist() {
 static int alloc_band_slot(sg_ctx* ctx, DevBufs& b, BandSlot& s, size_t n, int n_days) {
     const size_t nd = n * static_cast<size_t>(n_days);
     SG_CUDA(ctx, b.alloc(&s.planes, 6 * n));
-    SG_CUDA(ctx, b.alloc(&s.keys, n));
+    SG_CUDA(ctx, b.alloc(&s.keys, 2 * n));  // key, rank within the key
     SG_CUDA(ctx, b.alloc(&s.perm, n));
     SG_CUDA(ctx, b.alloc(&s.key_count, 2 * kOrderKeys));
     SG_CUDA(ctx, b.alloc(&s.D, nd));
@@ -1226,8 +1228,15 @@ static int alloc_band_slot(sg_ctx* ctx, DevBufs& b, BandSlot& s, size_t n, int n
 // the slot's day records reset for the selection.
 static int enqueue_band_order(sg_ctx* ctx, BandSlot& s, cudaStream_t st, const double* d_lo, const double* d_hi,
                               uint64_t seed, size_t n, int q, int n_days) {
-    if (const int rc = ensemble_order(ctx, d_lo, d_hi, seed, n, q, s.planes, s.keys, s.key_count, s.perm, st))
-        return rc;
+    static const bool ordered = [] {  // SG_BAND_ORDER=0: samples drawn in the ensemble kernel, unordered (A/B)
+        const char* e = std::getenv("SG_BAND_ORDER");
+        return !(e && e[0] == '0');
+    }();
+    if (ordered) {
+        if (const int rc = ensemble_order(ctx, d_lo, d_hi, seed, n, q, s.planes, s.keys, s.key_count, s.perm, st))
+            return rc;
+    }
+    s.unordered = !ordered;
     sel_init_kernel<<<static_cast<unsigned>((n_days + kBgThreads - 1) / kBgThreads), kBgThreads, 0, st>>>(
         s.days, n_days, fused_range(n_days - 1) && fused_hist() ? 1 : 0);
     ctx->launches += 1;
@@ -1246,7 +1255,8 @@ static int enqueue_band_eval(sg_ctx* ctx, sg_window* w, BandSlot& s, cudaStream_
     // day-major columns in evaluation order: the bands only need each day's multiset
     dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc,
                              fwin, d_lo, d_hi, seed, n, horizon, d_cost, static_cast<double*>(nullptr), s.D, size_t(1),
-                             n, s.perm, s.planes, 1, fused_range(horizon) ? s.days : nullptr, s.hist, w->smem, st, &err);
+                             n, s.unordered ? nullptr : s.perm, s.unordered ? nullptr : s.planes, 1, fused_range(horizon) ? s.days : nullptr,
+                             s.hist, w->smem, st, &err);
     ctx->launches += 1;
     if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
     return SG_OK;

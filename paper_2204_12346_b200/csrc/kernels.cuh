@@ -973,8 +973,9 @@ constexpr int kSampleThreads = 256;   // ens_sample / ens_scatter / sel_range / 
 constexpr int kHistThreads = 1024;    // sel_hist (a CTA histogram in shared memory)
 
 // Evaluation order of an ensemble: every sample's parameters into SoA
-// planes and a key (day of t1, day of t2, each in steps of `q` days and
-// capped at 63) — samples with equal keys ramp on the same days, so
+// planes, keys[k] = a key (day of t1, day of t2, each in steps of `q` days and
+// capped at 63) and keys[n + k] = its rank among the samples of that key —
+// samples with equal keys ramp on the same days, so
 // grouping them makes a warp's lanes ramp together (the warp pays a ramp
 // substep if any lane ramps).  The order never changes a result: every
 // sample is evaluated by the same code into its own slot, and the bands
@@ -995,7 +996,7 @@ __global__ void __launch_bounds__(kSampleThreads) ens_sample_kernel(const double
         for (int d = 0; d < 6; ++d) planes[d * n + k] = x[d];
         const uint32_t key = (min(day(x[2]), 63u) << 6) | min(day(x[3]), 63u);
         keys[k] = key;
-        atomicAdd(&key_count[key], 1u);
+        keys[n + k] = atomicAdd(&key_count[key], 1u);  // the sample's rank within its key
     }
 }
 
@@ -1038,12 +1039,14 @@ __global__ void __launch_bounds__(kBgThreads) ens_scan_kernel(unsigned int* __re
     }
 }
 
-// Counting-sort scatter: sample k takes the next slot of its key's bucket.
+// Counting-sort scatter: sample k goes to its key's bucket start plus its
+// rank within the key (taken by ens_sample_kernel's count), no atomics.
 __global__ void __launch_bounds__(kSampleThreads) ens_scatter_kernel(const uint32_t* __restrict__ keys, size_t n,
-                                                unsigned int* __restrict__ cursor, uint32_t* __restrict__ perm) {
+                                                const unsigned int* __restrict__ cursor,
+                                                uint32_t* __restrict__ perm) {
     for (size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
          k += static_cast<size_t>(gridDim.x) * blockDim.x)
-        perm[atomicAdd(&cursor[keys[k]], 1u)] = static_cast<uint32_t>(k);
+        perm[cursor[keys[k]] + keys[n + k]] = static_cast<uint32_t>(k);
 }
 
 // Reset a slot's day records for its next window; with `predict`, each
