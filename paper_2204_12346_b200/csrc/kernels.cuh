@@ -1690,13 +1690,36 @@ __device__ void finish_segment(const SelDay& sd, int d, int j, const double* __r
     // CTAs of one day's bins run concurrently)
     double* sa = scratch + static_cast<size_t>(d) * 2 * n + 2 * off;
     const unsigned long long base = sd.base + (static_cast<unsigned long long>(sd.seg_bin[j]) << sd.shift);
-    // each wanted rank is resolved by the group that starts at it (ranks
-    // split off inside select_in_bin are picked up by their own pass here)
-    for (int t = 0; t < n_want; ++t) {
-        const uint32_t w1 = want[t];
-        double* o1 = outp[t];
-        select_in_bin(src, cnt, base, sd.shift, &w1, 1, &o1, sa, sa + cnt, keys, hist);
+    // All the segment's wanted ranks in one pass (ascending: the first picks
+    // each level's sub-bin); a rank that leaves the group's sub-bin (rare:
+    // lo and lo+1 straddling a sub-bin boundary) stays unresolved and goes
+    // to the next pass.  Results are staged in shared memory with a NaN
+    // sentinel (a selected value is always finite).
+    constexpr long long kUnresolved = 0x7FF8DEADBEEF0001LL;
+    __shared__ double res[kBandRanks];
+    __shared__ uint32_t left_want[kBandRanks];
+    __shared__ double* left_out[kBandRanks];
+    __shared__ int n_left;
+    if (threadIdx.x == 0)
+        for (int t = 0; t < n_want; ++t) res[t] = __longlong_as_double(kUnresolved);
+    while (true) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int m = 0;
+            for (int t = 0; t < n_want; ++t) {
+                if (__double_as_longlong(res[t]) != kUnresolved) continue;
+                left_want[m] = want[t];
+                left_out[m] = &res[t];
+                ++m;
+            }
+            n_left = m;
+        }
+        __syncthreads();
+        if (n_left == 0) break;
+        select_in_bin(src, cnt, base, sd.shift, left_want, n_left, left_out, sa, sa + cnt, keys, hist);
     }
+    if (threadIdx.x == 0)
+        for (int t = 0; t < n_want; ++t) *outp[t] = res[t];
 }
 
 // One CTA per (gathered bin, day): the bin's wanted ranks.  vals: 14 per day,
