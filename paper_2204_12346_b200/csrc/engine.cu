@@ -1178,14 +1178,10 @@ struct BandSlot {
     bool unordered = false;  // SG_BAND_ORDER=0 (diagnostic)
 };
 
-// The key range of the band selection comes from a separate pass over the
-// deaths plane on the selection stream (default), or from the ensemble
-// kernel's epilogue with SG_FUSED_RANGE=1 (diagnostic A/B).  Measured, 139
-// windows: 187.9 ms separate vs 194.1 ms fused — the epilogue adds ~63 us
-// to every FP64-bound evaluation (profiles/r02h_c5_*), the separate pass
-// overlaps it on the other stream.
 // The ensemble kernel reduces each day's key range and finite count as the
-// forecast runs (lane d of a warp holds day d, so horizon < 32);
+// forecast runs (lane d of a warp holds day d, so horizon < 32: REDUX per
+// day, no barrier, no re-read of the plane — an earlier epilogue version that
+// re-read the row and folded per CTA cost ~63 us per evaluation);
 // SG_FUSED_RANGE=0 runs sel_range_kernel over the plane instead (A/B).
 static bool fused_range(int horizon) {
     static const bool on = [] {
@@ -1392,13 +1388,17 @@ static int ensure_band_streams(sg_ctx* ctx) {
     int least = 0, greatest = 0;
     SG_CUDA(ctx, cudaDeviceGetStreamPriorityRange(&least, &greatest));
     // SG_BAND_PRIO (diagnostic A/B): priority of the selection stream
-    // relative to the evaluation stream: high (default; 187.9 ms for the
-    // 139-window C5 vs 217.3 equal or low), equal or low
+    // relative to the evaluation streams: high (default), equal or low.  At
+    // low priority the selection's grids are dispatched only once an
+    // evaluation grid has no CTAs left to place, so the evaluations stall on
+    // the ordering (round 2: 217 ms vs 188 ms high; 213-268 ms with the
+    // selection kernels cut to fit beside the ensemble's CTAs)
     static const char* prio = std::getenv("SG_BAND_PRIO");
     const std::string p = prio ? prio : "high";
     const int eval_prio = p == "low" ? greatest : least;
     const int sel_prio = p == "high" ? greatest : least;
-    for (cudaStream_t& e : ctx->band_eval) SG_CUDA(ctx, cudaStreamCreateWithPriority(&e, cudaStreamNonBlocking, eval_prio));
+    for (cudaStream_t& e : ctx->band_eval)
+        SG_CUDA(ctx, cudaStreamCreateWithPriority(&e, cudaStreamNonBlocking, eval_prio));
     SG_CUDA(ctx, cudaStreamCreateWithPriority(&ctx->band_sel, cudaStreamNonBlocking, sel_prio));
     return SG_OK;
 }
