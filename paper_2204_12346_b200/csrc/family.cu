@@ -24,3 +24,9 @@ extern "C" int SG_CAT(sg_day_classes_u, SG_UNIT)(unsigned long long* out3) {
     return 0;
 }
 #endif
+
+#if SG_C1_PROBE && SG_FAMILY == 1 && SG_SUB == 24
+extern "C" int sg_c1_probe(unsigned long long* out) {
+    return static_cast<int>(cudaMemcpyFromSymbol(out, sirdgpu::g_c1, sizeof(sirdgpu::g_c1)));
+}
+#endif

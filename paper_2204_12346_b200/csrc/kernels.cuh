@@ -699,6 +699,21 @@ constexpr int kSwarmThreadsMax = 128;
 constexpr int kSwarmClusterMax = 8;
 constexpr int kPersistMax = kSwarmThreadsMax * kSwarmClusterMax;  // 1024 particles per swarm
 
+#if SG_C1_PROBE
+// diagnostic build (tools/c1_probe.py): per (warp of the cluster, iteration)
+// clock64 stamps of the iteration's phases
+static __device__ unsigned long long g_c1[8][512][6];
+#define SG_C1_STAMP(k)                                                                       \
+    do {                                                                                     \
+        const unsigned gw = rank * (blockDim.x >> 5) + (threadIdx.x >> 5);                   \
+        if ((threadIdx.x & 31) == 0 && gw < 8 && it < 512) g_c1[gw][it][k] = clock64();     \
+    } while (0)
+#else
+#define SG_C1_STAMP(k) \
+    do {               \
+    } while (0)
+#endif
+
 struct SwarmPartial {
     double cost;
     unsigned long long idx;
@@ -734,6 +749,7 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 1) pso_swarm_kernel(const De
     const size_t p = sw.offset + (active ? i : 0);
     double x[6], v[6], pb[6], pbc = __longlong_as_double(0x7FF0000000000000LL), c = pbc;
     double u[12];  // the next move's draws, taken one iteration ahead
+    MtBatch<12> next;  // their engine words, loaded during the evaluation
     if (active) {
         init_particle(sw, P, p, i);
 #pragma unroll
@@ -742,7 +758,6 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 1) pso_swarm_kernel(const De
             v[d] = 0.0;
             pb[d] = x[d];
         }
-        if (sw.max_iters > 1) mt_draw<12>(P.mt + pblock_base(p, kMtN), move_draw_word(1), u);
     }
     if (threadIdx.x == 0) {
         gbest_cost = __longlong_as_double(0x7FF0000000000000LL);
@@ -757,14 +772,15 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 1) pso_swarm_kernel(const De
     for (uint64_t it = 0; it < sw.max_iters; ++it) {
         double my_c = __longlong_as_double(0x7FF0000000000000LL);
         unsigned long long my_i = ~0ULL;
+        SG_C1_STAMP(0);
         if (active) {
-            if (it > 0) {
-                move_particle_regs(sw, gbest_cost, gbest, u, x, v, pb);
-                // draws of the next move, overlapped with this evaluation
-                if (it + 1 < sw.max_iters) mt_draw<12>(P.mt + pblock_base(p, kMtN), move_draw_word(it + 1), u);
-            }
+            if (it > 0) move_particle_regs(sw, gbest_cost, gbest, u, x, v, pb);
             int ramp = 0;
+            SG_C1_STAMP(1);
+            // the next move's engine words: loads in flight during the evaluation
+            if (it + 1 < sw.max_iters) mt_load<12>(P.mt + pblock_base(p, kMtN), move_draw_word(it + 1), next);
             c = eval_particle<FAM, MET, SUB>(x, *win.w, win.tg, win.obs, win.robs, win.flag, &ramp);
+            SG_C1_STAMP(2);
             ramp_acc += static_cast<unsigned long long>(ramp);
             if (c < pbc) {  // pso.cpp:83-89
                 pbc = c;
@@ -794,6 +810,7 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 1) pso_swarm_kernel(const De
             red_c[warp] = w_c;
             red_i[warp] = w_i;
         }
+        SG_C1_STAMP(3);
         __syncthreads();  // warp minima visible in the CTA
         SwarmPartial& mine = part[it & 1];
         if (threadIdx.x == 0) {
@@ -805,7 +822,15 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 1) pso_swarm_kernel(const De
             if (red_i[bw] != ~0ULL)
                 for (int d = 0; d < 6; ++d) mine.pos[d] = red_pos[bw][d];
         }
-        cluster.sync();  // every rank's partial of iteration `it` visible cluster-wide
+        // Every rank's partial of iteration `it` visible cluster-wide.  The
+        // barrier is split: between arrive and wait each particle twists and
+        // tempers the next move's 12 draws (the words were loaded during the
+        // evaluation), which do not depend on the global best — in the
+        // barrier's latency rather than on the iteration's critical path.
+        cluster.barrier_arrive();
+        if (active && it + 1 < sw.max_iters) mt_finish<12>(P.mt + pblock_base(p, kMtN), move_draw_word(it + 1), next, u);
+        cluster.barrier_wait();
+        SG_C1_STAMP(4);
         if (threadIdx.x == 0) {
             // Global-best scan (pso.cpp:90-96) over the ranks' partials in
             // rank order: identical in every CTA.
@@ -824,6 +849,7 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 1) pso_swarm_kernel(const De
             if (rank == 0) P.history[static_cast<size_t>(s) * P.hist_stride + it] = gbest_cost;
         }
         __syncthreads();  // global best published for the next move
+        SG_C1_STAMP(5);
     }
     if (active) {  // final particle state back to the planes
 #pragma unroll

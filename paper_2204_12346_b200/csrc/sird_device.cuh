@@ -586,14 +586,60 @@ __device__ __forceinline__ double to_uniform01(uint64_t x) {
 // it), and every "far" word lies outside the batch — so the loads are
 // independent and overlap.  Word addresses are a row pointer plus a
 // compile-time offset; the (warp-uniform) wrap past word 311 switches rows.
+// Split in two (mt_load, then mt_finish) a caller can issue the loads long
+// before it needs the values; mt_draw does both in one (its own code: the
+// step kernel's register allocation is tuned on it).
+template <int NDRAW>
+struct MtBatch {
+    uint64_t cur[NDRAW + 1];
+    uint64_t far[NDRAW];
+};
+
+template <int NDRAW>
+__device__ __forceinline__ void mt_load(const uint64_t* __restrict__ mt, int i0, MtBatch<NDRAW>& b) {
+    static_assert(NDRAW >= 1 && NDRAW < kMtM, "batch must not reach its own far words");
+    SG_CHECK(i0 >= 0 && i0 < kMtN);
+    const uint64_t* const row = mt + 32 * i0;            // word i0 + j at row[32*j] ...
+    const uint64_t* const row_w = row - 32 * kMtN;       // ... or, past word 311, at row_w[32*j]
+    const int wrap = kMtN - i0;                          // first j that wraps
+    const int f0 = i0 + kMtM < kMtN ? i0 + kMtM : i0 + kMtM - kMtN;  // far word of j = 0
+    const uint64_t* const frow = mt + 32 * f0;
+    const uint64_t* const frow_w = frow - 32 * kMtN;
+    const int fwrap = kMtN - f0;
+    if (wrap > NDRAW && fwrap >= NDRAW) {  // warp-uniform: no word of the batch wraps (24 moves in 26)
+#pragma unroll
+        for (int j = 0; j <= NDRAW; ++j) b.cur[j] = row[32 * j];
+#pragma unroll
+        for (int j = 0; j < NDRAW; ++j) b.far[j] = frow[32 * j];
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j <= NDRAW; ++j) b.cur[j] = (j < wrap ? row : row_w)[32 * j];
+#pragma unroll
+    for (int j = 0; j < NDRAW; ++j) b.far[j] = (j < fwrap ? frow : frow_w)[32 * j];
+}
+
+template <int NDRAW>
+__device__ __forceinline__ void mt_finish(uint64_t* __restrict__ mt, int i0, const MtBatch<NDRAW>& b, double* out) {
+    uint64_t* const row = mt + 32 * i0;
+    uint64_t* const row_w = row - 32 * kMtN;
+    const int wrap = kMtN - i0;
+#pragma unroll
+    for (int j = 0; j < NDRAW; ++j) {
+        const uint64_t v = mt_twist_word(b.cur[j], b.cur[j + 1], b.far[j]);
+        (j < wrap ? row : row_w)[32 * j] = v;
+        out[j] = to_uniform01(mt_temper(v));
+    }
+}
+
 template <int NDRAW>
 __device__ __forceinline__ void mt_draw(uint64_t* __restrict__ mt, int i0, double* out) {
     static_assert(NDRAW >= 1 && NDRAW < kMtM, "batch must not reach its own far words");
     SG_CHECK(i0 >= 0 && i0 < kMtN);
-    uint64_t* const row = mt + 32 * i0;            // word i0 + j at row[32*j] ...
-    uint64_t* const row_w = row - 32 * kMtN;       // ... or, past word 311, at row_w[32*j]
-    const int wrap = kMtN - i0;                    // first j that wraps
-    const int f0 = i0 + kMtM < kMtN ? i0 + kMtM : i0 + kMtM - kMtN;  // far word of j = 0
+    uint64_t* const row = mt + 32 * i0;
+    uint64_t* const row_w = row - 32 * kMtN;
+    const int wrap = kMtN - i0;
+    const int f0 = i0 + kMtM < kMtN ? i0 + kMtM : i0 + kMtM - kMtN;
     uint64_t* const frow = mt + 32 * f0;
     uint64_t* const frow_w = frow - 32 * kMtN;
     const int fwrap = kMtN - f0;
