@@ -80,11 +80,13 @@ uint64_t sg_ctx_launch_count(const sg_ctx* ctx);
  * (telemetry for bench: the e2e transfer volume, counted at every copy). */
 void sg_ctx_copy_bytes(const sg_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
 
-/* Band-selection telemetry of the context's C5 calls (cumulative): forecast
- * days whose quantiles were resolved from the ensemble kernel's fused
- * histogram (bins predicted from the slot's previous window) and days that
- * took the histogram pass over the deaths plane.  Synchronises the stream. */
-int sg_ctx_band_stats(sg_ctx* ctx, uint64_t* fused_days, uint64_t* pass_days);
+/* Band telemetry of the context's C5 calls (cumulative): forecast days
+ * whose quantiles were resolved from the ensemble kernel's fused histogram
+ * (bins predicted from the slot's previous window), days that took the
+ * histogram pass over the deaths plane, and the ramp substeps of the
+ * evaluated windows (the roofline's ramp credit, as sg_plan_ramp_substeps).
+ * Any pointer may be NULL.  Synchronises the stream. */
+int sg_ctx_band_stats(sg_ctx* ctx, uint64_t* fused_days, uint64_t* pass_days, uint64_t* ramp_substeps);
 /* Underlying cudaStream_t used by every call of this context. */
 void* sg_ctx_stream(const sg_ctx* ctx);
 

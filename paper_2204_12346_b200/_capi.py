@@ -82,7 +82,7 @@ SIGNATURES = {
     "sg_ctx_launch_count": (ctypes.c_uint64, [ctypes.c_void_p]),
     "sg_ctx_stream": (ctypes.c_void_p, [ctypes.c_void_p]),
     "sg_ctx_copy_bytes": (None, [ctypes.c_void_p, _u64p, _u64p]),
-    "sg_ctx_band_stats": (ctypes.c_int, [ctypes.c_void_p, _u64p, _u64p]),
+    "sg_ctx_band_stats": (ctypes.c_int, [ctypes.c_void_p, _u64p, _u64p, _u64p]),
     "sg_window_create": (ctypes.c_int, [ctypes.c_void_p, _dp, _dp, _dp, ctypes.c_int, sg_state, ctypes.c_double,
                                         ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
     "sg_window_destroy": (None, [ctypes.c_void_p]),
@@ -238,12 +238,13 @@ class Context:
         return int(a.value), int(b.value)
 
     @property
-    def band_stats(self) -> tuple[int, int]:
+    def band_stats(self) -> tuple[int, int, int]:
         """(days resolved from the ensemble's fused histogram, days that took
-        the histogram pass) over this context's band selections so far."""
-        a, b = ctypes.c_uint64(), ctypes.c_uint64()
-        self.check(lib().sg_ctx_band_stats(self._h, ctypes.byref(a), ctypes.byref(b)))
-        return int(a.value), int(b.value)
+        the histogram pass, ramp substeps evaluated) over this context's band
+        calls so far."""
+        a, b, c = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        self.check(lib().sg_ctx_band_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return int(a.value), int(b.value), int(c.value)
 
     @property
     def stream(self) -> int:

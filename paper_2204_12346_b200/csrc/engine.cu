@@ -206,10 +206,10 @@ void sg_ctx_copy_bytes(const sg_ctx* ctx, uint64_t* h2d, uint64_t* d2h) {
     if (d2h) *d2h = ctx ? ctx->d2h_bytes.load() : 0;
 }
 
-int sg_ctx_band_stats(sg_ctx* ctx, uint64_t* fused_days, uint64_t* pass_days) {
+int sg_ctx_band_stats(sg_ctx* ctx, uint64_t* fused_days, uint64_t* pass_days, uint64_t* ramp_substeps) {
     if (!ctx) return SG_ERR_INVALID_ARGUMENT;
     SG_ENTRY(ctx, "sg_ctx_band_stats");
-    unsigned long long v[2] = {0, 0};
+    unsigned long long v[3] = {0, 0, 0};
     if (ctx->band_stats) {
         SG_CUDA(ctx, cudaSetDevice(ctx->device));
         SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -217,6 +217,7 @@ int sg_ctx_band_stats(sg_ctx* ctx, uint64_t* fused_days, uint64_t* pass_days) {
     }
     if (fused_days) *fused_days = v[0];
     if (pass_days) *pass_days = v[1];
+    if (ramp_substeps) *ramp_substeps = v[2];
     return SG_OK;
 }
 
@@ -1157,7 +1158,8 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
     dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc,
                              fwin, d_lo, d_hi, seed, n, horizon, d_cost, d_par, d_D,
                              static_cast<size_t>(horizon + 1), size_t(1), perm, planes, 0, static_cast<SelDay*>(nullptr),
-                             static_cast<unsigned int*>(nullptr), w->smem, ctx->stream, &err);
+                             static_cast<unsigned int*>(nullptr), static_cast<unsigned long long*>(nullptr), w->smem,
+                             ctx->stream, &err);
     ctx->launches += 1;
     if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
     if (costs) SG_CUDA(ctx, copy_async(ctx, costs, d_cost, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1240,6 +1242,16 @@ static int enqueue_band_order(sg_ctx* ctx, BandSlot& s, cudaStream_t st, const d
     return SG_OK;
 }
 
+// Band telemetry (device): [0] days from the fused histogram, [1] days
+// through the histogram pass, [2] ramp substeps of the evaluated windows.
+static int ensure_band_stats(sg_ctx* ctx) {
+    if (ctx->band_stats) return SG_OK;
+    SG_CUDA(ctx, cudaMalloc(&ctx->band_stats, 3 * sizeof(unsigned long long)));
+    SG_CUDA(ctx, cudaMemsetAsync(ctx->band_stats, 0, 3 * sizeof(unsigned long long), ctx->stream));
+    SG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // once per context; zero before any stream adds to it
+    return SG_OK;
+}
+
 // C5, stage 2 (FP64-bound): evaluation of the window and forecast into the
 // slot's day-major deaths plane (with each day's key range and finite count
 // reduced in the kernel's epilogue when SG_FUSED_RANGE is on).
@@ -1247,12 +1259,13 @@ static int enqueue_band_eval(sg_ctx* ctx, sg_window* w, BandSlot& s, cudaStream_
                              const double* d_hi, uint64_t seed, size_t n, int horizon, double* d_cost) {
     const int n_days = horizon + 1;
     const DevWindow fwin = integration_window(n_days, w->host.substeps, w->host.N);
+    if (const int rc = ensure_band_stats(ctx)) return rc;
     cudaError_t err = cudaSuccess;
     // day-major columns in evaluation order: the bands only need each day's multiset
     dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc,
                              fwin, d_lo, d_hi, seed, n, horizon, d_cost, static_cast<double*>(nullptr), s.D, size_t(1),
                              n, s.unordered ? nullptr : s.perm, s.unordered ? nullptr : s.planes, 1, fused_range(horizon) ? s.days : nullptr,
-                             s.hist, w->smem, st, &err);
+                             s.hist, ctx->band_stats ? ctx->band_stats + 2 : nullptr, w->smem, st, &err);
     ctx->launches += 1;
     if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
     return SG_OK;
@@ -1264,10 +1277,7 @@ static int enqueue_band_eval(sg_ctx* ctx, sg_window* w, BandSlot& s, cudaStream_
 // and quantile_sorted turns them into the bands.
 static int enqueue_band_select(sg_ctx* ctx, BandSlot& s, cudaStream_t st, size_t n, int n_days, double* d_bands,
                                unsigned long long* d_counts, bool standalone = false) {
-    if (!ctx->band_stats) {
-        SG_CUDA(ctx, cudaMalloc(&ctx->band_stats, 2 * sizeof(unsigned long long)));
-        SG_CUDA(ctx, cudaMemset(ctx->band_stats, 0, 2 * sizeof(unsigned long long)));
-    }
+    if (const int rc = ensure_band_stats(ctx)) return rc;
     const unsigned chunks = static_cast<unsigned>(std::min<size_t>(64, (n + 4095) / 4096));
     const dim3 grid(chunks, static_cast<unsigned>(n_days));
     if (!fused_range(n_days - 1) && !standalone) {  // standalone: the caller ran it
@@ -1429,6 +1439,7 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
     SG_CUDA(ctx, cudaSetDevice(ctx->device));
     if (const int rc = ensure_lanes(ctx)) return rc;
     if (const int rc = ensure_band_streams(ctx)) return rc;
+    if (const int rc = ensure_band_stats(ctx)) return rc;
     DevBufs b;
     b.st = ctx->stream;
     double *d_lo, *d_hi, *d_bands;

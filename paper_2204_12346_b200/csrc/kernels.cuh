@@ -1165,7 +1165,8 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
                                                                 size_t dstride, const uint32_t* __restrict__ perm,
                                                                 const double* __restrict__ planes, int out_by_slot,
                                                                 SelDay* __restrict__ days,
-                                                                unsigned int* __restrict__ hist) {
+                                                                unsigned int* __restrict__ hist,
+                                                                unsigned long long* __restrict__ ramp_count) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ DevWindow sdesc;
     __shared__ unsigned long long s_pbase[32];
@@ -1213,6 +1214,10 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
     // discard the result, so a band warp stays whole for its reductions.
     const Particle p = make_particle(x[0], x[1], x[2], x[3], x[4], x[5], w,
                                      SubKind<SUB>::kTable ? sw.tg.tgrid : nullptr);
+    if (ramp_count) {  // telemetry: the window's ramp substeps (the roofline's ramp credit)
+        const unsigned wr = __reduce_add_sync(0xFFFFFFFFu, live ? static_cast<unsigned>(p.k2 - p.k1) : 0u);
+        if ((threadIdx.x & 31) == 0 && wr) atomicAdd(ramp_count, static_cast<unsigned long long>(wr));
+    }
     double S = w.init[0], I = w.init[1], R = w.init[2], D = w.init[3];
     bool fin_w;
     if (costs) {

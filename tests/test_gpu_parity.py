@@ -330,9 +330,9 @@ def test_ensemble_bands_batch_prediction_hits_and_misses(ctx, poland):
         wins.append(eng.Window(ctx, I, R, D, [Ns - I[0] - R[0] - D[0], I[0], R[0], D[0]], Ns, "ird-mxse"))
     lo, hi = [0.0] * 6, [2.0, 2.0, 28.0, 28.0, 1.0, 0.1]
     seeds = [21, 22, 23, 24, 25, 26, 27, 28]
-    f0, p0 = ctx.band_stats
+    f0, p0, _ = ctx.band_stats
     bands, counts = ctx.forecast_ensemble_bands_batch(wins, lo, hi, seeds, 40_000, 21)
-    f1, p1 = ctx.band_stats
+    f1, p1, _ = ctx.band_stats
     assert f1 - f0 > 0 and p1 - p0 > 0, (f1 - f0, p1 - p0)
     for k, w in enumerate(wins):
         b1, c1, _ = w.forecast_ensemble_bands(lo, hi, seeds[k], 40_000, 21)

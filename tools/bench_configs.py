@@ -73,6 +73,14 @@ def main():
     only = set(args.only.split(","))
     ctx = eng.Context(0)
     peak = eng.probe_fp64_rate(ctx)
+    # nominal FP64 lane-op rate (bench.py's roofline denominator): SMs x 64 x max SM clock
+    import subprocess
+    try:
+        mhz = float(subprocess.run(["nvidia-smi", "--query-gpu=clocks.max.sm", "--format=csv,noheader,nounits"],
+                                   capture_output=True, text=True, timeout=30).stdout.split()[0])
+        nominal = torch.cuda.get_device_properties(0).multi_processor_count * 64 * mhz * 1e6
+    except Exception:  # noqa: BLE001 - no nvidia-smi: the probe stands in
+        nominal = peak
 
     if "c1" in only:
         # C1
@@ -142,6 +150,7 @@ def main():
         # the same work through the pipelined many-window call (warmed once:
         # the first call grows the device pool by the pipeline's buffers)
         ctx.forecast_ensemble_bands_batch(wins[:2], [0] * 6, stage2(35), seeds[:2], n, 21)
+        ramp0 = ctx.band_stats[2]
         t0 = time.perf_counter()
         with torch.cuda.stream(stream):
             e0.record(stream)
@@ -152,12 +161,19 @@ def main():
         wall = time.perf_counter() - t0
         dev_ms = e0.elapsed_time(e1)
         assert np.array_equal(all_bands[-1], bands, equal_nan=True)
+        ramp = ctx.band_stats[2] - ramp0  # the timed call's ramp substeps (counted by the ensemble kernel)
         ops = (35 * 24 * 14 + 21 * 24 * 14)  # window + forecast substeps per sample, no ramp credit
         print(json.dumps({"config": "C5", "windows": args.c5_windows, "samples_per_window": n, "horizon": 21,
                           "device_ms": dev_ms, "wall_ms": wall * 1e3, "per_window_calls_device_ms": single_ms,
                           "per_window_calls_wall_ms": wall_single * 1e3,
                           "samples_per_s": args.c5_windows * n / (dev_ms * 1e-3),
                           "fp64_frac_floor": args.c5_windows * n * ops / (dev_ms * 1e-3) / peak,
+                          "ramp_substeps_per_sample": ramp / (args.c5_windows * n),
+                          "fp64_frac_ramp_credit": (args.c5_windows * n * ops + bench.RAMP_OPS * ramp)
+                          / (dev_ms * 1e-3) / peak,
+                          "fp64_frac_floor_nominal": args.c5_windows * n * ops / (dev_ms * 1e-3) / nominal,
+                          "fp64_frac_ramp_credit_nominal": (args.c5_windows * n * ops + bench.RAMP_OPS * ramp)
+                          / (dev_ms * 1e-3) / nominal,
                           "last_window_day21_median_deaths": float(bands[0, -1]), "finite_last": int(counts[-1])}),
               flush=True)
 
