@@ -340,6 +340,22 @@ def test_ensemble_bands_batch_prediction_hits_and_misses(ctx, poland):
         assert_bitwise(bands[k].ravel(), b1.ravel(), f"window {k}")
 
 
+def test_ensemble_ramp_telemetry_is_exact(ctx, poland):
+    """The band path's ramp-substep count (the roofline's ramp credit) is
+    exact: switch times pinned by the box (t1 = 0, t2 = 10 days) ramp on
+    10 x 24 substeps in every sample; t1 = t2 never ramps."""
+    import paper_2204_12346_b200 as eng
+    N = poland["N"]
+    I, R, D = poland["I"][:36], poland["R"][:36], poland["D"][:36]
+    win = eng.Window(ctx, I, R, D, [N - I[0] - R[0] - D[0], I[0], R[0], D[0]], N, "ird-mxse")
+    n = 5000
+    for t1, t2, want in ((0.0, 10.0, 240), (7.0, 7.0, 0)):
+        lo, hi = [0.0, 0.0, t1, t2, 0.0, 0.0], [2.0, 2.0, t1, t2, 1.0, 0.1]
+        r0 = ctx.band_stats[2]
+        ctx.forecast_ensemble_bands_batch([win, win], lo, hi, [1, 2], n, 21)
+        assert ctx.band_stats[2] - r0 == 2 * n * want, (t1, t2)
+
+
 @pytest.mark.parametrize("case", ["cluster_outliers", "two_clusters", "spiky_key_range", "nan_mix", "constant",
                                   "tiny_counts"])
 def test_quantile_bands_selection_paths(ctx, reference, case):

@@ -1,5 +1,5 @@
-"""Throughput vs window length (tau): 40 swarms x 4096 particles x 100 iterations, ird-mxse, stage2 box
-(the series' windows of that length, repeated with other seeds when there are fewer than 40)."""
+"""Throughput vs window length (tau): 40 swarms (--swarms=N) x 4096 particles x 100 iterations, ird-mxse,
+stage2 box (the series' windows of that length, repeated with other seeds when there are fewer)."""
 import sys
 from pathlib import Path
 
@@ -13,11 +13,13 @@ from tools.bench_configs import stage2, window  # noqa: E402
 def main():
     ctx = eng.Context(0)
     peak = eng.probe_fp64_rate(ctx)
-    for tau in [int(x) for x in sys.argv[1:]] or [20, 35, 60, 85, 86, 100, 150, 200]:
-        n_win = max(1, min(40, 1 + (450 - tau - 1) // bench.DELTA))
+    args = [a for a in sys.argv[1:] if not a.startswith("--swarms=")]
+    n_sw = int(next((a.split("=")[1] for a in sys.argv[1:] if a.startswith("--swarms=")), 40))
+    for tau in [int(x) for x in args] or [20, 35, 60, 85, 86, 100, 150, 200]:
+        n_win = max(1, min(n_sw, 1 + (450 - tau - 1) // bench.DELTA))
         wins = [window(ctx, w, tau) for w in range(n_win)]
         swarms = [dict(window=wins[k % n_win], lower=[0] * 6, upper=stage2(tau), n_particles=4096, max_iters=100,
-                       seed=bench.mix_seed(5, k)) for k in range(40)]
+                       seed=bench.mix_seed(5, k)) for k in range(n_sw)]
         plan = eng.Plan(ctx, swarms)
         plan.run_timed()
         s, k = plan.run_timed()

@@ -14,6 +14,7 @@ def main():
     ap.add_argument("--iters", type=int, default=8)
     ap.add_argument("--spec", default=bench.SPEC)
     ap.add_argument("--reps", type=int, default=1, help="timed runs (the first includes lazy module loading)")
+    ap.add_argument("--substeps", type=int, default=24)
     args = ap.parse_args()
     I, R, D = bench.load_series()
     ctx = eng.Context(0)
@@ -22,7 +23,7 @@ def main():
         a = w * bench.DELTA
         sl = slice(a, a + bench.TAU + 1)
         wins.append(eng.Window(ctx, I[sl], R[sl], D[sl], [bench.POPULATION - I[a] - R[a] - D[a], I[a], R[a], D[a]],
-                               bench.POPULATION, args.spec))
+                               bench.POPULATION, args.spec, substeps=args.substeps))
     swarms = [dict(window=w, lower=[0.0] * 6, upper=bench.STAGE2_HI, n_particles=bench.PARTICLES,
                    max_iters=args.iters, seed=bench.mix_seed(bench.BASE_SEED, k)) for k, w in enumerate(wins)]
     plan = eng.Plan(ctx, swarms)

@@ -14,15 +14,17 @@ def main():
     peak = eng.probe_fp64_rate(ctx)
     I, R, D = bench.load_series()
     N = bench.POPULATION
-    for sub in [int(x) for x in sys.argv[1:]] or [6, 12, 24, 48, 96]:
+    args = [a for a in sys.argv[1:] if not a.startswith("--swarms=")]
+    n_sw = int(next((a.split("=")[1] for a in sys.argv[1:] if a.startswith("--swarms=")), 40))
+    for sub in [int(x) for x in args] or [6, 12, 24, 48, 96]:
         wins = []
-        for w in range(40):
+        for w in range(n_sw):
             a = w * bench.DELTA
             sl = slice(a, a + 36)
             wins.append(eng.Window(ctx, I[sl], R[sl], D[sl], [N - I[a] - R[a] - D[a], I[a], R[a], D[a]], N,
                                    bench.SPEC, substeps=sub))
         swarms = [dict(window=wins[w], lower=[0] * 6, upper=stage2(35), n_particles=4096, max_iters=100,
-                       seed=bench.mix_seed(5, w)) for w in range(40)]
+                       seed=bench.mix_seed(5, w)) for w in range(n_sw)]
         plan = eng.Plan(ctx, swarms)
         plan.run_timed()
         s, k = plan.run_timed()
