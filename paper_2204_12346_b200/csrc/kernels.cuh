@@ -561,6 +561,18 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
+// Address of the same shared-memory location in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+// 16 bytes into another CTA's shared memory, completing that many bytes of
+// the transaction count of its mbarrier (no fence, no cluster barrier).
+__device__ __forceinline__ void st_async_16(uint32_t raddr, uint64_t a, uint64_t b, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];"
+                 ::"r"(raddr), "l"(a), "l"(b), "r"(rbar) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     uint32_t done = 0;
     while (!done) {
@@ -732,11 +744,15 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 1) pso_swarm_kernel(const De
     __shared__ double red_c[kSwarmThreadsMax / 32];
     __shared__ unsigned long long red_i[kSwarmThreadsMax / 32];
     __shared__ double red_pos[kSwarmThreadsMax / 32][6];
-    __shared__ SwarmPartial part[2];
+    // every rank's partial of the iteration, pushed by the ranks themselves
+    // (st.async); double-buffered by iteration parity, one mbarrier each
+    __shared__ __align__(16) SwarmPartial part[2][kSwarmClusterMax];
+    __shared__ __align__(8) uint64_t part_bar[2];
     __shared__ double gbest[6];
     __shared__ double gbest_cost;
     const unsigned rank = cluster.block_rank();
     const unsigned n_ranks = cluster.num_blocks();
+    static_assert(sizeof(SwarmPartial) == 64, "a partial is four 16-byte stores");
     const int s = static_cast<int>(blockIdx.x / n_ranks + swarm_offset);
     const DevSwarm& sw = swarms[s];
     const SmemWindow win = stage_window<MET, SUB>(windows + sw.window, &sdesc, smem);
@@ -763,6 +779,8 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 1) pso_swarm_kernel(const De
         gbest_cost = __longlong_as_double(0x7FF0000000000000LL);
         for (int d = 0; d < 6; ++d) gbest[d] = 0.0;
         if (rank == 0) state[s].ramp_substeps = 0;
+        mbar_init(smem_u32(&part_bar[0]), 1);  // (fence.mbarrier_init: visible to the cluster's st.async)
+        mbar_init(smem_u32(&part_bar[1]), 1);
     }
     unsigned long long ramp_acc = 0;
     const int lane = threadIdx.x & 31;
@@ -812,32 +830,43 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 1) pso_swarm_kernel(const De
         }
         SG_C1_STAMP(3);
         __syncthreads();  // warp minima visible in the CTA
-        SwarmPartial& mine = part[it & 1];
+        const int par = static_cast<int>(it & 1);
+        const uint32_t bar = smem_u32(&part_bar[par]);
         if (threadIdx.x == 0) {
+            // The CTA's partial, pushed into slot `rank` of every rank's
+            // part[par] (itself included); each rank's mbarrier phase
+            // completes when all n_ranks partials have landed.  A rank
+            // pushes iteration it+2's partial (same slots) only after it has
+            // received this rank's it+1 partial, which this rank sends after
+            // its fold of iteration it — so no slot is overwritten early.
             int bw = 0;
             for (int k = 1; k < n_warps; ++k)
                 if (better(red_c[k], red_i[k], red_c[bw], red_i[bw])) bw = k;
-            mine.cost = red_c[bw];
-            mine.idx = red_i[bw];
-            if (red_i[bw] != ~0ULL)
-                for (int d = 0; d < 6; ++d) mine.pos[d] = red_pos[bw][d];
+            uint64_t w8[8];
+            w8[0] = static_cast<uint64_t>(__double_as_longlong(red_c[bw]));
+            w8[1] = red_i[bw];
+            for (int d = 0; d < 6; ++d)
+                w8[2 + d] = red_i[bw] != ~0ULL ? static_cast<uint64_t>(__double_as_longlong(red_pos[bw][d])) : 0ULL;
+            mbar_expect_tx(bar, n_ranks * static_cast<uint32_t>(sizeof(SwarmPartial)));
+            const uint32_t slot = smem_u32(&part[par][rank]);
+            for (unsigned r = 0; r < n_ranks; ++r) {
+                const uint32_t dst = mapa_u32(slot, r), rbar = mapa_u32(bar, r);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) st_async_16(dst + 16 * q, w8[2 * q], w8[2 * q + 1], rbar);
+            }
         }
-        // Every rank's partial of iteration `it` visible cluster-wide.  The
-        // barrier is split: between arrive and wait each particle twists and
-        // tempers the next move's 12 draws (the words were loaded during the
-        // evaluation), which do not depend on the global best — in the
-        // barrier's latency rather than on the iteration's critical path.
-        cluster.barrier_arrive();
+        // the next move's draws (engine words loaded during the evaluation),
+        // while the other ranks' partials are on their way
         if (active && it + 1 < sw.max_iters) mt_finish<12>(P.mt + pblock_base(p, kMtN), move_draw_word(it + 1), next, u);
-        cluster.barrier_wait();
+        mbar_wait(bar, static_cast<uint32_t>((it >> 1) & 1));  // every rank's partial of iteration `it` here
         SG_C1_STAMP(4);
         if (threadIdx.x == 0) {
             // Global-best scan (pso.cpp:90-96) over the ranks' partials in
             // rank order: identical in every CTA.
             const SwarmPartial* best = nullptr;
             for (unsigned r = 0; r < n_ranks; ++r) {
-                const SwarmPartial* q = cluster.map_shared_rank(&part[it & 1], r);
-                SG_CHECK(q->idx == ~0ULL || q->idx < n);  // a partial of THIS iteration (double buffer)
+                const SwarmPartial* q = &part[par][r];
+                SG_CHECK(q->idx == ~0ULL || q->idx < n);
                 if (!best || better(q->cost, q->idx, best->cost, best->idx)) best = q;
             }
             SG_CHECK(best != nullptr && best->idx < n);
