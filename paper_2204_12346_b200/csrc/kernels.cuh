@@ -702,11 +702,11 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
 // warp per SM sub-partition) instead of stacking warps on one SM.  CTA r of
 // the cluster owns particles r*blockDim + t (+ k*cluster*blockDim).  Per
 // iteration each CTA folds its warps' minima into a partial (cost, index,
-// personal-best position) in its shared memory; after one cluster barrier
-// every CTA folds the partials of all ranks in rank order through
-// distributed shared memory, so all CTAs hold the same global best.  The
-// partials are double-buffered by iteration parity, which makes one cluster
-// barrier per iteration enough.
+// personal-best position) and pushes it into every rank's shared memory
+// (st.async, completing on the receiver's mbarrier); each CTA then folds the
+// partials of all ranks in rank order locally, so all CTAs hold the same
+// global best.  The partials and their mbarriers are double-buffered by
+// iteration parity.
 constexpr int kSwarmThreadsMax = 128;
 constexpr int kSwarmClusterMax = 8;
 constexpr int kPersistMax = kSwarmThreadsMax * kSwarmClusterMax;  // 1024 particles per swarm
@@ -786,7 +786,7 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 1) pso_swarm_kernel(const De
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int n_warps = (blockDim.x + 31) >> 5;
-    cluster.sync();  // ramp counter cleared before any CTA adds to it; gbest initialised
+    cluster.sync();  // ramp counter cleared, gbest initialised, every rank's partial mbarriers initialised
     for (uint64_t it = 0; it < sw.max_iters; ++it) {
         double my_c = __longlong_as_double(0x7FF0000000000000LL);
         unsigned long long my_i = ~0ULL;
@@ -897,7 +897,7 @@ __global__ void __launch_bounds__(kSwarmThreadsMax, 1) pso_swarm_kernel(const De
         state[s].arrived = 0;
     }
     if (lane == 0) atomicAdd(&state[s].ramp_substeps, wr);
-    cluster.sync();  // no CTA leaves while another may still read its partials
+    cluster.sync();  // no CTA leaves while a push to it may still be in flight
 }
 
 #ifndef SG_FAMILY_TU  // engine.cu only (family.cu holds the templated kernels)
