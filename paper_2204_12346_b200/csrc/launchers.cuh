@@ -11,9 +11,14 @@
 
 namespace sirdgpu {
 
+// Opt in to the dynamic shared memory a launch needs beyond the default
+// 48 KB, which covers static + dynamic together: every kernel here has less
+// than 8 KB of static shared memory (the cluster kernel's partials 1 KB,
+// its warp minima and window descriptor ~3.6 KB), so dynamic segments past
+// 40 KB opt in.
 template <class KernelPtr>
 cudaError_t prepare_smem(KernelPtr k, size_t smem) {
-    if (smem > 48 * 1024)
+    if (smem > 40 * 1024)
         return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     return cudaSuccess;
 }

@@ -83,6 +83,24 @@ def test_cluster_kernel_every_cluster_size(ctx, port, poland, n_particles):
     _check(port, swarms, data, plan.results())
 
 
+@pytest.mark.parametrize("n_days,substeps,spec", [(118, 48, "ird-mse"), (117, 48, "d-mae"), (217, 24, "ird-mxse"),
+                                                   (230, 24, "ird-mape")])
+def test_cluster_kernel_shared_memory_edges(ctx, port, poland, n_days, substeps, spec):
+    """Windows whose staged image (~47 KB) plus the cluster kernel's static
+    shared memory (2.6 KB) passes the 48 KB a launch gets without opting in:
+    the launcher opts in above 40 KB (tools/fuzz_long.py batch 81 of seed
+    base 4000000 — an ird-mse window of 118 days at 48 substeps — once
+    failed with cudaErrorInvalidValue)."""
+    import paper_2204_12346_b200 as eng
+    win, (I, R, D, init, N) = _window(eng, ctx, poland, 100, n_days, spec, substeps)
+    swarms = [dict(window=win, lower=[0.0] * 6, upper=[2, 2, n_days - 8, n_days - 8, 1, 0.1], n_particles=178,
+                   max_iters=4, seed=5)]
+    plan = eng.Plan(ctx, swarms)
+    assert plan.step_launches == 1  # the persistent cluster kernel
+    plan.run()
+    _check(port, swarms, [(I, R, D, init, N, substeps)], plan.results())
+
+
 def test_plan_reruns_are_identical(ctx, poland):
     import paper_2204_12346_b200 as eng
     wins = [_window(eng, ctx, poland, 3 * w, 36, "ird-mxse")[0] for w in range(12)]

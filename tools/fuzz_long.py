@@ -27,7 +27,14 @@ def main():
             wins.append(w)
             swarms.append(dict(window=w, lower=c["lo"], upper=c["hi"], n_particles=c["n"], max_iters=c["iters"],
                                seed=c["seed"], repair=c["repair"], **c["coeffs"]))
-        out = ctx.fit_swarms(swarms)
+        try:
+            out = ctx.fit_swarms(swarms)
+        except Exception as e:  # noqa: BLE001 - report the batch that failed, then stop
+            print("ERROR batch", batch, repr(e), flush=True)
+            for k, c in enumerate(cases):
+                print("  case", k, c["spec"], "days", len(c["I"]), "sub", c["sub"], "n", c["n"], "iters", c["iters"],
+                      flush=True)
+            return 2
         for k, c in enumerate(cases):
             rc, best, cost, hist = port.fit_swarm(c["spec"], c["I"], c["R"], c["D"], c["init"], c["N"], c["lo"],
                                                   c["hi"], c["n"], c["iters"], seed=c["seed"], repair=c["repair"],
