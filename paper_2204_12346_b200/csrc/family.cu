@@ -30,3 +30,9 @@ extern "C" int sg_c1_probe(unsigned long long* out) {
     return static_cast<int>(cudaMemcpyFromSymbol(out, sirdgpu::g_c1, sizeof(sirdgpu::g_c1)));
 }
 #endif
+
+#if SG_CTA_TIMES && SG_FAMILY == 1 && SG_SUB == 24
+extern "C" int sg_cta_times(unsigned long long* out) {
+    return static_cast<int>(cudaMemcpyFromSymbol(out, sirdgpu::g_cta_times, sizeof(sirdgpu::g_cta_times)));
+}
+#endif

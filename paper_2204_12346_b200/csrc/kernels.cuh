@@ -634,10 +634,20 @@ __device__ __forceinline__ SmemWindow stage_window_async(const CtaTask& t, DevWi
 // the move of iteration it-1 (which closes step it-1 in the reference), then
 // evaluate, personal best, and the global-best fold.  Thread t of a swarm's
 // CTA range owns particle t for all iterations.  Used for large swarms.
+#if SG_CTA_TIMES
+static __device__ unsigned long long g_cta_times[1 << 14][3];
+#endif
+
 template <int FAM, int MET, int SUB>
 __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
     pso_step_kernel(const CtaTask* __restrict__ tasks, const DevSwarm* __restrict__ swarms, PsoPlanes P,
                     DevSwarmState* __restrict__ state, uint64_t it, uint32_t cta_offset) {
+#if SG_CTA_TIMES
+    // diagnostic build (tools/cta_times.py): globaltimer at CTA start / end and
+    // the SM of every CTA of iteration SG_CTA_TIMES
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(16) DevWindow sdesc;
     __shared__ __align__(8) uint64_t bar;
@@ -689,6 +699,18 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
     if (active[0]) c[0] = eval_particle<FAM, MET, SUB>(x[0], *win.w, win.tg, win.obs, win.robs, win.flag, &ramp[0]);
     finish_step<kNP>(sw, state[s], P, s, active, p, i, c, x, pbc,
                      (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it, ramp);
+#if SG_CTA_TIMES
+    __syncthreads();
+    if (threadIdx.x == 0 && it == SG_CTA_TIMES && cta < (1u << 14)) {
+        unsigned long long t_end;
+        unsigned smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_cta_times[cta][0] = t_start;
+        g_cta_times[cta][1] = t_end;
+        g_cta_times[cta][2] = smid;
+    }
+#endif
 }
 
 // ---- small swarms: one persistent thread-block cluster per swarm ---------------
