@@ -635,7 +635,7 @@ __device__ __forceinline__ SmemWindow stage_window_async(const CtaTask& t, DevWi
 // evaluate, personal best, and the global-best fold.  Thread t of a swarm's
 // CTA range owns particle t for all iterations.  Used for large swarms.
 #if SG_CTA_TIMES
-static __device__ unsigned long long g_cta_times[1 << 14][3];
+static __device__ unsigned long long g_cta_times[6 * 8192][3];
 #endif
 
 template <int FAM, int MET, int SUB>
@@ -701,14 +701,15 @@ __global__ void __launch_bounds__(kStepThreads, SG_STEP_MIN_BLOCKS)
                      (cta - sw.cta_begin) * kStepWarps + (threadIdx.x >> 5), it, ramp);
 #if SG_CTA_TIMES
     __syncthreads();
-    if (threadIdx.x == 0 && it == SG_CTA_TIMES && cta < (1u << 14)) {
+    const uint64_t rec = (it - SG_CTA_TIMES) * 8192 + cta;  // iterations SG_CTA_TIMES..+5, <= 8192 CTAs each
+    if (threadIdx.x == 0 && it >= SG_CTA_TIMES && it < SG_CTA_TIMES + 6 && cta < 8192) {
         unsigned long long t_end;
         unsigned smid;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        g_cta_times[cta][0] = t_start;
-        g_cta_times[cta][1] = t_end;
-        g_cta_times[cta][2] = smid;
+        g_cta_times[rec][0] = t_start;
+        g_cta_times[rec][1] = t_end;
+        g_cta_times[rec][2] = smid;
     }
 #endif
 }

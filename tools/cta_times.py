@@ -1,4 +1,5 @@
-"""CTA start/end times of one step-kernel launch of C3 (one 2^20-particle swarm), from a
+"""CTA start/end times of one step-kernel iteration of C3 (one 2^20-particle swarm) or C2 (argument c2:
+the bench plan, every lane), from a
 diagnostic build (-DSG_CTA_TIMES=<iteration>): the occupancy profile over the launch —
 how long the grid fills, runs full, and drains.
 
@@ -21,29 +22,36 @@ from tools.bench_configs import stage2, window  # noqa: E402
 
 def main():
     ctx = eng.Context(0)
-    win = window(ctx, 60, 35)
-    plan = eng.Plan(ctx, [dict(window=win, lower=[0] * 6, upper=stage2(35), n_particles=1 << 20, max_iters=8,
-                               seed=7)])
+    if len(sys.argv) > 1 and sys.argv[1] == "c2":  # the bench plan: 139 windows x 4096, all lanes
+        import bench
+        wins = [window(ctx, w, 35) for w in range(139)]
+        swarms = [dict(window=w, lower=[0.0] * 6, upper=bench.STAGE2_HI, n_particles=4096, max_iters=12,
+                       seed=bench.mix_seed(bench.BASE_SEED, k)) for k, w in enumerate(wins)]
+        n = 139 * 32
+    else:  # C3: one swarm of 2^20 particles
+        win = window(ctx, 60, 35)
+        swarms = [dict(window=win, lower=[0] * 6, upper=stage2(35), n_particles=1 << 20, max_iters=12, seed=7)]
+        n = 8192
+    plan = eng.Plan(ctx, swarms)
     plan.run_timed()
-    buf = np.zeros((1 << 14, 3), dtype=np.uint64)
+    buf = np.zeros((6 * 8192, 3), dtype=np.uint64)
     _capi.lib().sg_cta_times(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
-    n = 8192
-    t = buf[:n].astype(np.int64)
-    t0 = t[:, 0].min()
-    st, en = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3  # us
-    span = en.max()
-    dur = en - st
-    # occupancy over time: CTAs resident at each microsecond
-    grid = np.arange(0, int(span) + 1)
+    t = buf.reshape(6, 8192, 3)[:, :n].astype(np.int64)  # iterations T..T+5
+    t0 = t[..., 0].min()
+    st, en = (t[..., 0] - t0) / 1e3, (t[..., 1] - t0) / 1e3  # us
+    # a window inside which every running CTA belongs to a recorded iteration:
+    # from the first start of iteration T+2 to the last end of iteration T+3
+    a, b = st[2].min(), en[3].max()
+    grid = np.arange(int(a), int(b))
     occ = np.array([np.count_nonzero((st <= g) & (en > g)) for g in grid])
-    full = occ.max()
-    busy = dur.sum() / (full * span)
-    drain_start = float(np.max(st))  # the last CTA starts
-    print(json.dumps({"span_us": float(span), "cta_us_mean": float(dur.mean()), "cta_us_p10": float(np.percentile(dur, 10)),
-                      "cta_us_p90": float(np.percentile(dur, 90)), "max_resident": int(full),
-                      "slot_utilisation": float(busy), "last_start_us": drain_start,
-                      "drain_us": float(span - drain_start),
-                      "occupancy_profile_every_50us": [int(occ[g]) for g in range(0, len(occ), 50)]}, indent=1))
+    one = t[0]
+    d0 = (one[:, 1] - one[:, 0]) / 1e3
+    print(json.dumps({"window_us": [float(a), float(b)], "max_resident": int(occ.max()),
+                      "slot_utilisation_in_window": float(occ.mean() / occ.max()),
+                      "cta_us_mean": float(d0.mean()), "cta_us_p10": float(np.percentile(d0, 10)),
+                      "cta_us_p90": float(np.percentile(d0, 90)),
+                      "one_iteration_span_us": float((one[:, 1].max() - one[:, 0].min()) / 1e3),
+                      "occupancy_profile_every_25us": [int(occ[g]) for g in range(0, len(occ), 25)]}, indent=1))
 
 
 if __name__ == "__main__":
