@@ -2,7 +2,7 @@
 cluster and staging invariants, sird_device.cuh) into
 build_variants/checked/libsirdgpu.so.  Run the GPU suite against it with
 SG_LIB=build_variants/checked/libsirdgpu.so (compute-sanitizer is closed on
-the GPU pool; profiles/r02c_checked_tests.log)."""
+the GPU pool; profiles/r02t_checked_tests.log)."""
 import sys
 from pathlib import Path
 
