@@ -340,6 +340,48 @@ def test_ensemble_bands_batch_prediction_hits_and_misses(ctx, poland):
         assert_bitwise(bands[k].ravel(), b1.ravel(), f"window {k}")
 
 
+def _random_band_batch(eng, ctx, poland, rng):
+    """A batch of random ensemble windows (lengths, populations, boxes, a
+    horizon on either side of the fused-range limit of 31 days, sample
+    counts that are no multiple of the CTA) for the pipelined band call."""
+    N0 = poland["N"]
+    horizon = int(rng.choice([0, 1, 7, 21, 31, 32, 40]))
+    n = int(rng.choice([1, 2, 127, 129, 1000, 4099, 20000]))
+    wins, seeds = [], []
+    for _ in range(int(rng.integers(1, 6))):
+        a, days = int(rng.integers(0, 300)), int(rng.integers(2, 60))
+        scale = float(10.0 ** rng.uniform(-3, 3))
+        I, R, D = (poland[c][a:a + days] * scale for c in "IRD")
+        N = N0 * scale
+        wins.append(eng.Window(ctx, I, R, D, [N - I[0] - R[0] - D[0], I[0], R[0], D[0]], N,
+                               str(rng.choice(["ird-mxse", "d-mse", "ird-mape"]))))
+        seeds.append(int(rng.integers(1 << 62)))
+    tmax = float(rng.uniform(0.0, 80.0))
+    hi = [float(rng.uniform(0.0, 3.0)), float(rng.uniform(0.0, 3.0)), tmax, tmax,
+          float(rng.uniform(0.0, 2.0)), float(rng.uniform(0.0, 0.5))]
+    if rng.random() < 0.2:
+        hi = [1e150, 1e150, tmax, tmax, 1e150, 1e150]  # many blow-ups
+    return wins, [0.0] * 6, hi, seeds, n, horizon
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_ensemble_bands_batch_random_against_host_sort(ctx, poland, seed):
+    """Random pipelined band batches (the fused range and predicted-bin
+    histogram, misses and hits, the non-fused path past 31 days, blow-ups,
+    tiny and ragged ensembles) against sorting each window's forecast
+    deaths on the host, bit for bit."""
+    import paper_2204_12346_b200 as eng
+    rng = np.random.default_rng(7000 + seed)
+    wins, lo, hi, seeds, n, horizon = _random_band_batch(eng, ctx, poland, rng)
+    bands, counts = ctx.forecast_ensemble_bands_batch(wins, lo, hi, seeds, n, horizon)
+    for k, w in enumerate(wins):
+        _, _, deaths = w.forecast_ensemble(lo, hi, seed=seeds[k], n=n, horizon=horizon, want_costs=False,
+                                           want_params=False)
+        want, want_counts = _host_bands(deaths)
+        assert counts[k].tolist() == want_counts, (seed, k)
+        assert_bitwise(bands[k].ravel(), want.ravel(), f"seed {seed} window {k}")
+
+
 def test_ensemble_ramp_telemetry_is_exact(ctx, poland):
     """The band path's ramp-substep count (the roofline's ramp credit) is
     exact: switch times pinned by the box (t1 = 0, t2 = 10 days) ramp on
