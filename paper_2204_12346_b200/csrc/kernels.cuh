@@ -8,9 +8,12 @@
 //                         personal best -> warp argmin -> last-warp global best
 //                         (two-level for swarms over 32 CTAs)
 //   pso_swarm_kernel      whole optimize() of small swarms, one thread-block
-//                         cluster per swarm (global best through DSMEM)
+//                         cluster per swarm (partials pushed into every rank's
+//                         shared memory with st.async + mbarrier)
 //   ens_sample_kernel,    forecast-scenario ensemble (sample in ramp-coherent
-//   ensemble_kernel       order, score, forecast)
+//   ens_scan/scatter,     order, score when asked, forecast; on the band path
+//   ensemble_kernel       also each day's key range, finite count and
+//                         histogram over predicted bins)
 //   sel_*_kernel          quantile bands by order-statistic selection
 //
 // Layout in HBM: particle state in particle blocks (32 particles x fields,
