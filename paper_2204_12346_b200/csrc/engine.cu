@@ -1253,8 +1253,9 @@ static int ensure_band_stats(sg_ctx* ctx) {
 }
 
 // C5, stage 2 (FP64-bound): evaluation of the window and forecast into the
-// slot's day-major deaths plane (with each day's key range and finite count
-// reduced in the kernel's epilogue when SG_FUSED_RANGE is on).
+// slot's day-major deaths plane; with horizon < 32 the kernel also reduces
+// each day's key range and finite count and fills the predicted-bin
+// histogram as the forecast days arrive (BandDSink).
 static int enqueue_band_eval(sg_ctx* ctx, sg_window* w, BandSlot& s, cudaStream_t st, const double* d_lo,
                              const double* d_hi, uint64_t seed, size_t n, int horizon, double* d_cost) {
     const int n_days = horizon + 1;
@@ -1264,17 +1265,20 @@ static int enqueue_band_eval(sg_ctx* ctx, sg_window* w, BandSlot& s, cudaStream_
     // day-major columns in evaluation order: the bands only need each day's multiset
     dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc,
                              fwin, d_lo, d_hi, seed, n, horizon, d_cost, static_cast<double*>(nullptr), s.D, size_t(1),
-                             n, s.unordered ? nullptr : s.perm, s.unordered ? nullptr : s.planes, 1, fused_range(horizon) ? s.days : nullptr,
-                             s.hist, ctx->band_stats ? ctx->band_stats + 2 : nullptr, w->smem, st, &err);
+                             n, s.unordered ? nullptr : s.perm, s.unordered ? nullptr : s.planes, 1,
+                             fused_range(horizon) ? s.days : nullptr, s.hist,
+                             ctx->band_stats ? ctx->band_stats + 2 : nullptr, w->smem, st, &err);
     ctx->launches += 1;
     if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
     return SG_OK;
 }
 
 // C5, stage 3 (memory-bound): per forecast day the bins of the wanted
-// ranks (calibration.cpp:17-25, 324-361) — histogram, locate, gather — then
-// one CTA per (bin, day) resolves the bin's wanted ranks in shared memory,
-// and quantile_sorted turns them into the bands.
+// ranks (calibration.cpp:17-25, 324-361) — located in the ensemble's fused
+// histogram, or for the days whose prediction missed in a histogram pass
+// over the plane — then a gather of those bins' values, one CTA per (bin,
+// day) resolving the bin's wanted ranks in shared memory, and
+// quantile_sorted turning them into the bands.
 static int enqueue_band_select(sg_ctx* ctx, BandSlot& s, cudaStream_t st, size_t n, int n_days, double* d_bands,
                                unsigned long long* d_counts, bool standalone = false) {
     if (const int rc = ensure_band_stats(ctx)) return rc;
