@@ -1106,13 +1106,19 @@ static int order_step(const double upper[6]) {
 // keys (ranking each sample within its key); a scan and an atomic-free
 // scatter complete the counting sort into perm.
 // key_count: 2 x kOrderKeys, the counts zero on entry (and again on exit).
+// sample = false: the samples and key counts were drawn elsewhere (an
+// earlier window's ensemble launch, EnsNext); only the scan and scatter run.
 static int ensemble_order(sg_ctx* ctx, const double* d_lo, const double* d_hi, uint64_t seed, size_t n, int q,
-                          double* planes, uint32_t* keys, unsigned int* key_count, uint32_t* perm, cudaStream_t st) {
+                          double* planes, uint32_t* keys, unsigned int* key_count, uint32_t* perm, cudaStream_t st,
+                          bool sample = true) {
     const unsigned grid = static_cast<unsigned>((n + kSampleThreads - 1) / kSampleThreads);
-    ens_sample_kernel<<<grid, kSampleThreads, 0, st>>>(d_lo, d_hi, seed, n, q, planes, keys, key_count);
+    if (sample) {
+        ens_sample_kernel<<<grid, kSampleThreads, 0, st>>>(d_lo, d_hi, seed, n, q, planes, keys, key_count);
+        ctx->launches += 1;
+    }
     ens_scan_kernel<<<1, kBgThreads, 0, st>>>(key_count);
     ens_scatter_kernel<<<grid, kSampleThreads, 0, st>>>(keys, n, key_count + kOrderKeys, perm);
-    ctx->launches += 3;
+    ctx->launches += 2;
     SG_CUDA(ctx, cudaGetLastError());
     return SG_OK;
 }
@@ -1158,8 +1164,8 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
     dispatch<EnsembleLaunch>(w->host.family, w->host.metric, kernel_sub(w->host.n_days, w->host.substeps), w->d_desc,
                              fwin, d_lo, d_hi, seed, n, horizon, d_cost, d_par, d_D,
                              static_cast<size_t>(horizon + 1), size_t(1), perm, planes, 0, static_cast<SelDay*>(nullptr),
-                             static_cast<unsigned int*>(nullptr), static_cast<unsigned long long*>(nullptr), w->smem,
-                             ctx->stream, &err);
+                             static_cast<unsigned int*>(nullptr), static_cast<unsigned long long*>(nullptr), EnsNext{},
+                             w->smem, ctx->stream, &err);
     ctx->launches += 1;
     if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
     if (costs) SG_CUDA(ctx, copy_async(ctx, costs, d_cost, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1171,7 +1177,26 @@ int sg_forecast_ensemble(sg_window* w, const double lower[6], const double upper
     return SG_OK;
 }
 
-// Device buffers of one window in flight in the C5 pipeline.
+// Order buffers of one window (samples, keys + ranks, permutation, key
+// counts + cursors).
+struct OrderBufs {
+    double* planes = nullptr;
+    uint32_t *keys = nullptr, *perm = nullptr;
+    unsigned int* key_count = nullptr;
+};
+
+static int alloc_order_bufs(sg_ctx* ctx, DevBufs& b, OrderBufs& o, size_t n) {
+    SG_CUDA(ctx, b.alloc(&o.planes, 6 * n));
+    SG_CUDA(ctx, b.alloc(&o.keys, 2 * n));  // key, rank within the key
+    SG_CUDA(ctx, b.alloc(&o.perm, n));
+    SG_CUDA(ctx, b.alloc(&o.key_count, 2 * kOrderKeys));
+    // zero once: ens_scan_kernel leaves the counts zero
+    SG_CUDA(ctx, cudaMemsetAsync(o.key_count, 0, sizeof(unsigned int) * kOrderKeys, b.st));
+    return SG_OK;
+}
+
+// Device buffers of one window in flight in the C5 pipeline (the order
+// buffers bound per window from an OrderBufs).
 struct BandSlot {
     double *planes = nullptr, *D = nullptr, *cand = nullptr, *scratch = nullptr, *vals = nullptr;
     uint32_t *keys = nullptr, *perm = nullptr;
@@ -1203,20 +1228,27 @@ static bool fused_hist() {
     return on;
 }
 
-static int alloc_band_slot(sg_ctx* ctx, DevBufs& b, BandSlot& s, size_t n, int n_days) {
+static void bind_order(BandSlot& s, const OrderBufs& o) {
+    s.planes = o.planes;
+    s.keys = o.keys;
+    s.perm = o.perm;
+    s.key_count = o.key_count;
+}
+
+static int alloc_band_slot(sg_ctx* ctx, DevBufs& b, BandSlot& s, size_t n, int n_days, bool with_order = true) {
     const size_t nd = n * static_cast<size_t>(n_days);
-    SG_CUDA(ctx, b.alloc(&s.planes, 6 * n));
-    SG_CUDA(ctx, b.alloc(&s.keys, 2 * n));  // key, rank within the key
-    SG_CUDA(ctx, b.alloc(&s.perm, n));
-    SG_CUDA(ctx, b.alloc(&s.key_count, 2 * kOrderKeys));
+    if (with_order) {
+        OrderBufs o;
+        if (const int rc = alloc_order_bufs(ctx, b, o, n)) return rc;
+        bind_order(s, o);
+    }
     SG_CUDA(ctx, b.alloc(&s.D, nd));
     SG_CUDA(ctx, b.alloc(&s.cand, nd));
     SG_CUDA(ctx, b.alloc(&s.scratch, 2 * nd));  // only bins too full for one CTA's shared memory touch it
     SG_CUDA(ctx, b.alloc(&s.days, n_days));
     SG_CUDA(ctx, b.alloc(&s.hist, static_cast<size_t>(n_days) * kSelBins));
     SG_CUDA(ctx, b.alloc(&s.vals, static_cast<size_t>(n_days) * kBandRanks));
-    // zero once: ens_scan_kernel and sel_locate_kernel leave them zero
-    SG_CUDA(ctx, cudaMemsetAsync(s.key_count, 0, sizeof(unsigned int) * kOrderKeys, b.st));
+    // zero once: sel_locate_kernel leaves it zero
     SG_CUDA(ctx, cudaMemsetAsync(s.hist, 0, sizeof(unsigned int) * n_days * kSelBins, b.st));
     SG_CUDA(ctx, cudaMemsetAsync(s.days, 0, sizeof(SelDay) * n_days, b.st));  // no prediction for the first window
     return SG_OK;
@@ -1225,13 +1257,14 @@ static int alloc_band_slot(sg_ctx* ctx, DevBufs& b, BandSlot& s, size_t n, int n
 // C5, stage 1 (integer work): the samples and their ramp-coherent order;
 // the slot's day records reset for the selection.
 static int enqueue_band_order(sg_ctx* ctx, BandSlot& s, cudaStream_t st, const double* d_lo, const double* d_hi,
-                              uint64_t seed, size_t n, int q, int n_days) {
+                              uint64_t seed, size_t n, int q, int n_days, bool sample = true) {
     static const bool ordered = [] {  // SG_BAND_ORDER=0: samples drawn in the ensemble kernel, unordered (A/B)
         const char* e = std::getenv("SG_BAND_ORDER");
         return !(e && e[0] == '0');
     }();
     if (ordered) {
-        if (const int rc = ensemble_order(ctx, d_lo, d_hi, seed, n, q, s.planes, s.keys, s.key_count, s.perm, st))
+        if (const int rc =
+                ensemble_order(ctx, d_lo, d_hi, seed, n, q, s.planes, s.keys, s.key_count, s.perm, st, sample))
             return rc;
     }
     s.unordered = !ordered;
@@ -1257,7 +1290,8 @@ static int ensure_band_stats(sg_ctx* ctx) {
 // each day's key range and finite count and fills the predicted-bin
 // histogram as the forecast days arrive (BandDSink).
 static int enqueue_band_eval(sg_ctx* ctx, sg_window* w, BandSlot& s, cudaStream_t st, const double* d_lo,
-                             const double* d_hi, uint64_t seed, size_t n, int horizon, double* d_cost) {
+                             const double* d_hi, uint64_t seed, size_t n, int horizon, double* d_cost,
+                             EnsNext next = EnsNext{}) {
     const int n_days = horizon + 1;
     const DevWindow fwin = integration_window(n_days, w->host.substeps, w->host.N);
     if (const int rc = ensure_band_stats(ctx)) return rc;
@@ -1267,7 +1301,7 @@ static int enqueue_band_eval(sg_ctx* ctx, sg_window* w, BandSlot& s, cudaStream_
                              fwin, d_lo, d_hi, seed, n, horizon, d_cost, static_cast<double*>(nullptr), s.D, size_t(1),
                              n, s.unordered ? nullptr : s.perm, s.unordered ? nullptr : s.planes, 1,
                              fused_range(horizon) ? s.days : nullptr, s.hist,
-                             ctx->band_stats ? ctx->band_stats + 2 : nullptr, w->smem, st, &err);
+                             ctx->band_stats ? ctx->band_stats + 2 : nullptr, next, w->smem, st, &err);
     ctx->launches += 1;
     if (err != cudaSuccess) return cuda_fail(ctx, err, "ensemble_kernel");
     return SG_OK;
@@ -1452,48 +1486,74 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
     SG_CUDA(ctx, b.alloc(&d_hi, 6));
     SG_CUDA(ctx, b.alloc(&d_bands, 7 * static_cast<size_t>(n_days) * n_windows));
     SG_CUDA(ctx, b.alloc(&d_counts, static_cast<size_t>(n_days) * n_windows));
-    constexpr int kSlots = sg_ctx::kBandSlots;
+    constexpr int kSlots = sg_ctx::kBandSlots;  // band buffers (deaths plane, day records, histograms)
+    constexpr int kOrd = 4;                      // order buffers: windows k..k+3 (samples drawn two ahead)
     BandSlot slot[kSlots];
     for (BandSlot& s : slot)
-        if (const int rc = alloc_band_slot(ctx, b, s, n, n_days)) return rc;
+        if (const int rc = alloc_band_slot(ctx, b, s, n, n_days, false)) return rc;
+    OrderBufs ord[kOrd];
+    for (OrderBufs& o : ord)
+        if (const int rc = alloc_order_bufs(ctx, b, o, n)) return rc;
+    // SG_BAND_AHEAD=0 (A/B): every window's samples drawn on the selection
+    // stream instead of by the ensemble launch two windows earlier
+    static const bool ahead = [] {
+        const char* e = std::getenv("SG_BAND_AHEAD");
+        return !(e && e[0] == '0');
+    }();
     SG_CUDA(ctx, copy_async(ctx, d_lo, lower, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     SG_CUDA(ctx, copy_async(ctx, d_hi, upper, 6 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    cudaEvent_t ordered[kSlots], evaluated[kSlots], selected[kSlots];
-    for (int k = 0; k < kSlots; ++k) {
+    cudaEvent_t ordered[kOrd], evaluated[kOrd], selected[kSlots];
+    for (int k = 0; k < kOrd; ++k) {
         SG_CUDA(ctx, cudaEventCreateWithFlags(&ordered[k], cudaEventDisableTiming));
         SG_CUDA(ctx, cudaEventCreateWithFlags(&evaluated[k], cudaEventDisableTiming));
-        SG_CUDA(ctx, cudaEventCreateWithFlags(&selected[k], cudaEventDisableTiming));
     }
-    // Three stages per window over kSlots slots: order (S) -> evaluate (E)
-    // -> select (S).  S runs window k+1's order while E evaluates window k,
-    // then window k's selection.  Each slot evaluates on its own stream:
+    for (int k = 0; k < kSlots; ++k) SG_CUDA(ctx, cudaEventCreateWithFlags(&selected[k], cudaEventDisableTiming));
+    // Three stages per window: order (S) -> evaluate (E) -> select (S).  S
+    // finishes window k+1's order while E evaluates window k, then runs
+    // window k's selection.  Each band slot evaluates on its own stream:
     // nothing orders window k+1's evaluation after window k's, so its CTAs
-    // fill the SMs window k's last wave leaves idle.
+    // fill the SMs window k's last wave leaves idle.  Window k's ensemble
+    // launch also draws window k+2's samples and key counts (EnsNext: integer
+    // work the FP64-bound launch absorbs), so S's order stage is the scan and
+    // the scatter.  Order buffers rotate over 4 windows: launch k reads
+    // ord[k%4] and writes ord[(k+2)%4], launch k+1 (concurrent) ord[(k+1)%4]
+    // and ord[(k+3)%4]; ord[(k+2)%4] was last read by launch k-2, which
+    // finished before window k-2's selection that launch k waits for.
     cudaStream_t S = ctx->band_sel;
     SG_CUDA(ctx, cudaEventRecord(ctx->fork, ctx->stream));  // buffers allocated, bounds uploaded
     for (cudaStream_t e : ctx->band_eval) SG_CUDA(ctx, cudaStreamWaitEvent(e, ctx->fork, 0));
     SG_CUDA(ctx, cudaStreamWaitEvent(S, ctx->fork, 0));
     auto step = [&](cudaError_t e) { return e == cudaSuccess ? SG_OK : cuda_fail(ctx, e, "band pipeline"); };
+    bind_order(slot[0], ord[0]);
     int rc = enqueue_band_order(ctx, slot[0], S, d_lo, d_hi, seeds[0], n, q, n_days);
     if (!rc) rc = step(cudaEventRecord(ordered[0], S));
     for (size_t k = 0; k < n_windows && !rc; ++k) {
-        const int j = static_cast<int>(k % kSlots);
+        const int j = static_cast<int>(k % kSlots), o = static_cast<int>(k % kOrd);
         cudaStream_t E = ctx->band_eval[j];
-        // E: window k once ordered, into a deaths plane its slot's previous
-        // window has been reduced from
-        rc = step(cudaStreamWaitEvent(E, ordered[j], 0));
+        // E: window k once ordered, into a band slot its previous window has
+        // been reduced from
+        rc = step(cudaStreamWaitEvent(E, ordered[o], 0));
         if (!rc && k >= kSlots) rc = step(cudaStreamWaitEvent(E, selected[j], 0));
-        if (!rc) rc = enqueue_band_eval(ctx, windows[k], slot[j], E, d_lo, d_hi, seeds[k], n, horizon, nullptr);
-        if (!rc) rc = step(cudaEventRecord(evaluated[j], E));
-        // S: the next window's order (its slot's planes were read by window
-        // k+1-kSlots's evaluation), then window k's selection
-        if (!rc && k + 1 < n_windows) {
-            const int j1 = static_cast<int>((k + 1) % kSlots);
-            if (k + 1 >= kSlots) rc = step(cudaStreamWaitEvent(S, evaluated[j1], 0));
-            if (!rc) rc = enqueue_band_order(ctx, slot[j1], S, d_lo, d_hi, seeds[k + 1], n, q, n_days);
-            if (!rc) rc = step(cudaEventRecord(ordered[j1], S));
+        EnsNext next{};
+        if (ahead && k + 2 < n_windows) {
+            const OrderBufs& a2 = ord[(k + 2) % kOrd];
+            next = EnsNext{seeds[k + 2], a2.planes, a2.keys, a2.key_count, q};
         }
-        if (!rc) rc = step(cudaStreamWaitEvent(S, evaluated[j], 0));
+        bind_order(slot[j], ord[o]);
+        if (!rc) rc = enqueue_band_eval(ctx, windows[k], slot[j], E, d_lo, d_hi, seeds[k], n, horizon, nullptr, next);
+        if (!rc) rc = step(cudaEventRecord(evaluated[o], E));
+        // S: the next window's order, then window k's selection
+        if (!rc && k + 1 < n_windows) {
+            const int j1 = static_cast<int>((k + 1) % kSlots), o1 = static_cast<int>((k + 1) % kOrd);
+            const bool drawn = ahead && k + 1 >= 2;  // by launch k-1
+            // drawn: wait for launch k-1; else the order buffers' last reader, launch k-3
+            if (drawn) rc = step(cudaStreamWaitEvent(S, evaluated[(k + kOrd - 1) % kOrd], 0));
+            else if (k + 1 >= kOrd) rc = step(cudaStreamWaitEvent(S, evaluated[o1], 0));
+            bind_order(slot[j1], ord[o1]);
+            if (!rc) rc = enqueue_band_order(ctx, slot[j1], S, d_lo, d_hi, seeds[k + 1], n, q, n_days, !drawn);
+            if (!rc) rc = step(cudaEventRecord(ordered[o1], S));
+        }
+        if (!rc) rc = step(cudaStreamWaitEvent(S, evaluated[o], 0));
         if (!rc)
             rc = enqueue_band_select(ctx, slot[j], S, n, n_days, d_bands + 7 * static_cast<size_t>(n_days) * k,
                                      d_counts + static_cast<size_t>(n_days) * k);
@@ -1506,11 +1566,11 @@ int sg_forecast_ensemble_bands_batch(sg_window* const* windows, size_t n_windows
     }
     SG_CUDA(ctx, cudaEventRecord(ctx->join[kSlots], S));
     SG_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->join[kSlots], 0));
-    for (int k = 0; k < kSlots; ++k) {
+    for (int k = 0; k < kOrd; ++k) {
         cudaEventDestroy(ordered[k]);
         cudaEventDestroy(evaluated[k]);
-        cudaEventDestroy(selected[k]);
     }
+    for (int k = 0; k < kSlots; ++k) cudaEventDestroy(selected[k]);
     if (rc) return rc;
     SG_CUDA(ctx, copy_async(ctx, bands, d_bands, 7 * n_days * n_windows * sizeof(double), cudaMemcpyDeviceToHost,
                             ctx->stream));

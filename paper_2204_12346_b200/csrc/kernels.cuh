@@ -1041,6 +1041,41 @@ __host__ __device__ __forceinline__ int sel_shift(unsigned long long range) {
     return bits > kSelBinBits ? bits - kSelBinBits : 0;
 }
 
+// Evaluation order of an ensemble: every sample's parameters into SoA
+// planes, keys[k] = a key (day of t1, day of t2, each in steps of `q` days and
+// capped at 63) and keys[n + k] = its rank among the samples of that key —
+// samples with equal keys ramp on the same days, so grouping them makes a
+// warp's lanes ramp together (the warp pays a ramp substep if any lane
+// ramps).  The order never changes a result: every sample is evaluated by
+// the same code into its own slot, and the bands only need each day's
+// multiset.  Fused: the key histogram of the counting sort
+// (ens_scan_kernel, ens_scatter_kernel).
+constexpr int kOrderKeys = 4096;
+__device__ __forceinline__ void sample_into(const double* __restrict__ lo, const double* __restrict__ hi,
+                                            uint64_t seed, size_t n, int q, size_t k, double* __restrict__ planes,
+                                            uint32_t* __restrict__ keys, unsigned int* __restrict__ key_count) {
+    auto day = [q](double t) -> uint32_t {  // NaN and negatives -> 0, capped at 63 steps
+        return t > 0.0 ? static_cast<uint32_t>(fmin(floor(t), 4096.0)) / q : 0u;
+    };
+    double x[6];
+    x_of_sample(lo, hi, seed, k, x);
+#pragma unroll
+    for (int d = 0; d < 6; ++d) planes[d * n + k] = x[d];
+    const uint32_t key = (min(day(x[2]), 63u) << 6) | min(day(x[3]), 63u);
+    keys[k] = key;
+    keys[n + k] = atomicAdd(&key_count[key], 1u);  // the sample's rank within its key
+}
+
+// A later window's samples drawn by an ensemble launch (the batch band
+// pipeline): its seed and order buffers; planes == nullptr for none.
+struct EnsNext {
+    uint64_t seed;
+    double* planes;
+    uint32_t* keys;
+    unsigned int* key_count;
+    int q;
+};
+
 #ifndef SG_FAMILY_TU  // engine.cu only (family.cu holds the templated kernels)
 // Thread counts of the selection stream's kernels (ordering and band
 // selection).  They run beside the FP64-bound ensemble kernel of the next
@@ -1053,32 +1088,14 @@ constexpr int kBgThreads = 128;       // small kernels (init, scan, locate, band
 constexpr int kSampleThreads = 256;   // ens_sample / ens_scatter / sel_range / sel_gather / sel_finish
 constexpr int kHistThreads = 1024;    // sel_hist (a CTA histogram in shared memory)
 
-// Evaluation order of an ensemble: every sample's parameters into SoA
-// planes, keys[k] = a key (day of t1, day of t2, each in steps of `q` days and
-// capped at 63) and keys[n + k] = its rank among the samples of that key —
-// samples with equal keys ramp on the same days, so
-// grouping them makes a warp's lanes ramp together (the warp pays a ramp
-// substep if any lane ramps).  The order never changes a result: every
-// sample is evaluated by the same code into its own slot, and the bands
-// only need each day's multiset.  Fused: the key histogram of the counting
-// sort (ens_scan_kernel, ens_scatter_kernel).
-constexpr int kOrderKeys = 4096;
-__global__ void __launch_bounds__(kSampleThreads) ens_sample_kernel(const double* __restrict__ lo, const double* __restrict__ hi,
-                                               uint64_t seed, size_t n, int q, double* __restrict__ planes,
-                                               uint32_t* __restrict__ keys, unsigned int* __restrict__ key_count) {
-    auto day = [q](double t) -> uint32_t {  // NaN and negatives -> 0, capped at 63 steps
-        return t > 0.0 ? static_cast<uint32_t>(fmin(floor(t), 4096.0)) / q : 0u;
-    };
+__global__ void __launch_bounds__(kSampleThreads) ens_sample_kernel(const double* __restrict__ lo,
+                                                                   const double* __restrict__ hi, uint64_t seed,
+                                                                   size_t n, int q, double* __restrict__ planes,
+                                                                   uint32_t* __restrict__ keys,
+                                                                   unsigned int* __restrict__ key_count) {
     for (size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
-         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        double x[6];
-        x_of_sample(lo, hi, seed, k, x);
-#pragma unroll
-        for (int d = 0; d < 6; ++d) planes[d * n + k] = x[d];
-        const uint32_t key = (min(day(x[2]), 63u) << 6) | min(day(x[3]), 63u);
-        keys[k] = key;
-        keys[n + k] = atomicAdd(&key_count[key], 1u);  // the sample's rank within its key
-    }
+         k += static_cast<size_t>(gridDim.x) * blockDim.x)
+        sample_into(lo, hi, seed, n, q, k, planes, keys, key_count);
 }
 
 // Exclusive scan of the kOrderKeys key counts into bucket cursors
@@ -1221,11 +1238,16 @@ __global__ void __launch_bounds__(kEvalThreads, 5) ensemble_kernel(const DevWind
                                                                 const double* __restrict__ planes, int out_by_slot,
                                                                 SelDay* __restrict__ days,
                                                                 unsigned int* __restrict__ hist,
-                                                                unsigned long long* __restrict__ ramp_count) {
+                                                                unsigned long long* __restrict__ ramp_count,
+                                                                EnsNext next) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ DevWindow sdesc;
     __shared__ unsigned long long s_pbase[32];
     __shared__ int s_pshift[32];
+    if (next.planes) {  // a later window's sample of this slot (integer work before the FP64-bound part)
+        const size_t s0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        if (s0 < n) sample_into(lo, hi, next.seed, n, next.q, s0, next.planes, next.keys, next.key_count);
+    }
     if (days && static_cast<int>(threadIdx.x) <= horizon) {  // the band path (horizon < 32)
         s_pbase[threadIdx.x] = days[threadIdx.x].pbase;
         s_pshift[threadIdx.x] = days[threadIdx.x].pshift;

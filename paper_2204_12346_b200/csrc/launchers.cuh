@@ -96,8 +96,8 @@ struct EnsembleLaunch {
     static void run(const DevWindow* w, const DevWindow& fwin, const double* lo, const double* hi, uint64_t seed,
                     size_t n, int horizon, double* costs, double* params, double* deaths, size_t sstride,
                     size_t dstride, const uint32_t* perm, const double* planes, int out_by_slot, SelDay* days,
-                    unsigned int* hist, unsigned long long* ramp_count, size_t smem, cudaStream_t st,
-                    cudaError_t* err);
+                    unsigned int* hist, unsigned long long* ramp_count, EnsNext next, size_t smem,
+                    cudaStream_t st, cudaError_t* err);
 };
 
 // out of class: not implicitly inline, so `extern template` keeps engine.cu from instantiating it
@@ -105,14 +105,14 @@ template <int F, int M, int S>
 void EnsembleLaunch<F, M, S>::run(const DevWindow* w, const DevWindow& fwin, const double* lo, const double* hi, uint64_t seed,
                     size_t n, int horizon, double* costs, double* params, double* deaths, size_t sstride,
                     size_t dstride, const uint32_t* perm, const double* planes, int out_by_slot, SelDay* days,
-                    unsigned int* hist, unsigned long long* ramp_count, size_t smem, cudaStream_t st,
-                    cudaError_t* err) {
+                    unsigned int* hist, unsigned long long* ramp_count, EnsNext next, size_t smem,
+                    cudaStream_t st, cudaError_t* err) {
     auto k = ensemble_kernel<F, M, S>;
     *err = prepare_smem(k, smem);
     if (*err != cudaSuccess) return;
     const unsigned grid = static_cast<unsigned>((n + kEvalThreads - 1) / kEvalThreads);
     k<<<grid, kEvalThreads, smem, st>>>(w, fwin, lo, hi, seed, n, horizon, costs, params, deaths, sstride,
-                                        dstride, perm, planes, out_by_slot, days, hist, ramp_count);
+                                        dstride, perm, planes, out_by_slot, days, hist, ramp_count, next);
     *err = cudaGetLastError();
 }
 
