@@ -17,6 +17,9 @@ against the pure reference and against the binding:
     python/sirdfit/__init__.py: the reference's tests/python/test_smoke.py
     passes on the engine (its two CLI cases included), and fit/forecast
     values equal the pure-reference module's bit for bit.
+  * tests/test_*.cpp, the reference's doctest unit suite (built against
+    oracle/doctest_standin): 73 test cases pass on the engine as on the pure
+    reference.
   * tools/main.cpp, the `sirdfit` CLI (built against oracle/cli11_standin:
     the reference does not ship its vendored CLI11): acceptance #4 and #8
     drive it, and every output file of preprocess / fit / compare / forecast
@@ -93,6 +96,23 @@ def test_acceptance_criterion_10_device_objective():
     r_serial, _ = (float(x) for x in pat.search(ref.stdout).groups())
     d_serial, d_parallel = (float(x) for x in pat.search(dev.stdout).groups())
     assert max(d_serial, d_parallel) < r_serial, (ref.stdout, dev.stdout)
+
+
+def test_reference_unit_tests_on_engine():
+    """The reference's own doctest suite (tests/test_model.cpp,
+    test_objectives.cpp, test_pso.cpp, test_calibration.cpp,
+    test_timeseries.cpp: 73 test cases, ~65k assertions), built unmodified
+    against oracle/doctest_standin, passes on the engine exactly as it does
+    on the pure reference."""
+    ref, b200 = REF / "unit_tests_ref", REF / "unit_tests_b200"
+    _need(ref, b200)
+    r = subprocess.run([str(ref)], capture_output=True, text=True, timeout=900)
+    e = subprocess.run([str(b200)], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:]
+    assert e.returncode == 0, e.stdout[-3000:]
+    summary = [ln for ln in e.stdout.splitlines() if ln.startswith("[doctest]")]
+    assert summary == [ln for ln in r.stdout.splitlines() if ln.startswith("[doctest]")], (summary, r.stdout[-500:])
+    assert "73 passed | 0 failed" in summary[0], summary
 
 
 def _run_py(pkg_dir, code):

@@ -18,7 +18,8 @@ def _need(*paths):
             pytest.skip(f"{p} not built (oracle/Makefile refcallers needs /root/reference)")
 
 
-@pytest.mark.parametrize("binary", ["acceptance_b200", "api_parity", "sirdfit_cli_b200", "py_b200/sirdfit/_core"])
+@pytest.mark.parametrize("binary", ["acceptance_b200", "api_parity", "sirdfit_cli_b200", "unit_tests_b200",
+                                    "py_b200/sirdfit/_core"])
 def test_binding_links_the_engine(binary):
     path = REF / binary
     if binary.endswith("_core"):
@@ -66,3 +67,14 @@ def test_reference_cli_builds_with_the_standin_and_passes_acceptance_4_and_8_on_
         assert r.returncode == 0 and "PASS" in r.stdout, r.stdout + r.stderr
     r = subprocess.run([str(REF / "sirdfit_cli_b200"), "fit", "--population", "1000"], capture_output=True, text=True)
     assert r.returncode != 0 and "--input is required" in r.stderr
+
+
+def test_reference_unit_suite_builds_with_the_standin_and_passes_on_cpu():
+    """The doctest stand-in (oracle/doctest_standin) compiles the reference's
+    unmodified unit tests; on the pure reference all 73 test cases pass (the
+    engine build of the same suite runs in tests/test_gpu_refbinding.py)."""
+    exe = REF / "unit_tests_ref"
+    _need(exe)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:]
+    assert "[doctest] test cases: 73 | 73 passed | 0 failed" in r.stdout, r.stdout[-500:]
