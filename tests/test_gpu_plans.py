@@ -196,3 +196,39 @@ print(h, sum(o[0] for o in out))
     split = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, timeout=300, env=env)
     assert plain.returncode == 0 and split.returncode == 0, plain.stderr[-800:] + split.stderr[-800:]
     assert plain.stdout.split() == split.stdout.split() and plain.stdout.split()[1] == "0"
+
+
+def test_no_device_memory_growth_across_calls(ctx, poland):
+    """Repeated plans, band pipelines, single-window bands and reused plans
+    on one context leave the device's free memory where it was after a
+    warm-up (stream-ordered buffers are returned to the pool each call)."""
+    import gc
+
+    import torch
+
+    import paper_2204_12346_b200 as eng
+
+    def one_round():
+        wins = [_window(eng, ctx, poland, 3 * w, 36, "ird-mxse")[0] for w in range(4)]
+        box = [2, 2, 28, 28, 1, 0.1]
+        ctx.fit_swarms([dict(window=w, lower=[0] * 6, upper=box, n_particles=300, max_iters=5, seed=k)
+                        for k, w in enumerate(wins)])
+        ctx.forecast_ensemble_bands_batch(wins, [0] * 6, box, [1, 2, 3, 4], 20000, 21)
+        wins[0].forecast_ensemble_bands([0] * 6, box, 1, 5000, 21)
+        plan = eng.Plan(ctx, [dict(window=wins[0], lower=[0] * 6, upper=box, n_particles=4096, max_iters=3, seed=1)])
+        for _ in range(3):
+            plan.run()
+        plan.close()
+        del wins
+        gc.collect()
+
+    def free():
+        torch.cuda.synchronize()
+        return torch.cuda.mem_get_info()[0]
+
+    for _ in range(3):
+        one_round()
+    before = free()
+    for _ in range(20):
+        one_round()
+    assert abs(before - free()) <= 2 << 20, (before, free())
