@@ -382,6 +382,29 @@ def test_ensemble_bands_batch_random_against_host_sort(ctx, poland, seed):
         assert_bitwise(bands[k].ravel(), want.ravel(), f"seed {seed} window {k}")
 
 
+def test_ensemble_bands_batch_with_a_non_finite_window(ctx, poland):
+    """A window whose initial state is not finite forecasts NaN for every
+    sample (calibration.cpp:301-303): its bands are NaN with zero counts,
+    and it does not disturb the pipeline around it — the samples it draws
+    for the window two ahead, the next windows' predicted bins."""
+    import paper_2204_12346_b200 as eng
+    N = poland["N"]
+    wins = []
+    for k, a in enumerate((0, 3, 6, 9, 12)):
+        I, R, D = poland["I"][a:a + 36], poland["R"][a:a + 36], poland["D"][a:a + 36]
+        init = [N - I[0] - R[0] - D[0], I[0], R[0], D[0]]
+        if k == 1:
+            init[1] = float("nan")
+        wins.append(eng.Window(ctx, I, R, D, init, N, "ird-mxse"))
+    lo, hi, seeds = [0.0] * 6, [2.0, 2.0, 28.0, 28.0, 1.0, 0.1], [31, 32, 33, 34, 35]
+    bands, counts = ctx.forecast_ensemble_bands_batch(wins, lo, hi, seeds, 30_000, 21)
+    assert counts[1].tolist() == [0] * 22 and np.all(np.isnan(bands[1]))
+    for k in (0, 2, 3, 4):
+        b1, c1, _ = wins[k].forecast_ensemble_bands(lo, hi, seeds[k], 30_000, 21)
+        assert counts[k].tolist() == c1.tolist() and c1[0] == 30_000
+        assert_bitwise(bands[k].ravel(), b1.ravel(), f"window {k}")
+
+
 def test_ensemble_ramp_telemetry_is_exact(ctx, poland):
     """The band path's ramp-substep count (the roofline's ramp credit) is
     exact: switch times pinned by the box (t1 = 0, t2 = 10 days) ramp on
