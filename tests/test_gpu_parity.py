@@ -267,7 +267,7 @@ def _host_bands(deaths):
     return bands, counts
 
 
-@pytest.mark.parametrize("case", ["wide", "narrow", "identical", "tiny", "blowups"])
+@pytest.mark.parametrize("case", ["wide", "narrow", "identical", "tiny", "blowups", "long_horizon"])
 def test_ensemble_band_selection_equals_full_sort(ctx, poland, case):
     """The device bands select 14 order statistics per day through key bins
     instead of sorting; they must equal sorting the same ensemble's deaths
@@ -291,7 +291,7 @@ def test_ensemble_band_selection_equals_full_sort(ctx, poland, case):
     elif case == "blowups":
         hi = [1e150, 1e150, 28.0, 28.0, 1e150, 1e150]
         n = 100_000
-    horizon = 21
+    horizon = 40 if case == "long_horizon" else 21  # past 31 days: the key-range pass instead of the fused one
     bands, counts, _ = win.forecast_ensemble_bands(lo, hi, seed=99, n=n, horizon=horizon)
     _, _, deaths = win.forecast_ensemble(lo, hi, seed=99, n=n, horizon=horizon, want_costs=False, want_params=False)
     want, want_counts = _host_bands(deaths)
