@@ -78,3 +78,34 @@ def test_window_objective_rejects_wrong_dimension(ctx, poland):
     with pytest.raises(eng.errors.Error) as exc:
         win.eval_costs(np.zeros((4, 5)))
     assert str(exc.value) == "window objective expects 6-dim positions"
+
+
+def test_band_calls_reject_bad_arguments_without_side_effects(ctx, poland):
+    """The C5 band calls validate before any device work: a bound outside
+    its box names its dimension like the PSO config check (pso.cpp:16-34),
+    a negative horizon and windows of two contexts are refused, and the
+    context keeps working afterwards."""
+    import paper_2204_12346_b200 as eng
+    from paper_2204_12346_b200.errors import Error
+    I, R, D, init, N = _series(poland, 0, 36)
+    win = eng.Window(ctx, I, R, D, init, N, "ird-mxse")
+    lo, hi = [0.0] * 6, [2.0, 2.0, 28.0, 28.0, 1.0, 0.1]
+    bad_hi = list(hi)
+    bad_hi[3] = -1.0
+    with pytest.raises(Error, match="bound 3 is invalid"):
+        ctx.forecast_ensemble_bands_batch([win, win], lo, bad_hi, [1, 2], 1000, 21)
+    with pytest.raises(Error, match="bound 3 is invalid"):
+        win.forecast_ensemble_bands(lo, bad_hi, 1, 1000, 21)
+    with pytest.raises(Error, match="horizon"):
+        ctx.forecast_ensemble_bands_batch([win], lo, hi, [1], 1000, -1)
+    other = eng.Context(0)
+    try:
+        w2 = eng.Window(other, I, R, D, init, N, "ird-mxse")
+        with pytest.raises(Error, match="share one context"):
+            ctx.forecast_ensemble_bands_batch([win, w2], lo, hi, [1, 2], 1000, 21)
+        del w2
+    finally:
+        other.close()
+    bands, counts = ctx.forecast_ensemble_bands_batch([win], lo, hi, [7], 1000, 21)
+    b1, c1, _ = win.forecast_ensemble_bands(lo, hi, 7, 1000, 21)
+    assert counts[0].tolist() == c1.tolist() and np.array_equal(bands[0], b1, equal_nan=True)
