@@ -12,6 +12,19 @@ def main():
     I, R, D = bench.load_series()
     N = bench.POPULATION
     ctx = eng.Context(0)
+    if "--batch" in sys.argv:  # the pipelined many-window call (fused selection passes, samples drawn ahead)
+        n_win = int(sys.argv[1]) if sys.argv[1] != "--batch" else 6
+        wins = []
+        for w in range(n_win):
+            a = w * bench.DELTA
+            sl = slice(a, a + 36)
+            wins.append(eng.Window(ctx, I[sl], R[sl], D[sl], [N - I[a] - R[a] - D[a], I[a], R[a], D[a]], N,
+                                   bench.SPEC))
+        bands, counts = ctx.forecast_ensemble_bands_batch(wins, [0] * 6, [2.0, 2.0, 28.0, 28.0, 1.0, 0.1],
+                                                          [bench.mix_seed(2204, w) for w in range(n_win)],
+                                                          1_000_000, 21)
+        print(float(bands[-1][0, -1]), int(counts[-1][-1]), flush=True)
+        return
     for w in range(int(sys.argv[1]) if len(sys.argv) > 1 else 3):
         a = w * bench.DELTA
         sl = slice(a, a + 36)

@@ -70,7 +70,7 @@ def opcode_mix(rep):
     return ops
 
 
-def step(rep, tag, cmd, note, kernel):
+def step(rep, tag, cmd, note, kernel, prefix="ncu_step_kernel"):
     m = raw_metrics(rep)
     ops = opcode_mix(rep)
 
@@ -99,14 +99,14 @@ def step(rep, tag, cmd, note, kernel):
          "other_ops_per_particle_executed": 32.0 * sum(v for k, v in ops.items()
                                                        if k not in ("DADD", "DMUL", "DFMA", "DSETP")) / particles,
          "note": note}
-    out = PROF / f"ncu_step_kernel_{tag}.json"
+    out = PROF / f"{prefix}_{tag}.json"
     out.write_text(json.dumps(d, indent=1) + "\n")
     print(json.dumps(d, indent=1))
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["launches", "step"])
+    ap.add_argument("what", choices=["launches", "step", "ensemble"])
     ap.add_argument("path")
     ap.add_argument("--tag", required=True)
     ap.add_argument("--cmd", default="")
@@ -116,7 +116,8 @@ def main():
     if a.what == "launches":
         launches(a.path, a.tag, a.cmd)
     else:
-        step(a.path, a.tag, a.cmd, a.note, a.kernel)
+        step(a.path, a.tag, a.cmd, a.note, a.kernel,
+             prefix="ncu_ensemble_kernel" if a.what == "ensemble" else "ncu_step_kernel")
 
 
 if __name__ == "__main__":
