@@ -9,9 +9,11 @@ arm import this module, as the checker.  The product package never does.
                           Swarm driving the GPU objective through the C-ABI
                           (the drop-in under test)
 
-build("refcallers") also builds the reference's own callers (acceptance
-harness, pybind module) against the unmodified reference and against
-ref_binding/ into oracle/_ref/.
+build("refcallers") also builds the reference's own callers (doctest unit
+suite, acceptance harness, pybind module, CLI — the first and last against
+the stand-in headers in oracle/doctest_standin and oracle/cli11_standin)
+against the unmodified reference and against ref_binding/ (INTEGRATION.md
+§2) into oracle/_ref/.
 """
 from __future__ import annotations
 
